@@ -1,0 +1,240 @@
+/*
+ * endor_cuda.h -- C ABI of the B200-native Endor decompression path.
+ *
+ * The reference (arXiv 2406.11674 "Endor", /root/reference/proj) is a
+ * header-only C++20 library; its hot path is the CPU scalar decompress.  This
+ * header is the drop-in boundary that replaces that path with sm_100a kernels:
+ * plain C, plain pointers and sizes, no CUDA or torch types (streams are
+ * passed as `void*` holding a cudaStream_t; NULL = legacy default stream).
+ * include/endor_cuda.hpp wraps it in the reference's own C++ signatures
+ * (endor::cuda::decompress(const EndorTensor&) -> DenseMatrix, ...), and
+ * INTEGRATION.md shows the binding a maintainer adds to the reference tree.
+ *
+ * Reference interfaces replaced (paths under proj/include/endor/):
+ *   endor_cuda_decompress            <- decompress             codec.hpp:157-166
+ *   endor_cuda_decompress_chunked    <- decompress_chunked     codec.hpp:205-216
+ *   endor_cuda_decompress_chunk_into <- decompress_chunk_into  codec.hpp:191-201
+ *   endor_cuda_rank_index            <- build_rank_index       bitmap.hpp:117-132
+ *   endor_cuda_popcount              <- Bitmap::count          bitmap.hpp:34-38
+ *   endor_cuda_compress              <- compress               codec.hpp:97-126
+ *   endor_cuda_synth_weight          <- synth_weight           weight_gen.hpp:40-55
+ *   endor_cuda_magnitude_prune       <- magnitude_prune        weight_gen.hpp:96-113
+ *   endor_cuda_gemv                  <- (absent; the consumer is modelled as a
+ *                                        constant compute time, sim.hpp:227)
+ *   endor_pipeline_*                 <- the Endor offload stages, modelled
+ *                                        only analytically at sim.hpp:196-224
+ *   endor_cuda_decompress_host       <- decompress() end to end over host
+ *                                        buffers (H2D -> kernels -> D2H)
+ *
+ * Errors.  Every entry point returns an endor_status that maps 1:1 onto the
+ * reference's exception classes (error.hpp:9-63) so the C++ wrapper can
+ * rethrow the same types.  Host-checkable conditions are returned
+ * synchronously.  Conditions only the device can see (bitmap popcount !=
+ * nnz, codec.hpp:158-160; rank index inconsistent with the bitmap,
+ * codec.hpp:170-184; nonzero bitmap padding bits, bitmap.hpp:78-84) are
+ * latched in the workspace and returned by endor_cuda_sync_status(); the
+ * kernels that follow a latched error write nothing.
+ *
+ * Memory.  Device pointers unless a name says _host.  bitmap: ceil(n/8)
+ * LSB-first bytes (bit i = byte i>>3, bit i&7; bitmap.hpp:14-17), 4-byte
+ * aligned.  values: nnz*elem_bytes raw little-endian elements in row-major
+ * order, any alignment.  dense output: 16-byte aligned.  The workspace is
+ * caller-owned device memory of endor_cuda_workspace_bytes() bytes; it must be
+ * zero-filled once before first use (endor_cuda_workspace_init) and is left
+ * zeroed by every successful call.  One workspace per in-flight stream.
+ * Nothing on the hot path allocates.
+ *
+ * Threading.  All entry points are reentrant per (stream, workspace) pair;
+ * like the reference inputs are never mutated.
+ */
+#ifndef ENDOR_CUDA_H
+#define ENDOR_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ENDOR_CUDA_ABI_VERSION 1
+
+typedef enum endor_status {
+    ENDOR_OK = 0,
+    ENDOR_ERR_SIZE = 1,             /* SizeError        error.hpp:15-18  */
+    ENDOR_ERR_CORRUPTION = 2,       /* CorruptionError  error.hpp:22-25  */
+    ENDOR_ERR_BOUNDS = 3,           /* BoundsError      error.hpp:28-31  */
+    ENDOR_ERR_INVALID_ARGUMENT = 4, /* std::invalid_argument             */
+    ENDOR_ERR_CUDA = 5,             /* CUDA runtime failure (no reference analogue) */
+    ENDOR_ERR_CONFIG = 6            /* ConfigError      error.hpp:34-37  */
+} endor_status;
+
+/* Dtype codes, dense_matrix.hpp:18-21 (also the on-disk codes). */
+#define ENDOR_DTYPE_F16 0
+#define ENDOR_DTYPE_I8 1
+
+/* Device-side view of an EndorTensor (codec.hpp:24-66). */
+typedef struct endor_tensor_view {
+    uint64_t rows;
+    uint64_t cols;
+    int32_t dtype;       /* ENDOR_DTYPE_* */
+    int32_t reserved;
+    const void* bitmap;  /* ceil(rows*cols/8) bytes, 4-byte aligned */
+    const void* values;  /* nnz * elem_bytes bytes */
+    uint64_t nnz;
+} endor_tensor_view;
+
+/* ---- library ------------------------------------------------------------ */
+int endor_cuda_abi_version(void);
+const char* endor_cuda_last_error_string(void); /* thread-local detail of the last failure */
+const char* endor_cuda_status_name(int status);
+
+/* Elements per expand tile (the kernel's natural unit, a multiple of every
+ * RankIndex chunk size <= it). */
+uint64_t endor_cuda_tile_elems(void);
+
+/* Workspace for any call on a tensor of up to n = rows*cols elements. */
+size_t endor_cuda_workspace_bytes(uint64_t rows, uint64_t cols);
+int endor_cuda_workspace_init(void* ws, size_t ws_bytes, void* stream);
+
+/* Wait for `stream` and return (and clear) any device-latched status. */
+int endor_cuda_sync_status(void* ws, void* stream);
+
+/* ---- hot path ----------------------------------------------------------- */
+
+/* decompress (codec.hpp:157-166): dense_out[n*eb] <- t.  Asynchronous. */
+int endor_cuda_decompress(const endor_tensor_view* t, void* dense_out, void* ws, size_t ws_bytes,
+                          void* stream);
+
+/* build_rank_index (bitmap.hpp:117-132) on device: prefix_out[ceil(n/cs)]
+ * u64 exclusive per-chunk popcounts.  cs must be a power of two >= 64, else
+ * ENDOR_ERR_INVALID_ARGUMENT (bitmap.hpp:118-120).  total_out (device u64,
+ * may be NULL) receives the popcount. */
+int endor_cuda_rank_index(const void* bitmap, uint64_t n, uint64_t chunk_size, uint64_t* prefix_out,
+                          uint64_t* total_out, void* ws, size_t ws_bytes, void* stream);
+
+/* Bitmap::count (bitmap.hpp:34-38) into a device u64. */
+int endor_cuda_popcount(const void* bitmap, uint64_t n, uint64_t* total_out, void* ws,
+                        size_t ws_bytes, void* stream);
+
+/* decompress_chunked (codec.hpp:205-216) with a device-resident RankIndex.
+ * chunk_count must equal ceil(n/cs) (else CORRUPTION, codec.hpp:174-176);
+ * every prefix entry is verified on device (a superset of check_index). */
+int endor_cuda_decompress_chunked(const endor_tensor_view* t, uint64_t chunk_size,
+                                  const uint64_t* prefix, uint64_t chunk_count, void* dense_out,
+                                  void* ws, size_t ws_bytes, void* stream);
+
+/* decompress_chunk_into (codec.hpp:191-201): writes exactly and only chunk
+ * k's byte range of dense_out (which must hold the full dense matrix,
+ * dense_out_bytes == n*eb, else INVALID_ARGUMENT; k >= chunk_count ->
+ * BOUNDS).  Like check_index, verifies prefix[last] + tail popcount == nnz. */
+int endor_cuda_decompress_chunk_into(const endor_tensor_view* t, uint64_t chunk_size,
+                                     const uint64_t* prefix, uint64_t chunk_count, uint64_t k,
+                                     void* dense_out, uint64_t dense_out_bytes, void* ws,
+                                     size_t ws_bytes, void* stream);
+
+/* Same as endor_cuda_decompress over HOST buffers: H2D of bitmap+values,
+ * decompress, D2H of the dense matrix, synchronous, device buffers cached
+ * per thread.  This is what endor::cuda::decompress(const EndorTensor&) calls. */
+int endor_cuda_decompress_host(uint64_t rows, uint64_t cols, int32_t dtype,
+                               const void* bitmap_host, const void* values_host, uint64_t nnz,
+                               void* dense_host_out);
+
+/* Host-buffer, synchronous forms of the other reference entry points (what
+ * the endor::cuda:: C++ wrappers call).  Check order and error codes follow
+ * the reference exactly: check_index (CORRUPTION) before the chunk bound
+ * (BOUNDS) before the destination size (INVALID_ARGUMENT), codec.hpp:193-197. */
+int endor_cuda_rank_index_host(const void* bitmap_host, uint64_t n, uint64_t chunk_size,
+                               uint64_t* prefix_host_out);
+int endor_cuda_decompress_chunked_host(uint64_t rows, uint64_t cols, int32_t dtype,
+                                       const void* bitmap_host, const void* values_host,
+                                       uint64_t nnz, uint64_t chunk_size,
+                                       const uint64_t* prefix_host, uint64_t chunk_count,
+                                       void* dense_host_out);
+int endor_cuda_decompress_chunk_into_host(uint64_t rows, uint64_t cols, int32_t dtype,
+                                          const void* bitmap_host, const void* values_host,
+                                          uint64_t nnz, uint64_t chunk_size,
+                                          const uint64_t* prefix_host, uint64_t chunk_count,
+                                          uint64_t k, void* dense_host, uint64_t dense_host_bytes);
+/* compress over host buffers: values_host_out needs n*eb capacity. */
+int endor_cuda_compress_host(uint64_t rows, uint64_t cols, int32_t dtype, const void* dense_host,
+                             void* bitmap_host_out, void* values_host_out, uint64_t* nnz_out,
+                             int32_t* negzero_out);
+
+/* ---- input producers (offline in the paper) ---------------- */
+
+/* compress (codec.hpp:97-126) on device.  values_out must hold n*eb bytes
+ * (worst case); *nnz_out_host and *negzero_out_host are written.  Synchronous. */
+int endor_cuda_compress(uint64_t rows, uint64_t cols, int32_t dtype, const void* dense,
+                        void* bitmap_out, void* values_out, uint64_t* nnz_out_host,
+                        int32_t* negzero_out_host, void* ws, size_t ws_bytes, void* stream);
+
+/* synth_weight (weight_gen.hpp:40-55), bit-exact, for rows [row0, row0+nrows)
+ * of a rows x cols matrix (element index i = global row-major index). */
+int endor_cuda_synth_weight(uint64_t rows, uint64_t cols, int32_t dtype, uint64_t seed,
+                            uint64_t row0, uint64_t nrows, void* out, void* stream);
+
+/* magnitude_prune (weight_gen.hpp:96-113) in place over n elements,
+ * bit-exact (exactly floor(s*n) smallest |v| zeroed, ties at the lower index).
+ * Synchronous (one small D2H for the threshold). */
+int endor_cuda_magnitude_prune(uint64_t n, int32_t dtype, double sparsity, void* w, void* ws,
+                               size_t ws_bytes, void* stream);
+
+/* ---- consumer ------------------------------------------------------------ */
+
+/* y[rows] = W[rows, cols] . x[cols]; f16 W and x, fp32 accumulate.  y_f32
+ * and/or y_f16 may be NULL.  W rows are outputs (catalog orientation). */
+int endor_cuda_gemv(uint64_t rows, uint64_t cols, const void* w_f16, const void* x_f16,
+                    float* y_f32, void* y_f16, void* stream);
+
+/* ---- offload pipeline ---------------------------------------------------- */
+/* Streams compressed ops from pinned host memory through a double-buffered
+ * device staging ring: H2D of op i+1 on the copy stream overlaps decompress
+ * + GEMV of op i on the compute stream (the Endor mode stages of
+ * sim.hpp:200-204, executed for real and overlapped). */
+
+typedef struct endor_pipeline endor_pipeline;
+
+typedef struct endor_pipeline_op {
+    uint64_t rows, cols;
+    int32_t dtype;           /* F16 only for the GEMV consumer */
+    int32_t reserved;
+    const void* bitmap_host; /* pinned (cudaHostAlloc / endor_host_alloc) */
+    const void* values_host; /* pinned */
+    uint64_t nnz;
+    const void* x_dev;       /* GEMV input, f16[cols]; NULL = decompress only */
+    float* y_dev;            /* GEMV output, f32[rows]; NULL = decompress only */
+    void* dense_dev;         /* optional: where the dense W lands (NULL = ring) */
+} endor_pipeline_op;
+
+typedef struct endor_pipeline_stats {
+    double total_ms;         /* first H2D start -> last op done (device events) */
+    double h2d_ms;           /* sum of per-op H2D durations */
+    double decompress_ms;    /* sum of per-op decompress durations */
+    double gemv_ms;          /* sum of per-op GEMV durations */
+    double exposed_compute_ms; /* total_ms minus the copy-engine busy span */
+    uint64_t h2d_bytes;
+    uint64_t dense_bytes;
+    uint64_t kernel_launches;
+} endor_pipeline_stats;
+
+/* device_ordinal: CUDA device to use.  max_op_*: largest op the pipeline
+ * will see (sizes the ring). */
+int endor_pipeline_create(int device_ordinal, uint64_t max_op_elems, int ring_depth,
+                          endor_pipeline** out);
+int endor_pipeline_destroy(endor_pipeline* p);
+/* Run ops[0..nops) in order; asynchronous w.r.t. the host unless sync != 0. */
+int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops, int sync);
+/* Timings of the most recent run (synchronises). */
+int endor_pipeline_stats_get(endor_pipeline* p, endor_pipeline_stats* out);
+/* The pipeline's compute stream (cudaStream_t as void*). */
+void* endor_pipeline_stream(endor_pipeline* p);
+
+/* Pinned host allocation helpers (cudaHostAlloc, portable). */
+void* endor_host_alloc(size_t bytes);
+void endor_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ENDOR_CUDA_H */

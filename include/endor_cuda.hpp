@@ -1,0 +1,108 @@
+// endor_cuda.hpp -- the reference's own C++ codec signatures, executed on a
+// B200 through the C ABI (endor_cuda.h).
+//
+// Drop-in for reference code that includes "endor/endor.hpp": replace
+//     endor::decompress(t)                 (codec.hpp:157)
+//     endor::decompress_chunked(t, idx)    (codec.hpp:205)
+//     endor::decompress_chunk_into(...)    (codec.hpp:191)
+//     endor::build_rank_index(b, cs)       (bitmap.hpp:117)
+//     endor::compress(w)                   (codec.hpp:97)
+// with the same calls in namespace endor::cuda.  Arguments, return types,
+// ownership (value semantics, caller-owned span for chunk_into) and the
+// exception types thrown (error.hpp) are the reference's.  Requires the
+// reference's headers on the include path and links libendor_cuda.so; no
+// CUDA headers are needed by the caller.
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "endor/codec.hpp"
+#include "endor_cuda.h"
+
+namespace endor::cuda {
+
+// Map an endor_status onto the reference's exception classes (error.hpp:9-63).
+inline void check(int status) {
+    if (status == ENDOR_OK) return;
+    const std::string what = endor_cuda_last_error_string();
+    switch (status) {
+        case ENDOR_ERR_SIZE: throw SizeError(what);
+        case ENDOR_ERR_CORRUPTION: throw CorruptionError(what);
+        case ENDOR_ERR_BOUNDS: throw BoundsError(what);
+        case ENDOR_ERR_INVALID_ARGUMENT: throw std::invalid_argument(what);
+        case ENDOR_ERR_CONFIG: throw ConfigError(what);
+        default: throw Error("CUDA: " + what);
+    }
+}
+
+inline int32_t dtype_code(Dtype d) { return static_cast<int32_t>(d); }
+
+// decompress (codec.hpp:157-166).  The reference re-checks values vs popcount
+// first (:158-160); EndorTensor's constructor already guarantees it and the
+// device re-verifies popcount == nnz.
+inline DenseMatrix decompress(const EndorTensor& t) {
+    if (t.values_bytes() != t.nnz() * elem_bytes(t.dtype()))
+        throw CorruptionError("values length does not match bitmap popcount");
+    DenseMatrix out(t.rows(), t.cols(), t.dtype());
+    if (t.element_count() == 0) return out;
+    const auto bm = t.bitmap().to_bytes();
+    check(endor_cuda_decompress_host(t.rows(), t.cols(), dtype_code(t.dtype()), bm.data(),
+                                     t.values().data(), t.nnz(), out.bytes().data()));
+    return out;
+}
+
+// build_rank_index (bitmap.hpp:117-132).
+inline RankIndex build_rank_index(const Bitmap& bitmap, std::uint64_t chunk_size) {
+    if (chunk_size < 64 || (chunk_size & (chunk_size - 1)) != 0)
+        throw std::invalid_argument("chunk_size must be a power of two >= 64");
+    const std::uint64_t n = bitmap.size();
+    const std::uint64_t chunks = n == 0 ? 0 : (n + chunk_size - 1) / chunk_size;
+    std::vector<std::uint64_t> prefix(chunks);
+    if (chunks) {
+        const auto bytes = bitmap.to_bytes();
+        check(endor_cuda_rank_index_host(bytes.data(), n, chunk_size, prefix.data()));
+    }
+    return RankIndex(chunk_size, std::move(prefix));
+}
+
+// decompress_chunked (codec.hpp:205-216).
+inline DenseMatrix decompress_chunked(const EndorTensor& t, const RankIndex& idx) {
+    DenseMatrix out(t.rows(), t.cols(), t.dtype());
+    const auto bm = t.bitmap().to_bytes();
+    check(endor_cuda_decompress_chunked_host(t.rows(), t.cols(), dtype_code(t.dtype()), bm.data(),
+                                             t.values().data(), t.nnz(), idx.chunk_size(),
+                                             idx.prefix().data(), idx.chunk_count(),
+                                             out.bytes().data()));
+    return out;
+}
+
+// decompress_chunk_into (codec.hpp:191-201): writes exactly chunk k's range.
+inline void decompress_chunk_into(const EndorTensor& t, const RankIndex& idx, std::uint64_t k,
+                                  std::span<std::byte> dst) {
+    const auto bm = t.bitmap().to_bytes();
+    check(endor_cuda_decompress_chunk_into_host(t.rows(), t.cols(), dtype_code(t.dtype()), bm.data(),
+                                                t.values().data(), t.nnz(), idx.chunk_size(),
+                                                idx.prefix().data(), idx.chunk_count(), k, dst.data(),
+                                                dst.size()));
+}
+
+// compress (codec.hpp:97-126).
+inline EndorTensor compress(const DenseMatrix& w) {
+    const std::uint64_t n = checked_element_count(w.rows(), w.cols());
+    std::vector<std::byte> bm((n + 7) / 8);
+    std::vector<std::byte> vals(w.size_bytes());
+    std::uint64_t nnz = 0;
+    int32_t negzero = 0;
+    check(endor_cuda_compress_host(w.rows(), w.cols(), dtype_code(w.dtype()), w.bytes().data(),
+                                   bm.data(), vals.data(), &nnz, &negzero));
+    vals.resize(nnz * elem_bytes(w.dtype()));
+    return EndorTensor(w.rows(), w.cols(), w.dtype(), Bitmap::from_bytes(bm, n), std::move(vals),
+                       std::nullopt, negzero != 0);
+}
+
+}  // namespace endor::cuda

@@ -1,0 +1,98 @@
+"""ctypes binding of the C ABI in include/endor_cuda.h (libendor_cuda.so).
+
+There is no fallback: if the shared library is missing or cannot be loaded,
+every entry point raises.  The library is built in-tree by
+``paper_2406_11674_b200/build.py`` (``__graft_entry__.build()``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libendor_cuda.so")
+
+_u64, _i32, _vp, _sz, _f64 = C.c_uint64, C.c_int32, C.c_void_p, C.c_size_t, C.c_double
+
+
+class TensorView(C.Structure):
+    """endor_tensor_view (include/endor_cuda.h)."""
+    _fields_ = [("rows", _u64), ("cols", _u64), ("dtype", _i32), ("reserved", _i32),
+                ("bitmap", _vp), ("values", _vp), ("nnz", _u64)]
+
+
+class PipelineOp(C.Structure):
+    """endor_pipeline_op."""
+    _fields_ = [("rows", _u64), ("cols", _u64), ("dtype", _i32), ("reserved", _i32),
+                ("bitmap_host", _vp), ("values_host", _vp), ("nnz", _u64),
+                ("x_dev", _vp), ("y_dev", _vp), ("dense_dev", _vp)]
+
+
+class PipelineStats(C.Structure):
+    """endor_pipeline_stats."""
+    _fields_ = [("total_ms", _f64), ("h2d_ms", _f64), ("decompress_ms", _f64), ("gemv_ms", _f64),
+                ("exposed_compute_ms", _f64), ("h2d_bytes", _u64), ("dense_bytes", _u64),
+                ("kernel_launches", _u64)]
+
+
+# name -> (restype, argtypes): every symbol include/endor_cuda.h declares
+SIGNATURES = {
+    "endor_cuda_abi_version": (C.c_int, []),
+    "endor_cuda_last_error_string": (C.c_char_p, []),
+    "endor_cuda_status_name": (C.c_char_p, [C.c_int]),
+    "endor_cuda_tile_elems": (_u64, []),
+    "endor_cuda_workspace_bytes": (_sz, [_u64, _u64]),
+    "endor_cuda_workspace_init": (C.c_int, [_vp, _sz, _vp]),
+    "endor_cuda_sync_status": (C.c_int, [_vp, _vp]),
+    "endor_cuda_decompress": (C.c_int, [C.POINTER(TensorView), _vp, _vp, _sz, _vp]),
+    "endor_cuda_rank_index": (C.c_int, [_vp, _u64, _u64, _vp, _vp, _vp, _sz, _vp]),
+    "endor_cuda_popcount": (C.c_int, [_vp, _u64, _vp, _vp, _sz, _vp]),
+    "endor_cuda_decompress_chunked": (C.c_int, [C.POINTER(TensorView), _u64, _vp, _u64, _vp, _vp,
+                                                _sz, _vp]),
+    "endor_cuda_decompress_chunk_into": (C.c_int, [C.POINTER(TensorView), _u64, _vp, _u64, _u64,
+                                                   _vp, _u64, _vp, _sz, _vp]),
+    "endor_cuda_decompress_host": (C.c_int, [_u64, _u64, _i32, _vp, _vp, _u64, _vp]),
+    "endor_cuda_rank_index_host": (C.c_int, [_vp, _u64, _u64, _vp]),
+    "endor_cuda_decompress_chunked_host": (C.c_int, [_u64, _u64, _i32, _vp, _vp, _u64, _u64, _vp,
+                                                     _u64, _vp]),
+    "endor_cuda_decompress_chunk_into_host": (C.c_int, [_u64, _u64, _i32, _vp, _vp, _u64, _u64, _vp,
+                                                        _u64, _u64, _vp, _u64]),
+    "endor_cuda_compress_host": (C.c_int, [_u64, _u64, _i32, _vp, _vp, _vp, C.POINTER(_u64),
+                                           C.POINTER(_i32)]),
+    "endor_cuda_compress": (C.c_int, [_u64, _u64, _i32, _vp, _vp, _vp, C.POINTER(_u64),
+                                      C.POINTER(_i32), _vp, _sz, _vp]),
+    "endor_cuda_synth_weight": (C.c_int, [_u64, _u64, _i32, _u64, _u64, _u64, _vp, _vp]),
+    "endor_cuda_magnitude_prune": (C.c_int, [_u64, _i32, _f64, _vp, _vp, _sz, _vp]),
+    "endor_cuda_gemv": (C.c_int, [_u64, _u64, _vp, _vp, _vp, _vp, _vp]),
+    "endor_pipeline_create": (C.c_int, [C.c_int, _u64, C.c_int, C.POINTER(_vp)]),
+    "endor_pipeline_destroy": (C.c_int, [_vp]),
+    "endor_pipeline_run": (C.c_int, [_vp, C.POINTER(PipelineOp), C.c_int, C.c_int]),
+    "endor_pipeline_stats_get": (C.c_int, [_vp, C.POINTER(PipelineStats)]),
+    "endor_pipeline_stream": (_vp, [_vp]),
+    "endor_host_alloc": (_vp, [_sz]),
+    "endor_host_free": (None, [_vp]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def lib():
+    """Load libendor_cuda.so (raises if absent -- no CPU fallback exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(
+                    f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                    "(there is no CPU fallback for the Endor CUDA path)")
+            L = C.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(L, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = L
+    return _lib

@@ -1,0 +1,414 @@
+"""Host-side mirror of the reference's codec API over the CUDA C ABI.
+
+Same names, argument meaning and error types as the reference's
+``proj/include/endor/`` headers, so parity tests read like the reference's
+own tests.  Data lives in device memory (torch uint8 tensors are used purely
+as allocations + stream plumbing); every compute call goes through
+``libendor_cuda.so`` -- there is no CPU path.
+
+Reference anchors:
+  EndorTensor              codec.hpp:24-66
+  compression_ratio etc.   codec.hpp:75-88
+  compress                 codec.hpp:97-126       -> endor_cuda_compress
+  decompress               codec.hpp:157-166      -> endor_cuda_decompress
+  decompress_chunk_into    codec.hpp:191-201      -> endor_cuda_decompress_chunk_into
+  decompress_chunked       codec.hpp:205-216      -> endor_cuda_decompress_chunked
+  Bitmap / RankIndex       bitmap.hpp:18-132      -> endor_cuda_popcount / _rank_index
+  DenseMatrix / Dtype      dense_matrix.hpp:18-99
+  synth_weight / magnitude_prune  weight_gen.hpp:40-113
+  error classes            error.hpp:9-63
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass
+from typing import Dict, Optional, Tuple
+
+import torch
+
+from . import _lib
+from ._lib import TensorView
+
+
+# ---- errors (error.hpp:9-63) -----------------------------------------------
+
+class Error(RuntimeError):
+    """endor::Error."""
+
+
+class SizeError(Error):
+    """endor::SizeError."""
+
+
+class CorruptionError(Error):
+    """endor::CorruptionError."""
+
+
+class BoundsError(Error):
+    """endor::BoundsError."""
+
+
+class ConfigError(Error):
+    """endor::ConfigError."""
+
+
+class CudaError(Error):
+    """A CUDA runtime failure (no reference analogue)."""
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument."""
+
+
+_STATUS = {1: SizeError, 2: CorruptionError, 3: BoundsError, 4: InvalidArgument, 5: CudaError,
+           6: ConfigError}
+
+
+def check(status: int) -> None:
+    if status != 0:
+        msg = _lib.lib().endor_cuda_last_error_string().decode(errors="replace")
+        raise _STATUS.get(status, Error)(msg)
+
+
+# ---- dtype (dense_matrix.hpp:18-23) -----------------------------------------
+
+class Dtype(enum.IntEnum):
+    F16 = 0
+    I8 = 1
+
+
+def elem_bytes(dtype: Dtype) -> int:
+    return 2 if dtype == Dtype.F16 else 1
+
+
+def checked_element_count(rows: int, cols: int) -> int:
+    """dense_matrix.hpp:28-33."""
+    if rows < 0 or cols < 0 or (rows != 0 and cols > (2 ** 64 - 1) // rows):
+        raise SizeError("matrix dimensions overflow the addressable element count")
+    return rows * cols
+
+
+# ---- size arithmetic (codec.hpp:75-88) --------------------------------------
+
+def compression_ratio(dtype: Dtype, sparsity: float) -> float:
+    if not (0.0 <= sparsity <= 1.0):
+        raise InvalidArgument("sparsity must be in [0, 1]")
+    return (1.0 - sparsity) + 1.0 / (8.0 * elem_bytes(dtype))
+
+
+def endor_values_bytes(dtype: Dtype, nnz: int) -> int:
+    return nnz * elem_bytes(dtype)
+
+
+def endor_bitmap_bytes(rows: int, cols: int) -> int:
+    return (checked_element_count(rows, cols) + 7) // 8
+
+
+# ---- device plumbing ----------------------------------------------------------
+
+def _dev(device=None) -> torch.device:
+    d = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if d.type != "cuda":
+        raise InvalidArgument("the Endor path runs on CUDA devices only")
+    if d.index is None:
+        d = torch.device("cuda", torch.cuda.current_device())
+    return d
+
+
+def _stream_ptr(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None or t.numel() == 0 else t.data_ptr()
+
+
+def _alloc(nbytes: int, device: torch.device, pad: int = 16) -> torch.Tensor:
+    """uint8 device buffer of nbytes (+pad so 16-byte vector loads stay inside)."""
+    return torch.empty(nbytes + pad, dtype=torch.uint8, device=device)[:nbytes]
+
+
+_WS: Dict[Tuple[int, int], torch.Tensor] = {}
+
+
+def workspace(n: int, device: torch.device) -> torch.Tensor:
+    """Zero-initialised workspace for tensors of up to n elements, one per
+    (device, stream) -- the library leaves it zeroed after every call."""
+    key = (device.index, _stream_ptr(device))
+    need = _lib.lib().endor_cuda_workspace_bytes(max(n, 1), 1)
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < need:
+        ws = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=device)
+        _WS[key] = ws
+    return ws
+
+
+def sync_status(ws: torch.Tensor, device: torch.device) -> None:
+    check(_lib.lib().endor_cuda_sync_status(ws.data_ptr(), _stream_ptr(device)))
+
+
+# ---- data model ------------------------------------------------------------------
+
+@dataclass
+class DenseMatrix:
+    """Row-major raw-byte matrix on the device (dense_matrix.hpp:38-99)."""
+    rows: int
+    cols: int
+    dtype: Dtype
+    data: torch.Tensor  # uint8, rows*cols*elem_bytes
+
+    @classmethod
+    def empty(cls, rows, cols, dtype=Dtype.F16, device=None) -> "DenseMatrix":
+        n = checked_element_count(rows, cols)
+        return cls(rows, cols, Dtype(dtype), _alloc(n * elem_bytes(dtype), _dev(device)))
+
+    @classmethod
+    def from_host(cls, rows, cols, dtype, data, device=None) -> "DenseMatrix":
+        n = checked_element_count(rows, cols)
+        buf = torch.as_tensor(bytearray(bytes(data))) if not isinstance(data, torch.Tensor) else data
+        buf = buf.reshape(-1).view(torch.uint8)
+        if buf.numel() != n * elem_bytes(dtype):
+            raise SizeError("dense data length does not match rows*cols*elem_bytes")
+        out = cls.empty(rows, cols, dtype, device)
+        out.data.copy_(buf)
+        return out
+
+    @property
+    def element_count(self) -> int:
+        return self.rows * self.cols
+
+    def elem_size(self) -> int:
+        return elem_bytes(self.dtype)
+
+    def size_bytes(self) -> int:
+        return self.data.numel()
+
+    def bytes(self) -> bytes:
+        return self.data.cpu().numpy().tobytes()
+
+    def __eq__(self, o) -> bool:  # bytewise, dense_matrix.hpp:90-92
+        return (isinstance(o, DenseMatrix) and self.rows == o.rows and self.cols == o.cols and
+                self.dtype == o.dtype and torch.equal(self.data.cpu(), o.data.cpu()))
+
+
+class Bitmap:
+    """Position bitmap on the device: ceil(size/8) LSB-first bytes
+    (bitmap.hpp:14-17)."""
+
+    def __init__(self, bit_count: int, data: Optional[torch.Tensor] = None, device=None):
+        self._n = int(bit_count)
+        nbytes = (self._n + 7) // 8
+        if data is None:
+            data = torch.zeros(nbytes + 16, dtype=torch.uint8, device=_dev(device))[:nbytes]
+        self.data = data
+
+    def size(self) -> int:
+        return self._n
+
+    def byte_size(self) -> int:
+        return (self._n + 7) // 8
+
+    @classmethod
+    def from_bytes(cls, data, bit_count: int, device=None) -> "Bitmap":
+        """bitmap.hpp:72-86: exact length and zero padding bits required."""
+        raw = bytes(data) if not isinstance(data, torch.Tensor) else data.cpu().numpy().tobytes()
+        if len(raw) != (bit_count + 7) // 8:
+            raise CorruptionError("bitmap byte length does not match bit count")
+        used = bit_count & 7
+        if used and raw and (raw[-1] >> used):
+            raise CorruptionError("bitmap has nonzero padding bits")
+        b = cls(bit_count, device=device)
+        if raw:
+            b.data.copy_(torch.frombuffer(bytearray(raw), dtype=torch.uint8))
+        return b
+
+    def to_bytes(self) -> bytes:
+        return self.data.cpu().numpy().tobytes()
+
+    def count(self) -> int:
+        """bitmap.hpp:34-38 (device popcount)."""
+        dev = self.data.device
+        out = torch.zeros(1, dtype=torch.int64, device=dev)
+        ws = workspace(self._n, dev)
+        check(_lib.lib().endor_cuda_popcount(_ptr(self.data), self._n, out.data_ptr(), ws.data_ptr(),
+                                             ws.numel(), _stream_ptr(dev)))
+        sync_status(ws, dev)
+        return int(out.item())
+
+    def __eq__(self, o) -> bool:
+        return isinstance(o, Bitmap) and self._n == o._n and torch.equal(self.data.cpu(), o.data.cpu())
+
+
+@dataclass
+class RankIndex:
+    """Exclusive per-chunk popcount prefix (bitmap.hpp:101-114), device u64."""
+    chunk_size: int
+    prefix: torch.Tensor  # int64 (bit-identical to u64 for these ranges)
+
+    def chunk_count(self) -> int:
+        return self.prefix.numel()
+
+
+class EndorTensor:
+    """Compressed tensor (codec.hpp:24-66): bitmap + packed row-major values."""
+
+    def __init__(self, rows: int, cols: int, dtype: Dtype, bitmap: Bitmap, values: torch.Tensor,
+                 quant_scale: Optional[float] = None, negative_zero_collapsed: bool = False,
+                 validate: bool = True, nnz: Optional[int] = None):
+        self.rows, self.cols, self.dtype = int(rows), int(cols), Dtype(dtype)
+        self.bitmap, self.values = bitmap, values.reshape(-1).view(torch.uint8)
+        self.quant_scale, self._negzero = quant_scale, bool(negative_zero_collapsed)
+        eb = elem_bytes(self.dtype)
+        if validate:  # codec.hpp:34-39
+            if bitmap.size() != checked_element_count(rows, cols):
+                raise CorruptionError("bitmap length does not match rows*cols")
+            if self.values.numel() != bitmap.count() * eb:
+                raise CorruptionError("values length does not match bitmap popcount")
+        self._nnz = self.values.numel() // eb if nnz is None else int(nnz)
+
+    def element_count(self) -> int:
+        return self.rows * self.cols
+
+    def nnz(self) -> int:
+        return self._nnz
+
+    def negative_zero_collapsed(self) -> bool:
+        return self._negzero
+
+    def values_bytes(self) -> int:
+        return self.values.numel()
+
+    def bitmap_bytes(self) -> int:
+        return self.bitmap.byte_size()
+
+    def compressed_bytes(self) -> int:
+        return self.values_bytes() + self.bitmap_bytes()
+
+    def dense_bytes(self) -> int:
+        return self.element_count() * elem_bytes(self.dtype)
+
+    def view(self) -> TensorView:
+        return TensorView(self.rows, self.cols, int(self.dtype), 0, _ptr(self.bitmap.data),
+                          _ptr(self.values), self._nnz)
+
+    @property
+    def device(self) -> torch.device:
+        return self.bitmap.data.device
+
+
+# ---- codec ------------------------------------------------------------------------
+
+def compress(w: DenseMatrix) -> EndorTensor:
+    """codec.hpp:97-126 on the device."""
+    dev = w.data.device
+    n = checked_element_count(w.rows, w.cols)
+    eb = elem_bytes(w.dtype)
+    bm = Bitmap(n, device=dev)
+    vals = _alloc(n * eb, dev)
+    ws = workspace(n, dev)
+    nnz, negz = C.c_uint64(0), C.c_int32(0)
+    check(_lib.lib().endor_cuda_compress(w.rows, w.cols, int(w.dtype), _ptr(w.data), _ptr(bm.data),
+                                         _ptr(vals), C.byref(nnz), C.byref(negz), ws.data_ptr(),
+                                         ws.numel(), _stream_ptr(dev)))
+    values = vals[: nnz.value * eb]
+    return EndorTensor(w.rows, w.cols, w.dtype, bm, values, None, bool(negz.value), validate=False,
+                       nnz=nnz.value)
+
+
+def decompress(t: EndorTensor, out: Optional[DenseMatrix] = None, sync: bool = True) -> DenseMatrix:
+    """codec.hpp:157-166 on the device.  With sync=False the call is
+    asynchronous on the current stream and device-detected corruption is only
+    reported by a later sync_status()."""
+    dev = t.device
+    if out is None:
+        out = DenseMatrix.empty(t.rows, t.cols, t.dtype, dev)
+    ws = workspace(t.element_count(), dev)
+    v = t.view()
+    check(_lib.lib().endor_cuda_decompress(C.byref(v), _ptr(out.data), ws.data_ptr(), ws.numel(),
+                                           _stream_ptr(dev)))
+    if sync:
+        sync_status(ws, dev)
+    return out
+
+
+def build_rank_index(bitmap: Bitmap, chunk_size: int) -> RankIndex:
+    """bitmap.hpp:117-132 on the device."""
+    dev = bitmap.data.device
+    n = bitmap.size()
+    chunks = 0 if (n == 0 or chunk_size <= 0) else (n + chunk_size - 1) // chunk_size
+    prefix = torch.zeros(max(chunks, 1), dtype=torch.int64, device=dev)
+    ws = workspace(n, dev)
+    check(_lib.lib().endor_cuda_rank_index(_ptr(bitmap.data), n, chunk_size, prefix.data_ptr(), None,
+                                           ws.data_ptr(), ws.numel(), _stream_ptr(dev)))
+    sync_status(ws, dev)
+    return RankIndex(chunk_size, prefix[:chunks])
+
+
+def _prefix_ptr(idx: RankIndex, dev: torch.device) -> Tuple[Optional[int], torch.Tensor]:
+    p = idx.prefix.to(device=dev, dtype=torch.int64).contiguous()
+    return (p.data_ptr() if p.numel() else None), p
+
+
+def decompress_chunked(t: EndorTensor, idx: RankIndex) -> DenseMatrix:
+    """codec.hpp:205-216 on the device."""
+    dev = t.device
+    out = DenseMatrix.empty(t.rows, t.cols, t.dtype, dev)
+    ws = workspace(t.element_count(), dev)
+    pp, keep = _prefix_ptr(idx, dev)
+    v = t.view()
+    check(_lib.lib().endor_cuda_decompress_chunked(C.byref(v), idx.chunk_size, pp, idx.chunk_count(),
+                                                   _ptr(out.data), ws.data_ptr(), ws.numel(),
+                                                   _stream_ptr(dev)))
+    sync_status(ws, dev)
+    del keep
+    return out
+
+
+def decompress_chunk_into(t: EndorTensor, idx: RankIndex, k: int, dst: torch.Tensor) -> None:
+    """codec.hpp:191-201 on the device: dst is the full dense buffer (uint8)."""
+    dev = t.device
+    ws = workspace(t.element_count(), dev)
+    pp, keep = _prefix_ptr(idx, dev)
+    v = t.view()
+    dst = dst.view(torch.uint8)
+    check(_lib.lib().endor_cuda_decompress_chunk_into(C.byref(v), idx.chunk_size, pp,
+                                                      idx.chunk_count(), k, _ptr(dst), dst.numel(),
+                                                      ws.data_ptr(), ws.numel(), _stream_ptr(dev)))
+    sync_status(ws, dev)
+    del keep
+
+
+# ---- synthetic inputs (weight_gen.hpp) ----------------------------------------------
+
+def synth_weight(rows: int, cols: int, seed: int, dtype: Dtype = Dtype.F16, device=None,
+                 row0: int = 0, nrows: Optional[int] = None) -> DenseMatrix:
+    """weight_gen.hpp:40-55, bit-exact, for rows [row0, row0+nrows)."""
+    dev = _dev(device)
+    nrows = rows - row0 if nrows is None else nrows
+    out = DenseMatrix.empty(nrows, cols, dtype, dev)
+    check(_lib.lib().endor_cuda_synth_weight(rows, cols, int(dtype), seed, row0, nrows,
+                                             _ptr(out.data), _stream_ptr(dev)))
+    return out
+
+
+def magnitude_prune(w: DenseMatrix, sparsity: float, inplace: bool = False) -> DenseMatrix:
+    """weight_gen.hpp:96-113, bit-exact."""
+    out = w if inplace else DenseMatrix(w.rows, w.cols, w.dtype, w.data.clone())
+    dev = out.data.device
+    n = out.element_count
+    ws = workspace(n, dev)
+    check(_lib.lib().endor_cuda_magnitude_prune(n, int(out.dtype), float(sparsity), _ptr(out.data),
+                                                ws.data_ptr(), ws.numel(), _stream_ptr(dev)))
+    return out
+
+
+def gemv(w: DenseMatrix, x: torch.Tensor, out_f32: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """y = W x (f16 in, fp32 accumulate/out) through the hand-written kernel."""
+    dev = w.data.device
+    if w.dtype != Dtype.F16 or x.dtype != torch.float16 or x.numel() != w.cols:
+        raise InvalidArgument("gemv needs f16 W [rows, cols] and f16 x [cols]")
+    y = out_f32 if out_f32 is not None else torch.empty(w.rows, dtype=torch.float32, device=dev)
+    check(_lib.lib().endor_cuda_gemv(w.rows, w.cols, _ptr(w.data), _ptr(x.contiguous()), _ptr(y), None,
+                                     _stream_ptr(dev)))
+    return y

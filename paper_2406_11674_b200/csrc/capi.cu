@@ -1,0 +1,559 @@
+// capi.cu -- the extern "C" boundary (include/endor_cuda.h): argument
+// validation with the reference's error semantics, workspace layout, and
+// launch sequencing.  Host code only; the kernels live in decompress.cu,
+// fixtures.cu and gemv.cu.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <cstdio>
+#include <string>
+
+#include "common.cuh"
+#include "endor_cuda.h"
+#include "kernels.h"
+
+using namespace endor_b200;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* what) {
+    g_last_error = what;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+    return ENDOR_ERR_CUDA;
+}
+
+#define CK(expr)                                              \
+    do {                                                      \
+        cudaError_t e_ = (expr);                              \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #expr);   \
+    } while (0)
+
+inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+// checked_element_count (dense_matrix.hpp:28-33)
+inline bool checked_n(uint64_t rows, uint64_t cols, uint64_t* n) {
+    if (rows != 0 && cols > UINT64_MAX / rows) return false;
+    *n = rows * cols;
+    return true;
+}
+
+inline int eb_of(int32_t dtype) { return dtype == ENDOR_DTYPE_F16 ? 2 : (dtype == ENDOR_DTYPE_I8 ? 1 : 0); }
+inline bool is_pow2_ge64(uint64_t cs) { return cs >= 64 && (cs & (cs - 1)) == 0; }
+inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
+
+// Common validation of a tensor view; fills n / eb.
+int check_view(const endor_tensor_view* t, uint64_t* n, int* eb) {
+    if (!t) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null tensor view");
+    *eb = eb_of(t->dtype);
+    if (!*eb) return fail(ENDOR_ERR_INVALID_ARGUMENT, "unknown dtype code");
+    if (!checked_n(t->rows, t->cols, n))
+        return fail(ENDOR_ERR_SIZE, "matrix dimensions overflow the addressable element count");
+    if (t->nnz > *n) return fail(ENDOR_ERR_CORRUPTION, "values length does not match bitmap popcount");
+    if (*n > 0 && !t->bitmap) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null bitmap");
+    if (t->nnz > 0 && !t->values) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null values");
+    if (!aligned(t->bitmap, 4)) return fail(ENDOR_ERR_INVALID_ARGUMENT, "bitmap must be 4-byte aligned");
+    return ENDOR_OK;
+}
+
+int check_ws(void* ws, size_t ws_bytes, uint64_t n, WsLayout* L) {
+    if (!ws) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null workspace");
+    if (!aligned(ws, 256)) return fail(ENDOR_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+    *L = ws_layout(ws, n);
+    if (ws_bytes < L->bytes) return fail(ENDOR_ERR_INVALID_ARGUMENT, "workspace too small");
+    return ENDOR_OK;
+}
+
+ScanArgs scan_args(const void* bitmap, uint64_t n, uint64_t e0, uint64_t e1, const WsLayout& L) {
+    ScanArgs a{};
+    a.bitmap = static_cast<const uint8_t*>(bitmap);
+    a.nbytes = (n + 7) / 8;
+    a.n = n;
+    a.e0 = e0;
+    a.e1 = e1;
+    a.lookback = L.lookback;
+    a.hdr = L.hdr;
+    return a;
+}
+
+ExpandArgs expand_args(const endor_tensor_view* t, uint64_t n, uint64_t e0, uint64_t e1,
+                       void* dst, const WsLayout& L) {
+    ExpandArgs x{};
+    x.bitmap = static_cast<const uint8_t*>(t->bitmap);
+    x.nbytes = (n + 7) / 8;
+    x.values = static_cast<const uint8_t*>(t->values);
+    x.nnz = t->nnz;
+    x.e0 = e0;
+    x.e1 = e1;
+    x.tprefix = L.tprefix;
+    x.dst = static_cast<uint8_t*>(dst);
+    x.hdr = L.hdr;
+    return x;
+}
+
+}  // namespace
+
+extern "C" {
+
+int endor_cuda_abi_version(void) { return ENDOR_CUDA_ABI_VERSION; }
+
+const char* endor_cuda_last_error_string(void) { return g_last_error.c_str(); }
+
+const char* endor_cuda_status_name(int s) {
+    switch (s) {
+        case ENDOR_OK: return "OK";
+        case ENDOR_ERR_SIZE: return "SizeError";
+        case ENDOR_ERR_CORRUPTION: return "CorruptionError";
+        case ENDOR_ERR_BOUNDS: return "BoundsError";
+        case ENDOR_ERR_INVALID_ARGUMENT: return "InvalidArgument";
+        case ENDOR_ERR_CUDA: return "CudaError";
+        case ENDOR_ERR_CONFIG: return "ConfigError";
+        default: return "Unknown";
+    }
+}
+
+uint64_t endor_cuda_tile_elems(void) { return kTileElems; }
+
+size_t endor_cuda_workspace_bytes(uint64_t rows, uint64_t cols) {
+    uint64_t n;
+    if (!checked_n(rows, cols, &n)) return 0;
+    return ws_layout(nullptr, n).bytes;
+}
+
+int endor_cuda_workspace_init(void* ws, size_t ws_bytes, void* stream) {
+    if (!ws) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null workspace");
+    CK(cudaMemsetAsync(ws, 0, ws_bytes, S(stream)));
+    return ENDOR_OK;
+}
+
+int endor_cuda_sync_status(void* ws, void* stream) {
+    if (!ws) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null workspace");
+    CK(cudaStreamSynchronize(S(stream)));
+    WsHeader* hdr = static_cast<WsHeader*>(ws);
+    uint32_t st = 0;
+    CK(cudaMemcpy(&st, &hdr->status, sizeof(st), cudaMemcpyDeviceToHost));
+    if (st) {
+        CK(cudaMemset(&hdr->status, 0, sizeof(uint32_t)));
+        return fail(int(st), st == ENDOR_ERR_CORRUPTION
+                                 ? "device check failed: bitmap popcount / rank index / padding bits "
+                                   "disagree with the tensor (codec.hpp:158-160,170-184, bitmap.hpp:78-84)"
+                                 : "device-latched error");
+    }
+    return ENDOR_OK;
+}
+
+int endor_cuda_decompress(const endor_tensor_view* t, void* dense_out, void* ws, size_t ws_bytes,
+                          void* stream) {
+    uint64_t n;
+    int eb, st;
+    if ((st = check_view(t, &n, &eb))) return st;
+    if (n == 0) return ENDOR_OK;  // nnz == 0 already implied by nnz <= n
+    if (!dense_out || !aligned(dense_out, 16))
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "dense output must be non-null and 16-byte aligned");
+    WsLayout L;
+    if ((st = check_ws(ws, ws_bytes, n, &L))) return st;
+    ScanArgs a = scan_args(t->bitmap, n, 0, n, L);
+    a.tprefix = L.tprefix;
+    a.check_total = 1;
+    a.expect_total = t->nnz;
+    CK(launch_scan(a, S(stream)));
+    CK(launch_expand(expand_args(t, n, 0, n, dense_out, L), eb, S(stream)));
+    return ENDOR_OK;
+}
+
+int endor_cuda_rank_index(const void* bitmap, uint64_t n, uint64_t chunk_size, uint64_t* prefix_out,
+                          uint64_t* total_out, void* ws, size_t ws_bytes, void* stream) {
+    if (!is_pow2_ge64(chunk_size))  // bitmap.hpp:118-120
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "chunk_size must be a power of two >= 64");
+    if (n == 0) {
+        if (total_out) CK(cudaMemsetAsync(total_out, 0, 8, S(stream)));
+        return ENDOR_OK;
+    }
+    if (!bitmap || !aligned(bitmap, 4)) return fail(ENDOR_ERR_INVALID_ARGUMENT, "bitmap must be non-null and 4-byte aligned");
+    if (!prefix_out) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null prefix output");
+    WsLayout L;
+    int st;
+    if ((st = check_ws(ws, ws_bytes, n, &L))) return st;
+    ScanArgs a = scan_args(bitmap, n, 0, n, L);
+    a.cs = chunk_size;
+    a.idx_out = reinterpret_cast<unsigned long long*>(prefix_out);
+    a.total_out = reinterpret_cast<unsigned long long*>(total_out);
+    CK(launch_scan(a, S(stream)));
+    return ENDOR_OK;
+}
+
+int endor_cuda_popcount(const void* bitmap, uint64_t n, uint64_t* total_out, void* ws,
+                        size_t ws_bytes, void* stream) {
+    if (!total_out) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null total output");
+    if (n == 0) {
+        CK(cudaMemsetAsync(total_out, 0, 8, S(stream)));
+        return ENDOR_OK;
+    }
+    if (!bitmap || !aligned(bitmap, 4)) return fail(ENDOR_ERR_INVALID_ARGUMENT, "bitmap must be non-null and 4-byte aligned");
+    WsLayout L;
+    int st;
+    if ((st = check_ws(ws, ws_bytes, n, &L))) return st;
+    ScanArgs a = scan_args(bitmap, n, 0, n, L);
+    a.total_out = reinterpret_cast<unsigned long long*>(total_out);
+    CK(launch_scan(a, S(stream)));
+    return ENDOR_OK;
+}
+
+int endor_cuda_decompress_chunked(const endor_tensor_view* t, uint64_t cs, const uint64_t* prefix,
+                                  uint64_t chunk_count, void* dense_out, void* ws, size_t ws_bytes,
+                                  void* stream) {
+    uint64_t n;
+    int eb, st;
+    if ((st = check_view(t, &n, &eb))) return st;
+    // check_index (codec.hpp:170-176): the index must cover the bitmap
+    const uint64_t chunks = (n == 0 || cs == 0) ? 0 : ceil_div(n, cs);
+    if (cs == 0 || chunk_count != chunks) return fail(ENDOR_ERR_CORRUPTION, "rank index does not cover the bitmap");
+    if (!is_pow2_ge64(cs))
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "device RankIndex chunk sizes must be powers of two >= 64");
+    if (n == 0) return ENDOR_OK;
+    if (!prefix) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null prefix");
+    if (!dense_out || !aligned(dense_out, 16))
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "dense output must be non-null and 16-byte aligned");
+    WsLayout L;
+    if ((st = check_ws(ws, ws_bytes, n, &L))) return st;
+    ScanArgs a = scan_args(t->bitmap, n, 0, n, L);
+    a.tprefix = L.tprefix;
+    a.check_total = 1;
+    a.expect_total = t->nnz;
+    a.cs = cs;
+    a.idx_in = reinterpret_cast<const unsigned long long*>(prefix);
+    CK(launch_scan(a, S(stream)));
+    CK(launch_expand(expand_args(t, n, 0, n, dense_out, L), eb, S(stream)));
+    return ENDOR_OK;
+}
+
+int endor_cuda_decompress_chunk_into(const endor_tensor_view* t, uint64_t cs, const uint64_t* prefix,
+                                     uint64_t chunk_count, uint64_t k, void* dense_out,
+                                     uint64_t dense_out_bytes, void* ws, size_t ws_bytes,
+                                     void* stream) {
+    uint64_t n;
+    int eb, st;
+    if ((st = check_view(t, &n, &eb))) return st;
+    const uint64_t chunks = (n == 0 || cs == 0) ? 0 : ceil_div(n, cs);
+    if (cs == 0 || chunk_count != chunks) return fail(ENDOR_ERR_CORRUPTION, "rank index does not cover the bitmap");
+    if (k >= chunk_count) return fail(ENDOR_ERR_BOUNDS, "chunk index out of range");  // codec.hpp:194
+    if (dense_out_bytes != n * uint64_t(eb))  // codec.hpp:195-197
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "destination buffer must hold the full dense matrix");
+    if (!is_pow2_ge64(cs))
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "device RankIndex chunk sizes must be powers of two >= 64");
+    if (!prefix) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null prefix");
+    if (!dense_out || !aligned(dense_out, 16))
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "dense output must be non-null and 16-byte aligned");
+    WsLayout L;
+    if ((st = check_ws(ws, ws_bytes, n, &L))) return st;
+    const auto* pre = reinterpret_cast<const unsigned long long*>(prefix);
+    const uint64_t last = chunk_count - 1;
+    // check_index tail (codec.hpp:177-183): prefix[last] + popcount(last chunk) == nnz
+    if (k != last) {
+        ScanArgs c = scan_args(t->bitmap, n, last * cs, n, L);
+        c.p0_ptr = pre + last;
+        c.check_total = 1;
+        c.expect_total = t->nnz;
+        CK(launch_scan(c, S(stream)));
+    }
+    const uint64_t b = k * cs, e = (b + cs < n) ? b + cs : n;
+    ScanArgs a = scan_args(t->bitmap, n, b, e, L);
+    a.p0_ptr = pre + k;
+    a.tprefix = L.tprefix;
+    if (k == last) {
+        a.check_total = 1;
+        a.expect_total = t->nnz;
+    }
+    CK(launch_scan(a, S(stream)));
+    CK(launch_expand(expand_args(t, n, b, e, dense_out, L), eb, S(stream)));
+    return ENDOR_OK;
+}
+
+int endor_cuda_compress(uint64_t rows, uint64_t cols, int32_t dtype, const void* dense,
+                        void* bitmap_out, void* values_out, uint64_t* nnz_out_host,
+                        int32_t* negzero_out_host, void* ws, size_t ws_bytes, void* stream) {
+    uint64_t n;
+    const int eb = eb_of(dtype);
+    if (!eb) return fail(ENDOR_ERR_INVALID_ARGUMENT, "unknown dtype code");
+    if (!checked_n(rows, cols, &n)) return fail(ENDOR_ERR_SIZE, "matrix dimensions overflow the addressable element count");
+    if (!nnz_out_host) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null nnz output");
+    if (n == 0) {
+        *nnz_out_host = 0;
+        if (negzero_out_host) *negzero_out_host = 0;
+        return ENDOR_OK;
+    }
+    if (!dense || !bitmap_out || !values_out) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null buffer");
+    if (!aligned(bitmap_out, 4) || !aligned(dense, eb)) return fail(ENDOR_ERR_INVALID_ARGUMENT, "misaligned buffer");
+    WsLayout L;
+    int st;
+    if ((st = check_ws(ws, ws_bytes, n, &L))) return st;
+    CK(cudaMemsetAsync(&L.hdr->aux[2], 0, 8, S(stream)));
+    CK(launch_bitmap(dense, n, eb, bitmap_out, L, S(stream)));
+    ScanArgs a = scan_args(bitmap_out, n, 0, n, L);
+    a.tprefix = L.tprefix;
+    CK(launch_scan(a, S(stream)));
+    CK(launch_compact(dense, n, eb, bitmap_out, L, values_out, S(stream)));
+    unsigned long long hv[2];
+    CK(cudaMemcpyAsync(&hv[0], &L.hdr->total, 8, cudaMemcpyDeviceToHost, S(stream)));
+    CK(cudaMemcpyAsync(&hv[1], &L.hdr->aux[2], 8, cudaMemcpyDeviceToHost, S(stream)));
+    CK(cudaStreamSynchronize(S(stream)));
+    *nnz_out_host = hv[0];
+    if (negzero_out_host) *negzero_out_host = hv[1] ? 1 : 0;
+    return endor_cuda_sync_status(ws, stream);
+}
+
+int endor_cuda_synth_weight(uint64_t rows, uint64_t cols, int32_t dtype, uint64_t seed,
+                            uint64_t row0, uint64_t nrows, void* out, void* stream) {
+    uint64_t n;
+    const int eb = eb_of(dtype);
+    if (!eb) return fail(ENDOR_ERR_INVALID_ARGUMENT, "unknown dtype code");
+    if (!checked_n(rows, cols, &n)) return fail(ENDOR_ERR_SIZE, "matrix dimensions overflow the addressable element count");
+    if (row0 > rows || nrows > rows - row0) return fail(ENDOR_ERR_BOUNDS, "row range outside the matrix");
+    if (nrows == 0 || cols == 0) return ENDOR_OK;
+    if (!out || !aligned(out, eb)) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null or misaligned output");
+    CK(launch_synth(row0 * cols, nrows * cols, eb, seed, out, S(stream)));
+    return ENDOR_OK;
+}
+
+int endor_cuda_magnitude_prune(uint64_t n, int32_t dtype, double sparsity, void* w, void* ws,
+                               size_t ws_bytes, void* stream) {
+    const int eb = eb_of(dtype);
+    if (!eb) return fail(ENDOR_ERR_INVALID_ARGUMENT, "unknown dtype code");
+    if (!(sparsity >= 0.0 && sparsity < 1.0))  // weight_gen.hpp:97-99
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "sparsity must be in [0, 1)");
+    const uint64_t target = uint64_t(sparsity * double(n));  // weight_gen.hpp:102
+    if (target == 0) return ENDOR_OK;
+    if (!w || !aligned(w, eb)) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null or misaligned weights");
+    WsLayout L;
+    int st;
+    if ((st = check_ws(ws, ws_bytes, n, &L))) return st;
+    CK(launch_prune(static_cast<uint8_t*>(w), n, eb, target, L, S(stream)));
+    return ENDOR_OK;
+}
+
+int endor_cuda_gemv(uint64_t rows, uint64_t cols, const void* w_f16, const void* x_f16, float* y_f32,
+                    void* y_f16, void* stream) {
+    uint64_t n;
+    if (!checked_n(rows, cols, &n)) return fail(ENDOR_ERR_SIZE, "matrix dimensions overflow the addressable element count");
+    if (rows == 0) return ENDOR_OK;
+    if ((cols > 0 && (!w_f16 || !x_f16)) || (!y_f32 && !y_f16))
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "null buffer");
+    if (!aligned(w_f16, 2) || !aligned(x_f16, 2)) return fail(ENDOR_ERR_INVALID_ARGUMENT, "misaligned f16 buffer");
+    CK(launch_gemv(rows, cols, w_f16, x_f16, y_f32, y_f16, S(stream)));
+    return ENDOR_OK;
+}
+
+// ---- host-buffer convenience (sync) --------------------------------------------
+namespace {
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t need(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaSuccess) cap = bytes;
+        return e;
+    }
+    ~DevBuf() { cudaFree(p); }
+};
+
+// Grow-only device buffers reused by the synchronous host-buffer entry points
+// (one set per host thread and device).
+struct HostSession {
+    int device = -1;
+    DevBuf bm, vals, dense, ws, prefix;
+};
+thread_local HostSession* g_sess = nullptr;
+
+int session(HostSession** out, uint64_t n) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (!g_sess || g_sess->device != dev) {
+        delete g_sess;
+        g_sess = new HostSession();
+        g_sess->device = dev;
+    }
+    const size_t wsb = ws_layout(nullptr, n).bytes;
+    if (wsb > g_sess->ws.cap) {
+        CK(g_sess->ws.need(wsb));
+        CK(cudaMemset(g_sess->ws.p, 0, g_sess->ws.cap));
+    }
+    *out = g_sess;
+    return ENDOR_OK;
+}
+
+// Validate + upload a host tensor; fills the device view.
+int upload(HostSession* s, uint64_t rows, uint64_t cols, int32_t dtype, const void* bitmap_host,
+           const void* values_host, uint64_t nnz, endor_tensor_view* v, uint64_t* n_out) {
+    uint64_t n;
+    const int eb = eb_of(dtype);
+    if (!eb) return fail(ENDOR_ERR_INVALID_ARGUMENT, "unknown dtype code");
+    if (!checked_n(rows, cols, &n)) return fail(ENDOR_ERR_SIZE, "matrix dimensions overflow the addressable element count");
+    if (nnz > n) return fail(ENDOR_ERR_CORRUPTION, "values length does not match bitmap popcount");
+    const size_t bmb = (n + 7) / 8, vb = nnz * eb;
+    CK(s->bm.need(bmb + 16));
+    CK(s->vals.need(vb + 16));
+    if (bmb) CK(cudaMemcpy(s->bm.p, bitmap_host, bmb, cudaMemcpyHostToDevice));
+    if (vb) CK(cudaMemcpy(s->vals.p, values_host, vb, cudaMemcpyHostToDevice));
+    *v = endor_tensor_view{rows, cols, dtype, 0, s->bm.p, s->vals.p, nnz};
+    *n_out = n;
+    return ENDOR_OK;
+}
+}  // namespace
+
+#define ST(expr)                   \
+    do {                           \
+        int st_ = (expr);          \
+        if (st_) return st_;       \
+    } while (0)
+
+int endor_cuda_decompress_host(uint64_t rows, uint64_t cols, int32_t dtype, const void* bitmap_host,
+                               const void* values_host, uint64_t nnz, void* dense_host_out) {
+    HostSession* s;
+    endor_tensor_view v;
+    uint64_t n;
+    ST(session(&s, 1));
+    ST(upload(s, rows, cols, dtype, bitmap_host, values_host, nnz, &v, &n));
+    if (n == 0) return ENDOR_OK;
+    ST(session(&s, n));
+    const size_t db = n * eb_of(dtype);
+    CK(s->dense.need(db + 16));
+    ST(endor_cuda_decompress(&v, s->dense.p, s->ws.p, s->ws.cap, nullptr));
+    ST(endor_cuda_sync_status(s->ws.p, nullptr));
+    CK(cudaMemcpy(dense_host_out, s->dense.p, db, cudaMemcpyDeviceToHost));
+    return ENDOR_OK;
+}
+
+int endor_cuda_rank_index_host(const void* bitmap_host, uint64_t n, uint64_t chunk_size,
+                               uint64_t* prefix_host_out) {
+    if (!is_pow2_ge64(chunk_size))
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "chunk_size must be a power of two >= 64");
+    if (n == 0) return ENDOR_OK;
+    HostSession* s;
+    ST(session(&s, n));
+    const size_t bmb = (n + 7) / 8, chunks = ceil_div(n, chunk_size);
+    CK(s->bm.need(bmb + 16));
+    CK(s->prefix.need(chunks * 8));
+    CK(cudaMemcpy(s->bm.p, bitmap_host, bmb, cudaMemcpyHostToDevice));
+    ST(endor_cuda_rank_index(s->bm.p, n, chunk_size, static_cast<uint64_t*>(s->prefix.p), nullptr,
+                             s->ws.p, s->ws.cap, nullptr));
+    ST(endor_cuda_sync_status(s->ws.p, nullptr));
+    CK(cudaMemcpy(prefix_host_out, s->prefix.p, chunks * 8, cudaMemcpyDeviceToHost));
+    return ENDOR_OK;
+}
+
+int endor_cuda_decompress_chunked_host(uint64_t rows, uint64_t cols, int32_t dtype,
+                                       const void* bitmap_host, const void* values_host,
+                                       uint64_t nnz, uint64_t chunk_size,
+                                       const uint64_t* prefix_host, uint64_t chunk_count,
+                                       void* dense_host_out) {
+    HostSession* s;
+    endor_tensor_view v;
+    uint64_t n;
+    ST(session(&s, 1));
+    ST(upload(s, rows, cols, dtype, bitmap_host, values_host, nnz, &v, &n));
+    ST(session(&s, n));
+    CK(s->prefix.need(chunk_count * 8 + 8));
+    if (chunk_count) CK(cudaMemcpy(s->prefix.p, prefix_host, chunk_count * 8, cudaMemcpyHostToDevice));
+    const size_t db = n * eb_of(dtype);
+    CK(s->dense.need(db + 16));
+    ST(endor_cuda_decompress_chunked(&v, chunk_size, static_cast<const uint64_t*>(s->prefix.p),
+                                     chunk_count, s->dense.p, s->ws.p, s->ws.cap, nullptr));
+    ST(endor_cuda_sync_status(s->ws.p, nullptr));
+    if (db) CK(cudaMemcpy(dense_host_out, s->dense.p, db, cudaMemcpyDeviceToHost));
+    return ENDOR_OK;
+}
+
+int endor_cuda_decompress_chunk_into_host(uint64_t rows, uint64_t cols, int32_t dtype,
+                                          const void* bitmap_host, const void* values_host,
+                                          uint64_t nnz, uint64_t cs, const uint64_t* prefix_host,
+                                          uint64_t chunk_count, uint64_t k, void* dense_host,
+                                          uint64_t dense_host_bytes) {
+    HostSession* s;
+    endor_tensor_view v;
+    uint64_t n;
+    ST(session(&s, 1));
+    ST(upload(s, rows, cols, dtype, bitmap_host, values_host, nnz, &v, &n));
+    ST(session(&s, n));
+    const int eb = eb_of(dtype);
+    // check_index first (codec.hpp:193), exactly as the reference orders it
+    const uint64_t chunks = (n == 0 || cs == 0) ? 0 : ceil_div(n, cs);
+    if (cs == 0 || chunk_count != chunks) return fail(ENDOR_ERR_CORRUPTION, "rank index does not cover the bitmap");
+    if (!is_pow2_ge64(cs))
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "device RankIndex chunk sizes must be powers of two >= 64");
+    CK(s->prefix.need(chunk_count * 8 + 8));
+    CK(cudaMemcpy(s->prefix.p, prefix_host, chunk_count * 8, cudaMemcpyHostToDevice));
+    const uint64_t last = chunk_count - 1;
+    {
+        WsLayout L = ws_layout(s->ws.p, n);
+        ScanArgs c = scan_args(v.bitmap, n, last * cs, n, L);
+        c.p0_ptr = static_cast<const unsigned long long*>(s->prefix.p) + last;
+        c.check_total = 1;
+        c.expect_total = nnz;
+        CK(launch_scan(c, nullptr));
+        ST(endor_cuda_sync_status(s->ws.p, nullptr));
+    }
+    if (k >= chunk_count) return fail(ENDOR_ERR_BOUNDS, "chunk index out of range");
+    if (dense_host_bytes != n * uint64_t(eb))
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "destination buffer must hold the full dense matrix");
+    // only chunk k's byte range moves in either direction
+    const uint64_t b = k * cs, e = (b + cs < n) ? b + cs : n;
+    CK(s->dense.need(n * eb + 16));
+    ST(endor_cuda_decompress_chunk_into(&v, cs, static_cast<const uint64_t*>(s->prefix.p), chunk_count,
+                                        k, s->dense.p, n * eb, s->ws.p, s->ws.cap, nullptr));
+    ST(endor_cuda_sync_status(s->ws.p, nullptr));
+    CK(cudaMemcpy(static_cast<uint8_t*>(dense_host) + b * eb, static_cast<uint8_t*>(s->dense.p) + b * eb,
+                  (e - b) * eb, cudaMemcpyDeviceToHost));
+    return ENDOR_OK;
+}
+
+int endor_cuda_compress_host(uint64_t rows, uint64_t cols, int32_t dtype, const void* dense_host,
+                             void* bitmap_host_out, void* values_host_out, uint64_t* nnz_out,
+                             int32_t* negzero_out) {
+    uint64_t n;
+    const int eb = eb_of(dtype);
+    if (!eb) return fail(ENDOR_ERR_INVALID_ARGUMENT, "unknown dtype code");
+    if (!checked_n(rows, cols, &n)) return fail(ENDOR_ERR_SIZE, "matrix dimensions overflow the addressable element count");
+    if (!nnz_out) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null nnz output");
+    if (n == 0) {
+        *nnz_out = 0;
+        if (negzero_out) *negzero_out = 0;
+        return ENDOR_OK;
+    }
+    HostSession* s;
+    ST(session(&s, n));
+    const size_t bmb = (n + 7) / 8, db = n * eb;
+    CK(s->dense.need(db + 16));
+    CK(s->bm.need(bmb + 16));
+    CK(s->vals.need(db + 16));
+    CK(cudaMemcpy(s->dense.p, dense_host, db, cudaMemcpyHostToDevice));
+    ST(endor_cuda_compress(rows, cols, dtype, s->dense.p, s->bm.p, s->vals.p, nnz_out, negzero_out,
+                           s->ws.p, s->ws.cap, nullptr));
+    CK(cudaMemcpy(bitmap_host_out, s->bm.p, bmb, cudaMemcpyDeviceToHost));
+    if (*nnz_out) CK(cudaMemcpy(values_host_out, s->vals.p, *nnz_out * eb, cudaMemcpyDeviceToHost));
+    return ENDOR_OK;
+}
+
+void* endor_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) {
+        g_last_error = "cudaHostAlloc failed";
+        return nullptr;
+    }
+    return p;
+}
+
+void endor_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"

@@ -1,0 +1,120 @@
+// common.cuh -- shared constants, workspace layout and device helpers for the
+// sm_100a Endor decompression path.  See DESIGN.md for the data layout.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "endor_cuda.h"
+
+namespace endor_b200 {
+
+// ---- geometry --------------------------------------------------------------
+// Expand tile: 8192 elements per CTA pass (= 256 u32 bitmap words, one per
+// thread).  A power of two, so every RankIndex chunk size <= it divides it.
+constexpr int kTileElems = 8192;
+constexpr int kTileWords = kTileElems / 32;  // 256
+constexpr int kExpandThreads = 256;
+
+// Scan (rank) kernel: 8 warps x 16 iterations x 32 lanes of u32 words.
+constexpr int kScanThreads = 256;
+constexpr int kScanWordsPerLane = 16;
+constexpr int kScanWarpWords = 32 * kScanWordsPerLane;                   // 512
+constexpr int kScanBlockWords = (kScanThreads / 32) * kScanWarpWords;    // 4096
+constexpr uint64_t kScanBlockBits = uint64_t(kScanBlockWords) * 32;     // 131072
+
+// ---- workspace ---------------------------------------------------------------
+// [0,256)                 WsHeader
+// [256, +8*(ntiles+1))    per-tile exclusive value offsets ("GPU RankIndex")
+// [.., +8*nscan)          decoupled look-back state of the scan kernel
+// [.., +8*32768)          magnitude_prune key histogram
+// [.., +8*(ntiles+1))     magnitude_prune per-tile tie counts / prefixes
+struct WsHeader {
+    uint32_t status;       // latched endor_status (0 = OK)
+    uint32_t pad0;
+    unsigned long long ticket;  // scan CTA ticket counter (self-resetting)
+    unsigned long long done;    // scan CTA completion counter (self-resetting)
+    unsigned long long total;   // last scan total (p0 + popcount of range)
+    unsigned long long aux[4];
+};
+
+struct WsLayout {
+    WsHeader* hdr;
+    unsigned long long* tprefix;
+    unsigned long long* lookback;
+    unsigned long long* hist;
+    unsigned long long* ties;
+    uint64_t ntiles, nscan;
+    size_t bytes;
+};
+
+__host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+inline WsLayout ws_layout(void* base, uint64_t n) {
+    WsLayout L{};
+    L.ntiles = ceil_div(n, kTileElems);
+    L.nscan = ceil_div(n, kScanBlockBits);
+    size_t off = 256;
+    char* b = static_cast<char*>(base);
+    L.hdr = reinterpret_cast<WsHeader*>(b);
+    L.tprefix = reinterpret_cast<unsigned long long*>(b + off);
+    off = align256(off + 8 * (L.ntiles + 1));
+    L.lookback = reinterpret_cast<unsigned long long*>(b + off);
+    off = align256(off + 8 * (L.nscan + 1));
+    L.hist = reinterpret_cast<unsigned long long*>(b + off);
+    off = align256(off + 8 * 32768);
+    L.ties = reinterpret_cast<unsigned long long*>(b + off);
+    off = align256(off + 8 * (L.ntiles + 1));
+    L.bytes = off;
+    return L;
+}
+
+// ---- device helpers ------------------------------------------------------------
+// Little-endian u32 bitmap word `w`; bytes at or past `nbytes` read as zero
+// (only the final word of a bitmap can be partial).
+__device__ __forceinline__ uint32_t load_word32(const uint8_t* __restrict__ bm, uint64_t w,
+                                                uint64_t nbytes) {
+    const uint64_t b0 = w * 4;
+    if (b0 + 4 <= nbytes) return __ldg(reinterpret_cast<const uint32_t*>(bm) + w);
+    uint32_t v = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (b0 + j < nbytes) v |= uint32_t(__ldg(bm + b0 + j)) << (8 * j);
+    return v;
+}
+
+__device__ __forceinline__ void latch_status(WsHeader* hdr, uint32_t code) {
+    atomicCAS(&hdr->status, 0u, code);
+}
+
+__device__ __forceinline__ uint32_t read_status(const WsHeader* hdr) {
+    return *reinterpret_cast<const volatile uint32_t*>(&hdr->status);
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v, int lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        T u = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= d) v += u;
+    }
+    return v;
+}
+
+// Look-back state word: [63:62] flag (1 = aggregate, 2 = inclusive prefix),
+// [61:0] value.
+constexpr unsigned long long kLbAgg = 1ull << 62;
+constexpr unsigned long long kLbPrefix = 2ull << 62;
+constexpr unsigned long long kLbValue = (1ull << 62) - 1;
+
+__device__ __forceinline__ void lb_store(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long lb_load(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+}  // namespace endor_b200

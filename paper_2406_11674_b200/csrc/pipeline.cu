@@ -1,0 +1,210 @@
+// pipeline.cu -- the Endor offload pipeline, executed for real.
+//
+// The reference only models these stages analytically, one after another
+// with no overlap (Endor mode: CpuToGpu c*B/bw -> Decompress -> Compute,
+// sim.hpp:200-204; overlap deliberately not modelled, sim.hpp:122-124).
+// Here each op's compressed bytes (bitmap + values, PCIe-side traffic =
+// compression_ratio x dense, codec.hpp:75-80) stream from pinned host memory
+// on a dedicated copy stream into a ring of device staging slots; the compute
+// stream waits on the slot's copy event, runs scan + expand + GEMV, and
+// releases the slot, so H2D of op i+1.. overlaps decompress+GEMV of op i.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <new>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "endor_cuda.h"
+#include "kernels.h"
+
+using namespace endor_b200;
+
+struct endor_pipeline {
+    int device = 0;
+    int depth = 2;
+    uint64_t max_elems = 0;
+    cudaStream_t copy = nullptr, compute = nullptr;
+    struct Slot {
+        uint8_t* bitmap = nullptr;  // ceil(max/8) rounded up
+        uint8_t* values = nullptr;  // max*2 bytes
+        cudaEvent_t free_ev = nullptr;
+    };
+    std::vector<Slot> slots;
+    uint8_t* dense[2] = {nullptr, nullptr};
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
+    // per-op timing events (grown on demand)
+    std::vector<cudaEvent_t> h2d_beg, h2d_end, dec_beg, dec_end, op_end;
+    int last_nops = 0;
+    uint64_t last_h2d_bytes = 0, last_dense_bytes = 0, last_launches = 0;
+};
+
+namespace {
+thread_local std::string p_err;
+
+int perr(cudaError_t e, const char* where) {
+    p_err = std::string(where) + ": " + cudaGetErrorString(e);
+    return ENDOR_ERR_CUDA;
+}
+#define PK(expr)                                             \
+    do {                                                     \
+        cudaError_t e_ = (expr);                             \
+        if (e_ != cudaSuccess) return perr(e_, #expr);       \
+    } while (0)
+
+int ensure_events(endor_pipeline* p, int nops) {
+    auto grow = [&](std::vector<cudaEvent_t>& v) -> cudaError_t {
+        while (int(v.size()) < nops) {
+            cudaEvent_t e;
+            cudaError_t r = cudaEventCreate(&e);
+            if (r != cudaSuccess) return r;
+            v.push_back(e);
+        }
+        return cudaSuccess;
+    };
+    PK(grow(p->h2d_beg));
+    PK(grow(p->h2d_end));
+    PK(grow(p->dec_beg));
+    PK(grow(p->dec_end));
+    PK(grow(p->op_end));
+    return ENDOR_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int endor_pipeline_create(int device_ordinal, uint64_t max_op_elems, int ring_depth,
+                          endor_pipeline** out) {
+    if (!out || max_op_elems == 0) return ENDOR_ERR_INVALID_ARGUMENT;
+    auto* p = new (std::nothrow) endor_pipeline();
+    if (!p) return ENDOR_ERR_CUDA;
+    p->device = device_ordinal;
+    p->depth = ring_depth < 2 ? 2 : ring_depth;
+    p->max_elems = max_op_elems;
+    PK(cudaSetDevice(device_ordinal));
+    PK(cudaStreamCreateWithFlags(&p->copy, cudaStreamNonBlocking));
+    PK(cudaStreamCreateWithFlags(&p->compute, cudaStreamNonBlocking));
+    const size_t bmb = align256((max_op_elems + 7) / 8 + 16);
+    const size_t vb = align256(max_op_elems * 2 + 16);
+    p->slots.resize(p->depth);
+    for (auto& s : p->slots) {
+        PK(cudaMalloc(&s.bitmap, bmb));
+        PK(cudaMalloc(&s.values, vb));
+        PK(cudaEventCreateWithFlags(&s.free_ev, cudaEventDisableTiming));
+        PK(cudaEventRecord(s.free_ev, p->compute));
+    }
+    for (auto& d : p->dense) PK(cudaMalloc(&d, align256(max_op_elems * 2)));
+    p->ws_bytes = endor_cuda_workspace_bytes(max_op_elems, 1);
+    PK(cudaMalloc(&p->ws, p->ws_bytes));
+    PK(cudaMemsetAsync(p->ws, 0, p->ws_bytes, p->compute));
+    PK(cudaStreamSynchronize(p->compute));
+    *out = p;
+    return ENDOR_OK;
+}
+
+int endor_pipeline_destroy(endor_pipeline* p) {
+    if (!p) return ENDOR_OK;
+    cudaSetDevice(p->device);
+    cudaStreamSynchronize(p->copy);
+    cudaStreamSynchronize(p->compute);
+    for (auto& s : p->slots) {
+        cudaFree(s.bitmap);
+        cudaFree(s.values);
+        cudaEventDestroy(s.free_ev);
+    }
+    for (auto& d : p->dense) cudaFree(d);
+    cudaFree(p->ws);
+    for (auto* v : {&p->h2d_beg, &p->h2d_end, &p->dec_beg, &p->dec_end, &p->op_end})
+        for (auto e : *v) cudaEventDestroy(e);
+    cudaStreamDestroy(p->copy);
+    cudaStreamDestroy(p->compute);
+    delete p;
+    return ENDOR_OK;
+}
+
+void* endor_pipeline_stream(endor_pipeline* p) { return p ? p->compute : nullptr; }
+
+int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops, int sync) {
+    if (!p || (nops > 0 && !ops)) return ENDOR_ERR_INVALID_ARGUMENT;
+    PK(cudaSetDevice(p->device));
+    int st = ensure_events(p, nops);
+    if (st) return st;
+    uint64_t h2d = 0, dense = 0, launches = 0;
+    for (int i = 0; i < nops; ++i) {
+        const endor_pipeline_op& op = ops[i];
+        const uint64_t n = op.rows * op.cols;
+        const int eb = op.dtype == ENDOR_DTYPE_F16 ? 2 : 1;
+        if (n > p->max_elems || (op.dtype != ENDOR_DTYPE_F16 && op.dtype != ENDOR_DTYPE_I8))
+            return ENDOR_ERR_INVALID_ARGUMENT;
+        if ((op.x_dev || op.y_dev) && op.dtype != ENDOR_DTYPE_F16) return ENDOR_ERR_INVALID_ARGUMENT;
+        auto& slot = p->slots[i % p->depth];
+        const size_t bmb = (n + 7) / 8, vb = op.nnz * eb;
+        // copy stream: wait until the slot's previous occupant was decompressed
+        PK(cudaStreamWaitEvent(p->copy, slot.free_ev, 0));
+        PK(cudaEventRecord(p->h2d_beg[i], p->copy));
+        PK(cudaMemcpyAsync(slot.bitmap, op.bitmap_host, bmb, cudaMemcpyHostToDevice, p->copy));
+        if (vb) PK(cudaMemcpyAsync(slot.values, op.values_host, vb, cudaMemcpyHostToDevice, p->copy));
+        PK(cudaEventRecord(p->h2d_end[i], p->copy));
+        // compute stream: decompress into the dense ring (or the caller's buffer), then GEMV
+        PK(cudaStreamWaitEvent(p->compute, p->h2d_end[i], 0));
+        PK(cudaEventRecord(p->dec_beg[i], p->compute));
+        void* dst = op.dense_dev ? op.dense_dev : p->dense[i & 1];
+        endor_tensor_view v{op.rows, op.cols, op.dtype, 0, slot.bitmap, slot.values, op.nnz};
+        st = endor_cuda_decompress(&v, dst, p->ws, p->ws_bytes, p->compute);
+        if (st) return st;
+        launches += 2;
+        PK(cudaEventRecord(p->dec_end[i], p->compute));
+        PK(cudaEventRecord(slot.free_ev, p->compute));
+        if (op.x_dev && op.y_dev) {
+            st = endor_cuda_gemv(op.rows, op.cols, dst, op.x_dev, op.y_dev, nullptr, p->compute);
+            if (st) return st;
+            launches += 1;
+        }
+        PK(cudaEventRecord(p->op_end[i], p->compute));
+        h2d += bmb + vb;
+        dense += n * eb;
+    }
+    p->last_nops = nops;
+    p->last_h2d_bytes = h2d;
+    p->last_dense_bytes = dense;
+    p->last_launches = launches;
+    if (sync) {
+        PK(cudaStreamSynchronize(p->compute));
+        return endor_cuda_sync_status(p->ws, p->compute);
+    }
+    return ENDOR_OK;
+}
+
+int endor_pipeline_stats_get(endor_pipeline* p, endor_pipeline_stats* out) {
+    if (!p || !out) return ENDOR_ERR_INVALID_ARGUMENT;
+    PK(cudaSetDevice(p->device));
+    PK(cudaStreamSynchronize(p->compute));
+    PK(cudaStreamSynchronize(p->copy));
+    endor_pipeline_stats s{};
+    const int n = p->last_nops;
+    if (n > 0) {
+        float ms = 0.f;
+        PK(cudaEventElapsedTime(&ms, p->h2d_beg[0], p->op_end[n - 1]));
+        s.total_ms = ms;
+        float copy_span = 0.f;
+        PK(cudaEventElapsedTime(&copy_span, p->h2d_beg[0], p->h2d_end[n - 1]));
+        s.exposed_compute_ms = ms - copy_span;
+        for (int i = 0; i < n; ++i) {
+            PK(cudaEventElapsedTime(&ms, p->h2d_beg[i], p->h2d_end[i]));
+            s.h2d_ms += ms;
+            PK(cudaEventElapsedTime(&ms, p->dec_beg[i], p->dec_end[i]));
+            s.decompress_ms += ms;
+            PK(cudaEventElapsedTime(&ms, p->dec_end[i], p->op_end[i]));
+            s.gemv_ms += ms;
+        }
+    }
+    s.h2d_bytes = p->last_h2d_bytes;
+    s.dense_bytes = p->last_dense_bytes;
+    s.kernel_launches = p->last_launches;
+    *out = s;
+    return ENDOR_OK;
+}
+
+}  // extern "C"
