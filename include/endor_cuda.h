@@ -106,6 +106,12 @@ int endor_cuda_sync_status(void* ws, void* stream);
 int endor_cuda_decompress(const endor_tensor_view* t, void* dense_out, void* ws, size_t ws_bytes,
                           void* stream);
 
+/* endor_cuda_decompress split into its two launches, for per-kernel timing:
+ * phase 1 = rank (count) kernel, phase 2 = expand kernel (needs phase 1 on
+ * the same workspace first).  phase 1 then 2 == endor_cuda_decompress. */
+int endor_cuda_decompress_phase(const endor_tensor_view* t, void* dense_out, int phase, void* ws,
+                                size_t ws_bytes, void* stream);
+
 /* build_rank_index (bitmap.hpp:117-132) on device: prefix_out[ceil(n/cs)]
  * u64 exclusive per-chunk popcounts.  cs must be a power of two >= 64, else
  * ENDOR_ERR_INVALID_ARGUMENT (bitmap.hpp:118-120).  total_out (device u64,
@@ -205,6 +211,7 @@ typedef struct endor_pipeline_op {
     const void* x_dev;       /* GEMV input, f16[cols]; NULL = decompress only */
     float* y_dev;            /* GEMV output, f32[rows]; NULL = decompress only */
     void* dense_dev;         /* optional: where the dense W lands (NULL = ring) */
+    float* y_host;           /* optional pinned f32[rows]: y is copied back (D2H) */
 } endor_pipeline_op;
 
 typedef struct endor_pipeline_stats {

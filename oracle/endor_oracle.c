@@ -440,3 +440,105 @@ void or_gemv_f16(uint64_t rows, uint64_t cols, const uint16_t* w, const uint16_t
     }
     free(xf);
 }
+
+/* ---- multi-threaded op generator (reference-arm inputs) ------------------ */
+
+typedef struct {
+    uint64_t i0, i1, seed, target_ties, K, tie_base, cnt;
+    int phase;
+    uint8_t* w;
+    uint64_t* hist;  /* 32768 per worker */
+    uint8_t *bitmap, *values;
+    uint64_t voff;
+} mk_job;
+
+static void* mk_worker(void* p) {
+    mk_job* j = (mk_job*)p;
+    if (j->phase == 0) {  /* synth + key histogram (weight_gen.hpp:40-55, 61-64) */
+        for (uint64_t i = j->i0; i < j->i1; ++i) {
+            double u = (double)(splitmix_at(j->seed, i + 1) >> 11) * 0x1.0p-53;
+            uint16_t h = or_f32_to_f16((float)(2.0 * u - 1.0));
+            j->w[2 * i] = (uint8_t)(h & 0xFF);
+            j->w[2 * i + 1] = (uint8_t)(h >> 8);
+            j->hist[h & 0x7FFFu]++;
+        }
+    } else if (j->phase == 1) {  /* count key == K in range */
+        uint64_t c = 0;
+        for (uint64_t i = j->i0; i < j->i1; ++i) c += ((j->w[2 * i] | (j->w[2 * i + 1] << 8)) & 0x7FFF) == j->K;
+        j->cnt = c;
+    } else if (j->phase == 2) {  /* prune (ties cut in index order) + count survivors */
+        uint64_t rank = j->tie_base, c = 0;
+        for (uint64_t i = j->i0; i < j->i1; ++i) {
+            uint32_t k = (uint32_t)(j->w[2 * i] | (j->w[2 * i + 1] << 8)) & 0x7FFFu;
+            int prune = k < j->K;
+            if (k == j->K) prune = rank++ < j->target_ties;
+            if (prune) { j->w[2 * i] = 0; j->w[2 * i + 1] = 0; }
+            else c += (k != 0);
+        }
+        j->cnt = c;
+    } else {  /* compress (codec.hpp:97-126); ranges are multiples of 8 elements */
+        uint64_t v = j->voff;
+        for (uint64_t i = j->i0; i < j->i1; ++i) {
+            uint16_t h = (uint16_t)(j->w[2 * i] | (j->w[2 * i + 1] << 8));
+            if (h & 0x7FFFu) {
+                j->bitmap[i >> 3] |= (uint8_t)(1u << (i & 7));
+                j->values[2 * v] = (uint8_t)(h & 0xFF);
+                j->values[2 * v + 1] = (uint8_t)(h >> 8);
+                ++v;
+            }
+        }
+    }
+    return NULL;
+}
+
+uint64_t or_make_op_mt(uint64_t rows, uint64_t cols, uint64_t seed, double sparsity, int threads,
+                       uint8_t* bitmap_out, uint8_t* values_out) {
+    uint64_t n = rows * cols;
+    if (threads < 1) threads = 1;
+    uint8_t* w = (uint8_t*)malloc((size_t)(n * 2 + 16));
+    mk_job* jobs = (mk_job*)calloc((size_t)threads, sizeof(mk_job));
+    pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)threads);
+    uint64_t* hist = (uint64_t*)calloc((size_t)threads * 32768, sizeof(uint64_t));
+    for (int t = 0; t < threads; ++t) {  /* ranges aligned to 8 elements for the bitmap */
+        jobs[t].i0 = (n * (uint64_t)t / (uint64_t)threads) & ~7ull;
+        jobs[t].i1 = t == threads - 1 ? n : ((n * (uint64_t)(t + 1) / (uint64_t)threads) & ~7ull);
+        jobs[t].seed = seed;
+        jobs[t].w = w;
+        jobs[t].hist = hist + (size_t)t * 32768;
+        jobs[t].bitmap = bitmap_out;
+        jobs[t].values = values_out;
+    }
+#define RUN_PHASE(ph)                                                            \
+    do {                                                                         \
+        for (int t = 0; t < threads; ++t) { jobs[t].phase = ph; pthread_create(&th[t], NULL, mk_worker, &jobs[t]); } \
+        for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);           \
+    } while (0)
+    RUN_PHASE(0);
+    uint64_t target = (uint64_t)(sparsity * (double)n), below = 0, K = 0;
+    if (target > 0) {
+        for (K = 0; K < 32768; ++K) {
+            uint64_t hk = 0;
+            for (int t = 0; t < threads; ++t) hk += hist[(size_t)t * 32768 + K];
+            if (below + hk >= target) break;
+            below += hk;
+        }
+    } else {
+        K = 0; /* prune nothing: no key < 0; ties = 0 */
+    }
+    for (int t = 0; t < threads; ++t) jobs[t].K = K;
+    RUN_PHASE(1);
+    uint64_t tb = 0;
+    for (int t = 0; t < threads; ++t) {
+        jobs[t].tie_base = tb;
+        tb += jobs[t].cnt;
+        jobs[t].target_ties = target > 0 ? target - below : 0;
+    }
+    RUN_PHASE(2);
+    uint64_t vo = 0;
+    for (int t = 0; t < threads; ++t) { jobs[t].voff = vo; vo += jobs[t].cnt; }
+    memset(bitmap_out, 0, (size_t)((n + 7) / 8));
+    RUN_PHASE(3);
+#undef RUN_PHASE
+    free(hist); free(th); free(jobs); free(w);
+    return vo;
+}

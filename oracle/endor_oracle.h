@@ -116,6 +116,13 @@ double or_decompress_parallel(uint64_t n, int eb, const uint8_t* bitmap, const u
                               uint64_t chunk_size, const uint64_t* prefix, uint8_t* dst,
                               int threads);
 
+/* synth_weight -> magnitude_prune -> compress for one f16 op, multi-threaded
+ * (identical output to the single-threaded functions above; used to build
+ * the --impl reference arm's inputs on the CPU).  bitmap_out: ceil(n/8)
+ * bytes; values_out: capacity n*2.  Returns nnz. */
+uint64_t or_make_op_mt(uint64_t rows, uint64_t cols, uint64_t seed, double sparsity, int threads,
+                       uint8_t* bitmap_out, uint8_t* values_out);
+
 /* fp32 GEMV reference y = W x over f16 W [rows, cols] row-major (the
  * consumer the reference only models as a constant, sim.hpp:227). */
 void or_gemv_f16(uint64_t rows, uint64_t cols, const uint16_t* w, const uint16_t* x, float* y);

@@ -26,7 +26,7 @@ class PipelineOp(C.Structure):
     """endor_pipeline_op."""
     _fields_ = [("rows", _u64), ("cols", _u64), ("dtype", _i32), ("reserved", _i32),
                 ("bitmap_host", _vp), ("values_host", _vp), ("nnz", _u64),
-                ("x_dev", _vp), ("y_dev", _vp), ("dense_dev", _vp)]
+                ("x_dev", _vp), ("y_dev", _vp), ("dense_dev", _vp), ("y_host", _vp)]
 
 
 class PipelineStats(C.Structure):
@@ -46,6 +46,7 @@ SIGNATURES = {
     "endor_cuda_workspace_init": (C.c_int, [_vp, _sz, _vp]),
     "endor_cuda_sync_status": (C.c_int, [_vp, _vp]),
     "endor_cuda_decompress": (C.c_int, [C.POINTER(TensorView), _vp, _vp, _sz, _vp]),
+    "endor_cuda_decompress_phase": (C.c_int, [C.POINTER(TensorView), _vp, C.c_int, _vp, _sz, _vp]),
     "endor_cuda_rank_index": (C.c_int, [_vp, _u64, _u64, _vp, _vp, _vp, _sz, _vp]),
     "endor_cuda_popcount": (C.c_int, [_vp, _u64, _vp, _vp, _sz, _vp]),
     "endor_cuda_decompress_chunked": (C.c_int, [C.POINTER(TensorView), _u64, _vp, _u64, _vp, _vp,

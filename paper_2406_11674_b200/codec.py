@@ -166,8 +166,11 @@ class DenseMatrix:
     @classmethod
     def from_host(cls, rows, cols, dtype, data, device=None) -> "DenseMatrix":
         n = checked_element_count(rows, cols)
-        buf = torch.as_tensor(bytearray(bytes(data))) if not isinstance(data, torch.Tensor) else data
-        buf = buf.reshape(-1).view(torch.uint8)
+        if isinstance(data, torch.Tensor):
+            buf = data.reshape(-1).view(torch.uint8)
+        else:
+            raw = bytearray(bytes(data))
+            buf = torch.frombuffer(raw, dtype=torch.uint8) if raw else torch.zeros(0, dtype=torch.uint8)
         if buf.numel() != n * elem_bytes(dtype):
             raise SizeError("dense data length does not match rows*cols*elem_bytes")
         out = cls.empty(rows, cols, dtype, device)

@@ -92,9 +92,40 @@ ExpandArgs expand_args(const endor_tensor_view* t, uint64_t n, uint64_t e0, uint
     x.e0 = e0;
     x.e1 = e1;
     x.tprefix = L.tprefix;
+    x.tsub = L.tsub;
+    x.blk = L.blk;
     x.dst = static_cast<uint8_t*>(dst);
     x.hdr = L.hdr;
     return x;
+}
+
+// scan + expand over the whole tensor.  A 16-byte aligned bitmap takes the
+// persistent TMA ring (sub-tile offsets); anything else the plain fallback.
+// phase: 0 = both launches, 1 = count only, 2 = expand only (TMA path).
+int full_expand(const endor_tensor_view* t, uint64_t n, int eb, void* dst, const WsLayout& L,
+                ScanArgs a, cudaStream_t s, int phase = 0) {
+    const ExpandArgs x = expand_args(t, n, 0, n, dst, L);
+    if (aligned(t->bitmap, 16) && !a.idx_in) {
+        // hot path: two-level count (no inter-CTA waits) + persistent TMA expand
+        CountArgs c{};
+        c.bitmap = a.bitmap;
+        c.nbytes = a.nbytes;
+        c.n = n;
+        c.tsub = L.tsub;
+        c.blk = L.blk;
+        c.check_total = a.check_total;
+        c.expect_total = a.expect_total;
+        c.hdr = L.hdr;
+        if (phase != 2) CK(launch_count(c, s));
+        if (phase != 1) CK(launch_expand_tma(x, eb, s));
+        return ENDOR_OK;
+    }
+    if (phase != 0) return fail(ENDOR_ERR_INVALID_ARGUMENT, "phase split needs a 16-byte aligned bitmap");
+    // general path (verifies a caller's RankIndex / unaligned bitmap)
+    a.tprefix = L.tprefix;
+    CK(launch_scan(a, s));
+    CK(launch_expand(x, eb, s));
+    return ENDOR_OK;
 }
 
 }  // namespace
@@ -159,12 +190,26 @@ int endor_cuda_decompress(const endor_tensor_view* t, void* dense_out, void* ws,
     WsLayout L;
     if ((st = check_ws(ws, ws_bytes, n, &L))) return st;
     ScanArgs a = scan_args(t->bitmap, n, 0, n, L);
-    a.tprefix = L.tprefix;
     a.check_total = 1;
     a.expect_total = t->nnz;
-    CK(launch_scan(a, S(stream)));
-    CK(launch_expand(expand_args(t, n, 0, n, dense_out, L), eb, S(stream)));
-    return ENDOR_OK;
+    return full_expand(t, n, eb, dense_out, L, a, S(stream));
+}
+
+int endor_cuda_decompress_phase(const endor_tensor_view* t, void* dense_out, int phase, void* ws,
+                                size_t ws_bytes, void* stream) {
+    uint64_t n;
+    int eb, st;
+    if (phase != 1 && phase != 2) return fail(ENDOR_ERR_INVALID_ARGUMENT, "phase must be 1 or 2");
+    if ((st = check_view(t, &n, &eb))) return st;
+    if (n == 0) return ENDOR_OK;
+    if (phase == 2 && (!dense_out || !aligned(dense_out, 16)))
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "dense output must be non-null and 16-byte aligned");
+    WsLayout L;
+    if ((st = check_ws(ws, ws_bytes, n, &L))) return st;
+    ScanArgs a = scan_args(t->bitmap, n, 0, n, L);
+    a.check_total = 1;
+    a.expect_total = t->nnz;
+    return full_expand(t, n, eb, dense_out, L, a, S(stream), phase);
 }
 
 int endor_cuda_rank_index(const void* bitmap, uint64_t n, uint64_t chunk_size, uint64_t* prefix_out,
@@ -223,14 +268,11 @@ int endor_cuda_decompress_chunked(const endor_tensor_view* t, uint64_t cs, const
     WsLayout L;
     if ((st = check_ws(ws, ws_bytes, n, &L))) return st;
     ScanArgs a = scan_args(t->bitmap, n, 0, n, L);
-    a.tprefix = L.tprefix;
     a.check_total = 1;
     a.expect_total = t->nnz;
     a.cs = cs;
     a.idx_in = reinterpret_cast<const unsigned long long*>(prefix);
-    CK(launch_scan(a, S(stream)));
-    CK(launch_expand(expand_args(t, n, 0, n, dense_out, L), eb, S(stream)));
-    return ENDOR_OK;
+    return full_expand(t, n, eb, dense_out, L, a, S(stream));
 }
 
 int endor_cuda_decompress_chunk_into(const endor_tensor_view* t, uint64_t cs, const uint64_t* prefix,

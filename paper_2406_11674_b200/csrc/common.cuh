@@ -44,12 +44,17 @@ struct WsLayout {
     unsigned long long* lookback;
     unsigned long long* hist;
     unsigned long long* ties;
-    uint64_t ntiles, nscan;
+    unsigned long long* tsub;  // per-1024-element sub-tile value offsets
+    unsigned long long* blk;   // count_kernel per-CTA bases (+ total)
+    uint64_t ntiles, nscan, nsub;
     size_t bytes;
 };
 
+constexpr int kSubElems = 1024;  // one warp's share of an expand tile
+
 __host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+__host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
 inline WsLayout ws_layout(void* base, uint64_t n) {
     WsLayout L{};
@@ -66,8 +71,54 @@ inline WsLayout ws_layout(void* base, uint64_t n) {
     off = align256(off + 8 * 32768);
     L.ties = reinterpret_cast<unsigned long long*>(b + off);
     off = align256(off + 8 * (L.ntiles + 1));
+    L.nsub = ceil_div(n, kSubElems);
+    L.tsub = reinterpret_cast<unsigned long long*>(b + off);
+    off = align256(off + 8 * (L.nsub + 16));
+    L.blk = reinterpret_cast<unsigned long long*>(b + off);
+    off = align256(off + 8 * (L.nscan + 2));
     L.bytes = off;
     return L;
+}
+
+// ---- PTX wrappers: shared memory, mbarrier, TMA bulk copies -------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ unsigned long long lds64(uint32_t addr) {
+    unsigned long long v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void sts8(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t tx) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n}" ::"r"(bar), "r"(parity) : "memory");
+}
+// 1-D TMA bulk copy global -> shared, completion counted on an mbarrier.
+// dst/src 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
 
 // ---- device helpers ------------------------------------------------------------

@@ -1,0 +1,380 @@
+// expand.cu -- the Endor decompress (expand) kernels for sm_100a.
+//
+// detail::scatter_range (codec.hpp:132-152) writes dense[i] = bit_i ?
+// values[rank(i)] : +0 one set bit at a time with a serial value cursor.  On
+// the GPU the cursor becomes prefix sums (scan.cu gives every 1024-element
+// sub-tile its value offset) and the per-element branch becomes a
+// table-driven byte permutation:
+//
+//   for each 4-element nibble q of the bitmap, the up-to-4 packed values it
+//   consumes are fetched as one unaligned 8-byte window (3 LDS.32 + 2 funnel
+//   shifts) and PRMT places them into their slots, zeros elsewhere, using a
+//   16-entry selector table (kLut) -- ~3 instructions per output element,
+//   branch-free, for any byte alignment of the values stream.
+//
+// expand_tma_kernel (the hot path): persistent, warp-specialised.  One
+// producer warp streams each 8192-element tile's bitmap (1 KiB), its eight
+// sub-tile offsets and its packed-values window into a 4-stage shared-memory
+// ring with 1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx); eight
+// consumer warps each expand one 1024-element sub-tile per tile, fully
+// independently, and write dense rows with coalesced 16-byte stores.  HBM
+// traffic per element: 1/8 (bitmap) + (1-s)*eb (values) read, eb written.
+//
+// expand_kernel (fallback): one CTA per tile, plain loads; used for
+// decompress_chunk_into's partial ranges and bitmaps that are not 16-byte
+// aligned.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace endor_b200 {
+
+// ---- selector tables ---------------------------------------------------------
+// A 4-element nibble q of the bitmap consumes popc(q) packed values.  The
+// next four packed values are fetched as an unaligned 8-byte window {x, y}
+// and PRMT drops each into its slot.  Zero bytes come from RZ (byte 4 of a
+// zero second operand), so no compare/select is needed:
+//   f16:  word0 (slots 0,1) = PRMT(x, 0, sel0)             -- needs v0..v1 at most
+//         ym               = PRMT(y, 0, selm)              -- y, or y with v3 zeroed
+//         word1 (slots 2,3) = PRMT(x, ym, sel1)            -- unset slots read ym bytes 6,7
+//   i8:   word  (slots 0-3) = PRMT(x, 0, sel)
+// selm keeps y whole only when q == 0xF (then no slot is unset).
+struct __align__(16) LutF16 {
+    uint32_t sel0, sel1, selm, pad;
+};
+__shared__ LutF16 g_lut16[16];
+__shared__ uint32_t g_lut8[16];
+
+__device__ __forceinline__ void init_luts(int tid) {
+    if (tid < 16) {
+        const uint32_t q = tid;
+        uint32_t s0 = 0, s1 = 0, j = 0, s8 = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const bool set = q & (1u << k);
+            const uint32_t b0 = set ? 2 * j : (k < 2 ? 4u : 6u);
+            const uint32_t b1 = set ? 2 * j + 1 : (k < 2 ? 4u : 7u);
+            const uint32_t pos = (k & 1) * 8;
+            if (k < 2) s0 |= (b0 << pos) | (b1 << (pos + 4));
+            else s1 |= (b0 << pos) | (b1 << (pos + 4));
+            s8 |= (set ? j : 4u) << (4 * k);
+            j += set;
+        }
+        g_lut16[q] = LutF16{s0, s1, q == 15 ? 0x3210u : 0x4410u, 0u};
+        g_lut8[q] = s8;
+    }
+}
+
+// Expand one 16-byte output chunk.  m: the chunk's bitmap bits; a: shared
+// address of its first packed value (any byte alignment).
+template <int EB>
+__device__ __forceinline__ uint4 gather_chunk(uint32_t m, uint32_t a) {
+    uint32_t o[4];
+    if constexpr (EB == 2) {
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+            const uint32_t qa = g == 0 ? ((m << 4) & 0xF0u) : (m & 0xF0u);  // 16 B per entry
+            const LutF16 L = *reinterpret_cast<const LutF16*>(reinterpret_cast<const char*>(g_lut16) + qa);
+            const uint32_t al = a & ~3u, sh = a << 3;  // funnel shifts wrap mod 32
+            const uint32_t w0 = lds32(al), w1 = lds32(al + 4), w2 = lds32(al + 8);
+            const uint32_t x = __funnelshift_r(w0, w1, sh);
+            const uint32_t y = __funnelshift_r(w1, w2, sh);
+            o[2 * g] = __byte_perm(x, 0u, L.sel0);
+            o[2 * g + 1] = __byte_perm(x, __byte_perm(y, 0u, L.selm), L.sel1);
+            a += 2 * __popc(qa);
+        }
+    } else {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            const uint32_t qa = (m >> (4 * g)) & 15u;
+            const uint32_t sel = g_lut8[qa];
+            const uint32_t al = a & ~3u, sh = a << 3;
+            const uint32_t x = __funnelshift_r(lds32(al), lds32(al + 4), sh);
+            o[g] = __byte_perm(x, 0u, sel);
+            a += __popc(qa);
+        }
+    }
+    return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
+__device__ __forceinline__ void store_partial(uint8_t* p, uint4 q, uint32_t valid_bytes) {
+    const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (uint32_t b = 0; b < 16; ++b)
+        if (b < valid_bytes) p[b] = uint8_t(qw[b >> 2] >> ((b & 3) * 8));
+}
+
+// Expand one warp's 1024-element sub-tile.  word/excl: this lane's bitmap word
+// (bits past the range already cleared) and its exclusive popcount within the
+// warp; vbase: shared address of the sub-tile's first packed value.  Lane l
+// writes chunks l, l+32, .. so every store instruction covers 512 contiguous
+// bytes.  FULL: all 1024 elements valid (no bounds checks).
+template <int EB, bool FULL>
+__device__ __forceinline__ void expand_subtile(uint32_t word, uint32_t excl, uint32_t vbase,
+                                               uint8_t* out, int32_t valid_elems, int lane) {
+    constexpr int EPC = 16 / EB;              // elements per 16-byte chunk
+    constexpr int CPW = 32 / EPC;             // chunks per bitmap word (4 or 2)
+    constexpr int ITERS = 32 * 32 / EPC / 32; // chunks per lane (4 or 2)
+    const uint32_t sh = (lane % CPW) * EPC;   // chunk position inside its word: lane-constant
+    const uint32_t low = (1u << sh) - 1u;
+    uint8_t* o = out + size_t(lane) * 16;
+#pragma unroll
+    for (int j = 0; j < ITERS; ++j) {
+        const int src = (32 * j + lane) / CPW;
+        const uint32_t wd = __shfl_sync(0xffffffffu, word, src);
+        const uint32_t pre = __shfl_sync(0xffffffffu, excl, src);
+        const uint32_t m = (wd >> sh) & ((1u << EPC) - 1u);
+        const uint32_t r = pre + __popc(wd & low);
+        const int e = (32 * j + lane) * EPC;
+        if (!FULL && e >= valid_elems) continue;
+        const uint4 q = gather_chunk<EB>(m, vbase + r * EB);
+        if (FULL || e + EPC <= valid_elems) *reinterpret_cast<uint4*>(o + j * 512) = q;
+        else store_partial(o + j * 512, q, uint32_t(valid_elems - e) * EB);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// persistent TMA kernel
+// ---------------------------------------------------------------------------
+constexpr int kStages = 4;
+constexpr int kConsumerWarps = kTileElems / kSubElems;  // 8
+constexpr int kTmaThreads = (kConsumerWarps + 1) * 32;  // + 1 producer warp
+
+template <int EB>
+struct Stage {
+    static constexpr uint32_t kBm = 0;                            // 1 KiB bitmap
+    static constexpr uint32_t kSub = kTileElems / 8;              // 8 x u64 sub-tile offsets
+    static constexpr uint32_t kVals = kSub + 128;                 // packed-values window
+    static constexpr uint32_t kBytes = kVals + kTileElems * EB + 64;
+};
+
+template <int EB>
+constexpr uint32_t tma_smem_bytes() {
+    return 256 /* 2*kStages mbarriers + lut */ + kStages * Stage<EB>::kBytes;
+}
+
+template <int EB>
+__global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(ExpandArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t full0 = sbase, empty0 = sbase + 8 * kStages;
+    const uint32_t st0 = sbase + 256;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t n = a.e1;  // the TMA kernel always covers [0, n)
+    const uint64_t ntiles = ceil_div(n, kTileElems);
+    const uint64_t nsub = ceil_div(n, kSubElems);
+
+    if (read_status(a.hdr)) return;  // a latched error: write nothing
+    init_luts(tid);
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(full0 + 8 * s, 2);                // producer: expect_tx arrive + fix-up arrive
+            mbar_init(empty0 + 8 * s, kConsumerWarps);  // one arrive per consumer warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == kConsumerWarps) {
+        // ================= producer warp =================
+        const uintptr_t vlo = reinterpret_cast<uintptr_t>(a.values);
+        const uintptr_t vhi = vlo + a.nnz * EB;
+        const uintptr_t vlo16 = (vlo + 15) & ~uintptr_t(15), vhi16 = vhi & ~uintptr_t(15);
+        const uint64_t nblk = ceil_div(ceil_div(n, 32), kScanBlockWords);
+        constexpr uint32_t kSubsPerBlk = kScanBlockWords / 32;  // 128
+        // absolute value offset of sub-tile `sub` (count_kernel's two levels)
+        auto prefix_at = [&](uint64_t sub) -> unsigned long long {
+            return sub >= nsub ? a.blk[nblk] : a.blk[sub / kSubsPerBlk] + a.tsub[sub];
+        };
+        unsigned long long tp_l = 0, te_l = 0;  // lane k: window of this CTA's tile i+k
+        int i = 0;
+        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+            const int s = i % kStages;
+            const uint32_t stg = st0 + s * Stage<EB>::kBytes;
+            const uint32_t full = full0 + 8 * s;
+            if ((i & 31) == 0) {  // one round trip fetches the next 32 tiles' windows
+                const uint64_t tl = t + uint64_t(lane) * gridDim.x;
+                if (tl < ntiles) {
+                    tp_l = prefix_at(tl * 8);
+                    te_l = prefix_at(tl * 8 + 8);
+                }
+            }
+            const unsigned long long tp = __shfl_sync(0xffffffffu, tp_l, i & 31);
+            const unsigned long long te = __shfl_sync(0xffffffffu, te_l, i & 31);
+            if (i >= kStages) mbar_wait(empty0 + 8 * s, ((i / kStages) - 1) & 1);
+            const uint64_t t0 = t * kTileElems;
+            const uint32_t count = uint32_t(umin64(kTileElems, n - t0));
+            const uint32_t bm_bytes = (count + 7) / 8;
+            const uint32_t bm_bulk = count == kTileElems ? 1024u : (bm_bytes & ~15u);
+            const uintptr_t ws = vlo + tp * EB, we = vlo + te * EB;
+            const uintptr_t as = ws & ~uintptr_t(15), ae = (we + 15) & ~uintptr_t(15);
+            const uintptr_t bs = as > vlo16 ? as : vlo16, be = ae < vhi16 ? ae : vhi16;
+            const uint32_t vbulk = be > bs ? uint32_t(be - bs) : 0u;
+            if (lane == 0) {
+                mbar_arrive_expect_tx(full, bm_bulk + 64 + vbulk);
+                if (bm_bulk) bulk_g2s(stg + Stage<EB>::kBm, a.bitmap + t0 / 8, bm_bulk, full);
+                bulk_g2s(stg + Stage<EB>::kSub, a.tsub + t * 8, 64, full);
+                if (vbulk) bulk_g2s(stg + Stage<EB>::kVals + uint32_t(bs - as), reinterpret_cast<const void*>(bs), vbulk, full);
+            }
+            // edge bytes the bulk copies cannot move (ends of the buffers)
+            for (uint32_t b = bm_bulk + lane; b < bm_bytes; b += 32)
+                sts8(stg + Stage<EB>::kBm + b, __ldg(a.bitmap + t0 / 8 + b));
+            const uint32_t win = uint32_t(ae - as);
+            if (vbulk != win) {
+                for (uint32_t b = lane; b < win; b += 32) {
+                    const uintptr_t x = as + b;
+                    if (x >= vlo && x < vhi && !(x >= bs && x < be))
+                        sts8(stg + Stage<EB>::kVals + b, *reinterpret_cast<const uint8_t*>(x));
+                }
+            }
+            if (lane == 0) {  // absolute offset of the window (the bulk-copied entries are CTA-local)
+                asm volatile("st.shared.u64 [%0], %1;" ::"r"(stg + Stage<EB>::kSub + 64), "l"(tp) : "memory");
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(full);
+        }
+    } else {
+        // ================= consumer warps =================
+        int i = 0;
+        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+            const int s = i % kStages;
+            const uint32_t stg = st0 + s * Stage<EB>::kBytes;
+            mbar_wait(full0 + 8 * s, (i / kStages) & 1);
+            const uint64_t t0 = t * kTileElems;
+            const int32_t count = int32_t(umin64(kTileElems, n - t0));
+            const int32_t wfirst = warp * kSubElems;
+            if (wfirst < count) {
+                const int32_t valid = min(count - wfirst, kSubElems);
+                const int32_t lbit = lane * 32;
+                uint32_t word = 0;
+                if (lbit < valid) {
+                    word = lds32(stg + Stage<EB>::kBm + (warp * 32 + lane) * 4);
+                    if (valid - lbit < 32) word &= (1u << (valid - lbit)) - 1u;
+                }
+                const uint32_t pc = __popc(word);
+                const uint32_t excl = warp_incl_scan(pc, lane) - pc;
+                const unsigned long long tp = lds64(stg + Stage<EB>::kSub);
+                const unsigned long long sw = lds64(stg + Stage<EB>::kSub + 8 * warp);
+                const unsigned long long tabs = lds64(stg + Stage<EB>::kSub + 64);
+                const uint32_t off = uint32_t((reinterpret_cast<uintptr_t>(a.values) + tabs * EB) & 15);
+                const uint32_t vbase = stg + Stage<EB>::kVals + off + uint32_t(sw - tp) * EB;
+                uint8_t* out = a.dst + (t0 + wfirst) * EB;
+                if (valid == kSubElems) expand_subtile<EB, true>(word, excl, vbase, out, valid, lane);
+                else expand_subtile<EB, false>(word, excl, vbase, out, valid, lane);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty0 + 8 * s);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// fallback: one CTA per tile, plain loads (partial ranges / unaligned bitmaps)
+// ---------------------------------------------------------------------------
+template <int EB>
+__global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandArgs a) {
+    __shared__ uint32_t s_warp[kExpandThreads / 32];
+    __shared__ __align__(16) uint8_t s_vals[kTileElems * EB + 64];
+
+    if (read_status(a.hdr)) return;  // a latched error: write nothing
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    init_luts(tid);
+    const uint64_t t0 = a.e0 + uint64_t(blockIdx.x) * kTileElems;
+    const uint64_t tend = min(a.e1, t0 + kTileElems);
+    const int32_t count = int32_t(tend - t0);
+
+    uint32_t wv = 0;
+    if (tid * 32 < count) {
+        wv = load_word32(a.bitmap, t0 / 32 + tid, a.nbytes);
+        const int32_t rem = count - tid * 32;
+        if (rem < 32) wv &= (1u << rem) - 1u;
+    }
+    const uint32_t pc = __popc(wv);
+    const uint32_t incl = warp_incl_scan(pc, lane);
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    uint32_t wexcl = 0, total = 0;
+#pragma unroll
+    for (int i = 0; i < kExpandThreads / 32; ++i) {
+        const uint32_t t = s_warp[i];
+        wexcl += (i < warp) ? t : 0u;
+        total += t;
+    }
+
+    const uint64_t vbase = a.tprefix[blockIdx.x];
+    if (vbase + total > a.nnz) {  // only reachable through an inconsistent RankIndex
+        if (tid == 0) latch_status(a.hdr, ENDOR_ERR_CORRUPTION);
+        return;
+    }
+    const uintptr_t vlo = reinterpret_cast<uintptr_t>(a.values);
+    const uintptr_t vhi = vlo + a.nnz * EB;
+    const uintptr_t wstart = vlo + vbase * EB;
+    const uintptr_t wend = wstart + uint64_t(total) * EB;
+    const uintptr_t astart = wstart & ~uintptr_t(15);
+    const uint32_t nvec = uint32_t((wend - astart + 15) >> 4);
+    for (uint32_t v = tid; v < nvec; v += kExpandThreads) {
+        const uintptr_t addr = astart + uintptr_t(v) * 16;
+        uint4 q;
+        if (addr >= vlo && addr + 16 <= vhi) {
+            q = __ldg(reinterpret_cast<const uint4*>(addr));
+        } else {  // first/last partial block of the whole values buffer
+            uint32_t r[4] = {0u, 0u, 0u, 0u};
+            for (int b = 0; b < 16; ++b) {
+                const uintptr_t x = addr + b;
+                if (x >= vlo && x < vhi) r[b >> 2] |= uint32_t(*reinterpret_cast<const uint8_t*>(x)) << ((b & 3) * 8);
+            }
+            q = make_uint4(r[0], r[1], r[2], r[3]);
+        }
+        *reinterpret_cast<uint4*>(s_vals + v * 16) = q;
+    }
+    __syncthreads();
+    // each warp expands its own 1024 elements from the staged window
+    const int32_t wfirst = warp * kSubElems;
+    if (wfirst < count) {
+        const uint32_t off = uint32_t(wstart - astart);
+        const uint32_t vb = smem_u32(s_vals) + off + (wexcl * EB);
+        expand_subtile<EB, false>(wv, incl - pc, vb, a.dst + (t0 + wfirst) * EB,
+                                  min(count - wfirst, kSubElems), lane);
+    }
+}
+
+// ---------------------------------------------------------------------------
+cudaError_t launch_expand(const ExpandArgs& a, int eb, cudaStream_t s) {
+    const uint64_t ntiles = ceil_div(a.e1 - a.e0, kTileElems);
+    if (ntiles == 0) return cudaSuccess;
+    if (eb == 2) expand_kernel<2><<<unsigned(ntiles), kExpandThreads, 0, s>>>(a);
+    else expand_kernel<1><<<unsigned(ntiles), kExpandThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int EB>
+static cudaError_t launch_tma_eb(const ExpandArgs& a, cudaStream_t s) {
+    static int blocks_per_sm = 0, sms = 0;
+    constexpr uint32_t smem = tma_smem_bytes<EB>();
+    if (!blocks_per_sm) {
+        cudaError_t e = cudaFuncSetAttribute(expand_tma_kernel<EB>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, expand_tma_kernel<EB>,
+                                                      kTmaThreads, smem);
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    const uint64_t ntiles = ceil_div(a.e1, kTileElems);
+    const uint64_t grid = umin64(ntiles, uint64_t(blocks_per_sm) * sms);
+    expand_tma_kernel<EB><<<unsigned(grid), kTmaThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+// Full-range expand [0, n) through the TMA ring (needs the sub-tile offsets
+// from scan_kernel and a 16-byte aligned bitmap).
+cudaError_t launch_expand_tma(const ExpandArgs& a, int eb, cudaStream_t s) {
+    if (a.e0 != 0 || a.e1 == 0) return cudaErrorInvalidValue;
+    return eb == 2 ? launch_tma_eb<2>(a, s) : launch_tma_eb<1>(a, s);
+}
+
+}  // namespace endor_b200

@@ -161,6 +161,9 @@ int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops
             st = endor_cuda_gemv(op.rows, op.cols, dst, op.x_dev, op.y_dev, nullptr, p->compute);
             if (st) return st;
             launches += 1;
+            if (op.y_host)
+                PK(cudaMemcpyAsync(op.y_host, op.y_dev, op.rows * sizeof(float), cudaMemcpyDeviceToHost,
+                                   p->compute));
         }
         PK(cudaEventRecord(p->op_end[i], p->compute));
         h2d += bmb + vb;

@@ -1,0 +1,307 @@
+// scan.cu -- rank (prefix-popcount) kernels: the GPU form of the reference's
+// serial value cursor and of build_rank_index (bitmap.hpp:117-132).
+//
+//   count_kernel   hot path.  Two-level, no inter-CTA waiting: every CTA
+//                  popcounts 131072 bits (16 expand tiles), writes the
+//                  CTA-local exclusive offset of each 1024-bit sub-tile and
+//                  its aggregate; the last CTA to finish scans the aggregates
+//                  into per-CTA bases and checks the total against nnz
+//                  (codec.hpp:158-160).  Reads the bitmap once (n/8 bytes).
+//   scan_kernel    general form: arbitrary [e0, e1) ranges with a base
+//                  offset, decoupled look-back across CTAs, writing or
+//                  verifying a caller's RankIndex at its chunk size
+//                  (check_index, codec.hpp:170-184) -- used by
+//                  build_rank_index, decompress_chunked and
+//                  decompress_chunk_into.
+//
+// HBM-bound integer kernels (no tensor cores: no GEMM-shaped work here).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace endor_b200 {
+
+// ---------------------------------------------------------------------------
+// count_kernel
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kScanThreads) count_kernel(CountArgs a) {
+    constexpr int kSubs = kScanBlockWords / 32;  // 128 sub-tiles of 1024 bits per CTA
+    __shared__ unsigned long long s_warp[kScanThreads / 32];
+    __shared__ uint32_t s_sub[kSubs];
+    __shared__ int s_last;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t nwords = (a.n + 31) / 32;
+    const uint64_t w0 = uint64_t(blockIdx.x) * kScanBlockWords;
+
+    if ((w0 + kScanBlockWords) * 32 <= a.n) {
+        // full CTA: 4 x 16-byte loads per thread; 8 consecutive lanes = 1 sub-tile
+        const uint4* src = reinterpret_cast<const uint4*>(a.bitmap) + w0 / 4;
+        uint4 v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = __ldcs(src + j * kScanThreads + tid);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint32_t c = __popc(v[j].x) + __popc(v[j].y) + __popc(v[j].z) + __popc(v[j].w);
+            c += __shfl_xor_sync(0xffffffffu, c, 1);
+            c += __shfl_xor_sync(0xffffffffu, c, 2);
+            c += __shfl_xor_sync(0xffffffffu, c, 4);
+            if ((lane & 7) == 0) s_sub[32 * j + tid / 8] = c;
+        }
+    } else {
+        // ragged last CTA: word loads with the tail masked and padding checked
+        for (int s = warp; s < kSubs; s += kScanThreads / 32) {
+            const uint64_t wi = w0 + uint64_t(s) * 32 + lane;
+            uint32_t v = 0;
+            if (wi < nwords) {
+                v = load_word32(a.bitmap, wi, a.nbytes);
+                const uint64_t bit0 = wi * 32;
+                if (bit0 + 32 > a.n) {
+                    const uint32_t keep = uint32_t(a.n - bit0);
+                    if (a.n & 7) {  // padding bits of the final byte must be zero (bitmap.hpp:78-84)
+                        const uint64_t pad_end = ((a.n + 7) & ~7ull) - bit0;
+                        const uint32_t padmask = (pad_end >= 32 ? 0xffffffffu : ((1u << pad_end) - 1u)) &
+                                                 ~((1u << keep) - 1u);
+                        if (v & padmask) latch_status(a.hdr, ENDOR_ERR_CORRUPTION);
+                    }
+                    v &= (1u << keep) - 1u;
+                }
+            }
+            const uint32_t c = __reduce_add_sync(0xffffffffu, __popc(v));
+            if (lane == 0) s_sub[s] = c;
+        }
+    }
+    __syncthreads();
+    // CTA-local exclusive offsets of the 128 sub-tiles (warp 0, 4 per lane)
+    unsigned long long agg = 0;
+    if (warp == 0) {
+        const uint32_t c0 = s_sub[4 * lane], c1 = s_sub[4 * lane + 1], c2 = s_sub[4 * lane + 2],
+                       c3 = s_sub[4 * lane + 3];
+        const uint32_t sum = c0 + c1 + c2 + c3;
+        const uint32_t incl = warp_incl_scan(sum, lane);
+        uint32_t e = incl - sum;
+        const uint64_t sub0 = w0 / 32 + 4 * lane;
+        const uint64_t nsubs = (nwords + 31) / 32;
+        const uint32_t cs[4] = {c0, c1, c2, c3};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (sub0 + k < nsubs) a.tsub[sub0 + k] = e;
+            e += cs[k];
+        }
+        agg = __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (tid == 0) {
+        a.blk[blockIdx.x] = agg;
+        __threadfence();
+        const unsigned long long d = atomicAdd(&a.hdr->done, 1ull);
+        s_last = (d == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+
+    // ---- last CTA: exclusive scan of the CTA aggregates -> CTA bases ---------
+    // Coalesced passes of 256 x 8 aggregates staged through shared memory, so
+    // the serial tail is a handful of L2 round trips regardless of nb.
+    __threadfence();
+    constexpr int K = 8;
+    __shared__ unsigned long long s_v[kScanThreads * K];
+    const uint32_t nb = gridDim.x;
+    unsigned long long carry = 0;
+    for (uint32_t base0 = 0; base0 < nb; base0 += kScanThreads * K) {
+        unsigned long long v[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const uint32_t b = base0 + k * kScanThreads + tid;
+            v[k] = b < nb ? __ldcg(&a.blk[b]) : 0ull;
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) s_v[k * kScanThreads + tid] = v[k];
+        __syncthreads();
+        unsigned long long sum = 0;  // thread owns entries [tid*K, tid*K+K)
+#pragma unroll
+        for (int k = 0; k < K; ++k) sum += s_v[tid * K + k];
+        const unsigned long long incl = warp_incl_scan(sum, lane);
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        unsigned long long run = carry + incl - sum;
+        unsigned long long all = 0;
+        for (int i = 0; i < kScanThreads / 32; ++i) {
+            run += (i < warp) ? s_warp[i] : 0ull;
+            all += s_warp[i];
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const unsigned long long x = s_v[tid * K + k];
+            s_v[tid * K + k] = run;
+            run += x;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const uint32_t b = base0 + k * kScanThreads + tid;
+            if (b < nb) a.blk[b] = s_v[k * kScanThreads + tid];
+        }
+        carry += all;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        a.blk[nb] = carry;
+        a.hdr->total = carry;
+        if (a.check_total && carry != a.expect_total) latch_status(a.hdr, ENDOR_ERR_CORRUPTION);
+        a.hdr->done = 0;
+    }
+}
+
+cudaError_t launch_count(const CountArgs& a, cudaStream_t s) {
+    const uint64_t nblocks = ceil_div((a.n + 31) / 32, kScanBlockWords);
+    if (nblocks == 0) return cudaSuccess;
+    count_kernel<<<unsigned(nblocks), kScanThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_kernel(ScanArgs a) {
+    __shared__ uint32_t s_ticket;
+    __shared__ unsigned long long s_warp_tot[kScanThreads / 32];
+    __shared__ unsigned long long s_excl;
+    __shared__ int s_last;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_ticket = uint32_t(atomicAdd(&a.hdr->ticket, 1ull));
+    __syncthreads();
+    const uint32_t blk = s_ticket;  // tickets are handed out in launch order
+
+    const uint64_t wbase = a.e0 / 32;                     // first word of the range
+    const uint64_t wend = (a.e1 + 31) / 32;               // one past the last word
+    const uint64_t seg = uint64_t(blk) * kScanBlockWords + uint64_t(warp) * kScanWarpWords;
+
+    // ---- phase 1: coalesced word loads + per-lane popcounts ----------------
+    uint32_t w[kScanWordsPerLane];
+    uint32_t lane_cnt = 0;
+#pragma unroll
+    for (int j = 0; j < kScanWordsPerLane; ++j) {
+        const uint64_t rel = seg + uint64_t(j) * 32 + lane;  // word index relative to e0
+        const uint64_t wi = wbase + rel;
+        uint32_t v = 0;
+        if (wi < wend) {
+            v = load_word32(a.bitmap, wi, a.nbytes);
+            const uint64_t bit0 = wi * 32;
+            if (bit0 + 32 > a.e1) {
+                const uint32_t keep = uint32_t(a.e1 - bit0);  // 1..31
+                // Padding bits of the final byte must be zero (bitmap.hpp:78-84).
+                if (a.e1 == a.n && (a.n & 7)) {
+                    const uint64_t pad_end = ((a.n + 7) & ~7ull) - bit0;  // bits < pad_end loaded
+                    const uint32_t padmask = (pad_end >= 32 ? 0xffffffffu : ((1u << pad_end) - 1u)) &
+                                             ~((1u << keep) - 1u);
+                    if (v & padmask) latch_status(a.hdr, ENDOR_ERR_CORRUPTION);
+                }
+                v &= (1u << keep) - 1u;
+            }
+        }
+        w[j] = v;
+        lane_cnt += __popc(v);
+    }
+    uint32_t warp_cnt = lane_cnt;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) warp_cnt += __shfl_xor_sync(0xffffffffu, warp_cnt, d);
+    if (lane == 0) s_warp_tot[warp] = warp_cnt;
+    __syncthreads();
+
+    // ---- phase 2: block aggregate + warp-parallel decoupled look-back -----------
+    if (warp == 0) {
+        unsigned long long agg = 0;
+        if (lane == 0) {
+            for (int i = 0; i < kScanThreads / 32; ++i) {
+                const unsigned long long t = s_warp_tot[i];
+                s_warp_tot[i] = agg;  // now the warp's exclusive offset within the block
+                agg += t;
+            }
+            lb_store(&a.lookback[blk], (blk == 0 ? kLbPrefix : kLbAgg) | (agg & kLbValue));
+        }
+        agg = __shfl_sync(0xffffffffu, agg, 0);
+        unsigned long long excl = 0;
+        if (blk > 0) {
+            // window of 32 predecessors per step: lane i looks at block j - i
+            for (int64_t j = int64_t(blk) - 1;;) {
+                const int64_t idx = j - lane;
+                const unsigned long long s = idx >= 0 ? lb_load(&a.lookback[idx]) : kLbPrefix;
+                const unsigned long long f = s & ~kLbValue;
+                const uint32_t pmask = __ballot_sync(0xffffffffu, f == kLbPrefix);
+                const uint32_t imask = __ballot_sync(0xffffffffu, f == 0);
+                const int limit = pmask ? __ffs(pmask) - 1 : 31;  // nearest inclusive prefix
+                if (imask & ((2u << limit) - 1u)) continue;       // someone not published: re-poll
+                unsigned long long v = lane <= limit ? (s & kLbValue) : 0ull;
+#pragma unroll
+                for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+                excl += v;
+                if (pmask) break;
+                j -= 32;
+            }
+            if (lane == 0) lb_store(&a.lookback[blk], kLbPrefix | ((excl + agg) & kLbValue));
+        }
+        if (lane == 0) {
+            const unsigned long long base = a.p0_ptr ? *a.p0_ptr : a.p0;
+            s_excl = base + excl;
+            if (blk == a.nblocks - 1) {
+                const unsigned long long total = base + excl + agg;
+                if (a.total_out) *a.total_out = total;
+                if (a.tsub) a.tsub[ceil_div(wend - wbase, 32)] = total;  // window end of the last tile
+                a.hdr->total = total;
+                if (a.check_total && total != a.expect_total) latch_status(a.hdr, ENDOR_ERR_CORRUPTION);
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- phase 3: per-word exclusive offsets at tile / chunk starts -----------
+    unsigned long long running = s_excl + s_warp_tot[warp];
+    const bool want_chunks = a.cs != 0 && (a.idx_out || a.idx_in);
+#pragma unroll
+    for (int j = 0; j < kScanWordsPerLane; ++j) {
+        const uint32_t pc = __popc(w[j]);
+        const uint32_t incl = warp_incl_scan(pc, lane);
+        const unsigned long long excl = running + (incl - pc);
+        const uint64_t rel = seg + uint64_t(j) * 32 + lane;
+        const uint64_t wi = wbase + rel;
+        if (wi < wend) {
+            if (a.tprefix && (rel % kTileWords) == 0) a.tprefix[rel / kTileWords] = excl;
+            if (a.tsub && lane == 0) a.tsub[rel / 32] = excl;  // 1024-element sub-tiles
+            if (want_chunks) {
+                const uint64_t bit = wi * 32;
+                if ((bit & (a.cs - 1)) == 0) {
+                    const uint64_t k = bit / a.cs;
+                    if (a.idx_out) a.idx_out[k] = excl;
+                    else if (a.idx_in[k] != excl) latch_status(a.hdr, ENDOR_ERR_CORRUPTION);
+                }
+            }
+        }
+        running += __shfl_sync(0xffffffffu, incl, 31);
+    }
+
+    // ---- self-reset of the look-back state (workspace stays zeroed) -----------
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        const unsigned long long d = atomicAdd(&a.hdr->done, 1ull);
+        s_last = (d == a.nblocks - 1);
+    }
+    __syncthreads();
+    if (s_last) {
+        for (uint32_t i = tid; i < a.nblocks; i += kScanThreads) a.lookback[i] = 0;
+        if (tid == 0) {
+            a.hdr->ticket = 0;
+            a.hdr->done = 0;
+        }
+    }
+}
+
+cudaError_t launch_scan(const ScanArgs& in, cudaStream_t s) {
+    ScanArgs a = in;
+    const uint64_t words = (a.e1 + 31) / 32 - a.e0 / 32;
+    a.nblocks = uint32_t(ceil_div(words, kScanBlockWords));
+    if (a.nblocks == 0) return cudaSuccess;
+    scan_kernel<<<a.nblocks, kScanThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace endor_b200

@@ -1,0 +1,90 @@
+"""Host front-end of the offload pipeline (endor_pipeline_* in the C ABI).
+
+The reference models an offloaded op as CpuToGpu(compressed bytes) ->
+Decompress -> Compute, strictly sequential (sim.hpp:196-224).  Here the
+stages run for real and overlap: the C++ pipeline (csrc/pipeline.cu) streams
+each op's bitmap + values from pinned host memory on a copy stream into a
+double-buffered device ring while the compute stream decompresses and runs
+the GEMV of the previous op.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional
+
+import torch
+
+from . import _lib
+from .codec import check
+
+
+@dataclass
+class HostOp:
+    """One compressed op resident in pinned host memory."""
+    rows: int
+    cols: int
+    dtype: int
+    bitmap: torch.Tensor   # pinned uint8
+    values: torch.Tensor   # pinned uint8
+    nnz: int
+    x: Optional[torch.Tensor] = None       # device f16 [cols]
+    y: Optional[torch.Tensor] = None       # device f32 [rows]
+    y_host: Optional[torch.Tensor] = None  # pinned f32 [rows]
+    dense: Optional[torch.Tensor] = None   # device uint8 [rows*cols*eb] (optional)
+
+    @property
+    def compressed_bytes(self) -> int:
+        return self.bitmap.numel() + self.values.numel()
+
+    @property
+    def dense_bytes(self) -> int:
+        return self.rows * self.cols * (2 if self.dtype == 0 else 1)
+
+
+def _p(t: Optional[torch.Tensor]):
+    return None if t is None or t.numel() == 0 else t.data_ptr()
+
+
+class OffloadPipeline:
+    def __init__(self, device: int, max_op_elems: int, ring_depth: int = 2):
+        self._lib = _lib.lib()
+        h = C.c_void_p()
+        check(self._lib.endor_pipeline_create(device, max_op_elems, ring_depth, C.byref(h)))
+        self._h = h
+        self.device = device
+
+    def close(self) -> None:
+        if self._h:
+            self._lib.endor_pipeline_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream_ptr(self) -> int:
+        return self._lib.endor_pipeline_stream(self._h)
+
+    def run(self, ops: List[HostOp], sync: bool = True) -> None:
+        arr = (_lib.PipelineOp * len(ops))()
+        for i, o in enumerate(ops):
+            arr[i] = _lib.PipelineOp(o.rows, o.cols, o.dtype, 0, _p(o.bitmap), _p(o.values), o.nnz,
+                                     _p(o.x), _p(o.y), _p(o.dense), _p(o.y_host))
+        self._keep = (arr, ops)
+        check(self._lib.endor_pipeline_run(self._h, arr, len(ops), 1 if sync else 0))
+
+    def stats(self) -> dict:
+        s = _lib.PipelineStats()
+        check(self._lib.endor_pipeline_stats_get(self._h, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in _lib.PipelineStats._fields_}
+
+
+def pinned_copy(t: torch.Tensor) -> torch.Tensor:
+    """Copy a (device or host) uint8 tensor into fresh pinned host memory."""
+    h = torch.empty(t.numel(), dtype=torch.uint8, pin_memory=True)
+    h.copy_(t.reshape(-1).view(torch.uint8))
+    return h

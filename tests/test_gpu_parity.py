@@ -160,6 +160,22 @@ def test_unaligned_values_window(E, offset):
         assert E.decompress(t).bytes() == w.tobytes()
 
 
+@pytest.mark.parametrize("bm_offset", [4, 8, 12])
+def test_bitmap_not_16B_aligned_uses_fallback(E, bm_offset):
+    """A bitmap slice that is only 4-byte aligned (e.g. a row shard) takes
+    the plain-load expand kernel; results must be identical."""
+    for eb, (rows, cols) in [(2, (129, 515)), (1, (77, 300)), (2, (64, 8192 + 64))]:
+        w = O.random_dense(rows, cols, eb, 99 + bm_offset, 0.5)
+        bm, vals, nnz, _ = O.compress(w, rows, cols, eb)
+        n = rows * cols
+        bitmap = E.Bitmap(n, data=dev_bytes(bm, offset=bm_offset))
+        dt = E.Dtype.F16 if eb == 2 else E.Dtype.I8
+        t = E.EndorTensor(rows, cols, dt, bitmap, dev_bytes(vals, offset=3))
+        assert E.decompress(t).bytes() == w.tobytes()
+        idx = E.build_rank_index(bitmap, 256)
+        assert E.decompress_chunked(t, idx).bytes() == w.tobytes()
+
+
 def test_chunks_any_order_and_isolation(E):
     # test_codec.cpp:168-200
     w = O.random_dense(16, 100, 1, 21, 0.5)

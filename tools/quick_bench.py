@@ -5,7 +5,9 @@ import torch
 from paper_2406_11674_b200 import codec as E, _lib
 L = _lib.lib()
 dev = torch.device("cuda", 0)
-for (rows, cols, s) in [(9216, 36864, 0.5), (16384, 16384, 0.3), (16384, 16384, 0.9)]:
+CFGS = [(9216, 36864, 0.5), (16384, 16384, 0.3), (16384, 16384, 0.9)]
+if '--fc1' in sys.argv: CFGS = CFGS[:1]
+for (rows, cols, s) in CFGS:
     w = E.synth_weight(rows, cols, 7, device=dev)
     E.magnitude_prune(w, s, inplace=True)
     t = E.compress(w)
