@@ -106,6 +106,19 @@ int endor_cuda_sync_status(void* ws, void* stream);
 int endor_cuda_decompress(const endor_tensor_view* t, void* dense_out, void* ws, size_t ws_bytes,
                           void* stream);
 
+/* decompress of up to 16 tensors of one dtype in two launches total (one
+ * count, one persistent expand over all of their tiles) -- e.g. every weight
+ * matrix of a decoder layer.  Bitmaps and outputs 16-byte aligned; the
+ * workspace needs endor_cuda_workspace_bytes_batch(views, count) bytes.
+ * Same results and errors as endor_cuda_decompress on each tensor. */
+size_t endor_cuda_workspace_bytes_batch(const endor_tensor_view* views, int count);
+int endor_cuda_decompress_batch(const endor_tensor_view* views, void* const* dense_outs, int count,
+                                void* ws, size_t ws_bytes, void* stream);
+/* The same split into its launches (phase 1 = count, 2 = expand, 0 = both),
+ * for per-kernel timing. */
+int endor_cuda_decompress_batch_phase(const endor_tensor_view* views, void* const* dense_outs,
+                                      int count, int phase, void* ws, size_t ws_bytes, void* stream);
+
 /* endor_cuda_decompress split into its two launches, for per-kernel timing:
  * phase 1 = rank (count) kernel, phase 2 = expand kernel (needs phase 1 on
  * the same workspace first).  phase 1 then 2 == endor_cuda_decompress. */

@@ -46,6 +46,11 @@ SIGNATURES = {
     "endor_cuda_workspace_init": (C.c_int, [_vp, _sz, _vp]),
     "endor_cuda_sync_status": (C.c_int, [_vp, _vp]),
     "endor_cuda_decompress": (C.c_int, [C.POINTER(TensorView), _vp, _vp, _sz, _vp]),
+    "endor_cuda_workspace_bytes_batch": (_sz, [C.POINTER(TensorView), C.c_int]),
+    "endor_cuda_decompress_batch": (C.c_int, [C.POINTER(TensorView), C.POINTER(_vp), C.c_int, _vp, _sz,
+                                              _vp]),
+    "endor_cuda_decompress_batch_phase": (C.c_int, [C.POINTER(TensorView), C.POINTER(_vp), C.c_int,
+                                                    C.c_int, _vp, _sz, _vp]),
     "endor_cuda_decompress_phase": (C.c_int, [C.POINTER(TensorView), _vp, C.c_int, _vp, _sz, _vp]),
     "endor_cuda_rank_index": (C.c_int, [_vp, _u64, _u64, _vp, _vp, _vp, _sz, _vp]),
     "endor_cuda_popcount": (C.c_int, [_vp, _u64, _vp, _vp, _sz, _vp]),

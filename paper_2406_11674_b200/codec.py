@@ -335,6 +335,44 @@ def decompress(t: EndorTensor, out: Optional[DenseMatrix] = None, sync: bool = T
     return out
 
 
+class BatchPlan:
+    """A prepared batch decompress of up to 16 same-dtype tensors (e.g. one
+    decoder layer's weights): two kernel launches for the whole batch."""
+
+    def __init__(self, tensors, outs=None):
+        if not tensors:
+            raise InvalidArgument("empty batch")
+        self.tensors = list(tensors)
+        dev = self.tensors[0].device
+        self.outs = list(outs) if outs is not None else [
+            DenseMatrix.empty(t.rows, t.cols, t.dtype, dev) for t in self.tensors]
+        n = len(self.tensors)
+        self._views = (TensorView * n)(*[t.view() for t in self.tensors])
+        self._outs = (C.c_void_p * n)(*[_ptr(o.data) for o in self.outs])
+        need = _lib.lib().endor_cuda_workspace_bytes_batch(self._views, n)
+        if need == 0:
+            raise InvalidArgument(_lib.lib().endor_cuda_last_error_string().decode())
+        self.ws = torch.zeros(need, dtype=torch.uint8, device=dev)
+        self.device = dev
+
+    def launch(self, stream_ptr: Optional[int] = None, phase: int = 0) -> None:
+        sp = _stream_ptr(self.device) if stream_ptr is None else stream_ptr
+        check(_lib.lib().endor_cuda_decompress_batch_phase(self._views, self._outs, len(self.tensors), phase,
+                                                           self.ws.data_ptr(), self.ws.numel(), sp))
+
+    def sync(self, stream_ptr: Optional[int] = None) -> None:
+        sp = _stream_ptr(self.device) if stream_ptr is None else stream_ptr
+        check(_lib.lib().endor_cuda_sync_status(self.ws.data_ptr(), sp))
+
+
+def decompress_batch(tensors, outs=None):
+    """decompress() of several tensors in one count + one expand launch."""
+    plan = BatchPlan(tensors, outs)
+    plan.launch()
+    plan.sync()
+    return plan.outs
+
+
 def build_rank_index(bitmap: Bitmap, chunk_size: int) -> RankIndex:
     """bitmap.hpp:117-132 on the device."""
     dev = bitmap.data.device

@@ -99,6 +99,18 @@ ExpandArgs expand_args(const endor_tensor_view* t, uint64_t n, uint64_t e0, uint
     return x;
 }
 
+// Count CTAs per batch: ~8 per SM (full occupancy), each streaming a contiguous bitmap range.
+int count_ctas() {
+    static thread_local int dev_cached = -1, sms = 148;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 8 * 148;
+    if (dev != dev_cached) {
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        dev_cached = dev;
+    }
+    return 8 * sms;
+}
+
 // scan + expand over the whole tensor.  A 16-byte aligned bitmap takes the
 // persistent TMA ring (sub-tile offsets); anything else the plain fallback.
 // phase: 0 = both launches, 1 = count only, 2 = expand only (TMA path).
@@ -106,18 +118,23 @@ int full_expand(const endor_tensor_view* t, uint64_t n, int eb, void* dst, const
                 ScanArgs a, cudaStream_t s, int phase = 0) {
     const ExpandArgs x = expand_args(t, n, 0, n, dst, L);
     if (aligned(t->bitmap, 16) && !a.idx_in) {
-        // hot path: two-level count (no inter-CTA waits) + persistent TMA expand
-        CountArgs c{};
-        c.bitmap = a.bitmap;
-        c.nbytes = a.nbytes;
-        c.n = n;
-        c.tsub = L.tsub;
-        c.blk = L.blk;
-        c.check_total = a.check_total;
-        c.expect_total = a.expect_total;
-        c.hdr = L.hdr;
-        if (phase != 2) CK(launch_count(c, s));
-        if (phase != 1) CK(launch_expand_tma(x, eb, s));
+        // hot path: two-level count (no inter-CTA waits) + persistent TMA expand,
+        // as a batch of one tensor
+        Batch b{};
+        b.count = 1;
+        b.check_total = a.check_total;
+        b.t[0].bitmap = static_cast<const uint8_t*>(t->bitmap);
+        b.t[0].values = static_cast<const uint8_t*>(t->values);
+        b.t[0].dst = static_cast<uint8_t*>(dst);
+        b.t[0].n = n;
+        b.t[0].nnz = t->nnz;
+        uint64_t sub_cap, blk_cap;
+        batch_plan(b, &sub_cap, &blk_cap, count_ctas());  // within ws_layout(n)'s capacities
+        b.tsub = L.tsub;
+        b.blk = L.blk;
+        b.hdr = L.hdr;
+        if (phase != 2) CK(launch_count(b, s));
+        if (phase != 1) CK(launch_expand_tma(b, eb, s));
         return ENDOR_OK;
     }
     if (phase != 0) return fail(ENDOR_ERR_INVALID_ARGUMENT, "phase split needs a 16-byte aligned bitmap");
@@ -193,6 +210,81 @@ int endor_cuda_decompress(const endor_tensor_view* t, void* dense_out, void* ws,
     a.check_total = 1;
     a.expect_total = t->nnz;
     return full_expand(t, n, eb, dense_out, L, a, S(stream));
+}
+
+static int plan_batch(const endor_tensor_view* views, void* const* outs, int count, Batch* b,
+                      int* eb_out, uint64_t* nmax, size_t* bytes) {
+    if (count < 0 || count > kMaxBatch || (count > 0 && !views))
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "batch must hold 0..16 tensors");
+    *b = Batch{};
+    int eb = 0, st;
+    uint64_t mx = 1;
+    for (int i = 0; i < count; ++i) {
+        uint64_t n;
+        int e;
+        if ((st = check_view(&views[i], &n, &e))) return st;
+        if (eb && e != eb) return fail(ENDOR_ERR_INVALID_ARGUMENT, "batched tensors must share a dtype");
+        eb = e;
+        if (n && !aligned(views[i].bitmap, 16))
+            return fail(ENDOR_ERR_INVALID_ARGUMENT, "batched bitmaps must be 16-byte aligned");
+        if (outs && n && (!outs[i] || !aligned(outs[i], 16)))
+            return fail(ENDOR_ERR_INVALID_ARGUMENT, "dense outputs must be non-null and 16-byte aligned");
+        if (n == 0) continue;  // nothing to expand (nnz <= n already checked)
+        BatchTensor& T = b->t[b->count++];
+        T.bitmap = static_cast<const uint8_t*>(views[i].bitmap);
+        T.values = static_cast<const uint8_t*>(views[i].values);
+        T.dst = outs ? static_cast<uint8_t*>(outs[i]) : nullptr;
+        T.n = n;
+        T.nnz = views[i].nnz;
+        mx = n > mx ? n : mx;
+    }
+    uint64_t sub_cap, blk_cap, blk_bound = 0;
+    batch_plan(*b, &sub_cap, &blk_cap, count_ctas());
+    for (int i = 0; i < b->count; ++i)  // size for one count CTA per block: device-independent
+        blk_bound += ceil_div((b->t[i].n + 31) / 32, kScanBlockWords) + 2;
+    *eb_out = eb ? eb : 2;
+    *nmax = mx;
+    *bytes = ws_layout_caps(nullptr, mx, sub_cap, blk_bound).bytes;
+    return ENDOR_OK;
+}
+
+size_t endor_cuda_workspace_bytes_batch(const endor_tensor_view* views, int count) {
+    Batch b;
+    int eb;
+    uint64_t nmax;
+    size_t bytes = 0;
+    if (plan_batch(views, nullptr, count, &b, &eb, &nmax, &bytes)) return 0;
+    return bytes;
+}
+
+int endor_cuda_decompress_batch_phase(const endor_tensor_view* views, void* const* dense_outs,
+                                      int count, int phase, void* ws, size_t ws_bytes, void* stream) {
+    Batch b;
+    if (phase < 0 || phase > 2) return fail(ENDOR_ERR_INVALID_ARGUMENT, "phase must be 0, 1 or 2");
+    int eb, st;
+    uint64_t nmax;
+    size_t need;
+    if (!dense_outs && count) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null output array");
+    if ((st = plan_batch(views, dense_outs, count, &b, &eb, &nmax, &need))) return st;
+    if (b.count == 0) return ENDOR_OK;
+    if (!ws || !aligned(ws, 256)) return fail(ENDOR_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+    if (ws_bytes < need) return fail(ENDOR_ERR_INVALID_ARGUMENT, "workspace too small for the batch");
+    uint64_t sub_cap, blk_cap, blk_bound = 0;
+    batch_plan(b, &sub_cap, &blk_cap, count_ctas());
+    for (int i = 0; i < b.count; ++i) blk_bound += ceil_div((b.t[i].n + 31) / 32, kScanBlockWords) + 2;
+    const WsLayout L = ws_layout_caps(ws, nmax, sub_cap, blk_bound);
+    b.check_total = 1;
+    b.tsub = L.tsub;
+    b.blk = L.blk;
+    b.hdr = L.hdr;
+    if (phase != 2) CK(launch_count(b, S(stream)));
+    if (phase != 1) CK(launch_expand_tma(b, eb, S(stream)));
+    return ENDOR_OK;
+}
+
+int endor_cuda_decompress_batch(const endor_tensor_view* views, void* const* dense_outs, int count,
+                                void* ws, size_t ws_bytes, void* stream) {
+    return endor_cuda_decompress_batch_phase(views, dense_outs, count, 0, ws, ws_bytes, stream);
 }
 
 int endor_cuda_decompress_phase(const endor_tensor_view* t, void* dense_out, int phase, void* ws,

@@ -56,28 +56,35 @@ __host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a
 __host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 __host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
-inline WsLayout ws_layout(void* base, uint64_t n) {
+// n sizes the per-tensor regions; sub_cap / blk_cap size the count_kernel
+// arrays (a batch of tensors needs the sum of theirs, see batch_plan).
+inline WsLayout ws_layout_caps(void* base, uint64_t n, uint64_t sub_cap, uint64_t blk_cap) {
     WsLayout L{};
     L.ntiles = ceil_div(n, kTileElems);
     L.nscan = ceil_div(n, kScanBlockBits);
+    L.nsub = ceil_div(n, kSubElems);
     size_t off = 256;
     char* b = static_cast<char*>(base);
     L.hdr = reinterpret_cast<WsHeader*>(b);
+    L.tsub = reinterpret_cast<unsigned long long*>(b + off);
+    off = align256(off + 8 * sub_cap);
+    L.blk = reinterpret_cast<unsigned long long*>(b + off);
+    off = align256(off + 8 * blk_cap);
     L.tprefix = reinterpret_cast<unsigned long long*>(b + off);
     off = align256(off + 8 * (L.ntiles + 1));
-    L.lookback = reinterpret_cast<unsigned long long*>(b + off);
+    L.lookback = reinterpret_cast<unsigned long long*>(b + off);  // must stay zeroed between calls
     off = align256(off + 8 * (L.nscan + 1));
     L.hist = reinterpret_cast<unsigned long long*>(b + off);
     off = align256(off + 8 * 32768);
     L.ties = reinterpret_cast<unsigned long long*>(b + off);
     off = align256(off + 8 * (L.ntiles + 1));
-    L.nsub = ceil_div(n, kSubElems);
-    L.tsub = reinterpret_cast<unsigned long long*>(b + off);
-    off = align256(off + 8 * (L.nsub + 16));
-    L.blk = reinterpret_cast<unsigned long long*>(b + off);
-    off = align256(off + 8 * (L.nscan + 2));
     L.bytes = off;
     return L;
+}
+
+inline WsLayout ws_layout(void* base, uint64_t n) {
+    return ws_layout_caps(base, n, (ceil_div(n, kSubElems) + 16 + 7) & ~uint64_t(7),
+                          ceil_div(n, kScanBlockBits) + 2);
 }
 
 // ---- PTX wrappers: shared memory, mbarrier, TMA bulk copies -------------------------

@@ -40,11 +40,10 @@ namespace endor_b200 {
 //         ym               = PRMT(y, 0, selm)              -- y, or y with v3 zeroed
 //         word1 (slots 2,3) = PRMT(x, ym, sel1)            -- unset slots read ym bytes 6,7
 //   i8:   word  (slots 0-3) = PRMT(x, 0, sel)
-// selm keeps y whole only when q == 0xF (then no slot is unset).
-struct __align__(16) LutF16 {
-    uint32_t sel0, sel1, selm, pad;
-};
-__shared__ LutF16 g_lut16[16];
+// selm keeps y whole only when q == 0xF (then no slot is unset).  The f16
+// table packs sel0 | sel1 << 16 into one word: 16 words in 16 distinct banks,
+// so a warp's lookups never conflict (one wavefront per LDS).
+__shared__ uint32_t g_lut16[16];
 __shared__ uint32_t g_lut8[16];
 
 __device__ __forceinline__ void init_luts(int tid) {
@@ -62,7 +61,7 @@ __device__ __forceinline__ void init_luts(int tid) {
             s8 |= (set ? j : 4u) << (4 * k);
             j += set;
         }
-        g_lut16[q] = LutF16{s0, s1, q == 15 ? 0x3210u : 0x4410u, 0u};
+        g_lut16[q] = s0 | (s1 << 16);
         g_lut8[q] = s8;
     }
 }
@@ -75,15 +74,16 @@ __device__ __forceinline__ uint4 gather_chunk(uint32_t m, uint32_t a) {
     if constexpr (EB == 2) {
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
-            const uint32_t qa = g == 0 ? ((m << 4) & 0xF0u) : (m & 0xF0u);  // 16 B per entry
-            const LutF16 L = *reinterpret_cast<const LutF16*>(reinterpret_cast<const char*>(g_lut16) + qa);
+            const uint32_t q = (m >> (4 * g)) & 15u;
+            const uint32_t sel = g_lut16[q];
             const uint32_t al = a & ~3u, sh = a << 3;  // funnel shifts wrap mod 32
             const uint32_t w0 = lds32(al), w1 = lds32(al + 4), w2 = lds32(al + 8);
             const uint32_t x = __funnelshift_r(w0, w1, sh);
             const uint32_t y = __funnelshift_r(w1, w2, sh);
-            o[2 * g] = __byte_perm(x, 0u, L.sel0);
-            o[2 * g + 1] = __byte_perm(x, __byte_perm(y, 0u, L.selm), L.sel1);
-            a += 2 * __popc(qa);
+            const uint32_t ym = __byte_perm(y, 0u, q == 15u ? 0x3210u : 0x4410u);
+            o[2 * g] = __byte_perm(x, 0u, sel);
+            o[2 * g + 1] = __byte_perm(x, ym, sel >> 16);
+            a += 2 * __popc(q);
         }
     } else {
 #pragma unroll
@@ -136,37 +136,38 @@ __device__ __forceinline__ void expand_subtile(uint32_t word, uint32_t excl, uin
 }
 
 // ---------------------------------------------------------------------------
-// persistent TMA kernel
+// persistent TMA kernel (batched over whole tensors)
 // ---------------------------------------------------------------------------
-constexpr int kStages = 4;
+#ifndef ENDOR_TMA_STAGES
+#define ENDOR_TMA_STAGES 6  // 6 x 17.6 KB ring = 2 CTAs/SM; measured best of 2..12 (profiles/r01)
+#endif
+constexpr int kStages = ENDOR_TMA_STAGES;
 constexpr int kConsumerWarps = kTileElems / kSubElems;  // 8
 constexpr int kTmaThreads = (kConsumerWarps + 1) * 32;  // + 1 producer warp
 
 template <int EB>
 struct Stage {
     static constexpr uint32_t kBm = 0;                            // 1 KiB bitmap
-    static constexpr uint32_t kSub = kTileElems / 8;              // 8 x u64 sub-tile offsets
+    static constexpr uint32_t kSub = kTileElems / 8;              // 8 x u64 sub-tile offsets + abs base
     static constexpr uint32_t kVals = kSub + 128;                 // packed-values window
     static constexpr uint32_t kBytes = kVals + kTileElems * EB + 64;
 };
 
 template <int EB>
 constexpr uint32_t tma_smem_bytes() {
-    return 256 /* 2*kStages mbarriers + lut */ + kStages * Stage<EB>::kBytes;
+    return 256 /* 2*kStages mbarriers */ + kStages * Stage<EB>::kBytes;
 }
 
 template <int EB>
-__global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(ExpandArgs a) {
+__global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_constant__ Batch b) {
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t sbase = smem_u32(smem);
     const uint32_t full0 = sbase, empty0 = sbase + 8 * kStages;
     const uint32_t st0 = sbase + 256;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t n = a.e1;  // the TMA kernel always covers [0, n)
-    const uint64_t ntiles = ceil_div(n, kTileElems);
-    const uint64_t nsub = ceil_div(n, kSubElems);
+    const uint64_t ntiles = b.ntiles;
 
-    if (read_status(a.hdr)) return;  // a latched error: write nothing
+    if (read_status(b.hdr)) return;  // a latched error: write nothing
     init_luts(tid);
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -179,14 +180,17 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(ExpandArgs a) {
 
     if (warp == kConsumerWarps) {
         // ================= producer warp =================
-        const uintptr_t vlo = reinterpret_cast<uintptr_t>(a.values);
-        const uintptr_t vhi = vlo + a.nnz * EB;
-        const uintptr_t vlo16 = (vlo + 15) & ~uintptr_t(15), vhi16 = vhi & ~uintptr_t(15);
-        const uint64_t nblk = ceil_div(ceil_div(n, 32), kScanBlockWords);
         constexpr uint32_t kSubsPerBlk = kScanBlockWords / 32;  // 128
-        // absolute value offset of sub-tile `sub` (count_kernel's two levels)
-        auto prefix_at = [&](uint64_t sub) -> unsigned long long {
-            return sub >= nsub ? a.blk[nblk] : a.blk[sub / kSubsPerBlk] + a.tsub[sub];
+        // absolute [start, end) value offsets of global tile t (count_kernel's two levels)
+        auto window = [&](uint64_t t, unsigned long long& s0, unsigned long long& s1) {
+            const BatchTensor& T = b.t[batch_tensor_of_tile(b, t)];
+            const uint64_t lt = t - T.tile0, nsub = ceil_div(T.n, kSubElems);
+            const uint64_t subs_per_cta = uint64_t(kSubsPerBlk) * T.cbpc;  // one count CTA's range
+            const unsigned long long* blk = b.blk + T.blk0;
+            const unsigned long long* tsub = b.tsub + T.sub0;
+            const uint64_t a = lt * 8, e = lt * 8 + 8;
+            s0 = blk[a / subs_per_cta] + tsub[a];
+            s1 = e >= nsub ? blk[T.ncta] : blk[e / subs_per_cta] + tsub[e];
         };
         unsigned long long tp_l = 0, te_l = 0;  // lane k: window of this CTA's tile i+k
         int i = 0;
@@ -196,16 +200,18 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(ExpandArgs a) {
             const uint32_t full = full0 + 8 * s;
             if ((i & 31) == 0) {  // one round trip fetches the next 32 tiles' windows
                 const uint64_t tl = t + uint64_t(lane) * gridDim.x;
-                if (tl < ntiles) {
-                    tp_l = prefix_at(tl * 8);
-                    te_l = prefix_at(tl * 8 + 8);
-                }
+                if (tl < ntiles) window(tl, tp_l, te_l);
             }
             const unsigned long long tp = __shfl_sync(0xffffffffu, tp_l, i & 31);
             const unsigned long long te = __shfl_sync(0xffffffffu, te_l, i & 31);
+            const BatchTensor& T = b.t[batch_tensor_of_tile(b, t)];
+            const uint64_t lt = t - T.tile0;
+            const uintptr_t vlo = reinterpret_cast<uintptr_t>(T.values);
+            const uintptr_t vhi = vlo + T.nnz * EB;
+            const uintptr_t vlo16 = (vlo + 15) & ~uintptr_t(15), vhi16 = vhi & ~uintptr_t(15);
             if (i >= kStages) mbar_wait(empty0 + 8 * s, ((i / kStages) - 1) & 1);
-            const uint64_t t0 = t * kTileElems;
-            const uint32_t count = uint32_t(umin64(kTileElems, n - t0));
+            const uint64_t t0 = lt * kTileElems;
+            const uint32_t count = uint32_t(umin64(kTileElems, T.n - t0));
             const uint32_t bm_bytes = (count + 7) / 8;
             const uint32_t bm_bulk = count == kTileElems ? 1024u : (bm_bytes & ~15u);
             const uintptr_t ws = vlo + tp * EB, we = vlo + te * EB;
@@ -214,23 +220,24 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(ExpandArgs a) {
             const uint32_t vbulk = be > bs ? uint32_t(be - bs) : 0u;
             if (lane == 0) {
                 mbar_arrive_expect_tx(full, bm_bulk + 64 + vbulk);
-                if (bm_bulk) bulk_g2s(stg + Stage<EB>::kBm, a.bitmap + t0 / 8, bm_bulk, full);
-                bulk_g2s(stg + Stage<EB>::kSub, a.tsub + t * 8, 64, full);
+                if (bm_bulk) bulk_g2s(stg + Stage<EB>::kBm, T.bitmap + t0 / 8, bm_bulk, full);
+                bulk_g2s(stg + Stage<EB>::kSub, b.tsub + T.sub0 + lt * 8, 64, full);
                 if (vbulk) bulk_g2s(stg + Stage<EB>::kVals + uint32_t(bs - as), reinterpret_cast<const void*>(bs), vbulk, full);
             }
             // edge bytes the bulk copies cannot move (ends of the buffers)
-            for (uint32_t b = bm_bulk + lane; b < bm_bytes; b += 32)
-                sts8(stg + Stage<EB>::kBm + b, __ldg(a.bitmap + t0 / 8 + b));
+            for (uint32_t x = bm_bulk + lane; x < bm_bytes; x += 32)
+                sts8(stg + Stage<EB>::kBm + x, __ldg(T.bitmap + t0 / 8 + x));
             const uint32_t win = uint32_t(ae - as);
             if (vbulk != win) {
-                for (uint32_t b = lane; b < win; b += 32) {
-                    const uintptr_t x = as + b;
-                    if (x >= vlo && x < vhi && !(x >= bs && x < be))
-                        sts8(stg + Stage<EB>::kVals + b, *reinterpret_cast<const uint8_t*>(x));
+                for (uint32_t x = lane; x < win; x += 32) {
+                    const uintptr_t p = as + x;
+                    if (p >= vlo && p < vhi && !(p >= bs && p < be))
+                        sts8(stg + Stage<EB>::kVals + x, *reinterpret_cast<const uint8_t*>(p));
                 }
             }
-            if (lane == 0) {  // absolute offset of the window (the bulk-copied entries are CTA-local)
-                asm volatile("st.shared.u64 [%0], %1;" ::"r"(stg + Stage<EB>::kSub + 64), "l"(tp) : "memory");
+            if (lane == 0) {  // smem byte offset of the window start (the bulk-copied entries are CTA-local)
+                asm volatile("st.shared.u32 [%0], %1;" ::"r"(stg + Stage<EB>::kSub + 64),
+                             "r"(uint32_t(ws - as)) : "memory");
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(full);
@@ -241,9 +248,10 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(ExpandArgs a) {
         for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
             const int s = i % kStages;
             const uint32_t stg = st0 + s * Stage<EB>::kBytes;
+            const BatchTensor& T = b.t[batch_tensor_of_tile(b, t)];
+            const uint64_t t0 = (t - T.tile0) * kTileElems;
+            const int32_t count = int32_t(umin64(kTileElems, T.n - t0));
             mbar_wait(full0 + 8 * s, (i / kStages) & 1);
-            const uint64_t t0 = t * kTileElems;
-            const int32_t count = int32_t(umin64(kTileElems, n - t0));
             const int32_t wfirst = warp * kSubElems;
             if (wfirst < count) {
                 const int32_t valid = min(count - wfirst, kSubElems);
@@ -257,10 +265,9 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(ExpandArgs a) {
                 const uint32_t excl = warp_incl_scan(pc, lane) - pc;
                 const unsigned long long tp = lds64(stg + Stage<EB>::kSub);
                 const unsigned long long sw = lds64(stg + Stage<EB>::kSub + 8 * warp);
-                const unsigned long long tabs = lds64(stg + Stage<EB>::kSub + 64);
-                const uint32_t off = uint32_t((reinterpret_cast<uintptr_t>(a.values) + tabs * EB) & 15);
+                const uint32_t off = lds32(stg + Stage<EB>::kSub + 64);
                 const uint32_t vbase = stg + Stage<EB>::kVals + off + uint32_t(sw - tp) * EB;
-                uint8_t* out = a.dst + (t0 + wfirst) * EB;
+                uint8_t* out = T.dst + (t0 + wfirst) * EB;
                 if (valid == kSubElems) expand_subtile<EB, true>(word, excl, vbase, out, valid, lane);
                 else expand_subtile<EB, false>(word, excl, vbase, out, valid, lane);
             }
@@ -350,7 +357,7 @@ cudaError_t launch_expand(const ExpandArgs& a, int eb, cudaStream_t s) {
 }
 
 template <int EB>
-static cudaError_t launch_tma_eb(const ExpandArgs& a, cudaStream_t s) {
+static cudaError_t launch_tma_eb(const Batch& b, cudaStream_t s) {
     static int blocks_per_sm = 0, sms = 0;
     constexpr uint32_t smem = tma_smem_bytes<EB>();
     if (!blocks_per_sm) {
@@ -364,17 +371,16 @@ static cudaError_t launch_tma_eb(const ExpandArgs& a, cudaStream_t s) {
                                                       kTmaThreads, smem);
         if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
-    const uint64_t ntiles = ceil_div(a.e1, kTileElems);
-    const uint64_t grid = umin64(ntiles, uint64_t(blocks_per_sm) * sms);
-    expand_tma_kernel<EB><<<unsigned(grid), kTmaThreads, smem, s>>>(a);
+    const uint64_t grid = umin64(b.ntiles, uint64_t(blocks_per_sm) * sms);
+    if (grid == 0) return cudaSuccess;
+    expand_tma_kernel<EB><<<unsigned(grid), kTmaThreads, smem, s>>>(b);
     return cudaGetLastError();
 }
 
-// Full-range expand [0, n) through the TMA ring (needs the sub-tile offsets
-// from scan_kernel and a 16-byte aligned bitmap).
-cudaError_t launch_expand_tma(const ExpandArgs& a, int eb, cudaStream_t s) {
-    if (a.e0 != 0 || a.e1 == 0) return cudaErrorInvalidValue;
-    return eb == 2 ? launch_tma_eb<2>(a, s) : launch_tma_eb<1>(a, s);
+// Whole-tensor expand of a batch through the TMA ring (needs count_kernel's
+// offsets in the same workspace; 16-byte aligned bitmaps and outputs).
+cudaError_t launch_expand_tma(const Batch& b, int eb, cudaStream_t s) {
+    return eb == 2 ? launch_tma_eb<2>(b, s) : launch_tma_eb<1>(b, s);
 }
 
 }  // namespace endor_b200

@@ -41,22 +41,50 @@ struct ExpandArgs {
     WsHeader* hdr;
 };
 
-// count_kernel: two-level popcount of a whole bitmap [0, n).
-struct CountArgs {
-    const uint8_t* bitmap;
-    uint64_t nbytes;
-    uint64_t n;
-    unsigned long long* tsub;  // CTA-local exclusive offset per 1024-bit sub-tile
-    unsigned long long* blk;   // per-CTA aggregates -> exclusive bases; total at [nblk]
-    int check_total;
-    uint64_t expect_total;
+// ---- the hot path: a batch of whole tensors (one layer's ops) -----------------
+// count_kernel + expand_tma_kernel take the batch by value (__grid_constant__),
+// so one launch of each covers every tensor with no descriptor upload.
+constexpr int kMaxBatch = 16;
+struct BatchTensor {
+    const uint8_t* bitmap;  // 16-byte aligned, ceil(n/8) bytes
+    const uint8_t* values;  // nnz*eb bytes, any alignment
+    uint8_t* dst;           // 16-byte aligned, n*eb bytes
+    uint64_t n, nnz;
+    uint64_t tile0;         // first global expand tile of this tensor
+    uint64_t sub0;          // offset of its sub-tile entries in Batch::tsub
+    uint32_t blk0;          // offset of its count-CTA entries in Batch::blk (ncta + 1 used)
+    uint32_t cblk0;         // first global count CTA of this tensor
+    uint32_t cbpc;          // 131072-bit count blocks per count CTA (a contiguous range)
+    uint32_t ncta;          // count CTAs of this tensor
+};
+struct Batch {
+    BatchTensor t[kMaxBatch];
+    int count;
+    int check_total;        // latch CORRUPTION when a popcount != nnz (codec.hpp:158-160)
+    uint64_t ntiles;        // expand tiles over all tensors
+    uint32_t ncblk;         // count CTAs over all tensors
+    unsigned long long* tsub;  // CTA-local exclusive offset per 1024-element sub-tile
+    unsigned long long* blk;   // per-count-CTA aggregates -> exclusive bases; total at [nblk]
     WsHeader* hdr;
 };
-cudaError_t launch_count(const CountArgs& a, cudaStream_t s);
+__host__ __device__ inline int batch_tensor_of_tile(const Batch& b, uint64_t tile) {
+    int i = b.count - 1;
+    while (i > 0 && tile < b.t[i].tile0) --i;
+    return i;
+}
+__host__ __device__ inline int batch_tensor_of_cblk(const Batch& b, uint32_t g) {
+    int i = b.count - 1;
+    while (i > 0 && g < b.t[i].cblk0) --i;
+    return i;
+}
+// Fill the per-tensor offsets; returns the tsub / blk entries the batch needs
+// (ws_layout_caps capacities).
+void batch_plan(Batch& b, uint64_t* sub_total, uint64_t* blk_total, int count_ctas);
+cudaError_t launch_count(const Batch& b, cudaStream_t s);
+cudaError_t launch_expand_tma(const Batch& b, int eb, cudaStream_t s);
 
 cudaError_t launch_scan(const ScanArgs& a, cudaStream_t s);
 cudaError_t launch_expand(const ExpandArgs& a, int eb, cudaStream_t s);
-cudaError_t launch_expand_tma(const ExpandArgs& a, int eb, cudaStream_t s);
 cudaError_t launch_synth(uint64_t i0, uint64_t count, int eb, uint64_t seed, void* out,
                          cudaStream_t s);
 cudaError_t launch_prune(uint8_t* w, uint64_t n, int eb, uint64_t target, const WsLayout& L,

@@ -24,139 +24,191 @@
 namespace endor_b200 {
 
 // ---------------------------------------------------------------------------
-// count_kernel
+// count_kernel (batched)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kScanThreads) count_kernel(CountArgs a) {
-    constexpr int kSubs = kScanBlockWords / 32;  // 128 sub-tiles of 1024 bits per CTA
+__global__ void __launch_bounds__(kScanThreads) count_kernel(const __grid_constant__ Batch b) {
+    constexpr int kSubs = kScanBlockWords / 32;  // 128 sub-tiles of 1024 bits per count block
     __shared__ unsigned long long s_warp[kScanThreads / 32];
     __shared__ uint32_t s_sub[kSubs];
     __shared__ int s_last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t nwords = (a.n + 31) / 32;
-    const uint64_t w0 = uint64_t(blockIdx.x) * kScanBlockWords;
+    const int ti = batch_tensor_of_cblk(b, blockIdx.x);
+    const BatchTensor& T = b.t[ti];
+    const uint32_t lc = blockIdx.x - T.cblk0;  // CTA index within the tensor
+    const uint64_t n = T.n, nbytes = (n + 7) / 8;
+    const uint64_t nwords = (n + 31) / 32;
+    const uint64_t nblocks = ceil_div(nwords, kScanBlockWords);
+    const uint64_t cb0 = uint64_t(lc) * T.cbpc, cb1 = umin64(nblocks, cb0 + T.cbpc);
+    const uint64_t nsubs = (nwords + 31) / 32;
 
-    if ((w0 + kScanBlockWords) * 32 <= a.n) {
-        // full CTA: 4 x 16-byte loads per thread; 8 consecutive lanes = 1 sub-tile
-        const uint4* src = reinterpret_cast<const uint4*>(a.bitmap) + w0 / 4;
-        uint4 v[4];
+    // stream this CTA's range of 131072-bit count blocks; sub-tile offsets are
+    // relative to the range start (its base comes from the last-CTA scan)
+    unsigned long long running = 0;
+    const uint4* bm4 = reinterpret_cast<const uint4*>(T.bitmap);
+    auto full_block = [&](uint64_t cb) { return cb < cb1 && (cb + 1) * kScanBlockWords * 32 <= n; };
+    uint4 v[4], vn[4];
+    if (full_block(cb0)) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) v[j] = __ldcs(src + j * kScanThreads + tid);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            uint32_t c = __popc(v[j].x) + __popc(v[j].y) + __popc(v[j].z) + __popc(v[j].w);
-            c += __shfl_xor_sync(0xffffffffu, c, 1);
-            c += __shfl_xor_sync(0xffffffffu, c, 2);
-            c += __shfl_xor_sync(0xffffffffu, c, 4);
-            if ((lane & 7) == 0) s_sub[32 * j + tid / 8] = c;
-        }
-    } else {
-        // ragged last CTA: word loads with the tail masked and padding checked
-        for (int s = warp; s < kSubs; s += kScanThreads / 32) {
-            const uint64_t wi = w0 + uint64_t(s) * 32 + lane;
-            uint32_t v = 0;
-            if (wi < nwords) {
-                v = load_word32(a.bitmap, wi, a.nbytes);
-                const uint64_t bit0 = wi * 32;
-                if (bit0 + 32 > a.n) {
-                    const uint32_t keep = uint32_t(a.n - bit0);
-                    if (a.n & 7) {  // padding bits of the final byte must be zero (bitmap.hpp:78-84)
-                        const uint64_t pad_end = ((a.n + 7) & ~7ull) - bit0;
-                        const uint32_t padmask = (pad_end >= 32 ? 0xffffffffu : ((1u << pad_end) - 1u)) &
-                                                 ~((1u << keep) - 1u);
-                        if (v & padmask) latch_status(a.hdr, ENDOR_ERR_CORRUPTION);
-                    }
-                    v &= (1u << keep) - 1u;
-                }
-            }
-            const uint32_t c = __reduce_add_sync(0xffffffffu, __popc(v));
-            if (lane == 0) s_sub[s] = c;
-        }
+        for (int j = 0; j < 4; ++j) v[j] = __ldcs(bm4 + cb0 * (kScanBlockWords / 4) + j * kScanThreads + tid);
     }
-    __syncthreads();
-    // CTA-local exclusive offsets of the 128 sub-tiles (warp 0, 4 per lane)
-    unsigned long long agg = 0;
-    if (warp == 0) {
-        const uint32_t c0 = s_sub[4 * lane], c1 = s_sub[4 * lane + 1], c2 = s_sub[4 * lane + 2],
-                       c3 = s_sub[4 * lane + 3];
-        const uint32_t sum = c0 + c1 + c2 + c3;
-        const uint32_t incl = warp_incl_scan(sum, lane);
-        uint32_t e = incl - sum;
-        const uint64_t sub0 = w0 / 32 + 4 * lane;
-        const uint64_t nsubs = (nwords + 31) / 32;
-        const uint32_t cs[4] = {c0, c1, c2, c3};
+    for (uint64_t cb = cb0; cb < cb1; ++cb) {
+        const uint64_t w0 = cb * kScanBlockWords;
+        if (full_block(cb + 1)) {  // keep the next block's 16 KiB in flight (latency hiding)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            if (sub0 + k < nsubs) a.tsub[sub0 + k] = e;
-            e += cs[k];
+            for (int j = 0; j < 4; ++j)
+                vn[j] = __ldcs(bm4 + (cb + 1) * (kScanBlockWords / 4) + j * kScanThreads + tid);
         }
-        agg = __shfl_sync(0xffffffffu, incl, 31);
+        if (full_block(cb)) {
+            // full block: 4 x 16-byte loads per thread; 8 consecutive lanes = 1 sub-tile
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint32_t c = __popc(v[j].x) + __popc(v[j].y) + __popc(v[j].z) + __popc(v[j].w);
+                c += __shfl_xor_sync(0xffffffffu, c, 1);
+                c += __shfl_xor_sync(0xffffffffu, c, 2);
+                c += __shfl_xor_sync(0xffffffffu, c, 4);
+                if ((lane & 7) == 0) s_sub[32 * j + tid / 8] = c;
+            }
+        } else {
+            // ragged last block: word loads with the tail masked and padding checked
+            for (int s = warp; s < kSubs; s += kScanThreads / 32) {
+                const uint64_t wi = w0 + uint64_t(s) * 32 + lane;
+                uint32_t wv = 0;
+                if (wi < nwords) {
+                    wv = load_word32(T.bitmap, wi, nbytes);
+                    const uint64_t bit0 = wi * 32;
+                    if (bit0 + 32 > n) {
+                        const uint32_t keep = uint32_t(n - bit0);
+                        if (n & 7) {  // padding bits of the final byte must be zero (bitmap.hpp:78-84)
+                            const uint64_t pad_end = ((n + 7) & ~7ull) - bit0;
+                            const uint32_t padmask =
+                                (pad_end >= 32 ? 0xffffffffu : ((1u << pad_end) - 1u)) & ~((1u << keep) - 1u);
+                            if (wv & padmask) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
+                        }
+                        wv &= (1u << keep) - 1u;
+                    }
+                }
+                const uint32_t c = __reduce_add_sync(0xffffffffu, __popc(wv));
+                if (lane == 0) s_sub[s] = c;
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {  // exclusive offsets of the block's 128 sub-tiles (4 per lane)
+            const uint32_t c0 = s_sub[4 * lane], c1 = s_sub[4 * lane + 1], c2 = s_sub[4 * lane + 2],
+                           c3 = s_sub[4 * lane + 3];
+            const uint32_t sum = c0 + c1 + c2 + c3;
+            const uint32_t incl = warp_incl_scan(sum, lane);
+            unsigned long long e = running + (incl - sum);
+            const uint64_t sub = w0 / 32 + 4 * lane;
+            const uint32_t cs[4] = {c0, c1, c2, c3};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (sub + k < nsubs) b.tsub[T.sub0 + sub + k] = e;
+                e += cs[k];
+            }
+            running += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        __syncthreads();  // s_sub is rewritten by the next block
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = vn[j];
     }
     if (tid == 0) {
-        a.blk[blockIdx.x] = agg;
+        b.blk[T.blk0 + lc] = running;  // warp 0's lane 0 holds the range aggregate
         __threadfence();
-        const unsigned long long d = atomicAdd(&a.hdr->done, 1ull);
+        const unsigned long long d = atomicAdd(&b.hdr->done, 1ull);
         s_last = (d == gridDim.x - 1);
     }
     __syncthreads();
     if (!s_last) return;
 
-    // ---- last CTA: exclusive scan of the CTA aggregates -> CTA bases ---------
+    // ---- last CTA: per tensor, exclusive scan of its CTA aggregates -> bases -----
     // Coalesced passes of 256 x 8 aggregates staged through shared memory, so
-    // the serial tail is a handful of L2 round trips regardless of nb.
+    // the serial tail is a handful of L2 round trips.
     __threadfence();
-    constexpr int K = 8;
+    constexpr int K = 2;  // 512 aggregates per pass; keeps the static smem small (8 CTAs/SM)
     __shared__ unsigned long long s_v[kScanThreads * K];
-    const uint32_t nb = gridDim.x;
-    unsigned long long carry = 0;
-    for (uint32_t base0 = 0; base0 < nb; base0 += kScanThreads * K) {
-        unsigned long long v[K];
+    for (int i = 0; i < b.count; ++i) {
+        const BatchTensor& U = b.t[i];
+        unsigned long long* blk = b.blk + U.blk0;
+        const uint32_t nb = U.ncta;  // one aggregate per count CTA of this tensor
+        unsigned long long carry = 0;
+        for (uint32_t base0 = 0; base0 < nb; base0 += kScanThreads * K) {
+            unsigned long long v[K];
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const uint32_t b = base0 + k * kScanThreads + tid;
-            v[k] = b < nb ? __ldcg(&a.blk[b]) : 0ull;
+            for (int k = 0; k < K; ++k) {
+                const uint32_t x = base0 + k * kScanThreads + tid;
+                v[k] = x < nb ? __ldcg(&blk[x]) : 0ull;
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k) s_v[k * kScanThreads + tid] = v[k];
+            __syncthreads();
+            unsigned long long sum = 0;  // thread owns entries [tid*K, tid*K+K)
+#pragma unroll
+            for (int k = 0; k < K; ++k) sum += s_v[tid * K + k];
+            const unsigned long long incl = warp_incl_scan(sum, lane);
+            if (lane == 31) s_warp[warp] = incl;
+            __syncthreads();
+            unsigned long long run = carry + incl - sum;
+            unsigned long long all = 0;
+            for (int w = 0; w < kScanThreads / 32; ++w) {
+                run += (w < warp) ? s_warp[w] : 0ull;
+                all += s_warp[w];
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const unsigned long long x = s_v[tid * K + k];
+                s_v[tid * K + k] = run;
+                run += x;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const uint32_t x = base0 + k * kScanThreads + tid;
+                if (x < nb) blk[x] = s_v[k * kScanThreads + tid];
+            }
+            carry += all;
+            __syncthreads();
         }
-#pragma unroll
-        for (int k = 0; k < K; ++k) s_v[k * kScanThreads + tid] = v[k];
-        __syncthreads();
-        unsigned long long sum = 0;  // thread owns entries [tid*K, tid*K+K)
-#pragma unroll
-        for (int k = 0; k < K; ++k) sum += s_v[tid * K + k];
-        const unsigned long long incl = warp_incl_scan(sum, lane);
-        if (lane == 31) s_warp[warp] = incl;
-        __syncthreads();
-        unsigned long long run = carry + incl - sum;
-        unsigned long long all = 0;
-        for (int i = 0; i < kScanThreads / 32; ++i) {
-            run += (i < warp) ? s_warp[i] : 0ull;
-            all += s_warp[i];
+        if (tid == 0) {
+            blk[nb] = carry;
+            b.hdr->total = carry;
+            if (b.check_total && carry != U.nnz) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
         }
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const unsigned long long x = s_v[tid * K + k];
-            s_v[tid * K + k] = run;
-            run += x;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const uint32_t b = base0 + k * kScanThreads + tid;
-            if (b < nb) a.blk[b] = s_v[k * kScanThreads + tid];
-        }
-        carry += all;
-        __syncthreads();
     }
-    if (tid == 0) {
-        a.blk[nb] = carry;
-        a.hdr->total = carry;
-        if (a.check_total && carry != a.expect_total) latch_status(a.hdr, ENDOR_ERR_CORRUPTION);
-        a.hdr->done = 0;
-    }
+    if (tid == 0) b.hdr->done = 0;
 }
 
-cudaError_t launch_count(const CountArgs& a, cudaStream_t s) {
-    const uint64_t nblocks = ceil_div((a.n + 31) / 32, kScanBlockWords);
-    if (nblocks == 0) return cudaSuccess;
-    count_kernel<<<unsigned(nblocks), kScanThreads, 0, s>>>(a);
+void batch_plan(Batch& b, uint64_t* sub_total, uint64_t* blk_total, int count_ctas) {
+    uint64_t tile = 0, sub = 0, ntot = 0;
+    uint32_t blk = 0, cta = 0;
+    for (int i = 0; i < b.count; ++i) ntot += b.t[i].n;
+    for (int i = 0; i < b.count; ++i) {
+        BatchTensor& T = b.t[i];
+        const uint64_t nb = ceil_div((T.n + 31) / 32, kScanBlockWords);
+        // count CTAs in proportion to size (~count_ctas in total), whole blocks each
+        uint64_t want = ntot ? (uint64_t(count_ctas) * T.n + ntot - 1) / ntot : 1;
+        want = want < 1 ? 1 : (want > nb ? nb : want);
+        T.cbpc = uint32_t(ceil_div(nb, want));
+        T.ncta = uint32_t(ceil_div(nb, T.cbpc));
+        T.tile0 = tile;
+        T.sub0 = sub;
+        T.blk0 = blk;
+        T.cblk0 = cta;
+        tile += ceil_div(T.n, kTileElems);
+        // +16: the TMA copies 8 entries per tile; keep every tensor's entries
+        // 64-byte aligned (bulk-copy sources must be 16-byte aligned)
+        sub += (ceil_div(T.n, kSubElems) + 16 + 7) & ~uint64_t(7);
+        blk += T.ncta + 2;
+        cta += T.ncta;
+    }
+    b.ntiles = tile;
+    b.ncblk = cta;
+    *sub_total = sub;
+    *blk_total = blk;
+}
+
+cudaError_t launch_count(const Batch& b, cudaStream_t s) {
+    if (b.ncblk == 0) return cudaSuccess;
+    count_kernel<<<b.ncblk, kScanThreads, 0, s>>>(b);
     return cudaGetLastError();
 }
 

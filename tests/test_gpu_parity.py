@@ -176,6 +176,27 @@ def test_bitmap_not_16B_aligned_uses_fallback(E, bm_offset):
         assert E.decompress_chunked(t, idx).bytes() == w.tobytes()
 
 
+def test_batch_decompress_matches_oracle(E):
+    """One count + one expand launch over mixed tensors (ragged sizes, both
+    sparsity extremes, an empty one) == per-tensor oracle decompress."""
+    cases = [(37, 200, 0.6), (1, 1, 0.0), (129, 515, 0.5), (64, 8192, 0.0), (3, 5, 1.0),
+             (300, 1000, 0.95), (0, 7, 0.5), (512, 1024, 0.3)]
+    tensors, wants = [], []
+    for i, (r, c, z) in enumerate(cases):
+        w = O.random_dense(r, c, 2, 500 + i, z)
+        bm, vals, nnz, _ = O.compress(w, r, c, 2)
+        tensors.append(make_tensor(E, r, c, 2, bm, vals, nnz, values_offset=i % 3 * 2))
+        wants.append(w.tobytes())
+    outs = E.decompress_batch(tensors)
+    for o, w in zip(outs, wants):
+        assert o.bytes() == w
+    # a corrupt member (nnz one short) is reported for the whole batch
+    bad = tensors[2]
+    tensors[2] = E.EndorTensor(bad.rows, bad.cols, bad.dtype, bad.bitmap, bad.values[:-2], validate=False)
+    with pytest.raises(E.CorruptionError):
+        E.decompress_batch(tensors)
+
+
 def test_chunks_any_order_and_isolation(E):
     # test_codec.cpp:168-200
     w = O.random_dense(16, 100, 1, 21, 0.5)
