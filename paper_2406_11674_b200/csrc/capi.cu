@@ -241,7 +241,7 @@ static int plan_batch(const endor_tensor_view* views, void* const* outs, int cou
     uint64_t sub_cap, blk_cap, blk_bound = 0;
     batch_plan(*b, &sub_cap, &blk_cap, count_ctas());
     for (int i = 0; i < b->count; ++i)  // size for one count CTA per block: device-independent
-        blk_bound += ceil_div((b->t[i].n + 31) / 32, kScanBlockWords) + 2;
+        blk_bound += ceil_div((b->t[i].n + 31) / 32, kCountBlockWords) + 2;
     *eb_out = eb ? eb : 2;
     *nmax = mx;
     *bytes = ws_layout_caps(nullptr, mx, sub_cap, blk_bound).bytes;
@@ -271,7 +271,7 @@ int endor_cuda_decompress_batch_phase(const endor_tensor_view* views, void* cons
     if (ws_bytes < need) return fail(ENDOR_ERR_INVALID_ARGUMENT, "workspace too small for the batch");
     uint64_t sub_cap, blk_cap, blk_bound = 0;
     batch_plan(b, &sub_cap, &blk_cap, count_ctas());
-    for (int i = 0; i < b.count; ++i) blk_bound += ceil_div((b.t[i].n + 31) / 32, kScanBlockWords) + 2;
+    for (int i = 0; i < b.count; ++i) blk_bound += ceil_div((b.t[i].n + 31) / 32, kCountBlockWords) + 2;
     const WsLayout L = ws_layout_caps(ws, nmax, sub_cap, blk_bound);
     b.check_total = 1;
     b.tsub = L.tsub;

@@ -23,6 +23,10 @@ constexpr int kScanWarpWords = 32 * kScanWordsPerLane;                   // 512
 constexpr int kScanBlockWords = (kScanThreads / 32) * kScanWarpWords;    // 4096
 constexpr uint64_t kScanBlockBits = uint64_t(kScanBlockWords) * 32;     // 131072
 
+// count_kernel (hot path): 32 KiB count blocks = 256 sub-tiles of 1024 bits.
+constexpr int kCountBlockWords = 8192;
+constexpr int kCountSubs = kCountBlockWords / 32;  // 256
+
 // ---- workspace ---------------------------------------------------------------
 // [0,256)                 WsHeader
 // [256, +8*(ntiles+1))    per-tile exclusive value offsets ("GPU RankIndex")
@@ -158,6 +162,17 @@ __device__ __forceinline__ T warp_incl_scan(T v, int lane) {
         if (lane >= d) v += u;
     }
     return v;
+}
+
+// Exclusive warp prefix sum of small values (0..63) by bit-slicing: six
+// independent ballots instead of a five-deep dependent shuffle chain.
+__device__ __forceinline__ uint32_t warp_excl_scan_small(uint32_t v) {
+    uint32_t lt;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+    uint32_t r = 0;
+#pragma unroll
+    for (int b = 0; b < 6; ++b) r += uint32_t(__popc(__ballot_sync(0xffffffffu, (v >> b) & 1u) & lt)) << b;
+    return r;
 }
 
 // Look-back state word: [63:62] flag (1 = aggregate, 2 = inclusive prefix),

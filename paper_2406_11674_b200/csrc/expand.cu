@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
 
     if (warp == kConsumerWarps) {
         // ================= producer warp =================
-        constexpr uint32_t kSubsPerBlk = kScanBlockWords / 32;  // 128
+        constexpr uint32_t kSubsPerBlk = kCountSubs;  // 256 sub-tiles per count block
         // absolute [start, end) value offsets of global tile t (count_kernel's two levels)
         auto window = [&](uint64_t t, unsigned long long& s0, unsigned long long& s1) {
             const BatchTensor& T = b.t[batch_tensor_of_tile(b, t)];
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
             s1 = e >= nsub ? blk[T.ncta] : blk[e / subs_per_cta] + tsub[e];
         };
         unsigned long long tp_l = 0, te_l = 0;  // lane k: window of this CTA's tile i+k
-        int i = 0;
+        int i = 0, ti = 0;
         for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
             const int s = i % kStages;
             const uint32_t stg = st0 + s * Stage<EB>::kBytes;
@@ -204,7 +204,8 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
             }
             const unsigned long long tp = __shfl_sync(0xffffffffu, tp_l, i & 31);
             const unsigned long long te = __shfl_sync(0xffffffffu, te_l, i & 31);
-            const BatchTensor& T = b.t[batch_tensor_of_tile(b, t)];
+            while (ti + 1 < b.count && t >= b.t[ti + 1].tile0) ++ti;
+            const BatchTensor& T = b.t[ti];
             const uint64_t lt = t - T.tile0;
             const uintptr_t vlo = reinterpret_cast<uintptr_t>(T.values);
             const uintptr_t vhi = vlo + T.nnz * EB;
@@ -244,11 +245,12 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
         }
     } else {
         // ================= consumer warps =================
-        int i = 0;
+        int i = 0, ti = 0;
         for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
             const int s = i % kStages;
             const uint32_t stg = st0 + s * Stage<EB>::kBytes;
-            const BatchTensor& T = b.t[batch_tensor_of_tile(b, t)];
+            while (ti + 1 < b.count && t >= b.t[ti + 1].tile0) ++ti;  // tiles only move forward
+            const BatchTensor& T = b.t[ti];
             const uint64_t t0 = (t - T.tile0) * kTileElems;
             const int32_t count = int32_t(umin64(kTileElems, T.n - t0));
             mbar_wait(full0 + 8 * s, (i / kStages) & 1);
@@ -261,8 +263,7 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
                     word = lds32(stg + Stage<EB>::kBm + (warp * 32 + lane) * 4);
                     if (valid - lbit < 32) word &= (1u << (valid - lbit)) - 1u;
                 }
-                const uint32_t pc = __popc(word);
-                const uint32_t excl = warp_incl_scan(pc, lane) - pc;
+                const uint32_t excl = warp_excl_scan_small(__popc(word));
                 const unsigned long long tp = lds64(stg + Stage<EB>::kSub);
                 const unsigned long long sw = lds64(stg + Stage<EB>::kSub + 8 * warp);
                 const uint32_t off = lds32(stg + Stage<EB>::kSub + 64);

@@ -27,9 +27,8 @@ namespace endor_b200 {
 // count_kernel (batched)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kScanThreads) count_kernel(const __grid_constant__ Batch b) {
-    constexpr int kSubs = kScanBlockWords / 32;  // 128 sub-tiles of 1024 bits per count block
     __shared__ unsigned long long s_warp[kScanThreads / 32];
-    __shared__ uint32_t s_sub[kSubs];
+    __shared__ uint32_t s_sub[kCountSubs];
     __shared__ int s_last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ti = batch_tensor_of_cblk(b, blockIdx.x);
@@ -37,31 +36,24 @@ __global__ void __launch_bounds__(kScanThreads) count_kernel(const __grid_consta
     const uint32_t lc = blockIdx.x - T.cblk0;  // CTA index within the tensor
     const uint64_t n = T.n, nbytes = (n + 7) / 8;
     const uint64_t nwords = (n + 31) / 32;
-    const uint64_t nblocks = ceil_div(nwords, kScanBlockWords);
+    const uint64_t nblocks = ceil_div(nwords, kCountBlockWords);
     const uint64_t cb0 = uint64_t(lc) * T.cbpc, cb1 = umin64(nblocks, cb0 + T.cbpc);
     const uint64_t nsubs = (nwords + 31) / 32;
-
-    // stream this CTA's range of 131072-bit count blocks; sub-tile offsets are
-    // relative to the range start (its base comes from the last-CTA scan)
-    unsigned long long running = 0;
     const uint4* bm4 = reinterpret_cast<const uint4*>(T.bitmap);
-    auto full_block = [&](uint64_t cb) { return cb < cb1 && (cb + 1) * kScanBlockWords * 32 <= n; };
-    uint4 v[4], vn[4];
-    if (full_block(cb0)) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) v[j] = __ldcs(bm4 + cb0 * (kScanBlockWords / 4) + j * kScanThreads + tid);
-    }
+
+    // stream this CTA's range of 262144-bit count blocks (32 KiB each, 8 x 16 B
+    // loads in flight per thread); sub-tile offsets are relative to the range
+    // start, whose base comes from the last-CTA scan
+    unsigned long long running = 0;
     for (uint64_t cb = cb0; cb < cb1; ++cb) {
-        const uint64_t w0 = cb * kScanBlockWords;
-        if (full_block(cb + 1)) {  // keep the next block's 16 KiB in flight (latency hiding)
+        const uint64_t w0 = cb * kCountBlockWords;
+        if ((cb + 1) * kCountBlockWords * 32 <= n) {
+            // full block: 8 consecutive lanes (128 B) = one 1024-bit sub-tile
+            uint4 v[8];
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-                vn[j] = __ldcs(bm4 + (cb + 1) * (kScanBlockWords / 4) + j * kScanThreads + tid);
-        }
-        if (full_block(cb)) {
-            // full block: 4 x 16-byte loads per thread; 8 consecutive lanes = 1 sub-tile
+            for (int j = 0; j < 8; ++j) v[j] = __ldcs(bm4 + w0 / 4 + j * kScanThreads + tid);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < 8; ++j) {
                 uint32_t c = __popc(v[j].x) + __popc(v[j].y) + __popc(v[j].z) + __popc(v[j].w);
                 c += __shfl_xor_sync(0xffffffffu, c, 1);
                 c += __shfl_xor_sync(0xffffffffu, c, 2);
@@ -70,7 +62,7 @@ __global__ void __launch_bounds__(kScanThreads) count_kernel(const __grid_consta
             }
         } else {
             // ragged last block: word loads with the tail masked and padding checked
-            for (int s = warp; s < kSubs; s += kScanThreads / 32) {
+            for (int s = warp; s < kCountSubs; s += kScanThreads / 32) {
                 const uint64_t wi = w0 + uint64_t(s) * 32 + lane;
                 uint32_t wv = 0;
                 if (wi < nwords) {
@@ -92,24 +84,24 @@ __global__ void __launch_bounds__(kScanThreads) count_kernel(const __grid_consta
             }
         }
         __syncthreads();
-        if (warp == 0) {  // exclusive offsets of the block's 128 sub-tiles (4 per lane)
-            const uint32_t c0 = s_sub[4 * lane], c1 = s_sub[4 * lane + 1], c2 = s_sub[4 * lane + 2],
-                           c3 = s_sub[4 * lane + 3];
-            const uint32_t sum = c0 + c1 + c2 + c3;
+        if (warp == 0) {  // exclusive offsets of the block's 256 sub-tiles (8 per lane)
+            uint32_t cs[8], sum = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                cs[k] = s_sub[8 * lane + k];
+                sum += cs[k];
+            }
             const uint32_t incl = warp_incl_scan(sum, lane);
             unsigned long long e = running + (incl - sum);
-            const uint64_t sub = w0 / 32 + 4 * lane;
-            const uint32_t cs[4] = {c0, c1, c2, c3};
+            const uint64_t sub = w0 / 32 + 8 * lane;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < 8; ++k) {
                 if (sub + k < nsubs) b.tsub[T.sub0 + sub + k] = e;
                 e += cs[k];
             }
             running += __shfl_sync(0xffffffffu, incl, 31);
         }
         __syncthreads();  // s_sub is rewritten by the next block
-#pragma unroll
-        for (int j = 0; j < 4; ++j) v[j] = vn[j];
     }
     if (tid == 0) {
         b.blk[T.blk0 + lc] = running;  // warp 0's lane 0 holds the range aggregate
@@ -121,57 +113,29 @@ __global__ void __launch_bounds__(kScanThreads) count_kernel(const __grid_consta
     if (!s_last) return;
 
     // ---- last CTA: per tensor, exclusive scan of its CTA aggregates -> bases -----
-    // Coalesced passes of 256 x 8 aggregates staged through shared memory, so
-    // the serial tail is a handful of L2 round trips.
+    // One warp per tensor, all tensors at once: lane l sums a contiguous run of
+    // the tensor's aggregates (independent loads, one L2 round trip), a warp scan
+    // turns the run sums into bases, and the lane rewrites its run.
     __threadfence();
-    constexpr int K = 2;  // 512 aggregates per pass; keeps the static smem small (8 CTAs/SM)
-    __shared__ unsigned long long s_v[kScanThreads * K];
-    for (int i = 0; i < b.count; ++i) {
+    for (int i = warp; i < b.count; i += kScanThreads / 32) {
         const BatchTensor& U = b.t[i];
         unsigned long long* blk = b.blk + U.blk0;
         const uint32_t nb = U.ncta;  // one aggregate per count CTA of this tensor
-        unsigned long long carry = 0;
-        for (uint32_t base0 = 0; base0 < nb; base0 += kScanThreads * K) {
-            unsigned long long v[K];
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const uint32_t x = base0 + k * kScanThreads + tid;
-                v[k] = x < nb ? __ldcg(&blk[x]) : 0ull;
-            }
-#pragma unroll
-            for (int k = 0; k < K; ++k) s_v[k * kScanThreads + tid] = v[k];
-            __syncthreads();
-            unsigned long long sum = 0;  // thread owns entries [tid*K, tid*K+K)
-#pragma unroll
-            for (int k = 0; k < K; ++k) sum += s_v[tid * K + k];
-            const unsigned long long incl = warp_incl_scan(sum, lane);
-            if (lane == 31) s_warp[warp] = incl;
-            __syncthreads();
-            unsigned long long run = carry + incl - sum;
-            unsigned long long all = 0;
-            for (int w = 0; w < kScanThreads / 32; ++w) {
-                run += (w < warp) ? s_warp[w] : 0ull;
-                all += s_warp[w];
-            }
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const unsigned long long x = s_v[tid * K + k];
-                s_v[tid * K + k] = run;
-                run += x;
-            }
-            __syncthreads();
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const uint32_t x = base0 + k * kScanThreads + tid;
-                if (x < nb) blk[x] = s_v[k * kScanThreads + tid];
-            }
-            carry += all;
-            __syncthreads();
+        const uint32_t per = (nb + 31) / 32;
+        const uint32_t r0 = min(nb, lane * per), r1 = min(nb, r0 + per);
+        unsigned long long sum = 0;
+        for (uint32_t x = r0; x < r1; ++x) sum += __ldcg(&blk[x]);
+        const unsigned long long incl = warp_incl_scan(sum, lane);
+        unsigned long long run = incl - sum;
+        for (uint32_t x = r0; x < r1; ++x) {
+            const unsigned long long v = __ldcg(&blk[x]);
+            blk[x] = run;
+            run += v;
         }
-        if (tid == 0) {
-            blk[nb] = carry;
-            b.hdr->total = carry;
-            if (b.check_total && carry != U.nnz) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
+        if (lane == 31) {
+            blk[nb] = incl;  // grand total of the tensor
+            b.hdr->total = incl;
+            if (b.check_total && incl != U.nnz) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
         }
     }
     if (tid == 0) b.hdr->done = 0;
@@ -183,7 +147,7 @@ void batch_plan(Batch& b, uint64_t* sub_total, uint64_t* blk_total, int count_ct
     for (int i = 0; i < b.count; ++i) ntot += b.t[i].n;
     for (int i = 0; i < b.count; ++i) {
         BatchTensor& T = b.t[i];
-        const uint64_t nb = ceil_div((T.n + 31) / 32, kScanBlockWords);
+        const uint64_t nb = ceil_div((T.n + 31) / 32, kCountBlockWords);
         // count CTAs in proportion to size (~count_ctas in total), whole blocks each
         uint64_t want = ntot ? (uint64_t(count_ctas) * T.n + ntot - 1) / ntot : 1;
         want = want < 1 ? 1 : (want > nb ? nb : want);
