@@ -99,16 +99,17 @@ ExpandArgs expand_args(const endor_tensor_view* t, uint64_t n, uint64_t e0, uint
     return x;
 }
 
-// Count CTAs per batch: ~8 per SM (full occupancy), each streaming a contiguous bitmap range.
+// Count CTAs per batch: 3 per SM (each holds a 2 x 32 KiB TMA ring), each
+// streaming a contiguous bitmap range.
 int count_ctas() {
     static thread_local int dev_cached = -1, sms = 148;
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return 8 * 148;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 3 * 148;
     if (dev != dev_cached) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         dev_cached = dev;
     }
-    return 8 * sms;
+    return 3 * sms;
 }
 
 // scan + expand over the whole tensor.  A 16-byte aligned bitmap takes the

@@ -39,19 +39,40 @@ __global__ void __launch_bounds__(kScanThreads) count_kernel(const __grid_consta
     const uint64_t nblocks = ceil_div(nwords, kCountBlockWords);
     const uint64_t cb0 = uint64_t(lc) * T.cbpc, cb1 = umin64(nblocks, cb0 + T.cbpc);
     const uint64_t nsubs = (nwords + 31) / 32;
-    const uint4* bm4 = reinterpret_cast<const uint4*>(T.bitmap);
+    // 2-stage ring of 32 KiB blocks filled by 1-D TMA bulk copies: block cb+1 is
+    // in flight while block cb is counted, so HBM never idles between blocks
+    extern __shared__ __align__(128) uint4 s_blk[];  // [2][kCountBlockWords / 4]
+    __shared__ __align__(8) unsigned long long s_full[2];
+    const uint32_t full0 = smem_u32(&s_full[0]);
+    auto full_block = [&](uint64_t cb) { return cb < cb1 && (cb + 1) * kCountBlockWords * 32 <= n; };
+    auto issue = [&](uint64_t cb, int s) {  // thread 0 only
+        const uint32_t bar = full0 + 8 * s;
+        mbar_arrive_expect_tx(bar, kCountBlockWords * 4);
+        bulk_g2s(smem_u32(s_blk + s * (kCountBlockWords / 4)), T.bitmap + cb * kCountBlockWords * 4,
+                 kCountBlockWords * 4, bar);
+    };
+    if (tid == 0) {
+        mbar_init(full0, 1);
+        mbar_init(full0 + 8, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (full_block(cb0)) issue(cb0, 0);
+    }
+    __syncthreads();
 
-    // stream this CTA's range of 262144-bit count blocks (32 KiB each, 8 x 16 B
-    // loads in flight per thread); sub-tile offsets are relative to the range
-    // start, whose base comes from the last-CTA scan
+    // stream this CTA's range of 262144-bit count blocks; sub-tile offsets are
+    // relative to the range start, whose base comes from the last-CTA scan
     unsigned long long running = 0;
-    for (uint64_t cb = cb0; cb < cb1; ++cb) {
+    int it = 0;
+    for (uint64_t cb = cb0; cb < cb1; ++cb, ++it) {
         const uint64_t w0 = cb * kCountBlockWords;
-        if ((cb + 1) * kCountBlockWords * 32 <= n) {
+        const int s = it & 1;
+        if (tid == 0 && full_block(cb + 1)) issue(cb + 1, s ^ 1);  // stage s^1 freed by the last sync
+        if (full_block(cb)) {
             // full block: 8 consecutive lanes (128 B) = one 1024-bit sub-tile
+            mbar_wait(full0 + 8 * s, (it >> 1) & 1);
             uint4 v[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) v[j] = __ldcs(bm4 + w0 / 4 + j * kScanThreads + tid);
+            for (int j = 0; j < 8; ++j) v[j] = s_blk[s * (kCountBlockWords / 4) + j * kScanThreads + tid];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 uint32_t c = __popc(v[j].x) + __popc(v[j].y) + __popc(v[j].z) + __popc(v[j].w);
@@ -172,7 +193,14 @@ void batch_plan(Batch& b, uint64_t* sub_total, uint64_t* blk_total, int count_ct
 
 cudaError_t launch_count(const Batch& b, cudaStream_t s) {
     if (b.ncblk == 0) return cudaSuccess;
-    count_kernel<<<b.ncblk, kScanThreads, 0, s>>>(b);
+    constexpr int smem = 2 * kCountBlockWords * 4;  // two 32 KiB stages
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    count_kernel<<<b.ncblk, kScanThreads, smem, s>>>(b);
     return cudaGetLastError();
 }
 
