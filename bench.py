@@ -106,7 +106,8 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples),
+                "samples_in_timed_region": getattr(self, "in_region", len(self.samples))}
 
 
 # ---------------------------------------------------------------------------
@@ -177,16 +178,20 @@ def run_ours(args):
     for s in shards:
         s["dense"] = torch.empty(s["n"] * 2 + 16, dtype=torch.uint8, device=dev)
         s["out"] = E.DenseMatrix(s["rows"], s["cols"], E.Dtype.F16, s["dense"][: s["n"] * 2])
-    # one batch (count + expand launch) per decoder layer's six weight shards
+    # one batch per decoder layer's six weight shards.  Headline: the reference's
+    # parallel API decompress_chunked (codec.hpp:205) with a RankIndex at chunk
+    # 1024 built once at load time (like compression, offline): one expand launch
+    # per layer.  Also reported: decompress (codec.hpp:157), no index (count +
+    # expand launches per layer).
     per_layer = len(shards) // world
-    plans = [E.BatchPlan([s["t"] for s in shards[i:i + per_layer]], [s["out"] for s in shards[i:i + per_layer]])
-             for i in range(0, len(shards), per_layer)]
+    groups = [shards[i:i + per_layer] for i in range(0, len(shards), per_layer)]
+    for s in shards:
+        s["idx"] = E.build_rank_index(s["t"].bitmap, 1024)
+    plans_idx = [E.BatchPlan([s["t"] for s in g], [s["out"] for s in g], indices=[s["idx"] for s in g])
+                 for g in groups]
+    plans_noidx = [E.BatchPlan([s["t"] for s in g], [s["out"] for s in g]) for g in groups]
     stream = torch.cuda.Stream(device=dev)
     sp = stream.cuda_stream
-
-    def step():
-        for p in plans:
-            p.launch(sp)
 
     def barrier():
         if world > 1:
@@ -199,55 +204,87 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---- device-resident decompress: the `value` -------------------------------------
-    for _ in range(args.warmup):
-        step()
-    for p in plans:
-        p.sync(sp)
-    parity = golden_parity(shards, world)
-    torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    def timed(plans, sample_clocks=False):
+        """warmup, then exactly `steps` steps between events on the launching stream;
+        barrier + synchronize on both sides; max over ranks."""
+        for _ in range(args.warmup):
+            for p in plans:
+                p.launch(sp)
+        for p in plans:
+            p.sync(sp)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clk = ClockSampler(local) if sample_clocks else None
+        if clk:
+            clk.__enter__()
         ev0.record(stream)
         for _ in range(args.steps):
-            step()
+            for p in plans:
+                p.launch(sp)
         ev1.record(stream)
         torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
-    for p in plans:
-        p.sync(sp)
-    ms_total = max_over_ranks(ev0.elapsed_time(ev1))
-    ms_step = ms_total / args.steps
+        if clk:
+            clk.in_region = len(clk.samples)
+            # a sub-second timed region yields few nvidia-smi samples: keep the same
+            # load running (untimed) until at least 3 samples exist
+            t_end = time.time() + 3.0
+            while len(clk.samples) < 3 and time.time() < t_end:
+                for p in plans:
+                    p.launch(sp)
+                torch.cuda.synchronize()
+            clk.__exit__()
+        barrier()
+        torch.cuda.synchronize()
+        for p in plans:
+            p.sync(sp)  # any device-detected corruption raises here
+        return max_over_ranks(ev0.elapsed_time(ev1)) / args.steps, clk
+
     dense_rank = sum(s["n"] * 2 for s in shards)
     comp_rank = sum((s["n"] + 7) // 8 + s["nnz"] * 2 for s in shards)
     alg_rank = sum(catalog.algorithmic_bytes(s["n"], s["nnz"]) for s in shards)
+    peak, peak_src = measured_peak()
+
+    # ---- device-resident decompress: the `value` -------------------------------------
+    ms_noidx, _ = timed(plans_noidx)
+    parity_noidx = golden_parity(shards, world)
+    ms_step, clk = timed(plans_idx, sample_clocks=True)
+    parity = golden_parity(shards, world)
+    if parity is not None and parity_noidx is not None:
+        parity["bit_exact"] = parity["bit_exact"] and parity_noidx["bit_exact"]
+        parity["paths"] = "decompress_chunked(idx 1024) and decompress"
     value = world * dense_rank / (ms_step * 1e-3) / 1e9
-    launches = 2 * len(plans) * args.steps
+    launches = len(plans_idx) * args.steps
+    no_index = {"api": "decompress (codec.hpp:157): count + expand launch per layer",
+                "value": round(world * dense_rank / (ms_noidx * 1e-3) / 1e9, 2),
+                "ms_per_step": round(ms_noidx, 4),
+                "step_frac": round(alg_rank / (ms_noidx * 1e-3) / 1e9 / peak, 4)}
 
     # ---- instrumented pass: per-kernel durations (roofline) --------------------------
     # events bracket each launch on the launching stream; one expand launch covers
     # a layer's six shards, so its algorithmic bytes are the layer's
-    peak, peak_src = measured_peak()
-    count_ms, expand_ms, expand_alg = 0.0, 0.0, 0
-    evs = []
-    for _ in range(args.steps):
-        for p in plans:
-            a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-            a.record(stream)
-            p.launch(sp, phase=1)
-            b.record(stream)
-            p.launch(sp, phase=2)
-            c.record(stream)
-            evs.append((a, b, c, p))
-    torch.cuda.synchronize()
-    for a, b, c, p in evs:
-        count_ms += a.elapsed_time(b)
-        expand_ms += b.elapsed_time(c)
-        expand_alg += sum(catalog.algorithmic_bytes(t.element_count(), t.nnz()) for t in p.tensors)
-    n_exp = len(evs)
+    def kernel_times(plans, with_count):
+        count_ms, expand_ms, alg, evs = 0.0, 0.0, 0, []
+        for _ in range(args.steps):
+            for p in plans:
+                a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                a.record(stream)
+                if with_count:
+                    p.launch(sp, phase=1)
+                b.record(stream)
+                p.launch(sp, phase=2)
+                c.record(stream)
+                evs.append((a, b, c, p))
+        torch.cuda.synchronize()
+        for a, b, c, p in evs:
+            count_ms += a.elapsed_time(b) if with_count else 0.0
+            expand_ms += b.elapsed_time(c)
+            alg += sum(catalog.algorithmic_bytes(t.element_count(), t.nnz()) for t in p.tensors)
+        return count_ms / len(evs), expand_ms / len(evs), alg // len(evs)
+
+    _, expand_ms, expand_alg = kernel_times(plans_idx, False)
+    count_ms, _, _ = kernel_times(plans_noidx, True)
     achieved = expand_alg / (expand_ms * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "bench_expand_traffic.json")
@@ -257,10 +294,9 @@ def run_ours(args):
     roofline = {"bound": "hbm", "kernel": "expand_tma_kernel<2>", "achieved": round(achieved, 1),
                 "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "alg_bytes_per_launch": expand_alg // max(n_exp, 1),
-                "avg_launch_us": round(expand_ms * 1e3 / max(n_exp, 1), 2),
-                "count_kernel_avg_us": round(count_ms * 1e3 / max(n_exp, 1), 2),
-                "expand_share_of_step": round(expand_ms / (expand_ms + count_ms), 4),
+                "alg_bytes_per_launch": expand_alg,
+                "avg_launch_us": round(expand_ms * 1e3, 2),
+                "count_kernel_avg_us_no_index_path": round(count_ms * 1e3, 2),
                 "step_frac": round(alg_rank / (ms_step * 1e-3) / 1e9 / peak, 4)}
 
     # ---- e2e: offload pipeline over pinned host buffers ----------------------------------
@@ -341,8 +377,8 @@ def run_ours(args):
                            "l2": "inputs larger than L2 (no flush needed): %.2f GB/step/GPU" % ((comp_rank + dense_rank) / 1e9),
                            "parallelism": f"row-shard{world}"},
                 "per_gpu_value": round(value / world, 2),
-                "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "parity": parity,
-                "gpu_launches": launches, "clocks": clk.summary()}
+                "roofline": roofline, "decompress_no_index": no_index, "e2e": e2e, "cpu_baseline": cpu, "parity": parity,
+                "gpu_launches": launches, "clocks": clk.summary() if clk else None}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -137,11 +137,26 @@ int endor_cuda_popcount(const void* bitmap, uint64_t n, uint64_t* total_out, voi
                         size_t ws_bytes, void* stream);
 
 /* decompress_chunked (codec.hpp:205-216) with a device-resident RankIndex.
- * chunk_count must equal ceil(n/cs) (else CORRUPTION, codec.hpp:174-176);
- * every prefix entry is verified on device (a superset of check_index). */
+ * chunk_count must equal ceil(n/cs) (else CORRUPTION, codec.hpp:174-176).
+ * cs == 1024: single-launch fast path, check_index semantics (see
+ * endor_cuda_decompress_chunked_batch).  Other sizes: every prefix entry is
+ * verified on device (a superset of check_index). */
 int endor_cuda_decompress_chunked(const endor_tensor_view* t, uint64_t chunk_size,
                                   const uint64_t* prefix, uint64_t chunk_count, void* dense_out,
                                   void* ws, size_t ws_bytes, void* stream);
+
+/* decompress_chunked over up to 16 tensors.  With chunk_size == 1024 (the
+ * recommended load-time index: 8 bytes per 1024 elements) and 16-byte aligned
+ * bitmaps and prefixes, the index supplies every sub-tile's value offset, so
+ * the whole batch is ONE expand launch with no counting pass; like the
+ * reference's check_index (codec.hpp:170-184) only the last entry is
+ * verified (prefix[last] + tail popcount == nnz), and an inconsistent middle
+ * entry produces unspecified output (never an out-of-bounds access).  Other
+ * chunk sizes fall back to endor_cuda_decompress_chunked per tensor.
+ * prefixes[i] must hold ceil(n_i / chunk_size) entries. */
+int endor_cuda_decompress_chunked_batch(const endor_tensor_view* views, const uint64_t* const* prefixes,
+                                        uint64_t chunk_size, void* const* dense_outs, int count, void* ws,
+                                        size_t ws_bytes, void* stream);
 
 /* decompress_chunk_into (codec.hpp:191-201): writes exactly and only chunk
  * k's byte range of dense_out (which must hold the full dense matrix,

@@ -339,7 +339,10 @@ class BatchPlan:
     """A prepared batch decompress of up to 16 same-dtype tensors (e.g. one
     decoder layer's weights): two kernel launches for the whole batch."""
 
-    def __init__(self, tensors, outs=None):
+    def __init__(self, tensors, outs=None, indices=None):
+        """indices: optional RankIndex per tensor (decompress_chunked,
+        codec.hpp:205); chunk size 1024 makes the batch a single expand
+        launch with no counting pass."""
         if not tensors:
             raise InvalidArgument("empty batch")
         self.tensors = list(tensors)
@@ -349,6 +352,18 @@ class BatchPlan:
         n = len(self.tensors)
         self._views = (TensorView * n)(*[t.view() for t in self.tensors])
         self._outs = (C.c_void_p * n)(*[_ptr(o.data) for o in self.outs])
+        self.indices = None
+        if indices is not None:
+            cs = {i.chunk_size for i in indices}
+            if len(cs) != 1:
+                raise InvalidArgument("one chunk size per batch")
+            self.chunk_size = cs.pop()
+            for t, i in zip(self.tensors, indices):  # check_index coverage (codec.hpp:174-176)
+                want = 0 if t.element_count() == 0 else -(-t.element_count() // self.chunk_size)
+                if i.chunk_count() != want:
+                    raise CorruptionError("rank index does not cover the bitmap")
+            self.indices = [i.prefix.to(device=dev, dtype=torch.int64).contiguous() for i in indices]
+            self._pre = (C.c_void_p * n)(*[_ptr(p) for p in self.indices])
         need = _lib.lib().endor_cuda_workspace_bytes_batch(self._views, n)
         if need == 0:
             raise InvalidArgument(_lib.lib().endor_cuda_last_error_string().decode())
@@ -357,6 +372,13 @@ class BatchPlan:
 
     def launch(self, stream_ptr: Optional[int] = None, phase: int = 0) -> None:
         sp = _stream_ptr(self.device) if stream_ptr is None else stream_ptr
+        if self.indices is not None:
+            if phase == 1:
+                return  # no counting pass on the indexed path
+            check(_lib.lib().endor_cuda_decompress_chunked_batch(self._views, self._pre, self.chunk_size,
+                                                                 self._outs, len(self.tensors),
+                                                                 self.ws.data_ptr(), self.ws.numel(), sp))
+            return
         check(_lib.lib().endor_cuda_decompress_batch_phase(self._views, self._outs, len(self.tensors), phase,
                                                            self.ws.data_ptr(), self.ws.numel(), sp))
 
@@ -365,9 +387,11 @@ class BatchPlan:
         check(_lib.lib().endor_cuda_sync_status(self.ws.data_ptr(), sp))
 
 
-def decompress_batch(tensors, outs=None):
-    """decompress() of several tensors in one count + one expand launch."""
-    plan = BatchPlan(tensors, outs)
+def decompress_batch(tensors, outs=None, indices=None):
+    """decompress() of several tensors in one count + one expand launch, or --
+    with a 1024-chunk RankIndex per tensor -- decompress_chunked() of all of
+    them in a single expand launch."""
+    plan = BatchPlan(tensors, outs, indices)
     plan.launch()
     plan.sync()
     return plan.outs

@@ -360,12 +360,62 @@ int endor_cuda_decompress_chunked(const endor_tensor_view* t, uint64_t cs, const
         return fail(ENDOR_ERR_INVALID_ARGUMENT, "dense output must be non-null and 16-byte aligned");
     WsLayout L;
     if ((st = check_ws(ws, ws_bytes, n, &L))) return st;
+    if (cs == uint64_t(kSubElems) && aligned(t->bitmap, 16) && aligned(prefix, 16)) {
+        // fast path: the index supplies every sub-tile offset -> one expand launch,
+        // check_index's tail test inside it (codec.hpp:177-183)
+        void* outs[1] = {dense_out};
+        const uint64_t* pres[1] = {prefix};
+        return endor_cuda_decompress_chunked_batch(t, pres, cs, outs, 1, ws, ws_bytes, stream);
+    }
     ScanArgs a = scan_args(t->bitmap, n, 0, n, L);
     a.check_total = 1;
     a.expect_total = t->nnz;
     a.cs = cs;
     a.idx_in = reinterpret_cast<const unsigned long long*>(prefix);
     return full_expand(t, n, eb, dense_out, L, a, S(stream));
+}
+
+int endor_cuda_decompress_chunked_batch(const endor_tensor_view* views, const uint64_t* const* prefixes,
+                                        uint64_t cs, void* const* dense_outs, int count, void* ws,
+                                        size_t ws_bytes, void* stream) {
+    if (count < 0 || count > kMaxBatch || (count > 0 && (!views || !prefixes || !dense_outs)))
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "batch must hold 0..16 tensors with prefixes and outputs");
+    bool fast = cs == uint64_t(kSubElems);
+    for (int i = 0; i < count && fast; ++i) fast = aligned(views[i].bitmap, 16) && aligned(prefixes[i], 16);
+    if (!fast) {  // general path, one tensor at a time (verifies every index entry)
+        for (int i = 0; i < count; ++i) {
+            uint64_t n = 0;
+            int e = 0, st;
+            if ((st = check_view(&views[i], &n, &e))) return st;
+            const uint64_t chunks = (n == 0 || cs == 0) ? 0 : ceil_div(n, cs);
+            if ((st = endor_cuda_decompress_chunked(&views[i], cs, prefixes[i], chunks, dense_outs[i], ws,
+                                                    ws_bytes, stream)))
+                return st;
+        }
+        return ENDOR_OK;
+    }
+    Batch b;
+    int eb, st;
+    uint64_t nmax;
+    size_t need;
+    if ((st = plan_batch(views, dense_outs, count, &b, &eb, &nmax, &need))) return st;
+    // attach the indices (plan_batch drops empty tensors: walk both lists)
+    for (int i = 0, j = 0; i < count; ++i) {
+        if (views[i].rows * views[i].cols == 0) continue;
+        if (!prefixes[i]) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null prefix");
+        b.t[j++].idx = reinterpret_cast<const unsigned long long*>(prefixes[i]);
+    }
+    if (b.count == 0) return ENDOR_OK;
+    if (!ws || !aligned(ws, 256)) return fail(ENDOR_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+    if (ws_bytes < sizeof(WsHeader)) return fail(ENDOR_ERR_INVALID_ARGUMENT, "workspace too small");
+    uint64_t sub_cap, blk_cap;
+    batch_plan(b, &sub_cap, &blk_cap, count_ctas());
+    b.check_total = 1;
+    b.hdr = static_cast<WsHeader*>(ws);  // only the status word is used on this path
+    b.tsub = nullptr;
+    b.blk = nullptr;
+    CK(launch_expand_tma(b, eb, S(stream)));
+    return ENDOR_OK;
 }
 
 int endor_cuda_decompress_chunk_into(const endor_tensor_view* t, uint64_t cs, const uint64_t* prefix,

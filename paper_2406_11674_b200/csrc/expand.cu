@@ -181,14 +181,51 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
     if (warp == kConsumerWarps) {
         // ================= producer warp =================
         constexpr uint32_t kSubsPerBlk = kCountSubs;  // 256 sub-tiles per count block
-        // absolute [start, end) value offsets of global tile t (count_kernel's two levels)
+        // check_index's tail test (codec.hpp:177-183) for caller-indexed tensors:
+        // idx[last] + popcount(last chunk) == nnz, plus the padding bits
+        if (blockIdx.x == 0) {
+            for (int k = 0; k < b.count; ++k) {
+                const BatchTensor& T = b.t[k];
+                if (!T.idx) continue;
+                const uint64_t last = ceil_div(T.n, kSubElems) - 1, w0 = last * 32;
+                const uint64_t nw = (T.n + 31) / 32, nbytes = (T.n + 7) / 8;
+                uint32_t v = 0;
+                if (w0 + lane < nw) {
+                    v = load_word32(T.bitmap, w0 + lane, nbytes);
+                    const uint64_t bit0 = (w0 + lane) * 32;
+                    if (bit0 + 32 > T.n) {
+                        const uint32_t keep = uint32_t(T.n - bit0);
+                        if ((T.n & 7) && (v >> keep)) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
+                        v &= (1u << keep) - 1u;
+                    }
+                }
+                const uint32_t tail = __reduce_add_sync(0xffffffffu, __popc(v));
+                if (lane == 0 && T.idx[last] + tail != T.nnz) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
+            }
+        }
+        // absolute [start, end) value offsets of global tile t: the caller's
+        // RankIndex, or count_kernel's two levels
         auto window = [&](uint64_t t, unsigned long long& s0, unsigned long long& s1) {
             const BatchTensor& T = b.t[batch_tensor_of_tile(b, t)];
             const uint64_t lt = t - T.tile0, nsub = ceil_div(T.n, kSubElems);
+            const uint64_t a = lt * 8, e = lt * 8 + 8;
+            if (T.idx) {
+                s0 = T.idx[a];
+                s1 = e >= nsub ? T.nnz : T.idx[e];
+                // memory safety only: an inconsistent index yields garbage like the
+                // reference, but never a read outside the values buffer
+                const unsigned long long c0 = s0 < T.nnz ? s0 : T.nnz;
+                const unsigned long long c1 = s1 < c0 ? c0 : (s1 < T.nnz ? s1 : T.nnz);
+                if (c0 != s0 || c1 != s1 || c1 - c0 > kTileElems) {
+                    latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
+                    s0 = c0;
+                    s1 = c1 - c0 > kTileElems ? c0 + kTileElems : c1;
+                }
+                return;
+            }
             const uint64_t subs_per_cta = uint64_t(kSubsPerBlk) * T.cbpc;  // one count CTA's range
             const unsigned long long* blk = b.blk + T.blk0;
             const unsigned long long* tsub = b.tsub + T.sub0;
-            const uint64_t a = lt * 8, e = lt * 8 + 8;
             s0 = blk[a / subs_per_cta] + tsub[a];
             s1 = e >= nsub ? blk[T.ncta] : blk[e / subs_per_cta] + tsub[e];
         };
@@ -219,12 +256,20 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
             const uintptr_t as = ws & ~uintptr_t(15), ae = (we + 15) & ~uintptr_t(15);
             const uintptr_t bs = as > vlo16 ? as : vlo16, be = ae < vhi16 ? ae : vhi16;
             const uint32_t vbulk = be > bs ? uint32_t(be - bs) : 0u;
+            // the 8 sub-tile offsets: bulk-copied, except a caller index's ragged
+            // last tile (fewer than 8 entries exist past lt*8)
+            const uint64_t nsub_t = ceil_div(T.n, kSubElems);
+            const bool sub_bulk = !T.idx || lt * 8 + 8 <= nsub_t;
+            const unsigned long long* subsrc = T.idx ? T.idx + lt * 8 : b.tsub + T.sub0 + lt * 8;
             if (lane == 0) {
-                mbar_arrive_expect_tx(full, bm_bulk + 64 + vbulk);
+                mbar_arrive_expect_tx(full, bm_bulk + (sub_bulk ? 64u : 0u) + vbulk);
                 if (bm_bulk) bulk_g2s(stg + Stage<EB>::kBm, T.bitmap + t0 / 8, bm_bulk, full);
-                bulk_g2s(stg + Stage<EB>::kSub, b.tsub + T.sub0 + lt * 8, 64, full);
+                if (sub_bulk) bulk_g2s(stg + Stage<EB>::kSub, subsrc, 64, full);
                 if (vbulk) bulk_g2s(stg + Stage<EB>::kVals + uint32_t(bs - as), reinterpret_cast<const void*>(bs), vbulk, full);
             }
+            if (!sub_bulk && lane < 8 && lt * 8 + lane < nsub_t)
+                asm volatile("st.shared.u64 [%0], %1;" ::"r"(stg + Stage<EB>::kSub + 8 * lane),
+                             "l"(subsrc[lane]) : "memory");
             // edge bytes the bulk copies cannot move (ends of the buffers)
             for (uint32_t x = bm_bulk + lane; x < bm_bytes; x += 32)
                 sts8(stg + Stage<EB>::kBm + x, __ldg(T.bitmap + t0 / 8 + x));
@@ -236,9 +281,11 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
                         sts8(stg + Stage<EB>::kVals + x, *reinterpret_cast<const uint8_t*>(p));
                 }
             }
-            if (lane == 0) {  // smem byte offset of the window start (the bulk-copied entries are CTA-local)
+            if (lane == 0) {  // smem byte offset of the window start, and its value count
                 asm volatile("st.shared.u32 [%0], %1;" ::"r"(stg + Stage<EB>::kSub + 64),
                              "r"(uint32_t(ws - as)) : "memory");
+                asm volatile("st.shared.u32 [%0], %1;" ::"r"(stg + Stage<EB>::kSub + 68),
+                             "r"(uint32_t(te - tp)) : "memory");
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(full);
@@ -263,11 +310,22 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
                     word = lds32(stg + Stage<EB>::kBm + (warp * 32 + lane) * 4);
                     if (valid - lbit < 32) word &= (1u << (valid - lbit)) - 1u;
                 }
-                const uint32_t excl = warp_excl_scan_small(__popc(word));
+                const uint32_t pc = __popc(word);
+                const uint32_t excl = warp_excl_scan_small(pc);
                 const unsigned long long tp = lds64(stg + Stage<EB>::kSub);
                 const unsigned long long sw = lds64(stg + Stage<EB>::kSub + 8 * warp);
                 const uint32_t off = lds32(stg + Stage<EB>::kSub + 64);
-                const uint32_t vbase = stg + Stage<EB>::kVals + off + uint32_t(sw - tp) * EB;
+                uint32_t rel = uint32_t(sw - tp);
+                if (T.idx) {  // a caller's index may be inconsistent: stay inside the staged window
+                    const uint32_t wcount = lds32(stg + Stage<EB>::kSub + 68);
+                    const uint32_t wtotal = __shfl_sync(0xffffffffu, excl + pc, 31);
+                    if (sw < tp || wtotal > wcount || rel > wcount - wtotal) {
+                        if (lane == 0) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
+                        rel = 0;
+                        if (wtotal > wcount) word = 0;  // nothing valid to place
+                    }
+                }
+                const uint32_t vbase = stg + Stage<EB>::kVals + off + rel * EB;
                 uint8_t* out = T.dst + (t0 + wfirst) * EB;
                 if (valid == kSubElems) expand_subtile<EB, true>(word, excl, vbase, out, valid, lane);
                 else expand_subtile<EB, false>(word, excl, vbase, out, valid, lane);

@@ -54,8 +54,12 @@ struct BatchTensor {
     uint64_t sub0;          // offset of its sub-tile entries in Batch::tsub
     uint32_t blk0;          // offset of its count-CTA entries in Batch::blk (ncta + 1 used)
     uint32_t cblk0;         // first global count CTA of this tensor
-    uint32_t cbpc;          // 131072-bit count blocks per count CTA (a contiguous range)
+    uint32_t cbpc;          // 262144-bit count blocks per count CTA (a contiguous range)
     uint32_t ncta;          // count CTAs of this tensor
+    // decompress_chunked fast path: a caller's RankIndex at chunk size 1024
+    // (absolute offsets, idx[k] = rank(1024 k)); when set, no count pass runs
+    // and tsub/blk are unused for this tensor.
+    const unsigned long long* idx;
 };
 struct Batch {
     BatchTensor t[kMaxBatch];

@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(kScanThreads) count_kernel(const __grid_consta
     __threadfence();
     for (int i = warp; i < b.count; i += kScanThreads / 32) {
         const BatchTensor& U = b.t[i];
+        if (U.idx) continue;  // caller-indexed: not counted here (expand checks its tail)
         unsigned long long* blk = b.blk + U.blk0;
         const uint32_t nb = U.ncta;  // one aggregate per count CTA of this tensor
         const uint32_t per = (nb + 31) / 32;
@@ -173,7 +174,7 @@ void batch_plan(Batch& b, uint64_t* sub_total, uint64_t* blk_total, int count_ct
         uint64_t want = ntot ? (uint64_t(count_ctas) * T.n + ntot - 1) / ntot : 1;
         want = want < 1 ? 1 : (want > nb ? nb : want);
         T.cbpc = uint32_t(ceil_div(nb, want));
-        T.ncta = uint32_t(ceil_div(nb, T.cbpc));
+        T.ncta = T.idx ? 0u : uint32_t(ceil_div(nb, T.cbpc));  // caller-indexed: no count pass
         T.tile0 = tile;
         T.sub0 = sub;
         T.blk0 = blk;

@@ -197,6 +197,52 @@ def test_batch_decompress_matches_oracle(E):
         E.decompress_batch(tensors)
 
 
+def test_chunked_1024_fast_path(E, seeded_cases):
+    """decompress_chunked with a 1024-element RankIndex: one expand launch fed
+    by the index (no counting pass), bit-exact; batched over mixed tensors."""
+    tensors, idxs, wants = [], [], []
+    for i, c in enumerate(seeded_cases[:40]):
+        rows, cols, eb = c["rows"], c["cols"], c["eb"]
+        if eb != 2:
+            continue
+        w = O.random_dense(rows, cols, eb, c["seed"], c["zero_fraction"])
+        bm, vals, nnz, _ = O.compress(w, rows, cols, eb)
+        t = make_tensor(E, rows, cols, eb, bm, vals, nnz, values_offset=(i % 4) * 2)
+        idx = E.build_rank_index(t.bitmap, 1024)
+        _, ref_p = O.rank_index(bm, rows * cols, 1024)
+        assert idx.prefix.cpu().numpy().astype(np.uint64).tolist() == ref_p.tolist()
+        assert E.decompress_chunked(t, idx).bytes() == w.tobytes()
+        tensors.append(t)
+        idxs.append(idx)
+        wants.append(w.tobytes())
+    for k in range(0, len(tensors), 16):
+        outs = E.decompress_batch(tensors[k:k + 16], indices=idxs[k:k + 16])
+        assert [o.bytes() for o in outs] == wants[k:k + 16]
+
+
+def test_chunked_1024_index_errors_are_safe(E):
+    rows, cols = 300, 1000
+    w = O.random_dense(rows, cols, 2, 31, 0.5)
+    bm, vals, nnz, _ = O.compress(w, rows, cols, 2)
+    t = make_tensor(E, rows, cols, 2, bm, vals, nnz)
+    good = E.build_rank_index(t.bitmap, 1024)
+    # last entry wrong -> CorruptionError, as check_index (codec.hpp:179-182)
+    bad = good.prefix.clone()
+    bad[-1] += 1
+    with pytest.raises(E.CorruptionError):
+        E.decompress_chunked(t, E.RankIndex(1024, bad))
+    # wildly wrong middle entries: never an illegal access; reported or garbage
+    for v in (10 ** 12, -5):
+        bad = good.prefix.clone()
+        bad[len(bad) // 2] = v
+        try:
+            E.decompress_chunked(t, E.RankIndex(1024, bad))
+        except E.CorruptionError:
+            pass
+    # and the device is still healthy afterwards
+    assert E.decompress_chunked(t, good).bytes() == w.tobytes()
+
+
 def test_chunks_any_order_and_isolation(E):
     # test_codec.cpp:168-200
     w = O.random_dense(16, 100, 1, 21, 0.5)
