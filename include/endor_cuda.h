@@ -119,6 +119,14 @@ int endor_cuda_decompress_batch(const endor_tensor_view* views, void* const* den
 int endor_cuda_decompress_batch_phase(const endor_tensor_view* views, void* const* dense_outs,
                                       int count, int phase, void* ws, size_t ws_bytes, void* stream);
 
+/* decompress(dequantize_values(t)) fused (codec.hpp:334-349 then :157): t is
+ * an I8 tensor (ENDOR_DTYPE_I8) quantized with `scale` (quantize_values,
+ * codec.hpp:306-331); dense_f16_out receives n f16 elements, each set one
+ * f32_to_f16(float(q) * scale) bit-exactly (float16.hpp:35-73), unset +0.
+ * Reads 1/8 + (1-s) bytes per element instead of 1/8 + 2(1-s). */
+int endor_cuda_decompress_dequant(const endor_tensor_view* t, float scale, void* dense_f16_out, void* ws,
+                                  size_t ws_bytes, void* stream);
+
 /* endor_cuda_decompress split into its two launches, for per-kernel timing:
  * phase 1 = rank (count) kernel, phase 2 = expand kernel (needs phase 1 on
  * the same workspace first).  phase 1 then 2 == endor_cuda_decompress. */

@@ -389,6 +389,24 @@ void or_dequantize_values(const uint8_t* q, uint64_t nnz, float scale, uint16_t*
     for (uint64_t i = 0; i < nnz; ++i) out[i] = or_f32_to_f16((float)(int8_t)q[i] * scale);
 }
 
+float or_quantize_values(const uint16_t* vals, uint64_t nnz, uint8_t* q_out) {
+    /* codec.hpp:306-331: scale = absmax/127 (1.0 if nnz == 0 or absmax == 0),
+     * q = clamp(lround(v / scale), -127, 127) */
+    float absmax = 0.0f;
+    for (uint64_t i = 0; i < nnz; ++i) {
+        float a = fabsf(or_f16_to_f32(vals[i]));
+        absmax = (absmax < a) ? a : absmax;  /* std::max(absmax, a) */
+    }
+    const float scale = (nnz == 0 || absmax == 0.0f) ? 1.0f : absmax / 127.0f;
+    for (uint64_t i = 0; i < nnz; ++i) {
+        long r = lroundf(or_f16_to_f32(vals[i]) / scale);
+        if (r < -127) r = -127;
+        if (r > 127) r = 127;
+        q_out[i] = (uint8_t)(int8_t)r;
+    }
+    return scale;
+}
+
 /* ---- parallel chunk fan-out (port CPU baseline) -------------------------- */
 
 typedef struct {

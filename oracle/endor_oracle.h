@@ -109,6 +109,10 @@ void or_acceptance_matrix(or_mt64* g, uint64_t rows, uint64_t cols, int eb, doub
 /* dequantize_values (codec.hpp:334-349): i8 * scale -> f16 (RNE). */
 void or_dequantize_values(const uint8_t* q, uint64_t nnz, float scale, uint16_t* out);
 
+/* quantize_values (codec.hpp:306-331): symmetric absmax f16 -> i8; returns
+ * the scale (1.0 for an all-zero tensor). */
+float or_quantize_values(const uint16_t* vals, uint64_t nnz, uint8_t* q_out);
+
 /* Multi-threaded decompress_chunk_into fan-out (the reference's documented
  * parallel contract, codec.hpp:188-190/203-204) used as the "port" CPU
  * baseline when oracle/_ref is unavailable.  Returns seconds. */

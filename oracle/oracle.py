@@ -81,6 +81,10 @@ def lib():
         L.or_acceptance_matrix.restype = None
         L.or_dequantize_values.argtypes = [_u8p, _u64, C.c_float, _u16p]
         L.or_dequantize_values.restype = None
+        L.or_quantize_values.argtypes = [_u16p, _u64, _u8p]
+        L.or_quantize_values.restype = C.c_float
+        L.or_make_op_mt.argtypes = [_u64, _u64, _u64, _f64, _i32, _u8p, _u8p]
+        L.or_make_op_mt.restype = _u64
         L.or_decompress_parallel.argtypes = [_u64, _i32, _u8p, _u8p, _u64, _u64p, _u8p, _i32]
         L.or_decompress_parallel.restype = _f64
         L.or_gemv_f16.argtypes = [_u64, _u64, _u16p, _u16p, _f32p]
@@ -125,6 +129,9 @@ def ref():
                                        C.POINTER(_i32), C.POINTER(_u64)]
         R.ref_f32_to_f16.argtypes = [C.c_float]
         R.ref_f32_to_f16.restype = C.c_uint16
+        R.ref_quantize_values.argtypes = [_u64, _u64, _u8p, _u8p, _u64, _u8p]
+        R.ref_quantize_values.restype = C.c_float
+        R.ref_decompress_dequant.argtypes = [_u64, _u64, _u8p, _u8p, _u64, C.c_float, _u8p]
     return _ref
 
 
@@ -213,6 +220,21 @@ def acceptance_cases(count: int = 1000):
         rsel = [r for r in range(rows) if g.coin() < 0.5]
         csel = [c for c in range(cols) if g.coin() < 0.5]
         yield it, rows, cols, eb, zeros, w, chunk, rsel, csel
+
+
+def quantize_values(vals_u8: np.ndarray, nnz: int):
+    """codec.hpp:306-331 -> (i8 bytes, scale)."""
+    v16 = np.ascontiguousarray(vals_u8).view(np.uint16) if nnz else np.zeros(1, np.uint16)
+    q = np.zeros(max(nnz, 1), np.uint8)
+    scale = lib().or_quantize_values(v16, nnz, q)
+    return q[:nnz], scale
+
+
+def decompress_dequant(rows, cols, bitmap, q, nnz, scale):
+    """decompress(dequantize_values(t)) on the CPU oracle -> f16 dense bytes."""
+    h = np.zeros(max(nnz, 1), np.uint16)
+    lib().or_dequantize_values(np.ascontiguousarray(q) if nnz else np.zeros(1, np.uint8), nnz, scale, h)
+    return decompress(rows, cols, 2, bitmap, h[:nnz].view(np.uint8), nnz)
 
 
 def gemv_f16(w_u16: np.ndarray, x_u16: np.ndarray, rows: int, cols: int) -> np.ndarray:

@@ -252,4 +252,29 @@ int ref_decode_endor(const uint8_t* data, uint64_t size, uint64_t* rows, uint64_
 
 uint16_t ref_f32_to_f16(float f) { return f32_to_f16(f); }
 
+// quantize_values (codec.hpp:306-331) of an f16 tensor: writes the i8 values,
+// returns the scale.
+float ref_quantize_values(uint64_t rows, uint64_t cols, const uint8_t* bitmap, const uint8_t* values,
+                          uint64_t nnz, uint8_t* q_out) {
+    EndorTensor q = quantize_values(make_tensor(rows, cols, 2, bitmap, values, nnz));
+    if (q.values_bytes()) std::memcpy(q_out, q.values().data(), q.values_bytes());
+    return *q.quant_scale();
+}
+
+// decompress(dequantize_values(t)) (codec.hpp:334-349 then :157) for an i8
+// tensor with a quantization scale; dst receives n f16 values.
+int ref_decompress_dequant(uint64_t rows, uint64_t cols, const uint8_t* bitmap, const uint8_t* q,
+                           uint64_t nnz, float scale, uint8_t* dst) {
+    try {
+        EndorTensor t0 = make_tensor(rows, cols, 1, bitmap, q, nnz);
+        EndorTensor t(rows, cols, Dtype::I8, t0.bitmap(),
+                      std::vector<std::byte>(t0.values().begin(), t0.values().end()), scale);
+        DenseMatrix out = decompress(dequantize_values(t));
+        if (out.size_bytes()) std::memcpy(dst, out.bytes().data(), out.size_bytes());
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
 }  // extern "C"

@@ -335,6 +335,22 @@ def decompress(t: EndorTensor, out: Optional[DenseMatrix] = None, sync: bool = T
     return out
 
 
+def decompress_dequant(t: EndorTensor, out: Optional[DenseMatrix] = None) -> DenseMatrix:
+    """decompress(dequantize_values(t)) fused on the device (codec.hpp:334-349
+    then :157): an I8 tensor with quant_scale -> f16 dense, bit-exact."""
+    if t.dtype != Dtype.I8 or t.quant_scale is None:  # codec.hpp:335-337
+        raise InvalidArgument("dequantize_values requires a quantized i8 tensor")
+    dev = t.device
+    if out is None:
+        out = DenseMatrix.empty(t.rows, t.cols, Dtype.F16, dev)
+    ws = workspace(t.element_count(), dev)
+    v = t.view()
+    check(_lib.lib().endor_cuda_decompress_dequant(C.byref(v), float(t.quant_scale), _ptr(out.data),
+                                                   ws.data_ptr(), ws.numel(), _stream_ptr(dev)))
+    sync_status(ws, dev)
+    return out
+
+
 class BatchPlan:
     """A prepared batch decompress of up to 16 same-dtype tensors (e.g. one
     decoder layer's weights): two kernel launches for the whole batch."""

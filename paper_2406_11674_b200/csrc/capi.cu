@@ -288,6 +288,55 @@ int endor_cuda_decompress_batch(const endor_tensor_view* views, void* const* den
     return endor_cuda_decompress_batch_phase(views, dense_outs, count, 0, ws, ws_bytes, stream);
 }
 
+int endor_cuda_decompress_dequant(const endor_tensor_view* t, float scale, void* dense_f16_out, void* ws,
+                                  size_t ws_bytes, void* stream) {
+    uint64_t n;
+    int eb, st;
+    if ((st = check_view(t, &n, &eb))) return st;
+    if (t->dtype != ENDOR_DTYPE_I8)  // codec.hpp:335-337
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "dequantize_values requires a quantized i8 tensor");
+    if (n == 0) return ENDOR_OK;
+    if (!dense_f16_out || !aligned(dense_f16_out, 16))
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "dense output must be non-null and 16-byte aligned");
+    WsLayout L;
+    if ((st = check_ws(ws, ws_bytes, n, &L))) return st;
+    uint32_t sbits;
+    memcpy(&sbits, &scale, 4);
+    // fast conversion is exact when no product can be NaN and unset slots give +0
+    const uint32_t fast = ((sbits & 0x7F800000u) != 0x7F800000u) && !(sbits >> 31);
+    if (aligned(t->bitmap, 16)) {
+        Batch b{};
+        b.count = 1;
+        b.check_total = 1;
+        BatchTensor& T = b.t[0];
+        T.bitmap = static_cast<const uint8_t*>(t->bitmap);
+        T.values = static_cast<const uint8_t*>(t->values);
+        T.dst = static_cast<uint8_t*>(dense_f16_out);
+        T.n = n;
+        T.nnz = t->nnz;
+        T.scale = scale;
+        T.deq_fast = fast;
+        uint64_t sub_cap, blk_cap;
+        batch_plan(b, &sub_cap, &blk_cap, count_ctas());
+        b.tsub = L.tsub;
+        b.blk = L.blk;
+        b.hdr = L.hdr;
+        CK(launch_count(b, S(stream)));
+        CK(launch_expand_tma(b, 3, S(stream)));
+        return ENDOR_OK;
+    }
+    ScanArgs a = scan_args(t->bitmap, n, 0, n, L);
+    a.check_total = 1;
+    a.expect_total = t->nnz;
+    a.tprefix = L.tprefix;
+    CK(launch_scan(a, S(stream)));
+    ExpandArgs x = expand_args(t, n, 0, n, dense_f16_out, L);
+    x.scale = scale;
+    x.deq_fast = fast;
+    CK(launch_expand(x, 3, S(stream)));
+    return ENDOR_OK;
+}
+
 int endor_cuda_decompress_phase(const endor_tensor_view* t, void* dense_out, int phase, void* ws,
                                 size_t ws_bytes, void* stream) {
     uint64_t n;

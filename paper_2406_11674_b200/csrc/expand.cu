@@ -14,7 +14,7 @@
 //
 // expand_tma_kernel (the hot path): persistent, warp-specialised.  One
 // producer warp streams each 8192-element tile's bitmap (1 KiB), its eight
-// sub-tile offsets and its packed-values window into a 4-stage shared-memory
+// sub-tile offsets and its packed-values window into a 6-stage shared-memory
 // ring with 1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx); eight
 // consumer warps each expand one 1024-element sub-tile per tile, fully
 // independently, and write dense rows with coalesced 16-byte stores.  HBM
@@ -23,6 +23,7 @@
 // expand_kernel (fallback): one CTA per tile, plain loads; used for
 // decompress_chunk_into's partial ranges and bitmaps that are not 16-byte
 // aligned.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -99,6 +100,64 @@ __device__ __forceinline__ uint4 gather_chunk(uint32_t m, uint32_t a) {
     return make_uint4(o[0], o[1], o[2], o[3]);
 }
 
+// Fused INT8 dequant + decompress (decompress(dequantize_values(t)),
+// codec.hpp:334-349 then :157): 8 output f16 slots per 16-byte chunk, each
+// set slot = f32_to_f16(float(q) * scale) (float16.hpp:35-73, RNE), unset = +0.
+// FAST (scale finite, sign bit clear): unset slots hold q = 0 -> +0 exactly,
+// and a finite product is converted with the hardware RNE (identical to the
+// reference's routine for every non-NaN input).  Otherwise the reference's
+// own bit routine runs per slot and unset slots are masked to +0.
+template <bool FAST>
+__device__ __forceinline__ uint4 gather_chunk_dequant(uint32_t m, uint32_t a, float scale) {
+    uint32_t o[4];
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+        const uint32_t q = (m >> (4 * g)) & 15u;
+        const uint32_t al = a & ~3u, sh = a << 3;
+        const uint32_t x = __byte_perm(__funnelshift_r(lds32(al), lds32(al + 4), sh), 0u, g_lut8[q]);
+        float f[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) f[k] = __fmul_rn(float(int8_t(x >> (8 * k))), scale);
+        if constexpr (FAST) {
+            const __half2 h0 = __floats2half2_rn(f[0], f[1]), h1 = __floats2half2_rn(f[2], f[3]);
+            o[2 * g] = *reinterpret_cast<const uint32_t*>(&h0);
+            o[2 * g + 1] = *reinterpret_cast<const uint32_t*>(&h1);
+        } else {
+            // NaN products follow the x86 SSE rules the reference runs under: a NaN
+            // operand propagates quieted, 0 * inf gives the default NaN 0xFFC00000
+            // (the GPU would produce a canonical 0x7FFFFFFF instead)
+            const uint32_t sb = __float_as_uint(scale);
+            const bool snan = (sb & 0x7FFFFFFFu) > 0x7F800000u;
+            uint32_t h[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                float v = f[k];
+                if (v != v) v = __uint_as_float(snan ? (sb | 0x00400000u) : 0xFFC00000u);
+                h[k] = (q >> k) & 1u ? f32_to_f16_bits(v) : 0u;
+            }
+            o[2 * g] = h[0] | (h[1] << 16);
+            o[2 * g + 1] = h[2] | (h[3] << 16);
+        }
+        a += __popc(q);
+    }
+    return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
+// Element modes of the expand kernels: bytes per packed value (IN) and per
+// dense output element (OUT).
+constexpr int kModeI8 = 1, kModeF16 = 2, kModeDequant = 3;
+__host__ __device__ constexpr int mode_in(int m) { return m == kModeF16 ? 2 : 1; }
+__host__ __device__ constexpr int mode_out(int m) { return m == kModeI8 ? 1 : 2; }
+
+template <int MODE>
+__device__ __forceinline__ uint4 gather_mode(uint32_t m, uint32_t a, float scale, bool fast) {
+    if constexpr (MODE == kModeDequant) {
+        return fast ? gather_chunk_dequant<true>(m, a, scale) : gather_chunk_dequant<false>(m, a, scale);
+    } else {
+        return gather_chunk<MODE>(m, a);
+    }
+}
+
 __device__ __forceinline__ void store_partial(uint8_t* p, uint4 q, uint32_t valid_bytes) {
     const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
@@ -111,10 +170,12 @@ __device__ __forceinline__ void store_partial(uint8_t* p, uint4 q, uint32_t vali
 // warp; vbase: shared address of the sub-tile's first packed value.  Lane l
 // writes chunks l, l+32, .. so every store instruction covers 512 contiguous
 // bytes.  FULL: all 1024 elements valid (no bounds checks).
-template <int EB, bool FULL>
+template <int MODE, bool FULL>
 __device__ __forceinline__ void expand_subtile(uint32_t word, uint32_t excl, uint32_t vbase,
-                                               uint8_t* out, int32_t valid_elems, int lane) {
-    constexpr int EPC = 16 / EB;              // elements per 16-byte chunk
+                                               uint8_t* out, int32_t valid_elems, int lane,
+                                               float scale = 1.f, bool fast = true) {
+    constexpr int IN = mode_in(MODE), OUT = mode_out(MODE);
+    constexpr int EPC = 16 / OUT;             // output elements per 16-byte chunk
     constexpr int CPW = 32 / EPC;             // chunks per bitmap word (4 or 2)
     constexpr int ITERS = 32 * 32 / EPC / 32; // chunks per lane (4 or 2)
     const uint32_t sh = (lane % CPW) * EPC;   // chunk position inside its word: lane-constant
@@ -129,9 +190,9 @@ __device__ __forceinline__ void expand_subtile(uint32_t word, uint32_t excl, uin
         const uint32_t r = pre + __popc(wd & low);
         const int e = (32 * j + lane) * EPC;
         if (!FULL && e >= valid_elems) continue;
-        const uint4 q = gather_chunk<EB>(m, vbase + r * EB);
+        const uint4 q = gather_mode<MODE>(m, vbase + r * IN, scale, fast);
         if (FULL || e + EPC <= valid_elems) *reinterpret_cast<uint4*>(o + j * 512) = q;
-        else store_partial(o + j * 512, q, uint32_t(valid_elems - e) * EB);
+        else store_partial(o + j * 512, q, uint32_t(valid_elems - e) * OUT);
     }
 }
 
@@ -158,8 +219,9 @@ constexpr uint32_t tma_smem_bytes() {
     return 256 /* 2*kStages mbarriers */ + kStages * Stage<EB>::kBytes;
 }
 
-template <int EB>
+template <int MODE>
 __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_constant__ Batch b) {
+    constexpr int EB = mode_in(MODE), OB = mode_out(MODE);  // packed-value / dense-element bytes
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t sbase = smem_u32(smem);
     const uint32_t full0 = sbase, empty0 = sbase + 8 * kStages;
@@ -326,9 +388,11 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
                     }
                 }
                 const uint32_t vbase = stg + Stage<EB>::kVals + off + rel * EB;
-                uint8_t* out = T.dst + (t0 + wfirst) * EB;
-                if (valid == kSubElems) expand_subtile<EB, true>(word, excl, vbase, out, valid, lane);
-                else expand_subtile<EB, false>(word, excl, vbase, out, valid, lane);
+                uint8_t* out = T.dst + (t0 + wfirst) * OB;
+                if (valid == kSubElems)
+                    expand_subtile<MODE, true>(word, excl, vbase, out, valid, lane, T.scale, T.deq_fast);
+                else
+                    expand_subtile<MODE, false>(word, excl, vbase, out, valid, lane, T.scale, T.deq_fast);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(empty0 + 8 * s);
@@ -339,8 +403,9 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
 // ---------------------------------------------------------------------------
 // fallback: one CTA per tile, plain loads (partial ranges / unaligned bitmaps)
 // ---------------------------------------------------------------------------
-template <int EB>
+template <int MODE>
 __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandArgs a) {
+    constexpr int EB = mode_in(MODE), OB = mode_out(MODE);  // packed-value / dense-element bytes
     __shared__ uint32_t s_warp[kExpandThreads / 32];
     __shared__ __align__(16) uint8_t s_vals[kTileElems * EB + 64];
 
@@ -401,45 +466,49 @@ __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandArgs a) {
     if (wfirst < count) {
         const uint32_t off = uint32_t(wstart - astart);
         const uint32_t vb = smem_u32(s_vals) + off + (wexcl * EB);
-        expand_subtile<EB, false>(wv, incl - pc, vb, a.dst + (t0 + wfirst) * EB,
-                                  min(count - wfirst, kSubElems), lane);
+        expand_subtile<MODE, false>(wv, incl - pc, vb, a.dst + (t0 + wfirst) * OB,
+                                  min(count - wfirst, kSubElems), lane, a.scale, a.deq_fast != 0);
     }
 }
 
 // ---------------------------------------------------------------------------
-cudaError_t launch_expand(const ExpandArgs& a, int eb, cudaStream_t s) {
+cudaError_t launch_expand(const ExpandArgs& a, int mode, cudaStream_t s) {
     const uint64_t ntiles = ceil_div(a.e1 - a.e0, kTileElems);
     if (ntiles == 0) return cudaSuccess;
-    if (eb == 2) expand_kernel<2><<<unsigned(ntiles), kExpandThreads, 0, s>>>(a);
-    else expand_kernel<1><<<unsigned(ntiles), kExpandThreads, 0, s>>>(a);
+    if (mode == kModeF16) expand_kernel<kModeF16><<<unsigned(ntiles), kExpandThreads, 0, s>>>(a);
+    else if (mode == kModeI8) expand_kernel<kModeI8><<<unsigned(ntiles), kExpandThreads, 0, s>>>(a);
+    else expand_kernel<kModeDequant><<<unsigned(ntiles), kExpandThreads, 0, s>>>(a);
     return cudaGetLastError();
 }
 
-template <int EB>
-static cudaError_t launch_tma_eb(const Batch& b, cudaStream_t s) {
+template <int MODE>
+static cudaError_t launch_tma_mode(const Batch& b, cudaStream_t s) {
     static int blocks_per_sm = 0, sms = 0;
-    constexpr uint32_t smem = tma_smem_bytes<EB>();
+    constexpr uint32_t smem = tma_smem_bytes<mode_in(MODE)>();
     if (!blocks_per_sm) {
-        cudaError_t e = cudaFuncSetAttribute(expand_tma_kernel<EB>,
+        cudaError_t e = cudaFuncSetAttribute(expand_tma_kernel<MODE>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, expand_tma_kernel<EB>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, expand_tma_kernel<MODE>,
                                                       kTmaThreads, smem);
         if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
     const uint64_t grid = umin64(b.ntiles, uint64_t(blocks_per_sm) * sms);
     if (grid == 0) return cudaSuccess;
-    expand_tma_kernel<EB><<<unsigned(grid), kTmaThreads, smem, s>>>(b);
+    expand_tma_kernel<MODE><<<unsigned(grid), kTmaThreads, smem, s>>>(b);
     return cudaGetLastError();
 }
 
 // Whole-tensor expand of a batch through the TMA ring (needs count_kernel's
 // offsets in the same workspace; 16-byte aligned bitmaps and outputs).
-cudaError_t launch_expand_tma(const Batch& b, int eb, cudaStream_t s) {
-    return eb == 2 ? launch_tma_eb<2>(b, s) : launch_tma_eb<1>(b, s);
+// mode: 1 = i8, 2 = f16 (== elem_bytes), 3 = i8 values dequantized to f16.
+cudaError_t launch_expand_tma(const Batch& b, int mode, cudaStream_t s) {
+    if (mode == kModeF16) return launch_tma_mode<kModeF16>(b, s);
+    if (mode == kModeI8) return launch_tma_mode<kModeI8>(b, s);
+    return launch_tma_mode<kModeDequant>(b, s);
 }
 
 }  // namespace endor_b200

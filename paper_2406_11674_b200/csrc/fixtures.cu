@@ -22,36 +22,6 @@
 
 namespace endor_b200 {
 
-// ---- f16 bit math, float16.hpp:35-73 (device restatement) -------------------
-__device__ __forceinline__ uint16_t f32_to_f16_bits(float f) {
-    const uint32_t x = __float_as_uint(f);
-    const uint16_t sign = uint16_t((x >> 16) & 0x8000u);
-    const uint32_t mag = x & 0x7FFFFFFFu;
-    if (mag >= 0x7F800000u) {
-        if (mag == 0x7F800000u) return uint16_t(sign | 0x7C00u);
-        uint16_t payload = uint16_t((mag >> 13) & 0x3FFu);
-        if (payload == 0) payload = 0x200u;
-        return uint16_t(sign | 0x7C00u | payload);
-    }
-    if (mag >= 0x477FF000u) return uint16_t(sign | 0x7C00u);
-    const uint32_t exp = mag >> 23;
-    if (exp >= 0x71u) {
-        const uint32_t mant = mag & 0x7FFFFFu;
-        uint32_t half = ((exp - 0x70u) << 10) | (mant >> 13);
-        const uint32_t rem = mant & 0x1FFFu;
-        half += (rem > 0x1000u) || (rem == 0x1000u && (half & 1u));
-        return uint16_t(sign | half);
-    }
-    const uint32_t m24 = (mag & 0x7FFFFFu) | 0x800000u;
-    const uint32_t shift = 126u - exp;
-    if (shift > 24u) return sign;
-    uint32_t m = m24 >> shift;
-    const uint32_t rem = m24 & ((1u << shift) - 1u);
-    const uint32_t halfway = 1u << (shift - 1);
-    m += (rem > halfway) || (rem == halfway && (m & 1u));
-    return uint16_t(sign | m);
-}
-
 __device__ __forceinline__ uint64_t splitmix_at(uint64_t seed, uint64_t k) {
     uint64_t z = seed + k * 0x9E3779B97F4A7C15ull;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;

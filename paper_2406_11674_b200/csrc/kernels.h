@@ -39,6 +39,8 @@ struct ExpandArgs {
     const unsigned long long* blk;      // count-CTA bases, total at [nblk] (TMA kernel)
     uint8_t* dst;  // base of the full dense matrix
     WsHeader* hdr;
+    float scale;        // dequant mode only (see BatchTensor)
+    uint32_t deq_fast;
 };
 
 // ---- the hot path: a batch of whole tensors (one layer's ops) -----------------
@@ -60,6 +62,8 @@ struct BatchTensor {
     // (absolute offsets, idx[k] = rank(1024 k)); when set, no count pass runs
     // and tsub/blk are unused for this tensor.
     const unsigned long long* idx;
+    float scale;            // dequant mode: f16 = f32_to_f16(float(q) * scale)
+    uint32_t deq_fast;      // dequant mode: scale finite with its sign bit clear
 };
 struct Batch {
     BatchTensor t[kMaxBatch];
@@ -85,10 +89,10 @@ __host__ __device__ inline int batch_tensor_of_cblk(const Batch& b, uint32_t g) 
 // (ws_layout_caps capacities).
 void batch_plan(Batch& b, uint64_t* sub_total, uint64_t* blk_total, int count_ctas);
 cudaError_t launch_count(const Batch& b, cudaStream_t s);
-cudaError_t launch_expand_tma(const Batch& b, int eb, cudaStream_t s);
+cudaError_t launch_expand_tma(const Batch& b, int mode, cudaStream_t s);  // mode 1 i8, 2 f16, 3 dequant
 
 cudaError_t launch_scan(const ScanArgs& a, cudaStream_t s);
-cudaError_t launch_expand(const ExpandArgs& a, int eb, cudaStream_t s);
+cudaError_t launch_expand(const ExpandArgs& a, int mode, cudaStream_t s);  // mode 1 i8, 2 f16, 3 dequant
 cudaError_t launch_synth(uint64_t i0, uint64_t count, int eb, uint64_t seed, void* out,
                          cudaStream_t s);
 cudaError_t launch_prune(uint8_t* w, uint64_t n, int eb, uint64_t target, const WsLayout& L,

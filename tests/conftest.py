@@ -35,6 +35,11 @@ def acceptance_cases():
 
 
 @pytest.fixture(scope="session")
+def quant_cases():
+    return load_golden("quant.json")
+
+
+@pytest.fixture(scope="session")
 def large_cases():
     p = os.path.join(GOLDEN, "large.json")
     if not os.path.exists(p):

@@ -198,6 +198,29 @@ def make_acceptance():
     return out
 
 
+def make_quant():
+    """quantize_values + decompress(dequantize_values(t)) (codec.hpp:306-349),
+    produced by the reference on seeded f16 tensors."""
+    out = []
+    g = O.MT64(99)
+    for it in range(40):
+        rows, cols = 1 + g() % 70, 1 + g() % 70
+        zeros = (g() % 101) / 100.0
+        seed = g()
+        w = ref_random_dense(rows, cols, 2, seed, zeros)
+        bm, vals, nnz, _ = ref_compress(w, rows, cols, 2)
+        q = np.zeros(max(nnz, 1), np.uint8)
+        scale = R().ref_quantize_values(rows, cols, bm if len(bm) else np.zeros(1, np.uint8),
+                                        vals if nnz else np.zeros(1, np.uint8), nnz, q)
+        dense = np.zeros(max(rows * cols * 2, 1), np.uint8)
+        assert R().ref_decompress_dequant(rows, cols, bm if len(bm) else np.zeros(1, np.uint8), q, nnz,
+                                          scale, dense) == 0
+        out.append(dict(rows=rows, cols=cols, seed=int(seed), zero_fraction=zeros, nnz=nnz,
+                        scale_bits=int(np.float32(scale).view(np.uint32)), crc_q=crc(q[:nnz]),
+                        crc_dense=crc(dense[: rows * cols * 2])))
+    return out
+
+
 def _large_one(args):
     name, rows, cols, seed, s = args
     n = rows * cols
@@ -236,6 +259,8 @@ def main():
         json.dump(make_seeded(), f)
     with open(os.path.join(HERE, "acceptance_1000.json"), "w") as f:
         json.dump(make_acceptance(), f)
+    with open(os.path.join(HERE, "quant.json"), "w") as f:
+        json.dump(make_quant(), f)
     if not skip_large:
         with open(os.path.join(HERE, "large.json"), "w") as f:
             json.dump(make_large(), f, indent=1)

@@ -140,6 +140,17 @@ def test_acceptance_1000(acceptance_cases):
         assert crc(O.rank_index(bm, rows * cols, chunk)[1].astype("<u8")) == g["crc_prefix"]
 
 
+def test_quantize_dequant_oracle_matches_golden(quant_cases):
+    """quantize_values / dequantize_values + decompress (codec.hpp:306-349)."""
+    for c in quant_cases:
+        w = O.random_dense(c["rows"], c["cols"], 2, c["seed"], c["zero_fraction"])
+        bm, vals, nnz, _ = O.compress(w, c["rows"], c["cols"], 2)
+        q, scale = O.quantize_values(vals, nnz)
+        assert np.float32(scale).view(np.uint32) == c["scale_bits"] and crc(q) == c["crc_q"]
+        st, dense = O.decompress_dequant(c["rows"], c["cols"], bm, q, nnz, scale)
+        assert st == 0 and crc(dense) == c["crc_dense"]
+
+
 def test_multithreaded_op_generator_matches_golden(large_cases):
     L = O.lib()
     L.or_make_op_mt.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_double, C.c_int, O._u8p, O._u8p]
