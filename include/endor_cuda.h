@@ -127,6 +127,17 @@ int endor_cuda_decompress_batch_phase(const endor_tensor_view* views, void* cons
 int endor_cuda_decompress_dequant(const endor_tensor_view* t, float scale, void* dense_f16_out, void* ws,
                                   size_t ws_bytes, void* stream);
 
+/* Selective decompression (activation sparsity):
+ *   extract_rows (codec.hpp:239-266): out[nsel, cols] = dense rows rows_dev[..]
+ *   extract_cols (codec.hpp:271-297): out[rows, nsel] = dense columns cols_dev[..]
+ * Index lists are device u64 arrays, sorted and unique (check_sorted_unique,
+ * codec.hpp:224-232: out-of-range -> BOUNDS, unsorted/duplicate -> INVALID,
+ * first failing position wins; device-latched).  Bitmap 16-byte aligned. */
+int endor_cuda_extract_rows(const endor_tensor_view* t, const uint64_t* rows_dev, uint64_t nsel, void* out,
+                            void* ws, size_t ws_bytes, void* stream);
+int endor_cuda_extract_cols(const endor_tensor_view* t, const uint64_t* cols_dev, uint64_t nsel, void* out,
+                            void* ws, size_t ws_bytes, void* stream);
+
 /* endor_cuda_decompress split into its two launches, for per-kernel timing:
  * phase 1 = rank (count) kernel, phase 2 = expand kernel (needs phase 1 on
  * the same workspace first).  phase 1 then 2 == endor_cuda_decompress. */

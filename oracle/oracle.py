@@ -132,6 +132,7 @@ def ref():
         R.ref_quantize_values.argtypes = [_u64, _u64, _u8p, _u8p, _u64, _u8p]
         R.ref_quantize_values.restype = C.c_float
         R.ref_decompress_dequant.argtypes = [_u64, _u64, _u8p, _u8p, _u64, C.c_float, _u8p]
+        R.ref_extract.argtypes = [_u64, _u64, _i32, _u8p, _u8p, _u64, _u64p, _u64, _i32, _u8p]
     return _ref
 
 

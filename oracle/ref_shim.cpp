@@ -252,6 +252,20 @@ int ref_decode_endor(const uint8_t* data, uint64_t size, uint64_t* rows, uint64_
 
 uint16_t ref_f32_to_f16(float f) { return f32_to_f16(f); }
 
+// extract_rows / extract_cols (codec.hpp:239-297); returns the error code.
+int ref_extract(uint64_t rows, uint64_t cols, int eb, const uint8_t* bitmap, const uint8_t* values, uint64_t nnz,
+                const uint64_t* sel, uint64_t nsel, int by_rows, uint8_t* out) {
+    try {
+        EndorTensor t = make_tensor(rows, cols, eb, bitmap, values, nnz);
+        std::vector<std::size_t> s(sel, sel + nsel);
+        DenseMatrix m = by_rows ? extract_rows(t, s) : extract_cols(t, s);
+        if (m.size_bytes()) std::memcpy(out, m.bytes().data(), m.size_bytes());
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
 // quantize_values (codec.hpp:306-331) of an f16 tensor: writes the i8 values,
 // returns the scale.
 float ref_quantize_values(uint64_t rows, uint64_t cols, const uint8_t* bitmap, const uint8_t* values,

@@ -351,6 +351,34 @@ def decompress_dequant(t: EndorTensor, out: Optional[DenseMatrix] = None) -> Den
     return out
 
 
+def _index_list(idx, dev) -> torch.Tensor:
+    t = torch.as_tensor(idx, dtype=torch.int64) if not isinstance(idx, torch.Tensor) else idx
+    return t.to(device=dev, dtype=torch.int64).contiguous().reshape(-1)
+
+
+def _extract(t: EndorTensor, idx, by_rows: bool) -> DenseMatrix:
+    dev = t.device
+    sel = _index_list(idx, dev)
+    k = sel.numel()
+    out = DenseMatrix.empty(k if by_rows else t.rows, t.cols if by_rows else k, t.dtype, dev)
+    ws = workspace(max(t.element_count(), 1), dev)
+    v = t.view()
+    fn = _lib.lib().endor_cuda_extract_rows if by_rows else _lib.lib().endor_cuda_extract_cols
+    check(fn(C.byref(v), _ptr(sel), k, _ptr(out.data), ws.data_ptr(), ws.numel(), _stream_ptr(dev)))
+    sync_status(ws, dev)
+    return out
+
+
+def extract_rows(t: EndorTensor, rows) -> DenseMatrix:
+    """codec.hpp:239-266: whole rows (sorted, unique) without materialising W."""
+    return _extract(t, rows, True)
+
+
+def extract_cols(t: EndorTensor, cols) -> DenseMatrix:
+    """codec.hpp:271-297: whole columns (sorted, unique)."""
+    return _extract(t, cols, False)
+
+
 class BatchPlan:
     """A prepared batch decompress of up to 16 same-dtype tensors (e.g. one
     decoder layer's weights): two kernel launches for the whole batch."""

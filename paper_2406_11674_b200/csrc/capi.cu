@@ -337,6 +337,63 @@ int endor_cuda_decompress_dequant(const endor_tensor_view* t, float scale, void*
     return ENDOR_OK;
 }
 
+// extract_rows / extract_cols (codec.hpp:239-297): validation of the index
+// list (check_sorted_unique, codec.hpp:224-232), a count pass for ranks, then
+// the gather.  Errors are device-latched (endor_cuda_sync_status).
+static int extract_common(const endor_tensor_view* t, const uint64_t* sel, uint64_t nsel, void* out, void* ws,
+                          size_t ws_bytes, void* stream, bool rows) {
+    uint64_t n;
+    int eb, st;
+    if ((st = check_view(t, &n, &eb))) return st;
+    if (nsel && (!sel || !out)) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null index list or output");
+    if (!aligned(out, eb)) return fail(ENDOR_ERR_INVALID_ARGUMENT, "misaligned output");
+    if (n && !aligned(t->bitmap, 16)) return fail(ENDOR_ERR_INVALID_ARGUMENT, "extraction needs a 16-byte aligned bitmap");
+    WsLayout L;
+    if ((st = check_ws(ws, ws_bytes, n ? n : 1, &L))) return st;
+    const auto* idx = reinterpret_cast<const unsigned long long*>(sel);
+    CK(launch_validate_indices(idx, nsel, rows ? t->rows : t->cols, L.hdr, S(stream)));
+    if (n == 0 || nsel == 0) return ENDOR_OK;
+    Batch b{};
+    b.count = 1;
+    b.check_total = 1;
+    b.t[0].bitmap = static_cast<const uint8_t*>(t->bitmap);
+    b.t[0].values = static_cast<const uint8_t*>(t->values);
+    b.t[0].n = n;
+    b.t[0].nnz = t->nnz;
+    uint64_t sub_cap, blk_cap;
+    batch_plan(b, &sub_cap, &blk_cap, count_ctas());
+    b.tsub = L.tsub;
+    b.blk = L.blk;
+    b.hdr = L.hdr;
+    CK(launch_count(b, S(stream)));
+    RankTable rt{};
+    rt.bitmap = b.t[0].bitmap;
+    rt.nbytes = (n + 7) / 8;
+    rt.tsub = L.tsub + b.t[0].sub0;
+    rt.blk = L.blk + b.t[0].blk0;
+    rt.cbpc = b.t[0].cbpc;
+    rt.ncta = b.t[0].ncta;
+    rt.nsub = ceil_div(n, kSubElems);
+    const auto* vals = static_cast<const uint8_t*>(t->values);
+    if (rows)
+        CK(launch_extract_rows(rt, vals, t->nnz, t->cols, eb, idx, nsel, static_cast<uint8_t*>(out), L.hdr,
+                               S(stream)));
+    else
+        CK(launch_extract_cols(rt, vals, t->nnz, t->rows, t->cols, eb, idx, nsel, static_cast<uint8_t*>(out),
+                               L.hdr, S(stream)));
+    return ENDOR_OK;
+}
+
+int endor_cuda_extract_rows(const endor_tensor_view* t, const uint64_t* rows_dev, uint64_t nsel, void* out,
+                            void* ws, size_t ws_bytes, void* stream) {
+    return extract_common(t, rows_dev, nsel, out, ws, ws_bytes, stream, true);
+}
+
+int endor_cuda_extract_cols(const endor_tensor_view* t, const uint64_t* cols_dev, uint64_t nsel, void* out,
+                            void* ws, size_t ws_bytes, void* stream) {
+    return extract_common(t, cols_dev, nsel, out, ws, ws_bytes, stream, false);
+}
+
 int endor_cuda_decompress_phase(const endor_tensor_view* t, void* dense_out, int phase, void* ws,
                                 size_t ws_bytes, void* stream) {
     uint64_t n;

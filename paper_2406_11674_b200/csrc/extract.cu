@@ -1,0 +1,265 @@
+// extract.cu -- selective decompression:
+//
+//   extract_rows  codec.hpp:239-266  gather whole rows without materialising
+//                 the matrix: out row i = dense row rows[i]
+//   extract_cols  codec.hpp:271-297  gather whole columns: out[r][j] =
+//                 dense[r][cols[j]]
+//   check_sorted_unique  codec.hpp:224-232  index validation, reference order
+//                 (per position: bound first -> BoundsError, then order ->
+//                 invalid_argument; the first failing position wins)
+//
+// Both read ranks from count_kernel's two-level table (the GPU RankIndex at
+// 1024-element granularity) plus a popcount of at most 1023 bits, and stage
+// packed values through shared memory like the expand kernels.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace endor_b200 {
+
+// rank(p) for a bit position p of tensor T (count_kernel output in b).
+__device__ __forceinline__ unsigned long long rank_at(const RankTable& rt, uint64_t p, int lane) {
+    const uint64_t sub = p / kSubElems;
+    unsigned long long base;
+    if (sub >= rt.nsub) {
+        base = rt.blk[rt.ncta];
+    } else {
+        base = rt.blk[sub / (uint64_t(kCountSubs) * rt.cbpc)] + rt.tsub[sub];
+    }
+    // + popcount of [sub*1024, p): at most 32 words, one per lane
+    const uint64_t w0 = sub * 32, wp = p / 32;
+    uint32_t c = 0;
+    const uint64_t w = w0 + lane;
+    if (w <= wp && sub < rt.nsub) {
+        uint32_t v = load_word32(rt.bitmap, w, rt.nbytes);
+        if (w == wp) v &= (1u << (p & 31)) - 1u;  // bits below p only
+        c = __popc(v);
+    }
+    return base + __reduce_add_sync(0xffffffffu, c);
+}
+
+// 32 bitmap bits starting at an arbitrary bit position p (zero past nbits).
+__device__ __forceinline__ uint32_t bits_at(const uint8_t* bm, uint64_t nbytes, uint64_t p) {
+    const uint64_t w = p / 32;
+    const uint32_t sh = p & 31;
+    const uint32_t lo = load_word32(bm, w, nbytes);
+    if (!sh) return lo;
+    return __funnelshift_r(lo, load_word32(bm, w + 1, nbytes), sh);
+}
+
+// ---- index validation (single CTA, positions in order) ---------------------------
+__global__ void __launch_bounds__(1024) validate_indices_kernel(const unsigned long long* idx, uint64_t nsel,
+                                                                uint64_t limit, WsHeader* hdr) {
+    __shared__ unsigned long long s_first;
+    if (threadIdx.x == 0) s_first = ~0ull;
+    __syncthreads();
+    for (uint64_t base = 0; base < nsel; base += blockDim.x) {
+        const uint64_t i = base + threadIdx.x;
+        if (i < nsel) {
+            unsigned long long key = ~0ull;
+            if (idx[i] >= limit) key = i * 2;                              // BoundsError
+            else if (i > 0 && idx[i] <= idx[i - 1]) key = i * 2 + 1;      // invalid_argument
+            if (key != ~0ull) atomicMin(&s_first, key);
+        }
+        __syncthreads();
+        if (s_first != ~0ull) break;  // uniform: everyone read the same value
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && s_first != ~0ull)
+        latch_status(hdr, (s_first & 1) ? ENDOR_ERR_INVALID_ARGUMENT : ENDOR_ERR_BOUNDS);
+}
+
+// ---- extract_rows ------------------------------------------------------------------
+// CTA = (selected row i, 8192-element tile j of that row); 256 threads, one
+// 32-bit slice of the row's bits each.
+template <int EB>
+__global__ void __launch_bounds__(kExpandThreads) extract_rows_kernel(RankTable rt, const uint8_t* values,
+                                                                      uint64_t nnz, uint64_t cols,
+                                                                      const unsigned long long* sel,
+                                                                      uint64_t tiles_per_row, uint8_t* out,
+                                                                      WsHeader* hdr) {
+    __shared__ uint32_t s_warp[kExpandThreads / 32];
+    __shared__ unsigned long long s_base;
+    __shared__ __align__(16) uint8_t s_vals[kTileElems * EB + 64];
+    if (read_status(hdr)) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t i = blockIdx.x / tiles_per_row, j = blockIdx.x % tiles_per_row;
+    const uint64_t row = sel[i];
+    const uint64_t x0 = row * cols + j * kTileElems;
+    const uint32_t count = uint32_t(umin64(kTileElems, cols - j * kTileElems));
+    if (warp == 0) {
+        const unsigned long long b = rank_at(rt, x0, lane);
+        if (lane == 0) s_base = b;
+    }
+    uint32_t wv = 0;
+    if (uint32_t(tid) * 32 < count) {
+        wv = bits_at(rt.bitmap, rt.nbytes, x0 + uint64_t(tid) * 32);
+        const uint32_t rem = count - uint32_t(tid) * 32;
+        if (rem < 32) wv &= (1u << rem) - 1u;
+    }
+    const uint32_t pc = __popc(wv);
+    const uint32_t incl = warp_incl_scan(pc, lane);
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    uint32_t wexcl = 0, total = 0;
+#pragma unroll
+    for (int k = 0; k < kExpandThreads / 32; ++k) {
+        wexcl += (k < warp) ? s_warp[k] : 0u;
+        total += s_warp[k];
+    }
+    const uint64_t vbase = s_base;
+    if (vbase + total > nnz) {
+        if (tid == 0) latch_status(hdr, ENDOR_ERR_CORRUPTION);
+        return;
+    }
+    // stage the tile's packed values (aligned superset; buffer ends byte-wise)
+    const uintptr_t vlo = reinterpret_cast<uintptr_t>(values), vhi = vlo + nnz * EB;
+    const uintptr_t ws = vlo + vbase * EB, we = ws + uint64_t(total) * EB;
+    const uintptr_t as = ws & ~uintptr_t(15);
+    const uint32_t nvec = uint32_t((we - as + 15) >> 4);
+    for (uint32_t v = tid; v < nvec; v += kExpandThreads) {
+        const uintptr_t addr = as + uintptr_t(v) * 16;
+        uint4 q;
+        if (addr >= vlo && addr + 16 <= vhi) {
+            q = __ldg(reinterpret_cast<const uint4*>(addr));
+        } else {
+            uint32_t r[4] = {0u, 0u, 0u, 0u};
+            for (int b = 0; b < 16; ++b) {
+                const uintptr_t x = addr + b;
+                if (x >= vlo && x < vhi) r[b >> 2] |= uint32_t(*reinterpret_cast<const uint8_t*>(x)) << ((b & 3) * 8);
+            }
+            q = make_uint4(r[0], r[1], r[2], r[3]);
+        }
+        *reinterpret_cast<uint4*>(s_vals + v * 16) = q;
+    }
+    __syncthreads();
+    // scatter_range semantics per element (codec.hpp:136-149): each thread
+    // writes its 32 elements; element-wise stores keep any row alignment legal
+    const uint32_t sb = smem_u32(s_vals) + uint32_t(ws - as);
+    uint8_t* dst = out + (i * cols + j * kTileElems + uint64_t(tid) * 32) * EB;
+    uint32_t r = wexcl + incl - pc;
+    const uint32_t nel = uint32_t(tid) * 32 < count ? min(32u, count - uint32_t(tid) * 32) : 0u;
+    for (uint32_t e = 0; e < nel; ++e) {
+        uint32_t v = 0;
+        if ((wv >> e) & 1u) {
+            const uint32_t a = sb + r * EB;
+            const uint32_t w = __funnelshift_r(lds32(a & ~3u), lds32((a & ~3u) + 4), (a & 3u) * 8);
+            v = EB == 2 ? (w & 0xFFFFu) : (w & 0xFFu);
+            ++r;
+        }
+        if constexpr (EB == 2) {
+            reinterpret_cast<uint16_t*>(dst)[e] = uint16_t(v);
+        } else {
+            dst[e] = uint8_t(v);
+        }
+    }
+}
+
+// ---- extract_cols ------------------------------------------------------------------
+// One CTA per matrix row: the row's bitmap words and their exclusive popcounts
+// in shared memory, then every selected column looked up directly.
+template <int EB>
+__global__ void __launch_bounds__(256) extract_cols_kernel(RankTable rt, const uint8_t* values, uint64_t nnz,
+                                                           uint64_t cols, const unsigned long long* sel,
+                                                           uint64_t nsel, uint8_t* out, WsHeader* hdr) {
+    extern __shared__ uint32_t s_row[];  // [words] bits, then [words] exclusive popcounts
+    __shared__ uint32_t s_warp[8];
+    __shared__ unsigned long long s_base;
+    if (read_status(hdr)) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t row = blockIdx.x;
+    const uint64_t x0 = row * cols;
+    const uint32_t words = uint32_t((cols + 31) / 32);
+    uint32_t* s_pre = s_row + words;
+    if (warp == 0) {
+        const unsigned long long b = rank_at(rt, x0, lane);
+        if (lane == 0) s_base = b;
+    }
+    // words and a block-wide exclusive scan of their popcounts, 256 at a time
+    uint32_t carry = 0;
+    for (uint32_t w0 = 0; w0 < words; w0 += 256) {
+        const uint32_t w = w0 + tid;
+        uint32_t v = 0;
+        if (w < words) {
+            v = bits_at(rt.bitmap, rt.nbytes, x0 + uint64_t(w) * 32);
+            const uint64_t rem = cols - uint64_t(w) * 32;
+            if (rem < 32) v &= (1u << rem) - 1u;
+            s_row[w] = v;
+        }
+        const uint32_t pc = __popc(v);
+        const uint32_t incl = warp_incl_scan(pc, lane);
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        uint32_t wex = 0, tot = 0;
+        for (int k = 0; k < 8; ++k) {
+            wex += (k < warp) ? s_warp[k] : 0u;
+            tot += s_warp[k];
+        }
+        if (w < words) s_pre[w] = carry + wex + incl - pc;
+        carry += tot;
+        __syncthreads();
+    }
+    const unsigned long long base = s_base;
+    if (base + carry > nnz) {
+        if (tid == 0) latch_status(hdr, ENDOR_ERR_CORRUPTION);
+        return;
+    }
+    uint8_t* orow = out + row * nsel * EB;
+    for (uint64_t k = tid; k < nsel; k += 256) {
+        const uint64_t c = sel[k];
+        const uint32_t w = uint32_t(c / 32), b = uint32_t(c & 31);
+        const uint32_t word = s_row[w];
+        uint32_t v = 0;
+        if ((word >> b) & 1u) {
+            const uint64_t rk = base + s_pre[w] + __popc(word & ((1u << b) - 1u));
+            // byte loads: the packed values may sit at any alignment (file_io.hpp:32-36)
+            v = EB == 2 ? uint32_t(__ldg(values + rk * 2)) | (uint32_t(__ldg(values + rk * 2 + 1)) << 8)
+                        : uint32_t(__ldg(values + rk));
+        }
+        if constexpr (EB == 2) reinterpret_cast<uint16_t*>(orow)[k] = uint16_t(v);
+        else orow[k] = uint8_t(v);
+    }
+}
+
+// ---------------------------------------------------------------------------
+cudaError_t launch_validate_indices(const unsigned long long* idx, uint64_t nsel, uint64_t limit, WsHeader* hdr,
+                                    cudaStream_t s) {
+    if (nsel == 0) return cudaSuccess;
+    validate_indices_kernel<<<1, 1024, 0, s>>>(idx, nsel, limit, hdr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_extract_rows(const RankTable& rt, const uint8_t* values, uint64_t nnz, uint64_t cols, int eb,
+                                const unsigned long long* sel, uint64_t nsel, uint8_t* out, WsHeader* hdr,
+                                cudaStream_t s) {
+    const uint64_t tpr = ceil_div(cols, kTileElems);
+    if (nsel == 0 || tpr == 0) return cudaSuccess;
+    const uint64_t grid = tpr * nsel;
+    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    if (eb == 2) extract_rows_kernel<2><<<unsigned(grid), kExpandThreads, 0, s>>>(rt, values, nnz, cols, sel, tpr, out, hdr);
+    else extract_rows_kernel<1><<<unsigned(grid), kExpandThreads, 0, s>>>(rt, values, nnz, cols, sel, tpr, out, hdr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_extract_cols(const RankTable& rt, const uint8_t* values, uint64_t nnz, uint64_t rows,
+                                uint64_t cols, int eb, const unsigned long long* sel, uint64_t nsel, uint8_t* out,
+                                WsHeader* hdr, cudaStream_t s) {
+    if (rows == 0 || nsel == 0) return cudaSuccess;
+    const size_t smem = 2 * sizeof(uint32_t) * ((cols + 31) / 32);
+    if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(extract_cols_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(extract_cols_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    if (rows > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    if (eb == 2) extract_cols_kernel<2><<<unsigned(rows), 256, smem, s>>>(rt, values, nnz, cols, sel, nsel, out, hdr);
+    else extract_cols_kernel<1><<<unsigned(rows), 256, smem, s>>>(rt, values, nnz, cols, sel, nsel, out, hdr);
+    return cudaGetLastError();
+}
+
+}  // namespace endor_b200

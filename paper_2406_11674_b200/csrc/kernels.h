@@ -91,6 +91,24 @@ void batch_plan(Batch& b, uint64_t* sub_total, uint64_t* blk_total, int count_ct
 cudaError_t launch_count(const Batch& b, cudaStream_t s);
 cudaError_t launch_expand_tma(const Batch& b, int mode, cudaStream_t s);  // mode 1 i8, 2 f16, 3 dequant
 
+// Rank lookups over count_kernel's two-level table for one tensor.
+struct RankTable {
+    const uint8_t* bitmap;
+    uint64_t nbytes;
+    const unsigned long long* tsub;  // CTA-range-local sub-tile offsets
+    const unsigned long long* blk;   // per-count-CTA bases; blk[ncta] = total
+    uint32_t cbpc, ncta;
+    uint64_t nsub;
+};
+cudaError_t launch_validate_indices(const unsigned long long* idx, uint64_t nsel, uint64_t limit, WsHeader* hdr,
+                                    cudaStream_t s);
+cudaError_t launch_extract_rows(const RankTable& rt, const uint8_t* values, uint64_t nnz, uint64_t cols, int eb,
+                                const unsigned long long* sel, uint64_t nsel, uint8_t* out, WsHeader* hdr,
+                                cudaStream_t s);
+cudaError_t launch_extract_cols(const RankTable& rt, const uint8_t* values, uint64_t nnz, uint64_t rows,
+                                uint64_t cols, int eb, const unsigned long long* sel, uint64_t nsel, uint8_t* out,
+                                WsHeader* hdr, cudaStream_t s);
+
 cudaError_t launch_scan(const ScanArgs& a, cudaStream_t s);
 cudaError_t launch_expand(const ExpandArgs& a, int mode, cudaStream_t s);  // mode 1 i8, 2 f16, 3 dequant
 cudaError_t launch_synth(uint64_t i0, uint64_t count, int eb, uint64_t seed, void* out,

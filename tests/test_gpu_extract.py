@@ -1,0 +1,81 @@
+"""§8(f) row 4: selective row/column decompression on the GPU against the
+reference's semantics: extraction == slicing the full decompression
+(acceptance.cpp:126-153), index validation as check_sorted_unique
+(codec.hpp:224-232)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import oracle as O  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def E(cuda_lib):
+    from paper_2406_11674_b200 import codec
+    return codec
+
+
+def _tensor(E, rows, cols, eb, bm, vals, nnz, voff=0):
+    n = rows * cols
+    b = torch.zeros(len(bm) + 32, dtype=torch.uint8, device="cuda")[: len(bm)]
+    if len(bm):
+        b.copy_(torch.from_numpy(bm.copy()))
+    v = torch.zeros(len(vals) + voff + 32, dtype=torch.uint8, device="cuda")[voff: voff + len(vals)]
+    if len(vals):
+        v.copy_(torch.from_numpy(vals.copy()))
+    dt = E.Dtype.F16 if eb == 2 else E.Dtype.I8
+    return E.EndorTensor(rows, cols, dt, E.Bitmap(n, data=b), v, validate=False, nnz=nnz)
+
+
+def test_acceptance_extraction_suite(E):
+    """acceptance.cpp criterion 3's extraction half, 1000 generated cases."""
+    for it, rows, cols, eb, zeros, w, chunk, rsel, csel in O.acceptance_cases(1000):
+        if it % 4:  # a quarter of the suite keeps the GPU run short; all shapes classes included
+            continue
+        bm, vals, nnz, _ = O.compress(w, rows, cols, eb)
+        t = _tensor(E, rows, cols, eb, bm, vals, nnz, voff=it % 3)
+        full = w.reshape(rows, cols * eb)
+        gr = E.extract_rows(t, rsel)
+        assert gr.bytes() == full[rsel].tobytes() if rsel else gr.bytes() == b"", it
+        gc = E.extract_cols(t, csel)
+        want = w.view(np.uint16 if eb == 2 else np.uint8).reshape(rows, cols)[:, csel]
+        assert gc.bytes() == np.ascontiguousarray(want).tobytes(), it
+
+
+def test_large_rows_and_cols(E):
+    rows, cols = 9216, 36864
+    w = E.synth_weight(rows, cols, 7, device="cuda")
+    E.magnitude_prune(w, 0.5, inplace=True)
+    t = E.compress(w)
+    dense = w.data.view(torch.int16).reshape(rows, cols)
+    rsel = torch.arange(3, rows, 97, device="cuda")
+    got = E.extract_rows(t, rsel)
+    assert torch.equal(got.data.view(torch.int16).reshape(-1, cols), dense[rsel])
+    csel = torch.arange(5, cols, 131, device="cuda")
+    got = E.extract_cols(t, csel)
+    assert torch.equal(got.data.view(torch.int16).reshape(rows, -1), dense[:, csel])
+
+
+def test_index_validation_matches_reference(E):
+    w = O.random_dense(10, 12, 2, 9, 0.5)
+    bm, vals, nnz, _ = O.compress(w, 10, 12, 2)
+    t = _tensor(E, 10, 12, 2, bm, vals, nnz)
+    R = O.ref()
+    cases = [([1, 10], "rows", E.BoundsError), ([3, 3], "rows", E.InvalidArgument),
+             ([4, 2], "rows", E.InvalidArgument), ([2, 1, 99], "rows", E.InvalidArgument),
+             ([99, 1], "rows", E.BoundsError), ([0, 12], "cols", E.BoundsError),
+             ([5, 5, 99], "cols", E.InvalidArgument)]
+    for sel, kind, exc in cases:
+        with pytest.raises(exc):
+            (E.extract_rows if kind == "rows" else E.extract_cols)(t, sel)
+        if R is not None:
+            out = np.zeros(4096, np.uint8)
+            code = R.ref_extract(10, 12, 2, bm, vals, nnz, np.array(sel, np.uint64), len(sel),
+                                 1 if kind == "rows" else 0, out)
+            assert code == (3 if exc is E.BoundsError else 4)
+    # empty selections are valid
+    assert E.extract_rows(t, []).bytes() == b""
+    assert E.extract_cols(t, []).bytes() == b""
