@@ -240,6 +240,17 @@ int endor_cuda_magnitude_prune(uint64_t n, int32_t dtype, double sparsity, void*
 int endor_cuda_gemv(uint64_t rows, uint64_t cols, const void* w_f16, const void* x_f16,
                     float* y_f32, void* y_f16, void* stream);
 
+/* Fused decompress -> GEMV: y = W x straight from the
+ * compressed W (bitmap + packed values) -- the dense W is never written, so
+ * HBM traffic is 1/8 + 2(1-s) bytes per weight instead of decompress (write
+ * 2) + GEMV (read 2).  f16 W with cols % 1024 == 0 (each 1024-element
+ * sub-tile is one row segment), x 16-byte aligned, fp32 accumulation; y_f32
+ * and/or y_f16.  prefix1024 (optional, device): the tensor's RankIndex at
+ * chunk 1024 -- when given no counting pass runs.  Deterministic: each row
+ * sums its cols/1024 sub-tile partials in order. */
+int endor_cuda_gemv_compressed(const endor_tensor_view* t, const uint64_t* prefix1024, const void* x_f16,
+                               float* y_f32, void* y_f16, void* ws, size_t ws_bytes, void* stream);
+
 /* ---- offload pipeline ---------------------------------------------------- */
 /* Streams compressed ops from pinned host memory through a double-buffered
  * device staging ring: H2D of op i+1 on the copy stream overlaps decompress

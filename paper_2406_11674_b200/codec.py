@@ -351,6 +351,28 @@ def decompress_dequant(t: EndorTensor, out: Optional[DenseMatrix] = None) -> Den
     return out
 
 
+def gemv_compressed(t: EndorTensor, x: torch.Tensor, index: Optional[RankIndex] = None,
+                    out_f32: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """y = W x straight from the compressed W (fused decompress -> GEMV, the
+    dense W is never written).  f16 W with cols % 1024 == 0; fp32 result."""
+    dev = t.device
+    if t.dtype != Dtype.F16 or x.dtype != torch.float16 or x.numel() != t.cols:
+        raise InvalidArgument("gemv_compressed needs an f16 W [rows, cols] and f16 x [cols]")
+    y = out_f32 if out_f32 is not None else torch.empty(t.rows, dtype=torch.float32, device=dev)
+    ws = workspace(t.element_count(), dev)
+    pre = None
+    if index is not None:
+        if index.chunk_size != 1024:
+            raise InvalidArgument("gemv_compressed takes a RankIndex at chunk size 1024")
+        pre = index.prefix.to(device=dev, dtype=torch.int64).contiguous()
+    xc = x.contiguous()
+    v = t.view()
+    check(_lib.lib().endor_cuda_gemv_compressed(C.byref(v), _ptr(pre), _ptr(xc), _ptr(y), None, ws.data_ptr(),
+                                                ws.numel(), _stream_ptr(dev)))
+    sync_status(ws, dev)
+    return y
+
+
 def _index_list(idx, dev) -> torch.Tensor:
     t = torch.as_tensor(idx, dtype=torch.int64) if not isinstance(idx, torch.Tensor) else idx
     return t.to(device=dev, dtype=torch.int64).contiguous().reshape(-1)

@@ -337,6 +337,45 @@ int endor_cuda_decompress_dequant(const endor_tensor_view* t, float scale, void*
     return ENDOR_OK;
 }
 
+int endor_cuda_gemv_compressed(const endor_tensor_view* t, const uint64_t* prefix1024, const void* x_f16,
+                               float* y_f32, void* y_f16, void* ws, size_t ws_bytes, void* stream) {
+    uint64_t n;
+    int eb, st;
+    if ((st = check_view(t, &n, &eb))) return st;
+    if (t->dtype != ENDOR_DTYPE_F16) return fail(ENDOR_ERR_INVALID_ARGUMENT, "fused GEMV needs an f16 tensor");
+    if (t->cols % kSubElems)
+        return fail(ENDOR_ERR_INVALID_ARGUMENT,
+                    "fused GEMV needs cols % 1024 == 0 (use endor_cuda_decompress + endor_cuda_gemv)");
+    if (t->rows == 0) return ENDOR_OK;
+    if (!x_f16 || !aligned(x_f16, 16) || (!y_f32 && !y_f16))
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "x must be 16-byte aligned f16[cols]; y must be given");
+    if (!aligned(t->bitmap, 16)) return fail(ENDOR_ERR_INVALID_ARGUMENT, "fused GEMV needs a 16-byte aligned bitmap");
+    if (prefix1024 && !aligned(prefix1024, 16)) return fail(ENDOR_ERR_INVALID_ARGUMENT, "misaligned prefix");
+    WsLayout L;
+    if ((st = check_ws(ws, ws_bytes, n, &L))) return st;
+    Batch b{};
+    b.count = 1;
+    b.check_total = 1;
+    BatchTensor& T = b.t[0];
+    T.bitmap = static_cast<const uint8_t*>(t->bitmap);
+    T.values = static_cast<const uint8_t*>(t->values);
+    T.n = n;
+    T.nnz = t->nnz;
+    T.idx = reinterpret_cast<const unsigned long long*>(prefix1024);  // optional load-time index
+    T.x = x_f16;
+    T.part = L.part;
+    T.cols = t->cols;
+    uint64_t sub_cap, blk_cap;
+    batch_plan(b, &sub_cap, &blk_cap, count_ctas());
+    b.tsub = L.tsub;
+    b.blk = L.blk;
+    b.hdr = L.hdr;
+    if (!T.idx) CK(launch_count(b, S(stream)));
+    CK(launch_expand_tma(b, 4, S(stream)));
+    CK(launch_row_reduce(L.part, t->rows, t->cols / kSubElems, y_f32, y_f16, S(stream)));
+    return ENDOR_OK;
+}
+
 // extract_rows / extract_cols (codec.hpp:239-297): validation of the index
 // list (check_sorted_unique, codec.hpp:224-232), a count pass for ranks, then
 // the gather.  Errors are device-latched (endor_cuda_sync_status).

@@ -50,6 +50,7 @@ struct WsLayout {
     unsigned long long* ties;
     unsigned long long* tsub;  // per-1024-element sub-tile value offsets
     unsigned long long* blk;   // count_kernel per-CTA bases (+ total)
+    float* part;               // fused GEMV: one fp32 partial per sub-tile
     uint64_t ntiles, nscan, nsub;
     size_t bytes;
 };
@@ -74,6 +75,8 @@ inline WsLayout ws_layout_caps(void* base, uint64_t n, uint64_t sub_cap, uint64_
     off = align256(off + 8 * sub_cap);
     L.blk = reinterpret_cast<unsigned long long*>(b + off);
     off = align256(off + 8 * blk_cap);
+    L.part = reinterpret_cast<float*>(b + off);  // fused-GEMV sub-tile partials
+    off = align256(off + 4 * sub_cap);
     L.tprefix = reinterpret_cast<unsigned long long*>(b + off);
     off = align256(off + 8 * (L.ntiles + 1));
     L.lookback = reinterpret_cast<unsigned long long*>(b + off);  // must stay zeroed between calls

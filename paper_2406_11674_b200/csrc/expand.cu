@@ -145,9 +145,46 @@ __device__ __forceinline__ uint4 gather_chunk_dequant(uint32_t m, uint32_t a, fl
 
 // Element modes of the expand kernels: bytes per packed value (IN) and per
 // dense output element (OUT).
-constexpr int kModeI8 = 1, kModeF16 = 2, kModeDequant = 3;
-__host__ __device__ constexpr int mode_in(int m) { return m == kModeF16 ? 2 : 1; }
+constexpr int kModeI8 = 1, kModeF16 = 2, kModeDequant = 3, kModeGemv = 4;
+__host__ __device__ constexpr int mode_in(int m) { return (m == kModeF16 || m == kModeGemv) ? 2 : 1; }
 __host__ __device__ constexpr int mode_out(int m) { return m == kModeI8 ? 1 : 2; }
+
+// dot of 8 f16 weights with 8 f16 activations, fp32 accumulate
+__device__ __forceinline__ float dot8_f16(const uint4& w, const uint4& x, float acc) {
+    const __half2* wh = reinterpret_cast<const __half2*>(&w);
+    const __half2* xh = reinterpret_cast<const __half2*>(&x);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 a = __half22float2(wh[i]), c = __half22float2(xh[i]);
+        acc = fmaf(a.x, c.x, acc);
+        acc = fmaf(a.y, c.y, acc);
+    }
+    return acc;
+}
+
+// Fused decompress -> GEMV over one warp's 1024-element sub-tile, which lies in
+// a single row of W (cols % 1024 == 0): the expanded weights never leave
+// registers; returns the warp's partial dot product (all lanes).
+__device__ __forceinline__ float gemv_subtile(uint32_t word, uint32_t excl, uint32_t vbase,
+                                              const uint4* __restrict__ x8, int32_t valid_elems, int lane) {
+    const uint32_t sh = (lane % 4) * 8;
+    const uint32_t low = (1u << sh) - 1u;
+    float acc = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int c = 32 * j + lane;
+        const uint32_t wd = __shfl_sync(0xffffffffu, word, c / 4);
+        const uint32_t pre = __shfl_sync(0xffffffffu, excl, c / 4);
+        if (c * 8 < valid_elems) {
+            const uint32_t m = (wd >> sh) & 0xFFu;
+            const uint4 w = gather_chunk<2>(m, vbase + (pre + __popc(wd & low)) * 2);
+            acc = dot8_f16(w, __ldg(x8 + c), acc);
+        }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+    return acc;
+}
 
 template <int MODE>
 __device__ __forceinline__ uint4 gather_mode(uint32_t m, uint32_t a, float scale, bool fast) {
@@ -388,11 +425,19 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
                     }
                 }
                 const uint32_t vbase = stg + Stage<EB>::kVals + off + rel * EB;
-                uint8_t* out = T.dst + (t0 + wfirst) * OB;
-                if (valid == kSubElems)
-                    expand_subtile<MODE, true>(word, excl, vbase, out, valid, lane, T.scale, T.deq_fast);
-                else
-                    expand_subtile<MODE, false>(word, excl, vbase, out, valid, lane, T.scale, T.deq_fast);
+                if constexpr (MODE == kModeGemv) {
+                    // the sub-tile is one row's columns [col0, col0 + 1024): dot with x there
+                    const uint64_t col0 = (t0 + wfirst) % T.cols;
+                    const float p = gemv_subtile(word, excl, vbase,
+                                                 reinterpret_cast<const uint4*>(T.x) + col0 / 8, valid, lane);
+                    if (lane == 0) T.part[(t - T.tile0) * 8 + warp] = p;
+                } else {
+                    uint8_t* out = T.dst + (t0 + wfirst) * OB;
+                    if (valid == kSubElems)
+                        expand_subtile<MODE, true>(word, excl, vbase, out, valid, lane, T.scale, T.deq_fast);
+                    else
+                        expand_subtile<MODE, false>(word, excl, vbase, out, valid, lane, T.scale, T.deq_fast);
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(empty0 + 8 * s);
@@ -508,7 +553,26 @@ static cudaError_t launch_tma_mode(const Batch& b, cudaStream_t s) {
 cudaError_t launch_expand_tma(const Batch& b, int mode, cudaStream_t s) {
     if (mode == kModeF16) return launch_tma_mode<kModeF16>(b, s);
     if (mode == kModeI8) return launch_tma_mode<kModeI8>(b, s);
+    if (mode == kModeGemv) return launch_tma_mode<kModeGemv>(b, s);
     return launch_tma_mode<kModeDequant>(b, s);
+}
+
+__global__ void __launch_bounds__(256) row_reduce_kernel(const float* __restrict__ part, uint64_t rows,
+                                                         uint64_t spr, float* y32, __half* y16) {
+    const uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    float acc = 0.f;
+    for (uint64_t k = 0; k < spr; ++k) acc += part[r * spr + k];
+    if (y32) y32[r] = acc;
+    if (y16) y16[r] = __float2half_rn(acc);
+}
+
+cudaError_t launch_row_reduce(const float* part, uint64_t rows, uint64_t subs_per_row, float* y32, void* y16,
+                              cudaStream_t s) {
+    if (rows == 0) return cudaSuccess;
+    row_reduce_kernel<<<unsigned(ceil_div(rows, 256)), 256, 0, s>>>(part, rows, subs_per_row, y32,
+                                                                     static_cast<__half*>(y16));
+    return cudaGetLastError();
 }
 
 }  // namespace endor_b200

@@ -64,6 +64,11 @@ struct BatchTensor {
     const unsigned long long* idx;
     float scale;            // dequant mode: f16 = f32_to_f16(float(q) * scale)
     uint32_t deq_fast;      // dequant mode: scale finite with its sign bit clear
+    // fused GEMV mode: y = W x with W this tensor (rows = outputs, cols % 1024 == 0);
+    // each 1024-element sub-tile's dot product lands in part[sub0 + sub]
+    const void* x;          // f16 [cols]
+    float* part;            // fp32 partials, one per sub-tile
+    uint64_t cols;
 };
 struct Batch {
     BatchTensor t[kMaxBatch];
@@ -89,7 +94,10 @@ __host__ __device__ inline int batch_tensor_of_cblk(const Batch& b, uint32_t g) 
 // (ws_layout_caps capacities).
 void batch_plan(Batch& b, uint64_t* sub_total, uint64_t* blk_total, int count_ctas);
 cudaError_t launch_count(const Batch& b, cudaStream_t s);
-cudaError_t launch_expand_tma(const Batch& b, int mode, cudaStream_t s);  // mode 1 i8, 2 f16, 3 dequant
+cudaError_t launch_expand_tma(const Batch& b, int mode, cudaStream_t s);  // 1 i8, 2 f16, 3 dequant, 4 gemv
+// y[r] = sum of the cols/1024 sub-tile partials of row r (fixed order: deterministic)
+cudaError_t launch_row_reduce(const float* part, uint64_t rows, uint64_t subs_per_row, float* y32, void* y16,
+                              cudaStream_t s);
 
 // Rank lookups over count_kernel's two-level table for one tensor.
 struct RankTable {

@@ -345,6 +345,12 @@ cudaError_t launch_scan(const ScanArgs& in, cudaStream_t s) {
     const uint64_t words = (a.e1 + 31) / 32 - a.e0 / 32;
     a.nblocks = uint32_t(ceil_div(words, kScanBlockWords));
     if (a.nblocks == 0) return cudaSuccess;
+    // The look-back state's position in the workspace depends on the tensor
+    // size, so a workspace reused across sizes may hold other data there:
+    // clear it (and the ticket/done counters) before every scan.
+    cudaError_t e = cudaMemsetAsync(a.lookback, 0, sizeof(unsigned long long) * a.nblocks, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(&a.hdr->ticket, 0, 2 * sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
     scan_kernel<<<a.nblocks, kScanThreads, 0, s>>>(a);
     return cudaGetLastError();
 }
