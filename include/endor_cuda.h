@@ -233,6 +233,12 @@ int endor_cuda_synth_weight(uint64_t rows, uint64_t cols, int32_t dtype, uint64_
 int endor_cuda_magnitude_prune(uint64_t n, int32_t dtype, double sparsity, void* w, void* ws,
                                size_t ws_bytes, void* stream);
 
+/* quantize_values (codec.hpp:306-331) on device, bit-exact: symmetric absmax
+ * f16 -> i8 over the packed values (the bitmap is unchanged); the scale
+ * (absmax/127, 1.0 for all-zero) is returned through scale_out_host.  Sync. */
+int endor_cuda_quantize_values(const void* values_f16, uint64_t nnz, void* q_out, float* scale_out_host,
+                               void* ws, size_t ws_bytes, void* stream);
+
 /* ---- consumer ------------------------------------------------------------ */
 
 /* y[rows] = W[rows, cols] . x[cols]; f16 W and x, fp32 accumulate.  y_f32
@@ -261,8 +267,9 @@ typedef struct endor_pipeline endor_pipeline;
 
 typedef struct endor_pipeline_op {
     uint64_t rows, cols;
-    int32_t dtype;           /* F16 only for the GEMV consumer */
-    int32_t reserved;
+    int32_t dtype;           /* F16; or I8 with flags bit0 (dequantized to f16 on the fly) */
+    int32_t flags;           /* bit0: values are i8 quantized with quant_scale (INT8 + Endor,
+                                PAPER.md:74): fused dequant + decompress -> f16 W */
     const void* bitmap_host; /* pinned (cudaHostAlloc / endor_host_alloc) */
     const void* values_host; /* pinned */
     uint64_t nnz;
@@ -270,6 +277,8 @@ typedef struct endor_pipeline_op {
     float* y_dev;            /* GEMV output, f32[rows]; NULL = decompress only */
     void* dense_dev;         /* optional: where the dense W lands (NULL = ring) */
     float* y_host;           /* optional pinned f32[rows]: y is copied back (D2H) */
+    float quant_scale;       /* flags bit0 only */
+    int32_t reserved2;
 } endor_pipeline_op;
 
 typedef struct endor_pipeline_stats {

@@ -24,9 +24,10 @@ class TensorView(C.Structure):
 
 class PipelineOp(C.Structure):
     """endor_pipeline_op."""
-    _fields_ = [("rows", _u64), ("cols", _u64), ("dtype", _i32), ("reserved", _i32),
+    _fields_ = [("rows", _u64), ("cols", _u64), ("dtype", _i32), ("flags", _i32),
                 ("bitmap_host", _vp), ("values_host", _vp), ("nnz", _u64),
-                ("x_dev", _vp), ("y_dev", _vp), ("dense_dev", _vp), ("y_host", _vp)]
+                ("x_dev", _vp), ("y_dev", _vp), ("dense_dev", _vp), ("y_host", _vp),
+                ("quant_scale", C.c_float), ("reserved2", _i32)]
 
 
 class PipelineStats(C.Structure):
@@ -74,6 +75,7 @@ SIGNATURES = {
                                            C.POINTER(_i32)]),
     "endor_cuda_compress": (C.c_int, [_u64, _u64, _i32, _vp, _vp, _vp, C.POINTER(_u64),
                                       C.POINTER(_i32), _vp, _sz, _vp]),
+    "endor_cuda_quantize_values": (C.c_int, [_vp, _u64, _vp, C.POINTER(C.c_float), _vp, _sz, _vp]),
     "endor_cuda_synth_weight": (C.c_int, [_u64, _u64, _i32, _u64, _u64, _u64, _vp, _vp]),
     "endor_cuda_magnitude_prune": (C.c_int, [_u64, _i32, _f64, _vp, _vp, _sz, _vp]),
     "endor_cuda_gemv": (C.c_int, [_u64, _u64, _vp, _vp, _vp, _vp, _vp]),

@@ -373,6 +373,21 @@ def gemv_compressed(t: EndorTensor, x: torch.Tensor, index: Optional[RankIndex] 
     return y
 
 
+def quantize_values(t: EndorTensor) -> EndorTensor:
+    """codec.hpp:306-331 on the device: f16 packed values -> i8 + scale (the
+    bitmap is shared, not copied)."""
+    if t.dtype != Dtype.F16:
+        raise InvalidArgument("quantize_values requires an f16 tensor")
+    dev = t.device
+    q = _alloc(t.nnz(), dev)
+    scale = C.c_float(0.0)
+    ws = workspace(1, dev)
+    check(_lib.lib().endor_cuda_quantize_values(_ptr(t.values), t.nnz(), _ptr(q), C.byref(scale), ws.data_ptr(),
+                                                ws.numel(), _stream_ptr(dev)))
+    return EndorTensor(t.rows, t.cols, Dtype.I8, t.bitmap, q, quant_scale=scale.value,
+                       negative_zero_collapsed=t.negative_zero_collapsed(), validate=False, nnz=t.nnz())
+
+
 def _index_list(idx, dev) -> torch.Tensor:
     t = torch.as_tensor(idx, dtype=torch.int64) if not isinstance(idx, torch.Tensor) else idx
     return t.to(device=dev, dtype=torch.int64).contiguous().reshape(-1)

@@ -638,6 +638,22 @@ int endor_cuda_compress(uint64_t rows, uint64_t cols, int32_t dtype, const void*
     return endor_cuda_sync_status(ws, stream);
 }
 
+int endor_cuda_quantize_values(const void* values_f16, uint64_t nnz, void* q_out, float* scale_out_host,
+                               void* ws, size_t ws_bytes, void* stream) {
+    if (!scale_out_host) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null scale output");
+    if (nnz && (!values_f16 || !q_out || !aligned(values_f16, 2)))
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "null or misaligned buffer");
+    WsLayout L;
+    int st;
+    if ((st = check_ws(ws, ws_bytes, 1, &L))) return st;
+    float* scale_dev = reinterpret_cast<float*>(&L.hdr->aux[3]);
+    unsigned int* amax = reinterpret_cast<unsigned int*>(&L.hdr->aux[3]) + 1;
+    CK(launch_quantize(values_f16, nnz, q_out, scale_dev, amax, S(stream)));
+    CK(cudaMemcpyAsync(scale_out_host, scale_dev, sizeof(float), cudaMemcpyDeviceToHost, S(stream)));
+    CK(cudaStreamSynchronize(S(stream)));
+    return ENDOR_OK;
+}
+
 int endor_cuda_synth_weight(uint64_t rows, uint64_t cols, int32_t dtype, uint64_t seed,
                             uint64_t row0, uint64_t nrows, void* out, void* stream) {
     uint64_t n;

@@ -14,6 +14,7 @@
 // The paper compresses offline; these exist so the benchmark
 // and the full-size parity tests can regenerate the BASELINE.json inputs in
 // milliseconds instead of minutes of CPU time.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -260,6 +261,52 @@ __global__ void __launch_bounds__(256) compact_kernel(const uint8_t* dense, uint
         ++v;
         m &= m - 1;
     }
+}
+
+// ---- quantize_values (codec.hpp:306-331) ---------------------------------------
+// absmax over |f16_to_f32(v)| (NaNs never win, like std::max(absmax, x)),
+// then q = clamp(lround(v / scale), -127, 127) with IEEE float division.
+__device__ __forceinline__ float f16_bits_to_f32(uint16_t h) { return __half2float(__ushort_as_half(h)); }
+
+__global__ void __launch_bounds__(256) absmax_kernel(const uint16_t* v, uint64_t nnz, unsigned int* amax_bits) {
+    float m = 0.f;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nnz; i += stride) {
+        const float a = fabsf(f16_bits_to_f32(v[i]));
+        m = (m < a) ? a : m;  // a NaN is never selected
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        const float o = __shfl_xor_sync(0xffffffffu, m, d);
+        m = (m < o) ? o : m;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(amax_bits, __float_as_uint(m));  // non-negative floats order as ints
+}
+
+__global__ void __launch_bounds__(256) quantize_kernel(const uint16_t* v, uint64_t nnz, const unsigned int* amax_bits,
+                                                       int8_t* q, float* scale_out) {
+    const float absmax = __uint_as_float(*amax_bits);
+    const float scale = (nnz == 0 || absmax == 0.0f) ? 1.0f : __fdiv_rn(absmax, 127.0f);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *scale_out = scale;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nnz; i += stride) {
+        const float x = __fdiv_rn(f16_bits_to_f32(v[i]), scale);
+        // x86-64 lround gives the "integer indefinite" LONG_MIN for NaN / out of range
+        long long r = (isfinite(x) && fabsf(x) < 9.2e18f) ? llroundf(x) : (-0x7fffffffffffffffll - 1);
+        r = r < -127 ? -127 : (r > 127 ? 127 : r);
+        q[i] = int8_t(r);
+    }
+}
+
+cudaError_t launch_quantize(const void* vals, uint64_t nnz, void* q, float* scale_dev, unsigned int* amax,
+                            cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(amax, 0, sizeof(unsigned int), s);
+    if (e != cudaSuccess) return e;
+    const unsigned g = unsigned(nnz ? (ceil_div(nnz, 256) < 148 * 16 ? ceil_div(nnz, 256) : 148 * 16) : 1);
+    absmax_kernel<<<g, 256, 0, s>>>(static_cast<const uint16_t*>(vals), nnz, amax);
+    quantize_kernel<<<g, 256, 0, s>>>(static_cast<const uint16_t*>(vals), nnz, amax, static_cast<int8_t*>(q),
+                                      scale_dev);
+    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------

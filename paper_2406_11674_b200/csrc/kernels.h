@@ -129,5 +129,7 @@ cudaError_t launch_compact(const void* dense, uint64_t n, int eb, const void* bi
                            const WsLayout& L, void* values, cudaStream_t s);
 cudaError_t launch_gemv(uint64_t rows, uint64_t cols, const void* w, const void* x, float* y32,
                         void* y16, cudaStream_t s);
+cudaError_t launch_quantize(const void* vals, uint64_t nnz, void* q, float* scale_dev, unsigned int* amax,
+                            cudaStream_t s);
 
 }  // namespace endor_b200

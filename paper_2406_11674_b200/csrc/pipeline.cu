@@ -135,10 +135,13 @@ int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops
     for (int i = 0; i < nops; ++i) {
         const endor_pipeline_op& op = ops[i];
         const uint64_t n = op.rows * op.cols;
-        const int eb = op.dtype == ENDOR_DTYPE_F16 ? 2 : 1;
-        if (n > p->max_elems || (op.dtype != ENDOR_DTYPE_F16 && op.dtype != ENDOR_DTYPE_I8))
+        const int eb = op.dtype == ENDOR_DTYPE_F16 ? 2 : 1;     // packed-value bytes (H2D)
+        const bool deq = (op.flags & 1) != 0;                    // i8 values -> f16 W
+        const int ob = (op.dtype == ENDOR_DTYPE_F16 || deq) ? 2 : 1;  // dense bytes
+        if (n > p->max_elems || (op.dtype != ENDOR_DTYPE_F16 && op.dtype != ENDOR_DTYPE_I8) ||
+            (deq && op.dtype != ENDOR_DTYPE_I8))
             return ENDOR_ERR_INVALID_ARGUMENT;
-        if ((op.x_dev || op.y_dev) && op.dtype != ENDOR_DTYPE_F16) return ENDOR_ERR_INVALID_ARGUMENT;
+        if ((op.x_dev || op.y_dev) && ob != 2) return ENDOR_ERR_INVALID_ARGUMENT;
         auto& slot = p->slots[i % p->depth];
         const size_t bmb = (n + 7) / 8, vb = op.nnz * eb;
         // copy stream: wait until the slot's previous occupant was decompressed
@@ -152,7 +155,8 @@ int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops
         PK(cudaEventRecord(p->dec_beg[i], p->compute));
         void* dst = op.dense_dev ? op.dense_dev : p->dense[i & 1];
         endor_tensor_view v{op.rows, op.cols, op.dtype, 0, slot.bitmap, slot.values, op.nnz};
-        st = endor_cuda_decompress(&v, dst, p->ws, p->ws_bytes, p->compute);
+        st = deq ? endor_cuda_decompress_dequant(&v, op.quant_scale, dst, p->ws, p->ws_bytes, p->compute)
+                 : endor_cuda_decompress(&v, dst, p->ws, p->ws_bytes, p->compute);
         if (st) return st;
         launches += 2;
         PK(cudaEventRecord(p->dec_end[i], p->compute));
@@ -167,7 +171,7 @@ int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops
         }
         PK(cudaEventRecord(p->op_end[i], p->compute));
         h2d += bmb + vb;
-        dense += n * eb;
+        dense += n * ob;
     }
     p->last_nops = nops;
     p->last_h2d_bytes = h2d;

@@ -32,6 +32,7 @@ class HostOp:
     y: Optional[torch.Tensor] = None       # device f32 [rows]
     y_host: Optional[torch.Tensor] = None  # pinned f32 [rows]
     dense: Optional[torch.Tensor] = None   # device uint8 [rows*cols*eb] (optional)
+    quant_scale: Optional[float] = None    # i8 values dequantized to f16 W (INT8 + Endor)
 
     @property
     def compressed_bytes(self) -> int:
@@ -39,7 +40,7 @@ class HostOp:
 
     @property
     def dense_bytes(self) -> int:
-        return self.rows * self.cols * (2 if self.dtype == 0 else 1)
+        return self.rows * self.cols * (2 if (self.dtype == 0 or self.quant_scale is not None) else 1)
 
 
 def _p(t: Optional[torch.Tensor]):
@@ -72,8 +73,10 @@ class OffloadPipeline:
     def run(self, ops: List[HostOp], sync: bool = True) -> None:
         arr = (_lib.PipelineOp * len(ops))()
         for i, o in enumerate(ops):
-            arr[i] = _lib.PipelineOp(o.rows, o.cols, o.dtype, 0, _p(o.bitmap), _p(o.values), o.nnz,
-                                     _p(o.x), _p(o.y), _p(o.dense), _p(o.y_host))
+            deq = o.quant_scale is not None
+            arr[i] = _lib.PipelineOp(o.rows, o.cols, o.dtype, 1 if deq else 0, _p(o.bitmap), _p(o.values), o.nnz,
+                                     _p(o.x), _p(o.y), _p(o.dense), _p(o.y_host),
+                                     float(o.quant_scale) if deq else 0.0, 0)
         self._keep = (arr, ops)
         check(self._lib.endor_pipeline_run(self._h, arr, len(ops), 1 if sync else 0))
 

@@ -89,6 +89,26 @@ def test_dequant_large_layer_shape(E):
     assert zlib.crc32(got.bytes()) == zlib.crc32(want.tobytes())
 
 
+def test_gpu_quantize_values_matches_reference(E, quant_cases):
+    for c in quant_cases:
+        w = O.random_dense(c["rows"], c["cols"], 2, c["seed"], c["zero_fraction"])
+        bm, vals, nnz, _ = O.compress(w, c["rows"], c["cols"], 2)
+        t = E.EndorTensor(c["rows"], c["cols"], E.Dtype.F16, E.Bitmap(c["rows"] * c["cols"], data=_dev(bm)),
+                          _dev(vals), validate=False, nnz=nnz)
+        q = E.quantize_values(t)
+        assert np.float32(q.quant_scale).view(np.uint32) == c["scale_bits"]
+        assert zlib.crc32(q.values.cpu().numpy().tobytes()) == c["crc_q"]
+        assert zlib.crc32(E.decompress_dequant(q).bytes()) == c["crc_dense"]
+    # special values: inf / NaN among the values (x86 lround semantics)
+    vals = np.array([0x3C00, 0x7C00, 0xFC00, 0x7E01, 0x0001, 0x8001, 0x4000], np.uint16)
+    q_ref, s_ref = O.quantize_values(vals.view(np.uint8), len(vals))
+    t = E.EndorTensor(1, 7, E.Dtype.F16, E.Bitmap(7, data=_dev(np.array([0x7F], np.uint8))),
+                      _dev(vals.view(np.uint8)), validate=False, nnz=7)
+    q = E.quantize_values(t)
+    assert np.float32(q.quant_scale) == np.float32(s_ref) or (np.isnan(q.quant_scale) and np.isnan(s_ref))
+    assert q.values.cpu().numpy().tobytes() == q_ref.tobytes()
+
+
 def test_dequant_errors(E):
     w = O.random_dense(10, 10, 2, 9, 0.5)
     bm, vals, nnz, _ = O.compress(w, 10, 10, 2)
