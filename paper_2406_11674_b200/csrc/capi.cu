@@ -372,7 +372,7 @@ int endor_cuda_gemv_compressed(const endor_tensor_view* t, const uint64_t* prefi
     b.hdr = L.hdr;
     if (!T.idx) CK(launch_count(b, S(stream)));
     CK(launch_expand_tma(b, 4, S(stream)));
-    CK(launch_row_reduce(L.part, t->rows, t->cols / kSubElems, y_f32, y_f16, S(stream)));
+    CK(launch_row_reduce(L.part, t->rows, t->cols / kWarpElems, y_f32, y_f16, S(stream)));
     return ENDOR_OK;
 }
 

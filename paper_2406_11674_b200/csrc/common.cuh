@@ -55,7 +55,17 @@ struct WsLayout {
     size_t bytes;
 };
 
-constexpr int kSubElems = 1024;  // one warp's share of an expand tile
+constexpr int kSubElems = 1024;  // granularity of the value-offset tables (count_kernel / RankIndex)
+
+// Expand consumers per TMA-kernel CTA: each handles kWarpElems elements of a
+// tile.  8 x 1024 measured 0.893 of roofline vs 0.678 for 16 x 512
+// (profiles/r01/README.md): per-warp ILP beats more, thinner warps here.
+#ifndef ENDOR_CONSUMER_WARPS
+#define ENDOR_CONSUMER_WARPS 8
+#endif
+constexpr int kConsumerWarps = ENDOR_CONSUMER_WARPS;
+constexpr int kWarpElems = kTileElems / kConsumerWarps;  // 512 (or 1024 with 8 warps)
+constexpr int kWarpWords = kWarpElems / 32;
 
 __host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -75,8 +85,8 @@ inline WsLayout ws_layout_caps(void* base, uint64_t n, uint64_t sub_cap, uint64_
     off = align256(off + 8 * sub_cap);
     L.blk = reinterpret_cast<unsigned long long*>(b + off);
     off = align256(off + 8 * blk_cap);
-    L.part = reinterpret_cast<float*>(b + off);  // fused-GEMV sub-tile partials
-    off = align256(off + 4 * sub_cap);
+    L.part = reinterpret_cast<float*>(b + off);  // fused-GEMV partials, one per consumer warp-tile
+    off = align256(off + 4 * sub_cap * (kSubElems / kWarpElems));
     L.tprefix = reinterpret_cast<unsigned long long*>(b + off);
     off = align256(off + 8 * (L.ntiles + 1));
     L.lookback = reinterpret_cast<unsigned long long*>(b + off);  // must stay zeroed between calls

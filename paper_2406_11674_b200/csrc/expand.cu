@@ -165,13 +165,14 @@ __device__ __forceinline__ float dot8_f16(const uint4& w, const uint4& x, float 
 // Fused decompress -> GEMV over one warp's 1024-element sub-tile, which lies in
 // a single row of W (cols % 1024 == 0): the expanded weights never leave
 // registers; returns the warp's partial dot product (all lanes).
+template <int WE>
 __device__ __forceinline__ float gemv_subtile(uint32_t word, uint32_t excl, uint32_t vbase,
                                               const uint4* __restrict__ x8, int32_t valid_elems, int lane) {
     const uint32_t sh = (lane % 4) * 8;
     const uint32_t low = (1u << sh) - 1u;
     float acc = 0.f;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < WE / 256; ++j) {
         const int c = 32 * j + lane;
         const uint32_t wd = __shfl_sync(0xffffffffu, word, c / 4);
         const uint32_t pre = __shfl_sync(0xffffffffu, excl, c / 4);
@@ -207,14 +208,14 @@ __device__ __forceinline__ void store_partial(uint8_t* p, uint4 q, uint32_t vali
 // warp; vbase: shared address of the sub-tile's first packed value.  Lane l
 // writes chunks l, l+32, .. so every store instruction covers 512 contiguous
 // bytes.  FULL: all 1024 elements valid (no bounds checks).
-template <int MODE, bool FULL>
+template <int MODE, bool FULL, int WE = 1024>
 __device__ __forceinline__ void expand_subtile(uint32_t word, uint32_t excl, uint32_t vbase,
                                                uint8_t* out, int32_t valid_elems, int lane,
                                                float scale = 1.f, bool fast = true) {
     constexpr int IN = mode_in(MODE), OUT = mode_out(MODE);
     constexpr int EPC = 16 / OUT;             // output elements per 16-byte chunk
     constexpr int CPW = 32 / EPC;             // chunks per bitmap word (4 or 2)
-    constexpr int ITERS = 32 * 32 / EPC / 32; // chunks per lane (4 or 2)
+    constexpr int ITERS = WE / EPC / 32;      // chunks per lane
     const uint32_t sh = (lane % CPW) * EPC;   // chunk position inside its word: lane-constant
     const uint32_t low = (1u << sh) - 1u;
     uint8_t* o = out + size_t(lane) * 16;
@@ -240,8 +241,7 @@ __device__ __forceinline__ void expand_subtile(uint32_t word, uint32_t excl, uin
 #define ENDOR_TMA_STAGES 6  // 6 x 17.6 KB ring = 2 CTAs/SM; measured best of 2..12 (profiles/r01)
 #endif
 constexpr int kStages = ENDOR_TMA_STAGES;
-constexpr int kConsumerWarps = kTileElems / kSubElems;  // 8
-constexpr int kTmaThreads = (kConsumerWarps + 1) * 32;  // + 1 producer warp
+constexpr int kTmaThreads = (kConsumerWarps + 1) * 32;  // consumers + 1 producer warp
 
 template <int EB>
 struct Stage {
@@ -400,21 +400,30 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
             const uint64_t t0 = (t - T.tile0) * kTileElems;
             const int32_t count = int32_t(umin64(kTileElems, T.n - t0));
             mbar_wait(full0 + 8 * s, (i / kStages) & 1);
-            const int32_t wfirst = warp * kSubElems;
+            const int32_t wfirst = warp * kWarpElems;
             if (wfirst < count) {
-                const int32_t valid = min(count - wfirst, kSubElems);
+                const int32_t valid = min(count - wfirst, kWarpElems);
                 const int32_t lbit = lane * 32;
                 uint32_t word = 0;
-                if (lbit < valid) {
-                    word = lds32(stg + Stage<EB>::kBm + (warp * 32 + lane) * 4);
+                if (lane < kWarpWords && lbit < valid) {
+                    word = lds32(stg + Stage<EB>::kBm + (warp * kWarpWords + lane) * 4);
                     if (valid - lbit < 32) word &= (1u << (valid - lbit)) - 1u;
                 }
                 const uint32_t pc = __popc(word);
                 const uint32_t excl = warp_excl_scan_small(pc);
                 const unsigned long long tp = lds64(stg + Stage<EB>::kSub);
-                const unsigned long long sw = lds64(stg + Stage<EB>::kSub + 8 * warp);
+                const int sub = wfirst / kSubElems;  // this warp's 1024-element offset entry
+                const unsigned long long sw = lds64(stg + Stage<EB>::kSub + 8 * sub);
                 const uint32_t off = lds32(stg + Stage<EB>::kSub + 64);
                 uint32_t rel = uint32_t(sw - tp);
+                if (kWarpElems < kSubElems && (wfirst % kSubElems)) {
+                    // second half of a 1024-element entry: skip the values of the first half
+                    // (its words precede ours and are always complete)
+                    uint32_t pw = 0;
+                    for (int k = lane; k < (wfirst % kSubElems) / 32; k += 32)
+                        pw += __popc(lds32(stg + Stage<EB>::kBm + (sub * 32 + k) * 4));
+                    rel += __reduce_add_sync(0xffffffffu, pw);
+                }
                 if (T.idx) {  // a caller's index may be inconsistent: stay inside the staged window
                     const uint32_t wcount = lds32(stg + Stage<EB>::kSub + 68);
                     const uint32_t wtotal = __shfl_sync(0xffffffffu, excl + pc, 31);
@@ -426,17 +435,20 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
                 }
                 const uint32_t vbase = stg + Stage<EB>::kVals + off + rel * EB;
                 if constexpr (MODE == kModeGemv) {
-                    // the sub-tile is one row's columns [col0, col0 + 1024): dot with x there
+                    // the warp's elements are one row's columns [col0, col0 + kWarpElems)
                     const uint64_t col0 = (t0 + wfirst) % T.cols;
-                    const float p = gemv_subtile(word, excl, vbase,
-                                                 reinterpret_cast<const uint4*>(T.x) + col0 / 8, valid, lane);
-                    if (lane == 0) T.part[(t - T.tile0) * 8 + warp] = p;
+                    const float p = gemv_subtile<kWarpElems>(word, excl, vbase,
+                                                             reinterpret_cast<const uint4*>(T.x) + col0 / 8, valid,
+                                                             lane);
+                    if (lane == 0) T.part[(t - T.tile0) * kConsumerWarps + warp] = p;
                 } else {
                     uint8_t* out = T.dst + (t0 + wfirst) * OB;
-                    if (valid == kSubElems)
-                        expand_subtile<MODE, true>(word, excl, vbase, out, valid, lane, T.scale, T.deq_fast);
+                    if (valid == kWarpElems)
+                        expand_subtile<MODE, true, kWarpElems>(word, excl, vbase, out, valid, lane, T.scale,
+                                                               T.deq_fast);
                     else
-                        expand_subtile<MODE, false>(word, excl, vbase, out, valid, lane, T.scale, T.deq_fast);
+                        expand_subtile<MODE, false, kWarpElems>(word, excl, vbase, out, valid, lane, T.scale,
+                                                                T.deq_fast);
                 }
             }
             __syncwarp();
