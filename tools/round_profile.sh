@@ -1,0 +1,21 @@
+#!/usr/bin/env bash
+# One GPU call that refreshes every judged artefact (run under gpurun):
+#   gpu tests, bench (both arms), ncu launch list of the bench command, one
+#   ncu --set full capture of the headline expand launch.
+# Usage: gpurun --timeout 2400 -- 'bash tools/round_profile.sh TAG'
+set -u
+TAG=${1:-r01}
+O=gpurun_out/$TAG
+mkdir -p "$O"
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > "$O/gpu.txt" 2>&1
+timeout 900 python -m pytest tests -x -q -m gpu > "$O/pytest_gpu.log" 2>&1; echo "pytest rc=$?" >> "$O/pytest_gpu.log"
+timeout 600 python bench.py > "$O/bench.json" 2> "$O/bench.err"
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > "$O/bench_reference.json" 2> "$O/bench_reference.err"
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    --csv --log-file "$O/launches.csv" python bench.py --steps 2 --warmup 3 --no-cpu-baseline > "$O/launches_bench.log" 2>&1
+# headline kernel: expand_tma_kernel<2> of the idx (decompress_chunked) plans.  The
+# no-index plans are timed first (one launch per step: 3 warmup + 1 timed), so skip 5.
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:expand_tma_kernel -s 5 -c 1 \
+    -o "$O/full_expand" -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-extras \
+    > "$O/full_expand.log" 2>&1
+echo done
