@@ -257,6 +257,15 @@ int endor_cuda_gemv(uint64_t rows, uint64_t cols, const void* w_f16, const void*
 int endor_cuda_gemv_compressed(const endor_tensor_view* t, const uint64_t* prefix1024, const void* x_f16,
                                float* y_f32, void* y_f16, void* ws, size_t ws_bytes, void* stream);
 
+/* Batched fused decompress -> GEMV: y_i = W_i x_i for up to 16 tensors (one
+ * decoder layer's ops) in one persistent launch (+ one counting launch when
+ * some prefix1024[i] is NULL, + one row-sum launch).  prefixes1024 may be
+ * NULL (count every tensor); y_f32 / y_f16 arrays may be NULL, entries too.
+ * Workspace: endor_cuda_workspace_bytes_batch(views, count). */
+int endor_cuda_gemv_compressed_batch(const endor_tensor_view* views, const uint64_t* const* prefixes1024,
+                                     const void* const* x_f16, float* const* y_f32, void* const* y_f16,
+                                     int count, void* ws, size_t ws_bytes, void* stream);
+
 /* ---- offload pipeline ---------------------------------------------------- */
 /* Streams compressed ops from pinned host memory through a double-buffered
  * device staging ring: H2D of op i+1 on the copy stream overlaps decompress

@@ -56,6 +56,8 @@ SIGNATURES = {
                                                       C.POINTER(_vp), C.c_int, _vp, _sz, _vp]),
     "endor_cuda_decompress_dequant": (C.c_int, [C.POINTER(TensorView), C.c_float, _vp, _vp, _sz, _vp]),
     "endor_cuda_gemv_compressed": (C.c_int, [C.POINTER(TensorView), _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "endor_cuda_gemv_compressed_batch": (C.c_int, [C.POINTER(TensorView), C.POINTER(_vp), C.POINTER(_vp),
+                                                   C.POINTER(_vp), C.POINTER(_vp), C.c_int, _vp, _sz, _vp]),
     "endor_cuda_extract_rows": (C.c_int, [C.POINTER(TensorView), _vp, _u64, _vp, _vp, _sz, _vp]),
     "endor_cuda_extract_cols": (C.c_int, [C.POINTER(TensorView), _vp, _u64, _vp, _vp, _sz, _vp]),
     "endor_cuda_decompress_phase": (C.c_int, [C.POINTER(TensorView), _vp, C.c_int, _vp, _sz, _vp]),

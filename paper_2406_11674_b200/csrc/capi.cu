@@ -339,40 +339,70 @@ int endor_cuda_decompress_dequant(const endor_tensor_view* t, float scale, void*
 
 int endor_cuda_gemv_compressed(const endor_tensor_view* t, const uint64_t* prefix1024, const void* x_f16,
                                float* y_f32, void* y_f16, void* ws, size_t ws_bytes, void* stream) {
-    uint64_t n;
+    if (!t) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null tensor view");
+    const uint64_t* pres[1] = {prefix1024};
+    const void* xs[1] = {x_f16};
+    float* y32[1] = {y_f32};
+    void* y16[1] = {y_f16};
+    if (!y_f32 && !y_f16) return fail(ENDOR_ERR_INVALID_ARGUMENT, "x must be 16-byte aligned f16[cols]; y must be given");
+    return endor_cuda_gemv_compressed_batch(t, pres, xs, y32, y16, 1, ws, ws_bytes, stream);
+}
+
+int endor_cuda_gemv_compressed_batch(const endor_tensor_view* views, const uint64_t* const* prefixes1024,
+                                     const void* const* x_f16, float* const* y_f32, void* const* y_f16,
+                                     int count, void* ws, size_t ws_bytes, void* stream) {
+    if (count < 0 || count > kMaxBatch || (count > 0 && (!views || !x_f16)))
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "batch must hold 0..16 tensors with x vectors");
+    for (int i = 0; i < count; ++i) {
+        const endor_tensor_view* t = &views[i];
+        uint64_t n;
+        int eb, st;
+        if ((st = check_view(t, &n, &eb))) return st;
+        if (t->dtype != ENDOR_DTYPE_F16) return fail(ENDOR_ERR_INVALID_ARGUMENT, "fused GEMV needs an f16 tensor");
+        if (t->cols % kSubElems)
+            return fail(ENDOR_ERR_INVALID_ARGUMENT,
+                        "fused GEMV needs cols % 1024 == 0 (use endor_cuda_decompress + endor_cuda_gemv)");
+        if (t->rows == 0) continue;
+        if (!x_f16[i] || !aligned(x_f16[i], 16) || (!(y_f32 && y_f32[i]) && !(y_f16 && y_f16[i])))
+            return fail(ENDOR_ERR_INVALID_ARGUMENT, "x must be 16-byte aligned f16[cols]; y must be given");
+        if (!aligned(t->bitmap, 16))
+            return fail(ENDOR_ERR_INVALID_ARGUMENT, "fused GEMV needs a 16-byte aligned bitmap");
+        if (prefixes1024 && prefixes1024[i] && !aligned(prefixes1024[i], 16))
+            return fail(ENDOR_ERR_INVALID_ARGUMENT, "misaligned prefix");
+    }
+    Batch b;
     int eb, st;
-    if ((st = check_view(t, &n, &eb))) return st;
-    if (t->dtype != ENDOR_DTYPE_F16) return fail(ENDOR_ERR_INVALID_ARGUMENT, "fused GEMV needs an f16 tensor");
-    if (t->cols % kSubElems)
-        return fail(ENDOR_ERR_INVALID_ARGUMENT,
-                    "fused GEMV needs cols % 1024 == 0 (use endor_cuda_decompress + endor_cuda_gemv)");
-    if (t->rows == 0) return ENDOR_OK;
-    if (!x_f16 || !aligned(x_f16, 16) || (!y_f32 && !y_f16))
-        return fail(ENDOR_ERR_INVALID_ARGUMENT, "x must be 16-byte aligned f16[cols]; y must be given");
-    if (!aligned(t->bitmap, 16)) return fail(ENDOR_ERR_INVALID_ARGUMENT, "fused GEMV needs a 16-byte aligned bitmap");
-    if (prefix1024 && !aligned(prefix1024, 16)) return fail(ENDOR_ERR_INVALID_ARGUMENT, "misaligned prefix");
-    WsLayout L;
-    if ((st = check_ws(ws, ws_bytes, n, &L))) return st;
-    Batch b{};
-    b.count = 1;
+    uint64_t nmax;
+    size_t need;
+    if ((st = plan_batch(views, nullptr, count, &b, &eb, &nmax, &need))) return st;
+    if (b.count == 0) return ENDOR_OK;
+    if (!ws || !aligned(ws, 256)) return fail(ENDOR_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+    if (ws_bytes < need) return fail(ENDOR_ERR_INVALID_ARGUMENT, "workspace too small for the batch");
+    // attach x / y / indices (plan_batch drops empty tensors: walk both lists)
+    float* y32[kMaxBatch] = {};
+    void* y16[kMaxBatch] = {};
+    for (int i = 0, j = 0; i < count; ++i) {
+        if (views[i].rows * views[i].cols == 0) continue;
+        BatchTensor& T = b.t[j];
+        T.x = x_f16[i];
+        T.cols = views[i].cols;
+        T.idx = prefixes1024 ? reinterpret_cast<const unsigned long long*>(prefixes1024[i]) : nullptr;
+        y32[j] = y_f32 ? y_f32[i] : nullptr;
+        y16[j] = y_f16 ? y_f16[i] : nullptr;
+        ++j;
+    }
+    uint64_t sub_cap, blk_cap, blk_bound = 0;
+    batch_plan(b, &sub_cap, &blk_cap, count_ctas());  // re-plan: indexed tensors need no count CTAs
+    for (int i = 0; i < b.count; ++i) blk_bound += ceil_div((b.t[i].n + 31) / 32, kCountBlockWords) + 2;
+    const WsLayout L = ws_layout_caps(ws, nmax, sub_cap, blk_bound);
+    for (int i = 0; i < b.count; ++i) b.t[i].part = L.part + b.t[i].sub0;
     b.check_total = 1;
-    BatchTensor& T = b.t[0];
-    T.bitmap = static_cast<const uint8_t*>(t->bitmap);
-    T.values = static_cast<const uint8_t*>(t->values);
-    T.n = n;
-    T.nnz = t->nnz;
-    T.idx = reinterpret_cast<const unsigned long long*>(prefix1024);  // optional load-time index
-    T.x = x_f16;
-    T.part = L.part;
-    T.cols = t->cols;
-    uint64_t sub_cap, blk_cap;
-    batch_plan(b, &sub_cap, &blk_cap, count_ctas());
     b.tsub = L.tsub;
     b.blk = L.blk;
     b.hdr = L.hdr;
-    if (!T.idx) CK(launch_count(b, S(stream)));
-    CK(launch_expand_tma(b, 4, S(stream)));
-    CK(launch_row_reduce(L.part, t->rows, t->cols / kWarpElems, y_f32, y_f16, S(stream)));
+    CK(launch_count(b, S(stream)));  // no-op when every tensor is indexed
+    CK(launch_gemv_fused(b, S(stream)));
+    CK(launch_row_reduce_batch(b, y32, y16, S(stream)));
     return ENDOR_OK;
 }
 

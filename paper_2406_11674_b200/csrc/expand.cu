@@ -28,77 +28,10 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "gather.cuh"
 #include "kernels.h"
 
 namespace endor_b200 {
-
-// ---- selector tables ---------------------------------------------------------
-// A 4-element nibble q of the bitmap consumes popc(q) packed values.  The
-// next four packed values are fetched as an unaligned 8-byte window {x, y}
-// and PRMT drops each into its slot.  Zero bytes come from RZ (byte 4 of a
-// zero second operand), so no compare/select is needed:
-//   f16:  word0 (slots 0,1) = PRMT(x, 0, sel0)             -- needs v0..v1 at most
-//         ym               = PRMT(y, 0, selm)              -- y, or y with v3 zeroed
-//         word1 (slots 2,3) = PRMT(x, ym, sel1)            -- unset slots read ym bytes 6,7
-//   i8:   word  (slots 0-3) = PRMT(x, 0, sel)
-// selm keeps y whole only when q == 0xF (then no slot is unset).  The f16
-// table packs sel0 | sel1 << 16 into one word: 16 words in 16 distinct banks,
-// so a warp's lookups never conflict (one wavefront per LDS).
-__shared__ uint32_t g_lut16[16];
-__shared__ uint32_t g_lut8[16];
-
-__device__ __forceinline__ void init_luts(int tid) {
-    if (tid < 16) {
-        const uint32_t q = tid;
-        uint32_t s0 = 0, s1 = 0, j = 0, s8 = 0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const bool set = q & (1u << k);
-            const uint32_t b0 = set ? 2 * j : (k < 2 ? 4u : 6u);
-            const uint32_t b1 = set ? 2 * j + 1 : (k < 2 ? 4u : 7u);
-            const uint32_t pos = (k & 1) * 8;
-            if (k < 2) s0 |= (b0 << pos) | (b1 << (pos + 4));
-            else s1 |= (b0 << pos) | (b1 << (pos + 4));
-            s8 |= (set ? j : 4u) << (4 * k);
-            j += set;
-        }
-        g_lut16[q] = s0 | (s1 << 16);
-        g_lut8[q] = s8;
-    }
-}
-
-// Expand one 16-byte output chunk.  m: the chunk's bitmap bits; a: shared
-// address of its first packed value (any byte alignment).
-template <int EB>
-__device__ __forceinline__ uint4 gather_chunk(uint32_t m, uint32_t a) {
-    uint32_t o[4];
-    if constexpr (EB == 2) {
-#pragma unroll
-        for (int g = 0; g < 2; ++g) {
-            const uint32_t q = (m >> (4 * g)) & 15u;
-            const uint32_t sel = g_lut16[q];
-            const uint32_t al = a & ~3u, sh = a << 3;  // funnel shifts wrap mod 32
-            const uint32_t w0 = lds32(al), w1 = lds32(al + 4), w2 = lds32(al + 8);
-            const uint32_t x = __funnelshift_r(w0, w1, sh);
-            const uint32_t y = __funnelshift_r(w1, w2, sh);
-            const uint32_t ym = __byte_perm(y, 0u, q == 15u ? 0x3210u : 0x4410u);
-            o[2 * g] = __byte_perm(x, 0u, sel);
-            o[2 * g + 1] = __byte_perm(x, ym, sel >> 16);
-            a += 2 * __popc(q);
-        }
-    } else {
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-            const uint32_t qa = (m >> (4 * g)) & 15u;
-            const uint32_t sel = g_lut8[qa];
-            const uint32_t al = a & ~3u, sh = a << 3;
-            const uint32_t x = __funnelshift_r(lds32(al), lds32(al + 4), sh);
-            o[g] = __byte_perm(x, 0u, sel);
-            a += __popc(qa);
-        }
-    }
-    return make_uint4(o[0], o[1], o[2], o[3]);
-}
 
 // Fused INT8 dequant + decompress (decompress(dequantize_values(t)),
 // codec.hpp:334-349 then :157): 8 output f16 slots per 16-byte chunk, each
@@ -145,47 +78,9 @@ __device__ __forceinline__ uint4 gather_chunk_dequant(uint32_t m, uint32_t a, fl
 
 // Element modes of the expand kernels: bytes per packed value (IN) and per
 // dense output element (OUT).
-constexpr int kModeI8 = 1, kModeF16 = 2, kModeDequant = 3, kModeGemv = 4;
-__host__ __device__ constexpr int mode_in(int m) { return (m == kModeF16 || m == kModeGemv) ? 2 : 1; }
+constexpr int kModeI8 = 1, kModeF16 = 2, kModeDequant = 3;
+__host__ __device__ constexpr int mode_in(int m) { return m == kModeF16 ? 2 : 1; }
 __host__ __device__ constexpr int mode_out(int m) { return m == kModeI8 ? 1 : 2; }
-
-// dot of 8 f16 weights with 8 f16 activations, fp32 accumulate
-__device__ __forceinline__ float dot8_f16(const uint4& w, const uint4& x, float acc) {
-    const __half2* wh = reinterpret_cast<const __half2*>(&w);
-    const __half2* xh = reinterpret_cast<const __half2*>(&x);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const float2 a = __half22float2(wh[i]), c = __half22float2(xh[i]);
-        acc = fmaf(a.x, c.x, acc);
-        acc = fmaf(a.y, c.y, acc);
-    }
-    return acc;
-}
-
-// Fused decompress -> GEMV over one warp's 1024-element sub-tile, which lies in
-// a single row of W (cols % 1024 == 0): the expanded weights never leave
-// registers; returns the warp's partial dot product (all lanes).
-template <int WE>
-__device__ __forceinline__ float gemv_subtile(uint32_t word, uint32_t excl, uint32_t vbase,
-                                              const uint4* __restrict__ x8, int32_t valid_elems, int lane) {
-    const uint32_t sh = (lane % 4) * 8;
-    const uint32_t low = (1u << sh) - 1u;
-    float acc = 0.f;
-#pragma unroll
-    for (int j = 0; j < WE / 256; ++j) {
-        const int c = 32 * j + lane;
-        const uint32_t wd = __shfl_sync(0xffffffffu, word, c / 4);
-        const uint32_t pre = __shfl_sync(0xffffffffu, excl, c / 4);
-        if (c * 8 < valid_elems) {
-            const uint32_t m = (wd >> sh) & 0xFFu;
-            const uint4 w = gather_chunk<2>(m, vbase + (pre + __popc(wd & low)) * 2);
-            acc = dot8_f16(w, __ldg(x8 + c), acc);
-        }
-    }
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
-    return acc;
-}
 
 template <int MODE>
 __device__ __forceinline__ uint4 gather_mode(uint32_t m, uint32_t a, float scale, bool fast) {
@@ -434,22 +329,13 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
                     }
                 }
                 const uint32_t vbase = stg + Stage<EB>::kVals + off + rel * EB;
-                if constexpr (MODE == kModeGemv) {
-                    // the warp's elements are one row's columns [col0, col0 + kWarpElems)
-                    const uint64_t col0 = (t0 + wfirst) % T.cols;
-                    const float p = gemv_subtile<kWarpElems>(word, excl, vbase,
-                                                             reinterpret_cast<const uint4*>(T.x) + col0 / 8, valid,
-                                                             lane);
-                    if (lane == 0) T.part[(t - T.tile0) * kConsumerWarps + warp] = p;
-                } else {
-                    uint8_t* out = T.dst + (t0 + wfirst) * OB;
-                    if (valid == kWarpElems)
-                        expand_subtile<MODE, true, kWarpElems>(word, excl, vbase, out, valid, lane, T.scale,
-                                                               T.deq_fast);
-                    else
-                        expand_subtile<MODE, false, kWarpElems>(word, excl, vbase, out, valid, lane, T.scale,
-                                                                T.deq_fast);
-                }
+                uint8_t* out = T.dst + (t0 + wfirst) * OB;
+                if (valid == kWarpElems)
+                    expand_subtile<MODE, true, kWarpElems>(word, excl, vbase, out, valid, lane, T.scale,
+                                                           T.deq_fast);
+                else
+                    expand_subtile<MODE, false, kWarpElems>(word, excl, vbase, out, valid, lane, T.scale,
+                                                            T.deq_fast);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(empty0 + 8 * s);
@@ -565,26 +451,7 @@ static cudaError_t launch_tma_mode(const Batch& b, cudaStream_t s) {
 cudaError_t launch_expand_tma(const Batch& b, int mode, cudaStream_t s) {
     if (mode == kModeF16) return launch_tma_mode<kModeF16>(b, s);
     if (mode == kModeI8) return launch_tma_mode<kModeI8>(b, s);
-    if (mode == kModeGemv) return launch_tma_mode<kModeGemv>(b, s);
     return launch_tma_mode<kModeDequant>(b, s);
-}
-
-__global__ void __launch_bounds__(256) row_reduce_kernel(const float* __restrict__ part, uint64_t rows,
-                                                         uint64_t spr, float* y32, __half* y16) {
-    const uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (r >= rows) return;
-    float acc = 0.f;
-    for (uint64_t k = 0; k < spr; ++k) acc += part[r * spr + k];
-    if (y32) y32[r] = acc;
-    if (y16) y16[r] = __float2half_rn(acc);
-}
-
-cudaError_t launch_row_reduce(const float* part, uint64_t rows, uint64_t subs_per_row, float* y32, void* y16,
-                              cudaStream_t s) {
-    if (rows == 0) return cudaSuccess;
-    row_reduce_kernel<<<unsigned(ceil_div(rows, 256)), 256, 0, s>>>(part, rows, subs_per_row, y32,
-                                                                     static_cast<__half*>(y16));
-    return cudaGetLastError();
 }
 
 }  // namespace endor_b200

@@ -1,0 +1,102 @@
+// gather.cuh -- the branch-free bitmap -> dense gather shared by the expand
+// and fused decompress->GEMV kernels (selector tables + PRMT byte permutes),
+// and the f16 dot product used by the GEMV consumers.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace endor_b200 {
+
+// ---- selector tables ---------------------------------------------------------
+// A 4-element nibble q of the bitmap consumes popc(q) packed values.  The
+// next four packed values are fetched as an unaligned 8-byte window {x, y}
+// and PRMT drops each into its slot.  Zero bytes come from RZ (byte 4 of a
+// zero second operand), so no compare/select is needed:
+//   f16:  word0 (slots 0,1) = PRMT(x, 0, sel0)             -- needs v0..v1 at most
+//         ym               = PRMT(y, 0, selm)              -- y, or y with v3 zeroed
+//         word1 (slots 2,3) = PRMT(x, ym, sel1)            -- unset slots read ym bytes 6,7
+//   i8:   word  (slots 0-3) = PRMT(x, 0, sel)
+// selm keeps y whole only when q == 0xF (then no slot is unset).  The f16
+// table packs sel0 | sel1 << 16 into one word: 16 words in 16 distinct banks,
+// so a warp's lookups never conflict (one wavefront per LDS).
+__shared__ uint32_t g_lut16[16];
+__shared__ uint32_t g_lut8[16];
+
+__device__ __forceinline__ void init_luts(int tid) {
+    if (tid < 16) {
+        const uint32_t q = tid;
+        uint32_t s0 = 0, s1 = 0, j = 0, s8 = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const bool set = q & (1u << k);
+            const uint32_t b0 = set ? 2 * j : (k < 2 ? 4u : 6u);
+            const uint32_t b1 = set ? 2 * j + 1 : (k < 2 ? 4u : 7u);
+            const uint32_t pos = (k & 1) * 8;
+            if (k < 2) s0 |= (b0 << pos) | (b1 << (pos + 4));
+            else s1 |= (b0 << pos) | (b1 << (pos + 4));
+            s8 |= (set ? j : 4u) << (4 * k);
+            j += set;
+        }
+        g_lut16[q] = s0 | (s1 << 16);
+        g_lut8[q] = s8;
+    }
+}
+
+// Expand one 16-byte output chunk.  m: the chunk's bitmap bits; a: shared
+// address of its first packed value (any byte alignment).
+template <int EB>
+__device__ __forceinline__ uint4 gather_chunk(uint32_t m, uint32_t a) {
+    uint32_t o[4];
+    if constexpr (EB == 2) {
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+            const uint32_t q = (m >> (4 * g)) & 15u;
+            const uint32_t sel = g_lut16[q];
+            const uint32_t al = a & ~3u, sh = a << 3;  // funnel shifts wrap mod 32
+            const uint32_t w0 = lds32(al), w1 = lds32(al + 4), w2 = lds32(al + 8);
+            const uint32_t x = __funnelshift_r(w0, w1, sh);
+            const uint32_t y = __funnelshift_r(w1, w2, sh);
+            const uint32_t ym = __byte_perm(y, 0u, q == 15u ? 0x3210u : 0x4410u);
+            o[2 * g] = __byte_perm(x, 0u, sel);
+            o[2 * g + 1] = __byte_perm(x, ym, sel >> 16);
+            a += 2 * __popc(q);
+        }
+    } else {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            const uint32_t qa = (m >> (4 * g)) & 15u;
+            const uint32_t sel = g_lut8[qa];
+            const uint32_t al = a & ~3u, sh = a << 3;
+            const uint32_t x = __funnelshift_r(lds32(al), lds32(al + 4), sh);
+            o[g] = __byte_perm(x, 0u, sel);
+            a += __popc(qa);
+        }
+    }
+    return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
+// acc += dot(w[0..7], x[0..7]) over f16 pairs with fp32 accumulation: the
+// sm_100 mixed-precision FMA (PTX fma.rn.f32.f16, SASS FHFMA with .H0/.H1
+// operand selects) -- one instruction per element, no f16->f32 conversions;
+// bit-identical to fmaf(float(w), float(x), acc).
+__device__ __forceinline__ float fma_f16x2(uint32_t w, uint32_t x, float acc) {
+    asm("{\n\t.reg .b16 wl, wh, xl, xh;\n\t"
+        "mov.b32 {wl, wh}, %1;\n\t"
+        "mov.b32 {xl, xh}, %2;\n\t"
+        "fma.rn.f32.f16 %0, wl, xl, %0;\n\t"
+        "fma.rn.f32.f16 %0, wh, xh, %0;\n\t}"
+        : "+f"(acc) : "r"(w), "r"(x));
+    return acc;
+}
+__device__ __forceinline__ float dot8_f16(const uint4& w, const uint4& x, float acc) {
+    acc = fma_f16x2(w.x, x.x, acc);
+    acc = fma_f16x2(w.y, x.y, acc);
+    acc = fma_f16x2(w.z, x.z, acc);
+    acc = fma_f16x2(w.w, x.w, acc);
+    return acc;
+}
+
+}  // namespace endor_b200

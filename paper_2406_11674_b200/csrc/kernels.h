@@ -69,6 +69,7 @@ struct BatchTensor {
     const void* x;          // f16 [cols]
     float* part;            // fp32 partials, one per sub-tile
     uint64_t cols;
+    uint64_t item0;         // fused GEMV: first work item (8 rows x 1024 cols) of this tensor
 };
 struct Batch {
     BatchTensor t[kMaxBatch];
@@ -94,10 +95,11 @@ __host__ __device__ inline int batch_tensor_of_cblk(const Batch& b, uint32_t g) 
 // (ws_layout_caps capacities).
 void batch_plan(Batch& b, uint64_t* sub_total, uint64_t* blk_total, int count_ctas);
 cudaError_t launch_count(const Batch& b, cudaStream_t s);
-cudaError_t launch_expand_tma(const Batch& b, int mode, cudaStream_t s);  // 1 i8, 2 f16, 3 dequant, 4 gemv
-// y[r] = sum of the cols/1024 sub-tile partials of row r (fixed order: deterministic)
-cudaError_t launch_row_reduce(const float* part, uint64_t rows, uint64_t subs_per_row, float* y32, void* y16,
-                              cudaStream_t s);
+cudaError_t launch_expand_tma(const Batch& b, int mode, cudaStream_t s);  // 1 i8, 2 f16, 3 dequant
+// fused decompress -> GEMV over a batch (f16, cols % 1024 == 0, part set per tensor),
+// then y[r] = sum of row r's cols/1024 segment partials in a fixed order
+cudaError_t launch_gemv_fused(Batch& b, cudaStream_t s);
+cudaError_t launch_row_reduce_batch(const Batch& b, float* const* y32, void* const* y16, cudaStream_t s);
 
 // Rank lookups over count_kernel's two-level table for one tensor.
 struct RankTable {
