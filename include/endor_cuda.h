@@ -246,6 +246,13 @@ int endor_cuda_quantize_values(const void* values_f16, uint64_t nnz, void* q_out
 int endor_cuda_gemv(uint64_t rows, uint64_t cols, const void* w_f16, const void* x_f16,
                     float* y_f32, void* y_f16, void* stream);
 
+/* Batched dense GEMV: y_i = W_i x_i for up to 16 matrices (one decoder
+ * layer) in one launch.  y_f32 / y_f16 arrays (and their entries) may be
+ * NULL, not both for a matrix.  Same numerics as endor_cuda_gemv. */
+int endor_cuda_gemv_batch(const uint64_t* rows, const uint64_t* cols, const void* const* w_f16,
+                          const void* const* x_f16, float* const* y_f32, void* const* y_f16, int count,
+                          void* stream);
+
 /* Fused decompress -> GEMV: y = W x straight from the
  * compressed W (bitmap + packed values) -- the dense W is never written, so
  * HBM traffic is 1/8 + 2(1-s) bytes per weight instead of decompress (write

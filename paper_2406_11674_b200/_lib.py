@@ -81,6 +81,8 @@ SIGNATURES = {
     "endor_cuda_synth_weight": (C.c_int, [_u64, _u64, _i32, _u64, _u64, _u64, _vp, _vp]),
     "endor_cuda_magnitude_prune": (C.c_int, [_u64, _i32, _f64, _vp, _vp, _sz, _vp]),
     "endor_cuda_gemv": (C.c_int, [_u64, _u64, _vp, _vp, _vp, _vp, _vp]),
+    "endor_cuda_gemv_batch": (C.c_int, [C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_vp), C.POINTER(_vp),
+                                        C.POINTER(_vp), C.POINTER(_vp), C.c_int, _vp]),
     "endor_pipeline_create": (C.c_int, [C.c_int, _u64, C.c_int, C.POINTER(_vp)]),
     "endor_pipeline_destroy": (C.c_int, [_vp]),
     "endor_pipeline_run": (C.c_int, [_vp, C.POINTER(PipelineOp), C.c_int, C.c_int]),

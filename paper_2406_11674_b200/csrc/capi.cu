@@ -725,6 +725,40 @@ int endor_cuda_gemv(uint64_t rows, uint64_t cols, const void* w_f16, const void*
     return ENDOR_OK;
 }
 
+int endor_cuda_gemv_batch(const uint64_t* rows, const uint64_t* cols, const void* const* w_f16,
+                          const void* const* x_f16, float* const* y_f32, void* const* y_f16, int count,
+                          void* stream) {
+    if (count < 0 || count > kMaxBatch || (count > 0 && (!rows || !cols || !w_f16 || !x_f16)))
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "batch must hold 0..16 GEMVs");
+    GemvBatch gb{};
+    for (int i = 0; i < count; ++i) {
+        uint64_t n;
+        if (!checked_n(rows[i], cols[i], &n))
+            return fail(ENDOR_ERR_SIZE, "matrix dimensions overflow the addressable element count");
+        float* y32 = y_f32 ? y_f32[i] : nullptr;
+        void* y16 = y_f16 ? y_f16[i] : nullptr;
+        if (rows[i] == 0) continue;
+        if ((cols[i] > 0 && (!w_f16[i] || !x_f16[i])) || (!y32 && !y16))
+            return fail(ENDOR_ERR_INVALID_ARGUMENT, "null buffer");
+        if (cols[i] % 8 || !aligned(w_f16[i], 16) || !aligned(x_f16[i], 16)) {
+            // outside the vector layout: run it alone on the generic kernel
+            if (!aligned(w_f16[i], 2) || !aligned(x_f16[i], 2))
+                return fail(ENDOR_ERR_INVALID_ARGUMENT, "misaligned f16 buffer");
+            CK(launch_gemv(rows[i], cols[i], w_f16[i], x_f16[i], y32, y16, S(stream)));
+            continue;
+        }
+        gb.rows[gb.count] = rows[i];
+        gb.cols[gb.count] = cols[i];
+        gb.w[gb.count] = w_f16[i];
+        gb.x[gb.count] = x_f16[i];
+        gb.y32[gb.count] = y32;
+        gb.y16[gb.count] = y16;
+        ++gb.count;
+    }
+    if (gb.count) CK(launch_gemv_batch(gb, S(stream)));
+    return ENDOR_OK;
+}
+
 // ---- host-buffer convenience (sync) --------------------------------------------
 namespace {
 struct DevBuf {

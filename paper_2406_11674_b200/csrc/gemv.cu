@@ -11,50 +11,53 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "gather.cuh"
 #include "kernels.h"
 
 namespace endor_b200 {
 
 constexpr int kGemvThreads = 256;
 
-__device__ __forceinline__ float dot8(const uint4& w, const uint4& x) {
-    const __half2* wh = reinterpret_cast<const __half2*>(&w);
-    const __half2* xh = reinterpret_cast<const __half2*>(&x);
-    float acc = 0.f;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const float2 a = __half22float2(wh[i]);
-        const float2 b = __half22float2(xh[i]);
-        acc = fmaf(a.x, b.x, acc);
-        acc = fmaf(a.y, b.y, acc);
-    }
-    return acc;
-}
-
-// cols % 8 == 0 and 16-byte aligned W / x: vector path.
-template <int R>
-__global__ void __launch_bounds__(kGemvThreads) gemv_vec_kernel(const uint4* __restrict__ W,
-                                                                 const uint4* __restrict__ x,
-                                                                 uint64_t rows, uint64_t cols8,
-                                                                 float* y32, __half* y16) {
+// One launch for a whole batch (a decoder layer's ops): warp g owns R rows of
+// tensor k (k found from the per-tensor warp prefix), lanes stride the rows
+// with 16-byte streaming loads, U iterations in flight; every x load is
+// reused across the R rows.  The f16 x f16 products accumulate in fp32 with
+// FHFMA (fma.rn.f32.f16, one instruction per weight).
+template <int R, int U>
+__global__ void __launch_bounds__(kGemvThreads) gemv_batch_kernel(const __grid_constant__ GemvBatch gb) {
     const int lane = threadIdx.x & 31;
-    const uint64_t warp = (uint64_t(blockIdx.x) * kGemvThreads + threadIdx.x) >> 5;
-    const uint64_t r0 = warp * R;
-    if (r0 >= rows) return;
-    float acc[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) acc[r] = 0.f;
+    const uint64_t g = (uint64_t(blockIdx.x) * kGemvThreads + threadIdx.x) >> 5;
+    if (g >= gb.warp0[gb.count]) return;
+    int k = 0;
+    while (g >= gb.warp0[k + 1]) ++k;
+    const uint64_t rows = gb.rows[k], cols8 = gb.cols[k] / 8;
+    const uint64_t r0 = (g - gb.warp0[k]) * R;
+    const uint4* __restrict__ W = static_cast<const uint4*>(gb.w[k]);
+    const uint4* __restrict__ x = static_cast<const uint4*>(gb.x[k]);
     const uint4* wr[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) wr[r] = W + min(r0 + r, rows - 1) * cols8;
-#pragma unroll 2
-    for (uint64_t c = lane; c < cols8; c += 32) {
+    float acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.f;
+    uint64_t c = lane;
+    for (; c + 32 * (U - 1) < cols8; c += 32 * U) {
+        uint4 xv[U], wv[U][R];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            xv[u] = __ldg(x + c + 32 * u);
+#pragma unroll
+            for (int r = 0; r < R; ++r) wv[u][r] = __ldcs(wr[r] + c + 32 * u);  // streamed once: evict-first
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc[r] = dot8_f16(wv[u][r], xv[u], acc[r]);
+    }
+    for (; c < cols8; c += 32) {
         const uint4 xv = __ldg(x + c);
-        uint4 wv[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) wv[r] = __ldcs(wr[r] + c);  // streamed once: evict-first
-#pragma unroll
-        for (int r = 0; r < R; ++r) acc[r] += dot8(wv[r], xv);
+        for (int r = 0; r < R; ++r) acc[r] = dot8_f16(__ldcs(wr[r] + c), xv, acc[r]);
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -65,11 +68,26 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_vec_kernel(const uint4* __r
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             if (r0 + r < rows) {
-                if (y32) y32[r0 + r] = acc[r];
-                if (y16) y16[r0 + r] = __float2half_rn(acc[r]);
+                if (gb.y32[k]) gb.y32[k][r0 + r] = acc[r];
+                if (gb.y16[k]) static_cast<__half*>(gb.y16[k])[r0 + r] = __float2half_rn(acc[r]);
             }
         }
     }
+}
+
+constexpr int kGemvRows = 2, kGemvUnroll = 4;
+
+cudaError_t launch_gemv_batch(GemvBatch& gb, cudaStream_t s) {
+    uint64_t warps = 0;
+    for (int k = 0; k < gb.count; ++k) {
+        gb.warp0[k] = warps;
+        warps += ceil_div(gb.rows[k], kGemvRows);
+    }
+    gb.warp0[gb.count] = warps;
+    if (warps == 0) return cudaSuccess;
+    const unsigned grid = unsigned(ceil_div(warps * 32, kGemvThreads));
+    gemv_batch_kernel<kGemvRows, kGemvUnroll><<<grid, kGemvThreads, 0, s>>>(gb);
+    return cudaGetLastError();
 }
 
 // Generic (any cols / alignment) path: one warp per row, scalar halves.
@@ -97,18 +115,19 @@ cudaError_t launch_gemv(uint64_t rows, uint64_t cols, const void* w, const void*
     const bool vec = (cols % 8 == 0) && ((reinterpret_cast<uintptr_t>(w) & 15) == 0) &&
                      ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
     if (vec) {
-        constexpr int R = 4;
-        const uint64_t warps = ceil_div(rows, R);
-        const unsigned grid = unsigned(ceil_div(warps * 32, kGemvThreads));
-        gemv_vec_kernel<R><<<grid, kGemvThreads, 0, s>>>(static_cast<const uint4*>(w),
-                                                          static_cast<const uint4*>(x), rows,
-                                                          cols / 8, y32, static_cast<__half*>(y16));
-    } else {
-        const unsigned grid = unsigned(ceil_div(rows * 32, kGemvThreads));
-        gemv_scalar_kernel<<<grid, kGemvThreads, 0, s>>>(static_cast<const __half*>(w),
-                                                          static_cast<const __half*>(x), rows, cols,
-                                                          y32, static_cast<__half*>(y16));
+        GemvBatch gb{};
+        gb.count = 1;
+        gb.rows[0] = rows;
+        gb.cols[0] = cols;
+        gb.w[0] = w;
+        gb.x[0] = x;
+        gb.y32[0] = y32;
+        gb.y16[0] = y16;
+        return launch_gemv_batch(gb, s);
     }
+    const unsigned grid = unsigned(ceil_div(rows * 32, kGemvThreads));
+    gemv_scalar_kernel<<<grid, kGemvThreads, 0, s>>>(static_cast<const __half*>(w), static_cast<const __half*>(x),
+                                                      rows, cols, y32, static_cast<__half*>(y16));
     return cudaGetLastError();
 }
 

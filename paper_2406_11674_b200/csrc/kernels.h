@@ -131,6 +131,17 @@ cudaError_t launch_compact(const void* dense, uint64_t n, int eb, const void* bi
                            const WsLayout& L, void* values, cudaStream_t s);
 cudaError_t launch_gemv(uint64_t rows, uint64_t cols, const void* w, const void* x, float* y32,
                         void* y16, cudaStream_t s);
+// dense GEMV over a batch: cols % 8 == 0, 16-byte aligned W and x
+struct GemvBatch {
+    const void* w[kMaxBatch];
+    const void* x[kMaxBatch];
+    float* y32[kMaxBatch];
+    void* y16[kMaxBatch];
+    uint64_t rows[kMaxBatch], cols[kMaxBatch];
+    uint64_t warp0[kMaxBatch + 1];  // filled by launch_gemv_batch
+    int count;
+};
+cudaError_t launch_gemv_batch(GemvBatch& gb, cudaStream_t s);
 cudaError_t launch_quantize(const void* vals, uint64_t nnz, void* q, float* scale_dev, unsigned int* amax,
                             cudaStream_t s);
 

@@ -55,6 +55,16 @@ def dense_gemv():
         E.gemv(dense[k], xs[k], ys[k])
 
 
+U64 = C.c_uint64
+g_rows = (U64 * len(ts))(*[r for r, c in ops])
+g_cols = (U64 * len(ts))(*[c for r, c in ops])
+g_w = (P * len(ts))(*[d.data.data_ptr() for d in dense])
+
+
+def dense_gemv_batch():
+    E.check(L.endor_cuda_gemv_batch(g_rows, g_cols, g_w, x_arr, y_arr, None, len(ts), st))
+
+
 def timeit(fn, reps=20):
     for _ in range(3):
         fn()
@@ -74,7 +84,8 @@ res = {}
 for name, fn, byts in (("fused_batch_idx", lambda: fused_batch(True), comp),
                        ("fused_batch_count", lambda: fused_batch(False), comp),
                        ("fused_per_op_idx", fused_per_op, comp),
-                       ("dense_gemv", dense_gemv, dn)):
+                       ("dense_gemv", dense_gemv, dn),
+                       ("dense_gemv_batch", dense_gemv_batch, dn)):
     ms = timeit(fn)
     res[name] = {"ms": round(ms, 4), "gbs": round(byts / ms / 1e6, 1), "frac": round(byts / ms / 1e6 / PEAK, 3)}
     print(name, res[name], flush=True)
