@@ -326,6 +326,15 @@ def run_ours(args):
             pipe.run(ops_all, sync=True)
         st = pipe.stats()
         barrier()
+        # the same ops with W materialised (decompress, then dense GEMV), for contrast
+        mops = [HostOp(h.rows, h.cols, 0, h.bitmap, h.values, h.nnz, x=h.x, y=h.y, y_host=h.y_host,
+                       materialize=True) for h in hops]
+        pipe.run(mops, sync=True)
+        barrier()
+        pipe.run(mops * args.steps, sync=True)
+        sm_ = pipe.stats()
+        mat_ms = max_over_ranks(sm_["total_ms"]) / args.steps
+        mat_exposed = sm_["exposed_compute_ms"]
         e2e_ms_total = max_over_ranks(st["total_ms"])
         e2e_step = e2e_ms_total / args.steps
         h2d_rank = sum(h.compressed_bytes for h in hops)
@@ -351,11 +360,17 @@ def run_ours(args):
                "h2d_gbs_per_gpu": round(h2d_gbs, 2) if h2d_gbs else None,
                "h2d_pinned_peak_gbs": round(h2d_peak, 2),
                "h2d_frac_of_pcie_gen5": round(h2d_gbs / PCIE_GEN5_X16_GBS, 4) if h2d_gbs else None,
-               "decompress_ms_per_step": round(st["decompress_ms"] / args.steps, 4),
-               "gemv_ms_per_step": round(st["gemv_ms"] / args.steps, 4),
+               "fused_decompress_gemv_ms_per_step": round(st["decompress_ms"] / args.steps, 4),
                "exposed_compute_ms_per_run": round(st["exposed_compute_ms"], 4),
+               "materialized_w": {"layer_ms": round(mat_ms / world, 4),
+                                  "value": round(world * dense_rank / (mat_ms * 1e-3) / 1e9, 2),
+                                  "decompress_ms_per_step": round(sm_["decompress_ms"] / args.steps, 4),
+                                  "gemv_ms_per_step": round(sm_["gemv_ms"] / args.steps, 4),
+                                  "exposed_compute_ms_per_run": round(mat_exposed, 4),
+                                  "note": "decompress to a dense W ring, then dense GEMV (flags bit1)"},
                "gemv_max_rel_err": gemv_err,
-               "api": "endor_pipeline_run (C ABI), pinned host buffers",
+               "api": "endor_pipeline_run (C ABI), pinned host buffers; each op y = W x by the fused "
+                      "decompress -> GEMV kernel (W never in HBM)",
                "clocks": clk2.summary()}
         launches_e2e = int(st["kernel_launches"])
         # INT8 + Endor: the same layer quantized with
@@ -386,24 +401,47 @@ def run_ours(args):
         xs = [((torch.rand(s["cols"], generator=gx) * 2 - 1).half()).to(dev) for s in shards]
         ys = [torch.empty(s["rows"], dtype=torch.float32, device=dev) for s in shards]
 
-        def run_split():
+        import ctypes as C
+        P, U64 = C.c_void_p, C.c_uint64
+        def garr(typ, vals):
+            return (typ * len(vals))(*vals)
+
+        gem = [(garr(U64, [s["rows"] for s in g]), garr(U64, [s["cols"] for s in g]),
+                garr(P, [s["out"].data.data_ptr() for s in g]),
+                garr(P, [xs[gi * per_layer + j].data_ptr() for j in range(len(g))]),
+                garr(P, [ys[gi * per_layer + j].data_ptr() for j in range(len(g))]), len(g))
+               for gi, g in enumerate(groups)]
+
+        def run_split():  # decompress_chunked (1 launch / layer) + batched dense GEMV (1 launch / layer)
             for p in plans_idx:
                 p.launch(sp)
-            with torch.cuda.stream(stream):
-                for s, x, y in zip(shards, xs, ys):
-                    E.gemv(s["out"], x, y)
+            for r_, c_, w_, x_, y_, n_ in gem:
+                E.check(L.endor_cuda_gemv_batch(r_, c_, w_, x_, y_, None, n_, sp))
 
-        import ctypes as C
-        fws = torch.zeros(L.endor_cuda_workspace_bytes(nmax, 1), dtype=torch.uint8, device=dev)
-        fargs = [(s["t"].view(), s["idx"].prefix.contiguous(), x, y) for s, x, y in zip(shards, xs, ys)]
+        fviews = [(_lib.TensorView * len(g))(*[s["t"].view() for s in g]) for g in groups]
+        fws = torch.zeros(max(L.endor_cuda_workspace_bytes_batch(v, len(v)) for v in fviews),
+                          dtype=torch.uint8, device=dev)
+        fpre = [(P * len(g))(*[s["idx"].prefix.data_ptr() for s in g]) for g in groups]
+        fx = [(P * len(g))(*[xs[gi * per_layer + j].data_ptr() for j in range(len(g))]) for gi, g in enumerate(groups)]
+        fy = [(P * len(g))(*[ys[gi * per_layer + j].data_ptr() for j in range(len(g))]) for gi, g in enumerate(groups)]
 
-        def run_fused():  # async C-ABI calls on the timed stream, like the split path
-            for v, pre, x, y in fargs:
-                E.check(L.endor_cuda_gemv_compressed(C.byref(v), pre.data_ptr(), x.data_ptr(), y.data_ptr(), None,
-                                                     fws.data_ptr(), fws.numel(), sp))
+        def run_fused():  # one endor_cuda_gemv_compressed_batch call per layer (load-time 1024 RankIndex)
+            for v, pre, x, y in zip(fviews, fpre, fx, fy):
+                E.check(L.endor_cuda_gemv_compressed_batch(v, pre, x, y, None, len(v), fws.data_ptr(), fws.numel(),
+                                                           sp))
+
+        def run_fused_noidx():  # no index: count + flatten + fused + row-sum launches per layer
+            for v, x, y in zip(fviews, fx, fy):
+                E.check(L.endor_cuda_gemv_compressed_batch(v, None, x, y, None, len(v), fws.data_ptr(), fws.numel(),
+                                                           sp))
+
+        def run_gemv_only():
+            for r_, c_, w_, x_, y_, n_ in gem:
+                E.check(L.endor_cuda_gemv_batch(r_, c_, w_, x_, y_, None, n_, sp))
 
         res = {}
-        for name, fn in (("decompress_then_gemv_ms", run_split), ("fused_ms", run_fused)):
+        for name, fn in (("decompress_then_gemv_ms", run_split), ("fused_ms", run_fused),
+                         ("fused_no_index_ms", run_fused_noidx), ("dense_gemv_ms", run_gemv_only)):
             for _ in range(args.warmup):
                 fn()
             torch.cuda.synchronize()
@@ -414,14 +452,25 @@ def run_ours(args):
             b.record(stream)
             torch.cuda.synchronize()
             res[name] = max_over_ranks(a.elapsed_time(b)) / args.steps
+        # HBM bytes: fused reads the compressed W (+ x, the 1024 index, y partials);
+        # the dense GEMV reads the dense W
+        x_bytes = sum(s["cols"] * 2 for s in shards)
+        idx_bytes = sum((s["n"] // 1024) * 8 for s in shards)
+        fused_bytes = comp_rank + x_bytes + idx_bytes
         fused = {"decompress_then_gemv_ms": round(res["decompress_then_gemv_ms"], 4),
                  "fused_ms": round(res["fused_ms"], 4),
+                 "fused_no_index_ms": round(res["fused_no_index_ms"], 4),
                  "speedup": round(res["decompress_then_gemv_ms"] / res["fused_ms"], 3),
                  "fused_weight_gb_per_s": round(world * dense_rank / (res["fused_ms"] * 1e-3) / 1e9, 1),
-                 "note": "y = W x for the layer's six shards, 1024-chunk RankIndex; fused never writes W "
-                         "(1/8 + 2(1-s) B per weight read vs 5.125 for decompress + GEMV)"}
+                 "fused_hbm_frac": round(fused_bytes / (res["fused_ms"] * 1e-3) / 1e9 / peak, 4),
+                 "dense_gemv_ms": round(res["dense_gemv_ms"], 4),
+                 "dense_gemv_hbm_frac": round(dense_rank / (res["dense_gemv_ms"] * 1e-3) / 1e9 / peak, 4),
+                 "note": "y = W x for the layer's six shards; fused (one batched call, load-time 1024 RankIndex) "
+                         "never writes W: 1/8 + 2(1-s) B per weight read vs 5.125 for decompress + GEMV"}
         E.check(L.endor_cuda_sync_status(fws.data_ptr(), sp))
         # the fused y must equal the split path's y within fp32 rounding
+        run_fused()
+        torch.cuda.synchronize()
         ysplit = [y.clone() for y in ys]
         run_split()
         torch.cuda.synchronize()

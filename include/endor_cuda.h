@@ -285,7 +285,11 @@ typedef struct endor_pipeline_op {
     uint64_t rows, cols;
     int32_t dtype;           /* F16; or I8 with flags bit0 (dequantized to f16 on the fly) */
     int32_t flags;           /* bit0: values are i8 quantized with quant_scale (INT8 + Endor,
-                                PAPER.md:74): fused dequant + decompress -> f16 W */
+                                PAPER.md:74): fused dequant + decompress -> f16 W;
+                                bit1: materialise W (decompress, then dense GEMV) even when
+                                only y is asked for -- by default an f16 op with x/y, no
+                                dense_dev and cols % 1024 == 0 runs the fused
+                                decompress -> GEMV */
     const void* bitmap_host; /* pinned (cudaHostAlloc / endor_host_alloc) */
     const void* values_host; /* pinned */
     uint64_t nnz;

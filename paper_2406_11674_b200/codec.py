@@ -23,7 +23,7 @@ from __future__ import annotations
 import ctypes as C
 import enum
 from dataclasses import dataclass
-from typing import Dict, Optional, Tuple
+from typing import Dict, List, Optional, Sequence, Tuple
 
 import torch
 
@@ -373,6 +373,42 @@ def gemv_compressed(t: EndorTensor, x: torch.Tensor, index: Optional[RankIndex] 
     return y
 
 
+def gemv_compressed_batch(tensors: Sequence[EndorTensor], xs: Sequence[torch.Tensor],
+                          indices: Optional[Sequence[Optional[RankIndex]]] = None) -> List[torch.Tensor]:
+    """y_i = W_i x_i for a batch (e.g. one decoder layer's ops) in one fused
+    decompress -> GEMV launch; indices: optional 1024-chunk RankIndex per
+    tensor (None entries are counted on the device)."""
+    if len(tensors) != len(xs) or (indices is not None and len(indices) != len(tensors)):
+        raise InvalidArgument("one x (and optional index) per tensor")
+    if not tensors:
+        return []
+    dev = tensors[0].device
+    ys, keep = [], []
+    for t, x in zip(tensors, xs):
+        if t.dtype != Dtype.F16 or x.dtype != torch.float16 or x.numel() != t.cols:
+            raise InvalidArgument("gemv_compressed_batch needs f16 W [rows, cols] and f16 x [cols]")
+        ys.append(torch.empty(t.rows, dtype=torch.float32, device=dev))
+        keep.append(x.contiguous())
+    pres = []
+    for i in range(len(tensors)):
+        ix = indices[i] if indices is not None else None
+        if ix is not None and ix.chunk_size != 1024:
+            raise InvalidArgument("gemv_compressed_batch takes RankIndex entries at chunk size 1024")
+        pres.append(None if ix is None else ix.prefix.to(device=dev, dtype=torch.int64).contiguous())
+    n = len(tensors)
+    views = (_lib.TensorView * n)(*[t.view() for t in tensors])
+    P = C.c_void_p
+    pre_arr = (P * n)(*[_ptr(p) for p in pres])
+    x_arr = (P * n)(*[_ptr(x) for x in keep])
+    y_arr = (P * n)(*[_ptr(y) for y in ys])
+    L = _lib.lib()
+    ws = torch.zeros(max(L.endor_cuda_workspace_bytes_batch(views, n), 256), dtype=torch.uint8, device=dev)
+    check(L.endor_cuda_gemv_compressed_batch(views, pre_arr, x_arr, y_arr, None, n, ws.data_ptr(), ws.numel(),
+                                             _stream_ptr(dev)))
+    sync_status(ws, dev)
+    return ys
+
+
 def quantize_values(t: EndorTensor) -> EndorTensor:
     """codec.hpp:306-331 on the device: f16 packed values -> i8 + scale (the
     bitmap is shared, not copied)."""
@@ -558,3 +594,24 @@ def gemv(w: DenseMatrix, x: torch.Tensor, out_f32: Optional[torch.Tensor] = None
     check(_lib.lib().endor_cuda_gemv(w.rows, w.cols, _ptr(w.data), _ptr(x.contiguous()), _ptr(y), None,
                                      _stream_ptr(dev)))
     return y
+
+
+def gemv_batch(ws_: Sequence[DenseMatrix], xs: Sequence[torch.Tensor]) -> List[torch.Tensor]:
+    """y_i = W_i x_i for a batch of dense f16 matrices in one launch."""
+    if len(ws_) != len(xs):
+        raise InvalidArgument("one x per matrix")
+    if not ws_:
+        return []
+    dev = ws_[0].data.device
+    ys, keep = [], []
+    for w, x in zip(ws_, xs):
+        if w.dtype != Dtype.F16 or x.dtype != torch.float16 or x.numel() != w.cols:
+            raise InvalidArgument("gemv_batch needs f16 W [rows, cols] and f16 x [cols]")
+        ys.append(torch.empty(w.rows, dtype=torch.float32, device=dev))
+        keep.append(x.contiguous())
+    n = len(ws_)
+    U, P = C.c_uint64, C.c_void_p
+    check(_lib.lib().endor_cuda_gemv_batch((U * n)(*[w.rows for w in ws_]), (U * n)(*[w.cols for w in ws_]),
+                                           (P * n)(*[_ptr(w.data) for w in ws_]), (P * n)(*[_ptr(x) for x in keep]),
+                                           (P * n)(*[_ptr(y) for y in ys]), None, n, _stream_ptr(dev)))
+    return ys

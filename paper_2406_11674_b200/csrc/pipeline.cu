@@ -8,6 +8,8 @@
 // on a dedicated copy stream into a ring of device staging slots; the compute
 // stream waits on the slot's copy event, runs scan + expand + GEMV, and
 // releases the slot, so H2D of op i+1.. overlaps decompress+GEMV of op i.
+// When the caller only wants y = W x (no dense_dev), the op runs as one fused
+// decompress -> GEMV (gemv_fused.cu): the dense W never touches HBM.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -153,22 +155,34 @@ int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops
         // compute stream: decompress into the dense ring (or the caller's buffer), then GEMV
         PK(cudaStreamWaitEvent(p->compute, p->h2d_end[i], 0));
         PK(cudaEventRecord(p->dec_beg[i], p->compute));
-        void* dst = op.dense_dev ? op.dense_dev : p->dense[i & 1];
         endor_tensor_view v{op.rows, op.cols, op.dtype, 0, slot.bitmap, slot.values, op.nnz};
-        st = deq ? endor_cuda_decompress_dequant(&v, op.quant_scale, dst, p->ws, p->ws_bytes, p->compute)
-                 : endor_cuda_decompress(&v, dst, p->ws, p->ws_bytes, p->compute);
-        if (st) return st;
-        launches += 2;
-        PK(cudaEventRecord(p->dec_end[i], p->compute));
-        PK(cudaEventRecord(slot.free_ev, p->compute));
-        if (op.x_dev && op.y_dev) {
-            st = endor_cuda_gemv(op.rows, op.cols, dst, op.x_dev, op.y_dev, nullptr, p->compute);
+        // y = W x with W never observed by the caller: fused decompress -> GEMV
+        // (no dense W in HBM) unless flags bit1 asks for the materialised path
+        const bool fused = op.x_dev && op.y_dev && !op.dense_dev && !deq && op.dtype == ENDOR_DTYPE_F16 &&
+                           op.cols % 1024 == 0 && !(op.flags & 2);
+        if (fused) {
+            st = endor_cuda_gemv_compressed(&v, nullptr, op.x_dev, op.y_dev, nullptr, p->ws, p->ws_bytes,
+                                            p->compute);
             if (st) return st;
-            launches += 1;
-            if (op.y_host)
-                PK(cudaMemcpyAsync(op.y_host, op.y_dev, op.rows * sizeof(float), cudaMemcpyDeviceToHost,
-                                   p->compute));
+            launches += 4;  // count, flatten, fused GEMV, row sum
+            PK(cudaEventRecord(p->dec_end[i], p->compute));
+            PK(cudaEventRecord(slot.free_ev, p->compute));
+        } else {
+            void* dst = op.dense_dev ? op.dense_dev : p->dense[i & 1];
+            st = deq ? endor_cuda_decompress_dequant(&v, op.quant_scale, dst, p->ws, p->ws_bytes, p->compute)
+                     : endor_cuda_decompress(&v, dst, p->ws, p->ws_bytes, p->compute);
+            if (st) return st;
+            launches += 2;
+            PK(cudaEventRecord(p->dec_end[i], p->compute));
+            PK(cudaEventRecord(slot.free_ev, p->compute));
+            if (op.x_dev && op.y_dev) {
+                st = endor_cuda_gemv(op.rows, op.cols, dst, op.x_dev, op.y_dev, nullptr, p->compute);
+                if (st) return st;
+                launches += 1;
+            }
         }
+        if (op.x_dev && op.y_dev && op.y_host)
+            PK(cudaMemcpyAsync(op.y_host, op.y_dev, op.rows * sizeof(float), cudaMemcpyDeviceToHost, p->compute));
         PK(cudaEventRecord(p->op_end[i], p->compute));
         h2d += bmb + vb;
         dense += n * ob;

@@ -5,7 +5,9 @@ Decompress -> Compute, strictly sequential (sim.hpp:196-224).  Here the
 stages run for real and overlap: the C++ pipeline (csrc/pipeline.cu) streams
 each op's bitmap + values from pinned host memory on a copy stream into a
 double-buffered device ring while the compute stream decompresses and runs
-the GEMV of the previous op.
+the GEMV of the previous op -- as one fused decompress -> GEMV kernel when
+only y is wanted (the dense W never lands in HBM), or decompress + dense GEMV
+when the op asks for W (``dense``) or ``materialize=True``.
 """
 from __future__ import annotations
 
@@ -33,6 +35,7 @@ class HostOp:
     y_host: Optional[torch.Tensor] = None  # pinned f32 [rows]
     dense: Optional[torch.Tensor] = None   # device uint8 [rows*cols*eb] (optional)
     quant_scale: Optional[float] = None    # i8 values dequantized to f16 W (INT8 + Endor)
+    materialize: bool = False              # decompress W, then dense GEMV (default: fused when possible)
 
     @property
     def compressed_bytes(self) -> int:
@@ -74,7 +77,8 @@ class OffloadPipeline:
         arr = (_lib.PipelineOp * len(ops))()
         for i, o in enumerate(ops):
             deq = o.quant_scale is not None
-            arr[i] = _lib.PipelineOp(o.rows, o.cols, o.dtype, 1 if deq else 0, _p(o.bitmap), _p(o.values), o.nnz,
+            flags = (1 if deq else 0) | (2 if o.materialize else 0)
+            arr[i] = _lib.PipelineOp(o.rows, o.cols, o.dtype, flags, _p(o.bitmap), _p(o.values), o.nnz,
                                      _p(o.x), _p(o.y), _p(o.dense), _p(o.y_host),
                                      float(o.quant_scale) if deq else 0.0, 0)
         self._keep = (arr, ops)

@@ -49,3 +49,73 @@ def test_fused_gemv_rejects_unsupported(E):
     t = E.EndorTensor(4, 1000, E.Dtype.F16, E.Bitmap(4000, data=b), v)
     with pytest.raises(E.InvalidArgument):  # cols % 1024 != 0
         E.gemv_compressed(t, torch.zeros(1000, dtype=torch.float16, device="cuda"))
+
+
+def _layer(E, shapes, s, seed0):
+    ts, ws, xs = [], [], []
+    for i, (r, c) in enumerate(shapes):
+        w = E.synth_weight(r, c, seed0 + i, device="cuda")
+        if s > 0:
+            E.magnitude_prune(w, s, inplace=True)
+        ts.append(E.compress(w))
+        ws.append(w)
+        g = torch.Generator(device="cpu").manual_seed(seed0 + 100 + i)
+        xs.append(((torch.rand(c, generator=g) * 2 - 1).half()).cuda())
+    return ts, ws, xs
+
+
+@pytest.mark.parametrize("with_index", [False, True])
+def test_fused_gemv_batch_mixed_shapes(E, with_index):
+    """One batched launch over ragged shapes (rows % 8 != 0, cols from 1 to 36
+    segments, a sub-8-sub-tile tensor) equals the per-tensor fused path and the
+    fp32 reference of the decompressed W."""
+    shapes = [(37, 2048), (9, 36864), (300, 9216), (1, 1024), (64, 8192), (3, 3072)]
+    ts, ws, xs = _layer(E, shapes, 0.5, 900)
+    idx = [E.build_rank_index(t.bitmap, 1024) for t in ts] if with_index else None
+    ys = E.gemv_compressed_batch(ts, xs, idx)
+    for t, w, x, y in zip(ts, ws, xs, ys):
+        ref = w.data.view(torch.float16).reshape(t.rows, t.cols).float() @ x.float()
+        assert (y - ref).abs().max().item() <= 1e-3 * ref.abs().max().item() + 1e-6
+        assert torch.equal(y, E.gemv_compressed(t, x))  # same partials, same order
+
+
+def test_fused_gemv_batch_detects_bad_index(E):
+    ts, ws, xs = _layer(E, [(64, 2048), (16, 4096)], 0.5, 77)
+    idx = [E.build_rank_index(t.bitmap, 1024) for t in ts]
+    bad = idx[1].prefix.clone()
+    bad[5] += 3  # a middle entry inconsistent with the bitmap
+    idx[1] = E.RankIndex(1024, bad)
+    with pytest.raises(E.CorruptionError):
+        E.gemv_compressed_batch(ts, xs, idx)
+
+
+def test_dense_gemv_batch_matches_fp32_reference(E):
+    shapes = [(9216, 1024), (5, 36864), (1000, 9216), (33, 8)]
+    ts, ws, xs = _layer(E, shapes, 0.3, 4242)
+    ys = E.gemv_batch(ws, xs)
+    for w, x, y in zip(ws, xs, ys):
+        ref = w.data.view(torch.float16).reshape(w.rows, w.cols).float() @ x.float()
+        assert (y - ref).abs().max().item() <= 1e-3 * ref.abs().max().item() + 1e-6
+        assert torch.equal(y, E.gemv(w, x))  # batched launch == single launch, bitwise
+
+
+def test_pipeline_fused_matches_materialized(E):
+    """The offload pipeline's default fused decompress -> GEMV and its
+    materialised path (flags bit1) give the same y within fp32 rounding."""
+    from paper_2406_11674_b200.pipeline import HostOp, OffloadPipeline, pinned_copy
+    shapes = [(96, 2048), (40, 9216), (7, 1000)]  # the last one cannot fuse (cols % 1024)
+    ts, ws, xs = _layer(E, shapes, 0.5, 31337)
+    outs = {}
+    for mat in (False, True):
+        ops = [HostOp(t.rows, t.cols, 0, pinned_copy(t.bitmap.data), pinned_copy(t.values), t.nnz(), x=x,
+                      y=torch.empty(t.rows, dtype=torch.float32, device="cuda"),
+                      y_host=torch.empty(t.rows, dtype=torch.float32, pin_memory=True), materialize=mat)
+               for t, x in zip(ts, xs)]
+        p = OffloadPipeline(0, max(t.element_count() for t in ts))
+        p.run(ops, sync=True)
+        p.close()
+        outs[mat] = [o.y_host.clone() for o in ops]
+    for a, b, w, x in zip(outs[False], outs[True], ws, xs):
+        ref = (w.data.view(torch.float16).reshape(w.rows, w.cols).float() @ x.float()).cpu()
+        tol = 1e-3 * ref.abs().max().item() + 1e-6
+        assert (a - ref).abs().max().item() <= tol and (b - ref).abs().max().item() <= tol
