@@ -66,8 +66,20 @@ typedef enum endor_status {
     ENDOR_ERR_BOUNDS = 3,           /* BoundsError      error.hpp:28-31  */
     ENDOR_ERR_INVALID_ARGUMENT = 4, /* std::invalid_argument             */
     ENDOR_ERR_CUDA = 5,             /* CUDA runtime failure (no reference analogue) */
-    ENDOR_ERR_CONFIG = 6            /* ConfigError      error.hpp:34-37  */
+    ENDOR_ERR_CONFIG = 6,           /* ConfigError      error.hpp:34-37  */
+    ENDOR_ERR_FORMAT = 7,           /* FormatError      error.hpp:42-60; kind: endor_cuda_last_format_kind() */
+    ENDOR_ERR_IO = 8                /* Error("cannot open ..." / "short read ...") file_io.hpp:159-172 */
 } endor_status;
+
+/* FormatError::Kind (error.hpp:45-52) */
+typedef enum endor_format_kind {
+    ENDOR_FMT_TRUNCATED = 0,
+    ENDOR_FMT_BAD_MAGIC = 1,
+    ENDOR_FMT_BAD_VERSION = 2,
+    ENDOR_FMT_BAD_CRC = 3,
+    ENDOR_FMT_COUNT_MISMATCH = 4,
+    ENDOR_FMT_MALFORMED = 5
+} endor_format_kind;
 
 /* Dtype codes, dense_matrix.hpp:18-21 (also the on-disk codes). */
 #define ENDOR_DTYPE_F16 0
@@ -272,6 +284,53 @@ int endor_cuda_gemv_compressed(const endor_tensor_view* t, const uint64_t* prefi
 int endor_cuda_gemv_compressed_batch(const endor_tensor_view* views, const uint64_t* const* prefixes1024,
                                      const void* const* x_f16, float* const* y_f32, void* const* y_f16,
                                      int count, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- storage: .endor containers straight to the GPU ---- */
+/* The EndorDirect mode (SsdToGpu, sim.hpp:205-214), executed
+ * for real.  Replaces read_endor_file / decode_endor (file_io.hpp:212-277)
+ * for a device-resident result: the bitmap and values sections land in
+ * caller-owned device buffers. */
+
+typedef struct endor_file_info {
+    uint64_t rows, cols, nnz;
+    int32_t dtype, flags;          /* flags bit0 quantized, bit1 negative-zero collapsed */
+    float quant_scale;             /* flags bit0 */
+    uint32_t crc;                  /* stored CRC-32 (IEEE, zlib) of every preceding byte */
+    uint32_t header_crc;           /* CRC-32 of the header bytes alone */
+    uint32_t reserved;
+    uint64_t header_bytes, bitmap_offset, bitmap_bytes, values_offset, values_bytes, file_bytes;
+} endor_file_info;
+
+/* Parse and validate the header and the declared layout in decode_endor's
+ * order (magic, version, dtype, flags, fields, rows*cols, nnz, size:
+ * file_io.hpp:212-252).  ENDOR_ERR_FORMAT + endor_cuda_last_format_kind(). */
+int endor_file_probe(const char* path, endor_file_info* out);
+int endor_cuda_last_format_kind(void);
+
+/* encode_endor (file_io.hpp:187-210), byte-identical: returns the container
+ * size (out == NULL: just the size; 0 on bad arguments / short out_cap). */
+size_t endor_file_encode(uint64_t rows, uint64_t cols, int32_t dtype, int32_t flags, float quant_scale,
+                         const void* bitmap, const void* values, uint64_t nnz, void* out, size_t out_cap);
+
+#define ENDOR_IO_AUTO 0          /* GDS if nvidia-fs is loaded, else POSIX */
+#define ENDOR_IO_GDS 1           /* cuFile with nvidia-fs: NVMe -> HBM DMA */
+#define ENDOR_IO_CUFILE_COMPAT 2 /* cuFile compatibility mode (POSIX inside cuFile); only with
+                                    ENDOR_ALLOW_CUFILE_COMPAT=1 -- its driver open hangs without
+                                    nvidia-fs on this pool's boxes */
+#define ENDOR_IO_POSIX 3         /* O_DIRECT reads into two pinned bounce buffers + async H2D */
+typedef struct endor_reader endor_reader;
+int endor_reader_create(int device_ordinal, size_t bounce_bytes, int mode, endor_reader** out);
+int endor_reader_destroy(endor_reader* r);
+int endor_reader_mode(const endor_reader* r); /* the ENDOR_IO_* actually in use */
+/* Read the bitmap and values sections of `path` (probed into f) into device
+ * buffers.  Returns after the data is on the device.  verify != 0 completes
+ * decode_endor's checks on the device copy (file_io.hpp:253-270): CRC-32 of
+ * the whole file computed on the GPU (BadCrc), padding bits (Malformed),
+ * popcount == nnz (CountMismatch); needs a workspace for rows*cols. */
+int endor_reader_read(endor_reader* r, const char* path, const endor_file_info* f, void* bitmap_dev,
+                      void* values_dev, int verify, void* ws, size_t ws_bytes, void* stream);
+/* Cumulative wall time and bytes of endor_reader_read's transfers. */
+int endor_reader_stats(const endor_reader* r, double* seconds, uint64_t* bytes);
 
 /* ---- offload pipeline ---------------------------------------------------- */
 /* Streams compressed ops from pinned host memory through a double-buffered

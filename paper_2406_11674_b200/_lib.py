@@ -37,6 +37,14 @@ class PipelineStats(C.Structure):
                 ("kernel_launches", _u64)]
 
 
+class FileInfo(C.Structure):
+    """endor_file_info."""
+    _fields_ = [("rows", _u64), ("cols", _u64), ("nnz", _u64), ("dtype", _i32), ("flags", _i32),
+                ("quant_scale", C.c_float), ("crc", C.c_uint32), ("header_crc", C.c_uint32),
+                ("reserved", C.c_uint32), ("header_bytes", _u64), ("bitmap_offset", _u64),
+                ("bitmap_bytes", _u64), ("values_offset", _u64), ("values_bytes", _u64), ("file_bytes", _u64)]
+
+
 # name -> (restype, argtypes): every symbol include/endor_cuda.h declares
 SIGNATURES = {
     "endor_cuda_abi_version": (C.c_int, []),
@@ -88,6 +96,14 @@ SIGNATURES = {
     "endor_pipeline_run": (C.c_int, [_vp, C.POINTER(PipelineOp), C.c_int, C.c_int]),
     "endor_pipeline_stats_get": (C.c_int, [_vp, C.POINTER(PipelineStats)]),
     "endor_pipeline_stream": (_vp, [_vp]),
+    "endor_cuda_last_format_kind": (C.c_int, []),
+    "endor_file_probe": (C.c_int, [C.c_char_p, C.POINTER(FileInfo)]),
+    "endor_file_encode": (_sz, [_u64, _u64, _i32, _i32, C.c_float, _vp, _vp, _u64, _vp, _sz]),
+    "endor_reader_create": (C.c_int, [C.c_int, _sz, C.c_int, C.POINTER(_vp)]),
+    "endor_reader_destroy": (C.c_int, [_vp]),
+    "endor_reader_mode": (C.c_int, [_vp]),
+    "endor_reader_read": (C.c_int, [_vp, C.c_char_p, C.POINTER(FileInfo), _vp, _vp, C.c_int, _vp, _sz, _vp]),
+    "endor_reader_stats": (C.c_int, [_vp, C.POINTER(_f64), C.POINTER(_u64)]),
     "endor_host_alloc": (_vp, [_sz]),
     "endor_host_free": (None, [_vp]),
 }

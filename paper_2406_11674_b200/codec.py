@@ -61,13 +61,32 @@ class InvalidArgument(ValueError):
     """std::invalid_argument."""
 
 
+class FormatError(Error):
+    """endor::FormatError (error.hpp:42-60) with its Kind."""
+
+    class Kind(enum.IntEnum):
+        Truncated = 0
+        BadMagic = 1
+        BadVersion = 2
+        BadCrc = 3
+        CountMismatch = 4
+        Malformed = 5
+
+    def __init__(self, msg: str, kind: "FormatError.Kind"):
+        super().__init__(msg)
+        self.kind = kind
+
+
 _STATUS = {1: SizeError, 2: CorruptionError, 3: BoundsError, 4: InvalidArgument, 5: CudaError,
-           6: ConfigError}
+           6: ConfigError, 8: Error}
 
 
 def check(status: int) -> None:
     if status != 0:
-        msg = _lib.lib().endor_cuda_last_error_string().decode(errors="replace")
+        L = _lib.lib()
+        msg = L.endor_cuda_last_error_string().decode(errors="replace")
+        if status == 7:
+            raise FormatError(msg, FormatError.Kind(L.endor_cuda_last_format_kind()))
         raise _STATUS.get(status, Error)(msg)
 
 

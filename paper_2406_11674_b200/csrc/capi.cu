@@ -24,6 +24,15 @@ int fail(int code, const char* what) {
     return code;
 }
 
+}  // namespace
+
+int endor_b200::set_last_error(int code, const char* what) {
+    g_last_error = what;
+    return code;
+}
+
+namespace {
+
 int cuda_fail(cudaError_t e, const char* where) {
     g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
     return ENDOR_ERR_CUDA;
@@ -163,6 +172,8 @@ const char* endor_cuda_status_name(int s) {
         case ENDOR_ERR_INVALID_ARGUMENT: return "InvalidArgument";
         case ENDOR_ERR_CUDA: return "CudaError";
         case ENDOR_ERR_CONFIG: return "ConfigError";
+        case ENDOR_ERR_FORMAT: return "FormatError";
+        case ENDOR_ERR_IO: return "Error";
         default: return "Unknown";
     }
 }

@@ -8,6 +8,9 @@
 
 namespace endor_b200 {
 
+// thread-local last-error detail of the C ABI (capi.cu); returns code
+int set_last_error(int code, const char* what);
+
 struct ScanArgs {
     const uint8_t* bitmap;
     uint64_t nbytes;         // ceil(n/8): readable bitmap bytes

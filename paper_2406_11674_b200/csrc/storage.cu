@@ -1,0 +1,543 @@
+// storage.cu -- .endor containers straight into device memory (SURVEY.md
+// 8(f) row 2: EndorDirect, SSD -> GPU; modelled only in the
+// reference, sim.hpp:205-214).
+//
+// The container (file_io.hpp:28-52) is "ENDR" | u16 version | u8 dtype |
+// u8 flags | u64 rows | u64 cols | u64 nnz | [f32 scale] | bitmap | values |
+// u32 CRC-32.  endor_file_probe parses and validates the header and layout in
+// decode_endor's order (file_io.hpp:212-252); endor_reader_read moves the two
+// sections into device buffers:
+//
+//   * cuFile (GPUDirect Storage), bound with dlopen so the library has no
+//     link dependency: DMA from NVMe into HBM when nvidia-fs is loaded
+//     (cuFile's compatibility mode only on explicit request: its driver open
+//     hangs on this pool's boxes, which have no nvidia-fs);
+//   * POSIX: O_DIRECT reads of 4 KiB-aligned spans into two pinned bounce
+//     buffers, each chunk's cudaMemcpyAsync overlapping the next read.
+//
+// verify = 1 completes decode_endor's checks on the device copy: the CRC-32
+// of the whole file (header on the host; bitmap and values on the GPU: one
+// slicing-by-8 CRC per 256-byte chunk, then a tree of zlib-style
+// crc32_combine steps), then padding bits (Malformed) and popcount == nnz
+// (CountMismatch), file_io.hpp:253-270.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <fcntl.h>
+#include <stdint.h>
+#include <string.h>
+#include <sys/stat.h>
+#include <time.h>
+#include <unistd.h>
+
+#include <new>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "endor_cuda.h"
+#include "kernels.h"
+
+using namespace endor_b200;
+
+namespace {
+
+thread_local int g_format_kind = -1;
+
+int fmt_fail(int kind, const char* what) {
+    g_format_kind = kind;
+    return set_last_error(ENDOR_ERR_FORMAT, what);
+}
+
+// ---- CRC-32 (IEEE 802.3, reflected 0xEDB88320; zlib's crc32 and crc32_combine) ----
+constexpr uint32_t kPoly = 0xEDB88320u;
+
+struct HostCrc {
+    uint32_t t[8][256];
+    uint32_t x2n[32];  // x^(2^k) mod p(x)
+    HostCrc() {
+        for (uint32_t i = 0; i < 256; ++i) {
+            uint32_t c = i;
+            for (int k = 0; k < 8; ++k) c = c & 1 ? (c >> 1) ^ kPoly : c >> 1;
+            t[0][i] = c;
+        }
+        for (int s = 1; s < 8; ++s)
+            for (uint32_t i = 0; i < 256; ++i) t[s][i] = (t[s - 1][i] >> 8) ^ t[0][t[s - 1][i] & 0xFF];
+        uint32_t p = 1u << 30;  // x^1
+        x2n[0] = p;
+        for (int k = 1; k < 32; ++k) x2n[k] = p = multmodp(p, p);
+    }
+    static uint32_t multmodp(uint32_t a, uint32_t b) {  // a(x) b(x) mod p(x), reflected
+        uint32_t m = 1u << 31, p = 0;
+        for (;;) {
+            if (a & m) {
+                p ^= b;
+                if ((a & (m - 1)) == 0) break;
+            }
+            m >>= 1;
+            b = b & 1 ? (b >> 1) ^ kPoly : b >> 1;
+        }
+        return p;
+    }
+    uint32_t x8n(uint64_t n) const {  // x^(8 n) mod p(x)
+        uint32_t p = 1u << 31;
+        unsigned k = 3;
+        while (n) {
+            if (n & 1) p = multmodp(x2n[k & 31], p);
+            n >>= 1;
+            ++k;
+        }
+        return p;
+    }
+    uint32_t update(uint32_t crc, const uint8_t* d, size_t n) const {  // zlib crc32(crc, d, n)
+        uint32_t c = ~crc;
+        for (size_t i = 0; i < n; ++i) c = t[0][(c ^ d[i]) & 0xFF] ^ (c >> 8);
+        return ~c;
+    }
+    uint32_t combine(uint32_t c1, uint32_t c2, uint64_t len2) const { return multmodp(x8n(len2), c1) ^ c2; }
+};
+
+const HostCrc& host_crc() {
+    static const HostCrc c;
+    return c;
+}
+
+// device: one zlib-style CRC per `chunk`-byte piece (the last may be short)
+constexpr int kCrcThreads = 256;
+constexpr uint32_t kCrcChunk = 256;
+
+__global__ void __launch_bounds__(kCrcThreads) crc_chunks_kernel(const uint8_t* __restrict__ p, uint64_t len,
+                                                                 const uint32_t* __restrict__ tab, uint32_t* out) {
+    __shared__ uint32_t t[8][256];
+    for (int i = threadIdx.x; i < 8 * 256; i += kCrcThreads) t[i >> 8][i & 255] = tab[i];
+    __syncthreads();
+    const uint64_t c = uint64_t(blockIdx.x) * kCrcThreads + threadIdx.x;
+    const uint64_t b0 = c * kCrcChunk;
+    if (b0 >= len) return;
+    const uint64_t n = len - b0 < kCrcChunk ? len - b0 : kCrcChunk;
+    uint32_t crc = 0xFFFFFFFFu;
+    uint64_t i = 0;
+    if ((reinterpret_cast<uintptr_t>(p + b0) & 7) == 0) {
+        for (; i + 8 <= n; i += 8) {  // slicing-by-8
+            const uint2 w = *reinterpret_cast<const uint2*>(p + b0 + i);
+            const uint32_t lo = w.x ^ crc, hi = w.y;
+            crc = t[7][lo & 0xFF] ^ t[6][(lo >> 8) & 0xFF] ^ t[5][(lo >> 16) & 0xFF] ^ t[4][lo >> 24] ^
+                  t[3][hi & 0xFF] ^ t[2][(hi >> 8) & 0xFF] ^ t[1][(hi >> 16) & 0xFF] ^ t[0][hi >> 24];
+        }
+    }
+    for (; i < n; ++i) crc = t[0][(crc ^ p[b0 + i]) & 0xFF] ^ (crc >> 8);
+    out[c] = ~crc;
+}
+
+__device__ uint32_t d_multmodp(uint32_t a, uint32_t b) {
+    uint32_t m = 1u << 31, p = 0;
+    for (;;) {
+        if (a & m) {
+            p ^= b;
+            if ((a & (m - 1)) == 0) break;
+        }
+        m >>= 1;
+        b = b & 1 ? (b >> 1) ^ kPoly : b >> 1;
+    }
+    return p;
+}
+
+// one tree level: out[i] = crc32_combine(in[2i], in[2i+1], len(in[2i+1]));
+// every right operand has length `full` except the last element (op_last)
+__global__ void crc_combine_kernel(const uint32_t* in, uint64_t m, uint32_t op_full, uint32_t op_last,
+                                   uint32_t* out) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t l = 2 * i, r = 2 * i + 1;
+    if (l >= m) return;
+    if (r >= m) {
+        out[i] = in[l];
+        return;
+    }
+    out[i] = d_multmodp(r == m - 1 ? op_last : op_full, in[l]) ^ in[r];
+}
+
+// CRC-32 of a device buffer (stream-ordered; result left in *out_dev).
+cudaError_t device_crc(const uint8_t* p, uint64_t len, const uint32_t* tab_dev, uint32_t* scratch,
+                       uint32_t* out_dev, cudaStream_t s) {
+    if (len == 0) return cudaMemsetAsync(out_dev, 0, 4, s);
+    uint64_t m = (len + kCrcChunk - 1) / kCrcChunk;
+    crc_chunks_kernel<<<unsigned((m + kCrcThreads - 1) / kCrcThreads), kCrcThreads, 0, s>>>(p, len, tab_dev,
+                                                                                              scratch);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const HostCrc& H = host_crc();
+    uint64_t full = kCrcChunk, last = len - (m - 1) * kCrcChunk;  // lengths of a full / the last element
+    uint32_t* a = scratch;
+    uint32_t* b = scratch + m;
+    while (m > 1) {
+        const uint64_t m2 = (m + 1) / 2;
+        crc_combine_kernel<<<unsigned((m2 + 255) / 256), 256, 0, s>>>(a, m, H.x8n(full), H.x8n(last), b);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        last = (m % 2) ? last : full + last;  // an odd count passes the last element through
+        full *= 2;
+        m = m2;
+        uint32_t* t = a;
+        a = b;
+        b = t;
+    }
+    return cudaMemcpyAsync(out_dev, a, 4, cudaMemcpyDeviceToDevice, s);
+}
+
+// ---- cuFile, bound at run time -------------------------------------------------
+struct CuFile {
+    struct Err {
+        int err;
+        int cu_err;
+    };
+    struct Descr {
+        int type;
+        union {
+            int fd;
+            void* handle;
+        } handle;
+        const void* fs_ops;
+    };
+    void* lib = nullptr;
+    Err (*driver_open)() = nullptr;
+    Err (*handle_register)(void**, Descr*) = nullptr;
+    void (*handle_deregister)(void*) = nullptr;
+    ssize_t (*read)(void*, void*, size_t, off_t, off_t) = nullptr;
+    bool ok = false;
+    // nvidia-fs present: true NVMe -> HBM DMA.  Without it cuFile falls back to
+    // its compatibility mode, whose cuFileDriverOpen was measured to hang on
+    // this pool's boxes (profiles/r01/storage_probe.txt), so the driver is only
+    // opened for real GDS, or when ENDOR_ALLOW_CUFILE_COMPAT=1 asks for it.
+    static bool gds_present() { return access("/proc/driver/nvidia-fs/version", F_OK) == 0; }
+    static bool compat_allowed() {
+        const char* e = getenv("ENDOR_ALLOW_CUFILE_COMPAT");
+        return e && e[0] == '1';
+    }
+    void open_driver() {
+        if (ok || lib) return;
+        lib = dlopen("libcufile.so.0", RTLD_NOW | RTLD_LOCAL);
+        if (!lib) lib = dlopen("libcufile.so", RTLD_NOW | RTLD_LOCAL);
+        if (!lib) return;
+        driver_open = reinterpret_cast<Err (*)()>(dlsym(lib, "cuFileDriverOpen"));
+        handle_register = reinterpret_cast<Err (*)(void**, Descr*)>(dlsym(lib, "cuFileHandleRegister"));
+        handle_deregister = reinterpret_cast<void (*)(void*)>(dlsym(lib, "cuFileHandleDeregister"));
+        read = reinterpret_cast<ssize_t (*)(void*, void*, size_t, off_t, off_t)>(dlsym(lib, "cuFileRead"));
+        if (!driver_open || !handle_register || !handle_deregister || !read) return;
+        ok = driver_open().err == 0;
+    }
+};
+
+CuFile& cufile() {
+    static CuFile c;
+    return c;
+}
+
+double now_s() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return double(ts.tv_sec) + 1e-9 * double(ts.tv_nsec);
+}
+
+uint64_t le(const uint8_t* p, int n) {
+    uint64_t v = 0;
+    for (int i = 0; i < n; ++i) v |= uint64_t(p[i]) << (8 * i);
+    return v;
+}
+
+}  // namespace
+
+struct endor_reader {
+    int device = 0;
+    int mode = 0;
+    size_t bounce_bytes = 0;
+    void* bounce[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    uint32_t* crc_tab = nullptr;  // 8 x 256 slicing tables
+    uint32_t* crc_scratch = nullptr;
+    size_t crc_cap = 0;  // u32 entries
+    uint32_t* crc_out = nullptr;  // 2 section CRCs
+    double seconds = 0;
+    uint64_t bytes = 0;
+};
+
+extern "C" {
+
+int endor_cuda_last_format_kind(void) { return g_format_kind; }
+
+size_t endor_file_encode(uint64_t rows, uint64_t cols, int32_t dtype, int32_t flags, float quant_scale,
+                         const void* bitmap, const void* values, uint64_t nnz, void* out, size_t out_cap) {
+    const int eb = dtype == ENDOR_DTYPE_F16 ? 2 : (dtype == ENDOR_DTYPE_I8 ? 1 : 0);
+    if (!eb || (rows && cols > UINT64_MAX / rows) || nnz > rows * cols) return 0;
+    const bool q = flags & 1;
+    const uint64_t n = rows * cols, bm = (n + 7) / 8, vb = nnz * eb;
+    const size_t hdr = 32 + (q ? 4 : 0), total = hdr + bm + vb + 4;
+    if (!out) return total;
+    if (out_cap < total || (bm && !bitmap) || (vb && !values)) return 0;
+    uint8_t* o = static_cast<uint8_t*>(out);
+    memcpy(o, "ENDR", 4);
+    auto put = [&](size_t at, uint64_t v, int nb) {
+        for (int i = 0; i < nb; ++i) o[at + i] = uint8_t(v >> (8 * i));
+    };
+    put(4, 1, 2);  // file_io.hpp:189-199
+    o[6] = uint8_t(dtype);
+    o[7] = uint8_t(flags & 3);
+    put(8, rows, 8);
+    put(16, cols, 8);
+    put(24, nnz, 8);
+    if (q) {
+        uint32_t bits;
+        memcpy(&bits, &quant_scale, 4);
+        put(32, bits, 4);
+    }
+    if (bm) memcpy(o + hdr, bitmap, bm);
+    if (vb) memcpy(o + hdr + bm, values, vb);
+    put(hdr + bm + vb, host_crc().update(0, o, hdr + bm + vb), 4);
+    return total;
+}
+
+int endor_file_probe(const char* path, endor_file_info* out) {
+    g_format_kind = -1;
+    if (!path || !out) return set_last_error(ENDOR_ERR_INVALID_ARGUMENT, "null path or output");
+    const int fd = open(path, O_RDONLY);
+    if (fd < 0) return set_last_error(ENDOR_ERR_IO, (std::string("cannot open ") + path).c_str());
+    struct stat sb;
+    uint8_t h[36];
+    ssize_t got = 0;
+    if (fstat(fd, &sb) != 0 || (got = pread(fd, h, sizeof(h), 0)) < 0) {
+        close(fd);
+        return set_last_error(ENDOR_ERR_IO, "cannot read the header");
+    }
+    const uint64_t size = uint64_t(sb.st_size);
+    // decode_endor's checks, in its order (file_io.hpp:212-252)
+    int st = ENDOR_OK;
+    endor_file_info f{};
+    auto need = [&](ssize_t k) { return got >= k; };
+    if (!need(4)) st = fmt_fail(ENDOR_FMT_TRUNCATED, "file ends mid-field");
+    else if (memcmp(h, "ENDR", 4) != 0) st = fmt_fail(ENDOR_FMT_BAD_MAGIC, "not an .endor container");
+    else if (!need(6)) st = fmt_fail(ENDOR_FMT_TRUNCATED, "file ends mid-field");
+    else if (le(h + 4, 2) != 1) st = fmt_fail(ENDOR_FMT_BAD_VERSION, "unsupported container version");
+    else if (!need(7)) st = fmt_fail(ENDOR_FMT_TRUNCATED, "file ends mid-field");
+    else if (h[6] > 1) st = fmt_fail(ENDOR_FMT_MALFORMED, "unknown dtype code");
+    else if (!need(8)) st = fmt_fail(ENDOR_FMT_TRUNCATED, "file ends mid-field");
+    else if (h[7] & ~3u) st = fmt_fail(ENDOR_FMT_MALFORMED, "unknown flag bits set");
+    else if (!need(32 + ((h[7] & 1) ? 4 : 0))) st = fmt_fail(ENDOR_FMT_TRUNCATED, "file ends mid-field");
+    if (st == ENDOR_OK) {
+        f.dtype = h[6];
+        f.flags = h[7];
+        f.rows = le(h + 8, 8);
+        f.cols = le(h + 16, 8);
+        f.nnz = le(h + 24, 8);
+        const uint64_t hdr = 32 + ((f.flags & 1) ? 4 : 0);
+        if (f.flags & 1) {
+            const uint32_t bits = uint32_t(le(h + 32, 4));
+            memcpy(&f.quant_scale, &bits, 4);
+        }
+        const int eb = f.dtype == ENDOR_DTYPE_F16 ? 2 : 1;
+        if (f.rows && f.cols > UINT64_MAX / f.rows) st = fmt_fail(ENDOR_FMT_MALFORMED, "rows*cols overflows");
+        else if (f.nnz > f.rows * f.cols) st = fmt_fail(ENDOR_FMT_MALFORMED, "nnz exceeds rows*cols");
+        else {
+            f.header_bytes = hdr;
+            f.bitmap_offset = hdr;
+            f.bitmap_bytes = (f.rows * f.cols + 7) / 8;
+            f.values_offset = hdr + f.bitmap_bytes;
+            f.values_bytes = f.nnz * eb;
+            f.file_bytes = f.values_offset + f.values_bytes + 4;
+            if (size < f.file_bytes) st = fmt_fail(ENDOR_FMT_TRUNCATED, "file shorter than declared layout");
+            else if (size > f.file_bytes)
+                st = fmt_fail(ENDOR_FMT_MALFORMED, "trailing bytes after declared layout");
+            else {
+                uint8_t c[4];
+                if (pread(fd, c, 4, off_t(f.file_bytes - 4)) != 4) st = set_last_error(ENDOR_ERR_IO, "short read");
+                f.crc = uint32_t(le(c, 4));
+                f.header_crc = host_crc().update(0, h, hdr);
+            }
+        }
+    }
+    close(fd);
+    if (st == ENDOR_OK) *out = f;
+    return st;
+}
+
+int endor_reader_create(int device, size_t bounce_bytes, int mode, endor_reader** out) {
+    if (!out || mode < 0 || mode > ENDOR_IO_POSIX) return set_last_error(ENDOR_ERR_INVALID_ARGUMENT, "bad argument");
+    auto* r = new (std::nothrow) endor_reader();
+    if (!r) return set_last_error(ENDOR_ERR_CUDA, "out of host memory");
+    r->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    CuFile& cf = cufile();
+    if (mode == ENDOR_IO_AUTO) mode = CuFile::gds_present() ? ENDOR_IO_GDS : ENDOR_IO_POSIX;
+    if ((mode == ENDOR_IO_GDS && !CuFile::gds_present()) ||
+        (mode == ENDOR_IO_CUFILE_COMPAT && !CuFile::compat_allowed())) {
+        delete r;
+        return set_last_error(ENDOR_ERR_IO, mode == ENDOR_IO_GDS
+                                                ? "GPUDirect Storage (nvidia-fs) is not loaded on this host"
+                                                : "cuFile compatibility mode needs ENDOR_ALLOW_CUFILE_COMPAT=1");
+    }
+    if (mode != ENDOR_IO_POSIX) {
+        cf.open_driver();
+        if (!cf.ok) {
+            delete r;
+            return set_last_error(ENDOR_ERR_IO, "cuFileDriverOpen failed");
+        }
+    }
+    r->mode = mode;
+    r->bounce_bytes = ((bounce_bytes ? bounce_bytes : (64u << 20)) + 4095) & ~size_t(4095);
+    if (e == cudaSuccess && mode == ENDOR_IO_POSIX)
+        for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+            e = cudaHostAlloc(&r->bounce[i], r->bounce_bytes + 4096, cudaHostAllocPortable);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r->done[i], cudaEventDisableTiming);
+        }
+    if (e == cudaSuccess) e = cudaMalloc(&r->crc_tab, 8 * 256 * 4);
+    if (e == cudaSuccess) e = cudaMemcpy(r->crc_tab, host_crc().t, 8 * 256 * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&r->crc_out, 16);
+    if (e != cudaSuccess) {
+        endor_reader_destroy(r);
+        return set_last_error(ENDOR_ERR_CUDA, cudaGetErrorString(e));
+    }
+    *out = r;
+    return ENDOR_OK;
+}
+
+int endor_reader_destroy(endor_reader* r) {
+    if (!r) return ENDOR_OK;
+    cudaSetDevice(r->device);
+    for (int i = 0; i < 2; ++i) {
+        if (r->done[i]) cudaEventSynchronize(r->done[i]), cudaEventDestroy(r->done[i]);
+        if (r->bounce[i]) cudaFreeHost(r->bounce[i]);
+    }
+    cudaFree(r->crc_tab);
+    cudaFree(r->crc_scratch);
+    cudaFree(r->crc_out);
+    delete r;
+    return ENDOR_OK;
+}
+
+int endor_reader_mode(const endor_reader* r) { return r ? r->mode : -1; }
+
+int endor_reader_stats(const endor_reader* r, double* seconds, uint64_t* bytes) {
+    if (!r) return set_last_error(ENDOR_ERR_INVALID_ARGUMENT, "null reader");
+    if (seconds) *seconds = r->seconds;
+    if (bytes) *bytes = r->bytes;
+    return ENDOR_OK;
+}
+
+static int read_posix(endor_reader* r, int fd, uint64_t off, uint64_t len, uint8_t* dst, cudaStream_t s) {
+    // 4 KiB-aligned spans through two pinned bounce buffers; the H2D of one
+    // chunk overlaps the read of the next
+    uint64_t done = 0;
+    int k = 0;
+    while (done < len) {
+        const uint64_t want = len - done < r->bounce_bytes ? len - done : r->bounce_bytes;
+        const uint64_t a0 = (off + done) & ~uint64_t(4095), head = off + done - a0;
+        const uint64_t span = (head + want + 4095) & ~uint64_t(4095);
+        cudaError_t e = cudaEventSynchronize(r->done[k]);
+        if (e != cudaSuccess) return set_last_error(ENDOR_ERR_CUDA, cudaGetErrorString(e));
+        uint8_t* b = static_cast<uint8_t*>(r->bounce[k]);
+        uint64_t got = 0;
+        while (got < head + want) {
+            const ssize_t n = pread(fd, b + got, size_t(span - got), off_t(a0 + got));
+            if (n <= 0) return set_last_error(ENDOR_ERR_IO, "short read from the container");
+            got += uint64_t(n);
+        }
+        if ((e = cudaMemcpyAsync(dst + done, b + head, want, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+            (e = cudaEventRecord(r->done[k], s)) != cudaSuccess)
+            return set_last_error(ENDOR_ERR_CUDA, cudaGetErrorString(e));
+        done += want;
+        k ^= 1;
+    }
+    return ENDOR_OK;
+}
+
+int endor_reader_read(endor_reader* r, const char* path, const endor_file_info* f, void* bitmap_dev,
+                      void* values_dev, int verify, void* ws, size_t ws_bytes, void* stream) {
+    g_format_kind = -1;
+    if (!r || !path || !f) return set_last_error(ENDOR_ERR_INVALID_ARGUMENT, "null argument");
+    if ((f->bitmap_bytes && !bitmap_dev) || (f->values_bytes && !values_dev))
+        return set_last_error(ENDOR_ERR_INVALID_ARGUMENT, "null device buffer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaSetDevice(r->device);
+    if (e != cudaSuccess) return set_last_error(ENDOR_ERR_CUDA, cudaGetErrorString(e));
+    const double t0 = now_s();
+    int st = ENDOR_OK;
+    if (r->mode == ENDOR_IO_POSIX) {
+        int fd = open(path, O_RDONLY | O_DIRECT);
+        if (fd < 0) fd = open(path, O_RDONLY);  // e.g. tmpfs: no O_DIRECT
+        if (fd < 0) return set_last_error(ENDOR_ERR_IO, (std::string("cannot open ") + path).c_str());
+        st = read_posix(r, fd, f->bitmap_offset, f->bitmap_bytes, static_cast<uint8_t*>(bitmap_dev), s);
+        if (!st) st = read_posix(r, fd, f->values_offset, f->values_bytes, static_cast<uint8_t*>(values_dev), s);
+        close(fd);
+        if (!st && (e = cudaStreamSynchronize(s)) != cudaSuccess) st = set_last_error(ENDOR_ERR_CUDA, cudaGetErrorString(e));
+    } else {
+        // cuFileRead is synchronous and not stream-ordered: drain the stream first
+        if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return set_last_error(ENDOR_ERR_CUDA, cudaGetErrorString(e));
+        CuFile& cf = cufile();
+        int fd = open(path, O_RDONLY | O_DIRECT);
+        if (fd < 0) fd = open(path, O_RDONLY);
+        if (fd < 0) return set_last_error(ENDOR_ERR_IO, (std::string("cannot open ") + path).c_str());
+        CuFile::Descr d{};
+        d.type = 1;  // CU_FILE_HANDLE_TYPE_OPAQUE_FD
+        d.handle.fd = fd;
+        void* h = nullptr;
+        if (cf.handle_register(&h, &d).err != 0) {
+            close(fd);
+            return set_last_error(ENDOR_ERR_IO, "cuFileHandleRegister failed");
+        }
+        auto rd = [&](uint64_t off, uint64_t len, void* dst) -> int {
+            uint64_t done = 0;
+            while (done < len) {
+                const ssize_t n = cf.read(h, dst, size_t(len - done), off_t(off + done), off_t(done));
+                if (n <= 0) return set_last_error(ENDOR_ERR_IO, "cuFileRead failed");
+                done += uint64_t(n);
+            }
+            return ENDOR_OK;
+        };
+        st = rd(f->bitmap_offset, f->bitmap_bytes, bitmap_dev);
+        if (!st) st = rd(f->values_offset, f->values_bytes, values_dev);
+        cf.handle_deregister(h);
+        close(fd);
+    }
+    r->seconds += now_s() - t0;
+    r->bytes += f->bitmap_bytes + f->values_bytes;
+    if (st || !verify) return st;
+
+    // ---- decode_endor's remaining checks on the device copy (file_io.hpp:253-270) ----
+    const uint64_t mb = (f->bitmap_bytes + kCrcChunk - 1) / kCrcChunk, mv = (f->values_bytes + kCrcChunk - 1) / kCrcChunk;
+    const size_t need = 2 * (mb > mv ? mb : mv) + 2;
+    if (need > r->crc_cap) {
+        cudaFree(r->crc_scratch);
+        r->crc_scratch = nullptr;
+        r->crc_cap = 0;
+        if ((e = cudaMalloc(&r->crc_scratch, need * 4)) != cudaSuccess)
+            return set_last_error(ENDOR_ERR_CUDA, cudaGetErrorString(e));
+        r->crc_cap = need;
+    }
+    if ((e = device_crc(static_cast<const uint8_t*>(bitmap_dev), f->bitmap_bytes, r->crc_tab, r->crc_scratch,
+                        r->crc_out, s)) != cudaSuccess ||
+        (e = device_crc(static_cast<const uint8_t*>(values_dev), f->values_bytes, r->crc_tab, r->crc_scratch,
+                        r->crc_out + 1, s)) != cudaSuccess)
+        return set_last_error(ENDOR_ERR_CUDA, cudaGetErrorString(e));
+    uint32_t c[2];
+    uint8_t lastb = 0;
+    if ((e = cudaMemcpyAsync(c, r->crc_out, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (f->bitmap_bytes && (e = cudaMemcpyAsync(&lastb, static_cast<const uint8_t*>(bitmap_dev) + f->bitmap_bytes - 1,
+                                                 1, cudaMemcpyDeviceToHost, s)) != cudaSuccess) ||
+        (e = cudaStreamSynchronize(s)) != cudaSuccess)
+        return set_last_error(ENDOR_ERR_CUDA, cudaGetErrorString(e));
+    const HostCrc& H = host_crc();
+    const uint32_t whole = H.combine(H.combine(f->header_crc, c[0], f->bitmap_bytes), c[1], f->values_bytes);
+    if (whole != f->crc) return fmt_fail(ENDOR_FMT_BAD_CRC, "CRC mismatch");
+    const uint64_t n = f->rows * f->cols;
+    if ((n & 7) && (lastb >> (n & 7))) return fmt_fail(ENDOR_FMT_MALFORMED, "bitmap padding bits must be zero");
+    if (n) {
+        unsigned long long* tot = reinterpret_cast<unsigned long long*>(r->crc_out + 2);
+        int st2 = endor_cuda_popcount(bitmap_dev, n, reinterpret_cast<uint64_t*>(tot), ws, ws_bytes, stream);
+        if (st2) return st2;
+        unsigned long long total = 0;
+        if ((e = cudaMemcpyAsync(&total, tot, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+            (e = cudaStreamSynchronize(s)) != cudaSuccess)
+            return set_last_error(ENDOR_ERR_CUDA, cudaGetErrorString(e));
+        if ((st2 = endor_cuda_sync_status(ws, stream))) return st2;
+        if (total != f->nnz) return fmt_fail(ENDOR_FMT_COUNT_MISMATCH, "nnz field disagrees with bitmap popcount");
+    }
+    return ENDOR_OK;
+}
+
+}  // extern "C"

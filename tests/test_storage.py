@@ -1,0 +1,181 @@
+""".endor containers straight to the GPU.
+
+CPU: the encoder is byte-identical to the reference's (test_io.cpp:30-57
+golden bytes; reference encoder on seeded cases) and endor_file_probe rejects
+each header/layout corruption with decode_endor's FormatError kind
+(test_io.cpp:106-176).  GPU: the reader (cuFile or POSIX) reproduces the
+tensor bit-exactly; verify catches BadCrc / CountMismatch / Malformed padding
+on the device copy; every single-byte flip of a valid file is rejected
+(test_io.cpp:178-186)."""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+KIND = {"Truncated": 0, "BadMagic": 1, "BadVersion": 2, "BadCrc": 3, "CountMismatch": 4, "Malformed": 5}
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2406_11674_b200 import _lib
+    return _lib.lib()
+
+
+def encode(L, rows, cols, dtype, bm, vals, nnz, flags=0, scale=0.0):
+    n = L.endor_file_encode(rows, cols, dtype, flags, scale, bm.ctypes.data if bm.size else None,
+                            vals.ctypes.data if vals.size else None, nnz, None, 0)
+    buf = C.create_string_buffer(n)
+    assert L.endor_file_encode(rows, cols, dtype, flags, scale, bm.ctypes.data if bm.size else None,
+                               vals.ctypes.data if vals.size else None, nnz, buf, n) == n
+    return buf.raw
+
+
+def tiny(L):
+    # test_io.cpp tiny_tensor: the 2x2 hand-built tensor (bitmap 1010, values 0x3C00 0x4200)
+    bm = np.array([0x05], np.uint8)
+    vals = np.array([0x00, 0x3C, 0x00, 0x42], np.uint8)
+    return encode(L, 2, 2, 0, bm, vals, 2)
+
+
+def test_encoder_matches_reference_golden_bytes(L, kats):
+    assert tiny(L).hex() == kats["endor_file_2x2"]["bytes"]
+    z = encode(L, 4, 4, 0, np.zeros(2, np.uint8), np.zeros(0, np.uint8), 0)
+    assert z.hex() == kats["endor_file_zero_4x4"]["bytes"] and len(z) == 38
+
+
+def test_encoder_matches_reference_encoder_on_random_cases(L):
+    R = O.ref()
+    if R is None:
+        pytest.skip("reference library not built")
+    for seed, (rows, cols, eb) in enumerate([(7, 9, 2), (16, 16, 2), (3, 64, 1), (1, 1, 2)]):
+        w = O.random_dense(rows, cols, eb, seed, 0.5)
+        bm, vals, nnz, _ = O.compress(w, rows, cols, eb)
+        mine = encode(L, rows, cols, 0 if eb == 2 else 1, bm, vals, nnz)
+        out = np.zeros(len(mine) + 64, np.uint8)
+        n = R.ref_encode_endor(rows, cols, eb, bm, vals, nnz, 0, out, out.size)
+        assert bytes(out[:n]) == mine
+
+
+def probe_kind(L, tmp_path, data):
+    from paper_2406_11674_b200 import _lib
+    p = tmp_path / "t.endor"
+    p.write_bytes(bytes(data))
+    info = _lib.FileInfo()
+    st = L.endor_file_probe(os.fsencode(str(p)), C.byref(info))
+    return st, (L.endor_cuda_last_format_kind() if st == 7 else None), info
+
+
+def test_probe_accepts_and_describes_a_valid_file(L, tmp_path):
+    st, _, info = probe_kind(L, tmp_path, tiny(L))
+    assert st == 0
+    assert (info.rows, info.cols, info.nnz, info.dtype) == (2, 2, 2, 0)
+    assert (info.bitmap_offset, info.bitmap_bytes, info.values_offset, info.values_bytes) == (32, 1, 33, 4)
+    assert info.file_bytes == 41
+
+
+@pytest.mark.parametrize("mutate,kind", [
+    (lambda b: b.__setitem__(0, ord("X")), "BadMagic"),       # test_io.cpp:109-118
+    (lambda b: b.__setitem__(4, 9), "BadVersion"),            # :119-128
+    (lambda b: b.pop(), "Truncated"),                         # :155-164
+    (lambda b: b.append(0), "Malformed"),                     # :165-174 trailing bytes
+    (lambda b: b.__setitem__(6, 7), "Malformed"),             # unknown dtype code
+    (lambda b: b.__setitem__(7, 0x80), "Malformed"),          # unknown flag bits
+    (lambda b: b.__setitem__(24, 9), "Malformed"),            # nnz > rows*cols
+    (lambda b: b.__setitem__(8, 20), "Truncated"),            # rows 20: layout longer than the file
+    (lambda b: b.__delitem__(slice(20, None)), "Truncated"),  # ends mid-field
+])
+def test_probe_rejects_each_header_corruption(L, tmp_path, mutate, kind):
+    b = bytearray(tiny(L))
+    mutate(b)
+    st, k, _ = probe_kind(L, tmp_path, b)
+    assert st == 7 and k == KIND[kind]
+
+
+# ---------------------------------------------------------------------------- GPU
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def S(cuda_lib):
+    from paper_2406_11674_b200 import storage
+    return storage
+
+
+@pytest.fixture(scope="module")
+def E(cuda_lib):
+    from paper_2406_11674_b200 import codec
+    return codec
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", [0, 3])  # auto = GDS when nvidia-fs is loaded, else POSIX
+@pytest.mark.parametrize("rows,cols,s,dtype", [(2, 2, 0.5, 0), (300, 1000, 0.5, 0), (1024, 9216, 0.7, 0),
+                                               (77, 333, 0.4, 1), (5, 5, 1.0, 0)])
+def test_reader_round_trip_bit_exact(S, E, tmp_path, mode, rows, cols, s, dtype):
+    eb = 2 if dtype == 0 else 1
+    w = O.random_dense(rows, cols, eb, rows + cols, s)
+    bm, vals, nnz, _ = O.compress(w, rows, cols, eb)
+    t = E.EndorTensor(rows, cols, E.Dtype(dtype), E.Bitmap.from_bytes(bm.tobytes(), rows * cols, device="cuda"),
+                      torch.from_numpy(vals.copy()).cuda())
+    p = str(tmp_path / "w.endor")
+    n = S.write_endor_file(t, p)
+    assert n == os.path.getsize(p) == 32 + bm.size + vals.size + 4
+    r = S.Reader("cuda", mode=mode, bounce_bytes=1 << 16)  # small bounce: many chunks
+    got = r.read(p, verify=True)
+    assert r.mode in ("gds", "cufile-compat", "posix-odirect")
+    assert got.bitmap.to_bytes() == bm.tobytes()
+    assert got.values.cpu().numpy().tobytes() == vals.tobytes()
+    assert E.decompress(got).bytes() == w.tobytes()
+    r.close()
+
+
+@pytest.mark.gpu
+def test_reader_verify_detects_payload_corruption(S, E, L, tmp_path):
+    w = O.random_dense(64, 100, 2, 5, 0.5)
+    bm, vals, nnz, _ = O.compress(w, 64, 100, 2)
+    good = bytearray(encode(L, 64, 100, 0, bm, vals, nnz))
+    p = str(tmp_path / "c.endor")
+
+    def kind_of(data):
+        open(p, "wb").write(bytes(data))
+        with pytest.raises(E.FormatError) as ei:
+            S.read_endor_file(p, "cuda", verify=True)
+        return ei.value.kind.name
+
+    bad = bytearray(good)
+    bad[-1] ^= 0xFF
+    assert kind_of(bad) == "BadCrc"
+    bad = bytearray(good)
+    bad[40] ^= 0x10  # a value byte: CRC catches it on the GPU
+    assert kind_of(bad) == "BadCrc"
+
+    def refix_crc(b):
+        import zlib
+        b[-4:] = (zlib.crc32(bytes(b[:-4])) & 0xFFFFFFFF).to_bytes(4, "little")
+        return b
+
+    bad = bytearray(good)
+    bad[32] ^= 0x01  # one set bit more or fewer; CRC fixed up
+    b2 = refix_crc(bad)
+    assert kind_of(b2) == "CountMismatch"  # test_io.cpp:139-154
+
+
+@pytest.mark.gpu
+def test_reader_rejects_every_single_byte_flip(S, E, L, tmp_path):
+    # test_io.cpp:178-186
+    w = O.random_dense(4, 6, 2, 2, 0.5)
+    bm, vals, nnz, _ = O.compress(w, 4, 6, 2)
+    good = encode(L, 4, 6, 0, bm, vals, nnz)
+    p = str(tmp_path / "f.endor")
+    r = S.Reader("cuda")
+    for i in range(len(good)):
+        bad = bytearray(good)
+        bad[i] ^= 0x5B
+        open(p, "wb").write(bytes(bad))
+        with pytest.raises(E.FormatError):
+            r.read(p, verify=True)
+    r.close()
