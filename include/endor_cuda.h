@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define ENDOR_CUDA_ABI_VERSION 1
+#define ENDOR_CUDA_ABI_VERSION 2
 
 typedef enum endor_status {
     ENDOR_OK = 0,
@@ -358,6 +358,10 @@ typedef struct endor_pipeline_op {
     float* y_host;           /* optional pinned f32[rows]: y is copied back (D2H) */
     float quant_scale;       /* flags bit0 only */
     int32_t reserved2;
+    const char* path;        /* non-NULL: the op's bitmap + values come from this .endor file
+                                (EndorDirect, SsdToGpu sim.hpp:205-214) through the pipeline's
+                                endor_reader instead of bitmap_host / values_host; rows, cols,
+                                dtype, nnz must match its header */
 } endor_pipeline_op;
 
 typedef struct endor_pipeline_stats {

@@ -39,6 +39,7 @@ struct endor_pipeline {
     size_t ws_bytes = 0;
     // per-op timing events (grown on demand)
     std::vector<cudaEvent_t> h2d_beg, h2d_end, dec_beg, dec_end, op_end;
+    endor_reader* reader = nullptr;  // file-sourced ops (created on first use)
     int last_nops = 0;
     uint64_t last_h2d_bytes = 0, last_dense_bytes = 0, last_launches = 0;
 };
@@ -118,6 +119,7 @@ int endor_pipeline_destroy(endor_pipeline* p) {
     }
     for (auto& d : p->dense) cudaFree(d);
     cudaFree(p->ws);
+    endor_reader_destroy(p->reader);
     for (auto* v : {&p->h2d_beg, &p->h2d_end, &p->dec_beg, &p->dec_end, &p->op_end})
         for (auto e : *v) cudaEventDestroy(e);
     cudaStreamDestroy(p->copy);
@@ -149,8 +151,19 @@ int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops
         // copy stream: wait until the slot's previous occupant was decompressed
         PK(cudaStreamWaitEvent(p->copy, slot.free_ev, 0));
         PK(cudaEventRecord(p->h2d_beg[i], p->copy));
-        PK(cudaMemcpyAsync(slot.bitmap, op.bitmap_host, bmb, cudaMemcpyHostToDevice, p->copy));
-        if (vb) PK(cudaMemcpyAsync(slot.values, op.values_host, vb, cudaMemcpyHostToDevice, p->copy));
+        if (op.path) {
+            // EndorDirect: storage -> device (the reader's H2D chunks go on the copy stream)
+            endor_file_info fi;
+            if ((st = endor_file_probe(op.path, &fi))) return st;
+            if (fi.rows != op.rows || fi.cols != op.cols || fi.dtype != op.dtype || fi.nnz != op.nnz)
+                return ENDOR_ERR_INVALID_ARGUMENT;
+            if (!p->reader && (st = endor_reader_create(p->device, 0, ENDOR_IO_AUTO, &p->reader))) return st;
+            if ((st = endor_reader_read(p->reader, op.path, &fi, slot.bitmap, slot.values, 0, nullptr, 0, p->copy)))
+                return st;
+        } else {
+            PK(cudaMemcpyAsync(slot.bitmap, op.bitmap_host, bmb, cudaMemcpyHostToDevice, p->copy));
+            if (vb) PK(cudaMemcpyAsync(slot.values, op.values_host, vb, cudaMemcpyHostToDevice, p->copy));
+        }
         PK(cudaEventRecord(p->h2d_end[i], p->copy));
         // compute stream: decompress into the dense ring (or the caller's buffer), then GEMV
         PK(cudaStreamWaitEvent(p->compute, p->h2d_end[i], 0));

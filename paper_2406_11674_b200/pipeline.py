@@ -12,6 +12,7 @@ when the op asks for W (``dense``) or ``materialize=True``.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 from typing import List, Optional
 
@@ -36,9 +37,13 @@ class HostOp:
     dense: Optional[torch.Tensor] = None   # device uint8 [rows*cols*eb] (optional)
     quant_scale: Optional[float] = None    # i8 values dequantized to f16 W (INT8 + Endor)
     materialize: bool = False              # decompress W, then dense GEMV (default: fused when possible)
+    path: Optional[str] = None             # EndorDirect: read bitmap + values from this .endor file
 
     @property
     def compressed_bytes(self) -> int:
+        if self.path is not None:
+            eb = 2 if self.dtype == 0 else 1
+            return (self.rows * self.cols + 7) // 8 + self.nnz * eb
         return self.bitmap.numel() + self.values.numel()
 
     @property
@@ -80,7 +85,8 @@ class OffloadPipeline:
             flags = (1 if deq else 0) | (2 if o.materialize else 0)
             arr[i] = _lib.PipelineOp(o.rows, o.cols, o.dtype, flags, _p(o.bitmap), _p(o.values), o.nnz,
                                      _p(o.x), _p(o.y), _p(o.dense), _p(o.y_host),
-                                     float(o.quant_scale) if deq else 0.0, 0)
+                                     float(o.quant_scale) if deq else 0.0, 0,
+                                     os.fsencode(o.path) if o.path is not None else None)
         self._keep = (arr, ops)
         check(self._lib.endor_pipeline_run(self._h, arr, len(ops), 1 if sync else 0))
 

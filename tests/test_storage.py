@@ -179,3 +179,36 @@ def test_reader_rejects_every_single_byte_flip(S, E, L, tmp_path):
         with pytest.raises(E.FormatError):
             r.read(p, verify=True)
     r.close()
+
+
+@pytest.mark.gpu
+def test_pipeline_file_sourced_ops_match_host_sourced(S, E, tmp_path):
+    """EndorDirect through the offload pipeline: ops read from .endor files give
+    the same y as the same ops streamed from pinned host memory."""
+    from paper_2406_11674_b200.pipeline import HostOp, OffloadPipeline, pinned_copy
+    shapes = [(64, 2048), (33, 1000), (128, 4096)]
+    ys = {}
+    for src in ("host", "file"):
+        ops = []
+        for i, (r, c) in enumerate(shapes):
+            w = E.synth_weight(r, c, 50 + i, device="cuda")
+            E.magnitude_prune(w, 0.5, inplace=True)
+            t = E.compress(w)
+            x = ((torch.rand(c, generator=torch.Generator().manual_seed(i)) * 2 - 1).half()).cuda()
+            kw = dict(x=x, y=torch.empty(r, dtype=torch.float32, device="cuda"),
+                      y_host=torch.empty(r, dtype=torch.float32, pin_memory=True))
+            if src == "file":
+                p = str(tmp_path / f"op{i}.endor")
+                S.write_endor_file(t, p)
+                e = torch.empty(0, dtype=torch.uint8)
+                ops.append(HostOp(r, c, 0, e, e, t.nnz(), path=p, **kw))
+            else:
+                ops.append(HostOp(r, c, 0, pinned_copy(t.bitmap.data), pinned_copy(t.values), t.nnz(), **kw))
+        pipe = OffloadPipeline(0, max(r * c for r, c in shapes))
+        pipe.run(ops, sync=True)
+        st = pipe.stats()
+        pipe.close()
+        assert st["h2d_bytes"] == sum(o.compressed_bytes for o in ops)
+        ys[src] = [o.y_host.clone() for o in ops]
+    for a, b in zip(ys["host"], ys["file"]):
+        assert torch.equal(a, b)
