@@ -394,6 +394,46 @@ def run_ours(args):
                 "note": "values quantized to int8 (lossy, codec.hpp:306-331); f16 W rebuilt on the fly"}
         pipe.close()
 
+    # ---- EndorDirect: the same layer streamed from .endor files on local storage (8(f) row 2) ----
+    storage = None
+    if not args.no_e2e and not args.no_extras:
+        import shutil
+        import tempfile
+        from paper_2406_11674_b200 import storage as ST
+        d = tempfile.mkdtemp(prefix=f"endor_r{rank}_", dir=os.environ.get("ENDOR_BENCH_DIR", "/tmp"))
+        try:
+            g = torch.Generator(device="cpu").manual_seed(4321 + rank)
+            fops, fbytes = [], 0
+            e0 = torch.empty(0, dtype=torch.uint8)
+            for i, s in enumerate(shards):
+                pth = os.path.join(d, f"op{i}.endor")
+                fbytes += ST.write_endor_file(s["t"], pth)
+                x = ((torch.rand(s["cols"], generator=g) * 2 - 1).half()).to(dev)
+                fops.append(HostOp(s["rows"], s["cols"], 0, e0, e0, s["nnz"], path=pth, x=x,
+                                   y=torch.empty(s["rows"], dtype=torch.float32, device=dev),
+                                   y_host=torch.empty(s["rows"], dtype=torch.float32, pin_memory=True)))
+            sreps = max(1, min(args.steps, 2))
+            fpipe = OffloadPipeline(local, nmax, ring_depth=2)
+            fpipe.run(fops, sync=True)
+            barrier()
+            fpipe.run(fops * sreps, sync=True)
+            sf = fpipe.stats()
+            fpipe.close()
+            r = ST.Reader(dev)
+            mode = r.mode
+            r.close()
+            s_ms = max_over_ranks(sf["total_ms"]) / sreps
+            storage = {"value": round(world * dense_rank / (s_ms * 1e-3) / 1e9, 2), "unit": UNIT,
+                       "layer_ms": round(s_ms / world, 3), "layers_per_step": world, "reps": sreps,
+                       "storage_gbs_per_gpu": round(sf["h2d_bytes"] / (sf["h2d_ms"] * 1e-3) / 1e9, 3),
+                       "io_mode": mode,
+                       "gds": "nvidia-fs not loaded on this box: O_DIRECT reads + pinned bounce buffers "
+                              "(cuFile compatibility mode hangs in cuFileDriverOpen here)" if mode != "gds" else "GDS",
+                       "file_bytes_per_gpu": fbytes,
+                       "api": "endor_pipeline_run with endor_pipeline_op.path (C ABI)"}
+        finally:
+            shutil.rmtree(d, ignore_errors=True)
+
     # ---- fused decompress -> GEMV vs decompress + GEMV, HBM-resident (8(f) row 1) -------------
     fused = None
     if not args.no_extras:
@@ -495,7 +535,7 @@ def run_ours(args):
                            "parallelism": f"row-shard{world}"},
                 "per_gpu_value": round(value / world, 2),
                 "roofline": roofline, "decompress_no_index": no_index, "e2e": e2e, "cpu_baseline": cpu, "parity": parity,
-                "fused_decompress_gemv": fused,
+                "fused_decompress_gemv": fused, "storage_direct": storage,
                 "gpu_launches": launches, "clocks": clk.summary() if clk else None}
         print(json.dumps(line), flush=True)
     if world > 1:
