@@ -18,4 +18,11 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:expand_tma_kernel -s 5 -c 1 \
     -o "$O/full_expand" -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-extras \
     > "$O/full_expand.log" 2>&1
-echo done
+
+# fused decompress -> GEMV (one batched launch per layer) and the batched dense GEMV
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemv_fused_kernel -c 1 \
+    -o "$O/full_fused" -f python tools/fused_bench.py > "$O/full_fused.log" 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemv_batch_kernel -c 1 \
+    -o "$O/full_gemv" -f python tools/fused_bench.py > "$O/full_gemv.log" 2>&1
+timeout 300 python tools/fused_bench.py > "$O/fused_bench.log" 2>&1
+echo done2
