@@ -41,6 +41,11 @@ constexpr int kGvThreads = (kGvWarps + 1) * 32;   // + 1 producer warp
 #define ENDOR_GV_STAGES 4
 #endif
 constexpr int kGvStages = ENDOR_GV_STAGES;
+// lane granularity of the gather: 1 = byte lanes (two nibbles per step, one
+// shuffle pair per 8 weights), 0 = nibble lanes (conflict-free LDS)
+#ifndef ENDOR_GV_BYTE_LANES
+#define ENDOR_GV_BYTE_LANES 1
+#endif
 constexpr uint32_t kGvBm = 0;                                  // 8 x 128-byte bitmap slices
 constexpr uint32_t kGvMeta = kGvWarps * 128;                   // 9 u32 sub-tile starts relative to the
                                                                // window, then the window's byte offset
@@ -259,12 +264,27 @@ __global__ void __launch_bounds__(kGvThreads, 3) gemv_fused_kernel(const __grid_
     uint32_t xrun = ~0u, run = 0;     // column run id: x reloads only when it changes
     uint64_t k = cur.item() * kGvWarps + warp, nsub = b.t[cur.ti].n / kSubElems;
     uint32_t xr[16];  // x[4n .. 4n+3] for this lane's nibbles n = lane + 32 q of the segment
-    const uint32_t nsh = (lane & 7) * 4, lowm = (1u << nsh) - 1u;
+#if ENDOR_GV_BYTE_LANES
+    const uint32_t nsh = (lane & 3) * 8, lowm = (1u << nsh) - 1u;  // lane's byte inside its word
+#else
+    const uint32_t nsh = (lane & 7) * 4, lowm = (1u << nsh) - 1u;  // lane's nibble inside its word
+#endif
     const uint32_t lut = smem_u32(g_lut16);
     const BatchTensor* T = &b.t[cur.ti];
     for (uint32_t i = 0; i < m; ++i) {
         const bool ok = k < nsub;
         if (ok && run != xrun) {  // x stays in registers along a column
+#if ENDOR_GV_BYTE_LANES
+            const uint4* xs = static_cast<const uint4*>(T->x) + (k % cur.segs) * (kSubElems / 8);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint4 v = __ldg(xs + 32 * q + lane);
+                xr[4 * q] = v.x;
+                xr[4 * q + 1] = v.y;
+                xr[4 * q + 2] = v.z;
+                xr[4 * q + 3] = v.w;
+            }
+#else
             const uint2* xs = static_cast<const uint2*>(T->x) + (k % cur.segs) * (kSubElems / 4);
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
@@ -272,6 +292,7 @@ __global__ void __launch_bounds__(kGvThreads, 3) gemv_fused_kernel(const __grid_
                 xr[2 * q] = v.x;
                 xr[2 * q + 1] = v.y;
             }
+#endif
             xrun = run;
         }
         const int s = int(i % kGvStages);
@@ -292,6 +313,28 @@ __global__ void __launch_bounds__(kGvThreads, 3) gemv_fused_kernel(const __grid_
                 wbase = stg + kGvVals;
             }
             float acc0 = 0.f, acc1 = 0.f;
+#if ENDOR_GV_BYTE_LANES
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int src = 8 * q + (lane >> 2);  // word of byte lane + 32 q
+                const uint32_t wd = __shfl_sync(0xffffffffu, word, src);
+                const uint32_t a0 = __shfl_sync(0xffffffffu, wbase, src) + 2 * __popc(wd & lowm);
+                const uint32_t byte = (wd >> nsh) & 0xFFu;
+                const uint32_t n0 = byte & 15u, n1 = byte >> 4;
+                const uint32_t a1 = a0 + 2 * __popc(n0);
+                // nibble 0 at a0, nibble 1 at a1: 4 packed values each -> 8 slots
+                const uint32_t s0 = lut_sel(lut, n0), s1 = lut_sel(lut, n1);
+                const uint32_t l0 = a0 & ~3u, h0 = a0 << 3, l1 = a1 & ~3u, h1 = a1 << 3;
+                const uint32_t u0 = lds32(l0), u1 = lds32(l0 + 4), u2 = lds32(l0 + 8);
+                const uint32_t v0 = lds32(l1), v1 = lds32(l1 + 4), v2 = lds32(l1 + 8);
+                const uint32_t x0 = __funnelshift_r(u0, u1, h0), y0 = __funnelshift_r(u1, u2, h0);
+                const uint32_t x1 = __funnelshift_r(v0, v1, h1), y1 = __funnelshift_r(v1, v2, h1);
+                acc0 = fma_f16x2(prmt(x0, 0u, s0), xr[4 * q], acc0);
+                acc1 = fma_f16x2_if<0x4u, 0x8u>(prmt(x0, y0, s0 >> 16), xr[4 * q + 1], acc1, byte);
+                acc0 = fma_f16x2(prmt(x1, 0u, s1), xr[4 * q + 2], acc0);
+                acc1 = fma_f16x2_if<0x40u, 0x80u>(prmt(x1, y1, s1 >> 16), xr[4 * q + 3], acc1, byte);
+            }
+#else
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 const int src = 4 * q + (lane >> 3);  // word of nibble lane + 32 q
@@ -306,6 +349,7 @@ __global__ void __launch_bounds__(kGvThreads, 3) gemv_fused_kernel(const __grid_
                 acc0 = fma_f16x2(prmt(x, 0u, sel), xr[2 * q], acc0);  // slots 0, 1 (unset -> +0)
                 acc1 = fma_f16x2_if<4u, 8u>(prmt(x, y, sel >> 16), xr[2 * q + 1], acc1, nib);  // slots 2, 3
             }
+#endif
             float a = acc0 + acc1;
 #pragma unroll
             for (int d = 16; d > 0; d >>= 1) a += __shfl_xor_sync(0xffffffffu, a, d);
