@@ -291,12 +291,19 @@ def run_ours(args):
     if os.path.exists(tp):
         with open(tp) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
+    mix_ceiling = None  # streaming ceiling for this read/write mix (profiles/r01/mix_ceiling.txt)
+    mp = os.path.join(ROOT, "profiles", "bench_expand_traffic.json")
+    if os.path.exists(mp):
+        with open(mp) as f:
+            mix_ceiling = json.load(f).get("mix_ceiling_gbs")
     roofline = {"bound": "hbm", "kernel": "expand_tma_kernel<2>", "achieved": round(achieved, 1),
                 "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "alg_bytes_per_launch": expand_alg,
                 "avg_launch_us": round(expand_ms * 1e3, 2),
                 "count_kernel_avg_us_no_index_path": round(count_ms * 1e3, 2),
+                "mix_ceiling_gbs": mix_ceiling,
+                "frac_of_mix_ceiling": round(achieved / mix_ceiling, 4) if mix_ceiling else None,
                 "step_frac": round(alg_rank / (ms_step * 1e-3) / 1e9 / peak, 4)}
 
     # ---- e2e: offload pipeline over pinned host buffers ----------------------------------
