@@ -72,6 +72,48 @@ def decomp_stats(tensors, label, steps=20):
         ms = time_plan(plan, steps)
         res[name] = {"ms": round(ms, 4), "dense_gbs": round(2 * n / (ms * 1e-3) / 1e9, 1),
                      "frac_of_hbm_roofline": round(alg / (ms * 1e-3) / 1e9 / PEAK, 4)}
+    # y = W x: fused decompress -> GEMV (one batched call, 1024 index) vs the
+    # materialised path's dense GEMV (one batched launch over the dense W)
+    if all(t.dtype == E.Dtype.F16 and t.cols % 1024 == 0 for t in tensors):
+        xs = [(torch.rand(t.cols, device=DEV) * 2 - 1).half() for t in tensors]
+        st = torch.cuda.Stream(device=DEV)
+
+        def timed(fn, reps=steps):
+            with torch.cuda.stream(st):
+                for _ in range(3):
+                    fn()
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                for _ in range(reps):
+                    fn()
+                b.record(st)
+                torch.cuda.synchronize()
+            return a.elapsed_time(b) / reps
+
+        comp = sum(t.compressed_bytes() + (t.element_count() // 1024) * 8 + t.cols * 2 for t in tensors)
+        import ctypes as C
+        from paper_2406_11674_b200 import _lib
+        L, P, nt = _lib.lib(), C.c_void_p, len(tensors)
+        views = (_lib.TensorView * nt)(*[t.view() for t in tensors])
+        pres = [ix.prefix.contiguous() for ix in idx]
+        ys = [torch.empty(t.rows, dtype=torch.float32, device=DEV) for t in tensors]
+        pa, xa, ya = ((P * nt)(*[v.data_ptr() for v in vs]) for vs in (pres, xs, ys))
+        ws = torch.zeros(L.endor_cuda_workspace_bytes_batch(views, nt), dtype=torch.uint8, device=DEV)
+
+        def fused():  # the C ABI call alone: asynchronous, no host sync
+            E.check(L.endor_cuda_gemv_compressed_batch(views, pa, xa, ya, None, nt, ws.data_ptr(), ws.numel(),
+                                                       st.cuda_stream))
+
+        ms_f = timed(fused)
+        E.check(L.endor_cuda_sync_status(ws.data_ptr(), st.cuda_stream))
+        for o, t in zip(outs, tensors):
+            E.decompress(t, out=o)
+        ms_g = timed(lambda: E.gemv_batch(outs, xs))
+        res["fused_gemv_idx1024"] = {"ms": round(ms_f, 4), "weight_gbs": round(2 * n / (ms_f * 1e-3) / 1e9, 1),
+                                     "frac_of_hbm_roofline": round(comp / (ms_f * 1e-3) / 1e9 / PEAK, 4)}
+        res["dense_gemv"] = {"ms": round(ms_g, 4), "frac_of_hbm_roofline": round(2 * n / (ms_g * 1e-3) / 1e9 / PEAK, 4)}
+        res["decompress_then_gemv_ms"] = round(res["decompress_chunked_idx1024"]["ms"] + ms_g, 4)
     res["l2"] = "inputs larger than L2" if alg > 3 * 126e6 else "fits in L2 (launch-bound regime)"
     return res
 
