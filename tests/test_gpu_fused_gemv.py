@@ -119,3 +119,26 @@ def test_pipeline_fused_matches_materialized(E):
         ref = (w.data.view(torch.float16).reshape(w.rows, w.cols).float() @ x.float()).cpu()
         tol = 1e-3 * ref.abs().max().item() + 1e-6
         assert (a - ref).abs().max().item() <= tol and (b - ref).abs().max().item() <= tol
+
+
+def test_fused_gemv_nonfinite_weights_stay_in_their_rows(E):
+    """Raw-bit NaN / inf weights (legal in the format, test_codec.cpp:123-130)
+    poison only their own row's y; every other row matches the fp32 reference
+    (the gather never lets a neighbouring row's values into a product)."""
+    rows, cols = 24, 2048
+    w = E.synth_weight(rows, cols, 99, device="cuda")
+    E.magnitude_prune(w, 0.5, inplace=True)
+    wh = w.data.view(torch.float16).reshape(rows, cols)
+    nz = (wh[0] != 0).nonzero()[0].item()
+    wh[0, nz] = float("nan")
+    nz5 = (wh[5] != 0).nonzero()[3].item()
+    wh[5, nz5] = float("inf")
+    t = E.compress(w)
+    x = (torch.rand(cols, generator=torch.Generator().manual_seed(3)) + 0.5).half().cuda()  # finite, > 0
+    y = E.gemv_compressed(t, x)
+    ref = wh.float() @ x.float()
+    assert torch.isnan(y[0]) and torch.isinf(y[5]) and y[5] > 0
+    ok = torch.ones(rows, dtype=torch.bool, device="cuda")
+    ok[0] = ok[5] = False
+    tol = 1e-3 * ref[ok].abs().max().item() + 1e-6
+    assert torch.isfinite(y[ok]).all() and (y[ok] - ref[ok]).abs().max().item() <= tol
