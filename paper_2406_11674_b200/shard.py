@@ -107,3 +107,20 @@ def all_gather_dense(shard_dense, full_rows: int, group=None):
                       dtype=torch.uint8, device=shard_dense.data.device)
     dist.all_gather_into_tensor(out, shard_dense.data.contiguous(), group=group)
     return out
+
+
+def all_gather_y(y_shard, full_rows: int, group=None):
+    """Concatenate the row-shard GEMV outputs y_g (rows r0..r1 of y = W x) into
+    the full y on every rank (the only exchange a row-sharded
+    GEMV ever needs; rows * 4 bytes).  Ragged shards (R % world != 0) are
+    padded to the largest shard for the collective and trimmed after."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    shards = row_shards(full_rows, 1, world)
+    width = max(sh.rows for sh in shards)
+    buf = torch.zeros(width, dtype=y_shard.dtype, device=y_shard.device)
+    buf[: y_shard.numel()] = y_shard
+    out = torch.empty(width * world, dtype=y_shard.dtype, device=y_shard.device)
+    dist.all_gather_into_tensor(out, buf, group=group)
+    return torch.cat([out[g * width: g * width + sh.rows] for g, sh in enumerate(shards)])
