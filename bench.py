@@ -186,13 +186,13 @@ def run_ours(args):
     for s in shards:
         s["dense"] = torch.empty(s["n"] * 2 + 16, dtype=torch.uint8, device=dev)
         s["out"] = E.DenseMatrix(s["rows"], s["cols"], E.Dtype.F16, s["dense"][: s["n"] * 2])
-    # one batch per decoder layer's six weight shards.  Headline: the reference's
-    # parallel API decompress_chunked (codec.hpp:205) with a RankIndex at chunk
-    # 1024 built once at load time (like compression, offline): one expand launch
-    # per layer.  Also reported: decompress (codec.hpp:157), no index (count +
-    # expand launches per layer).
-    per_layer = len(shards) // world
-    groups = [shards[i:i + per_layer] for i in range(0, len(shards), per_layer)]
+    # one batch per step: every weight shard this rank owns (6 per layer, 6 N at N
+    # GPUs, <= 64 per launch).  Headline: the reference's parallel API
+    # decompress_chunked (codec.hpp:205) with a RankIndex at chunk 1024 built once
+    # at load time (like compression, offline): one expand launch per step.  Also
+    # reported: decompress (codec.hpp:157), no index (count + expand launches).
+    per_layer = len(shards)
+    groups = [shards]
     for s in shards:
         s["idx"] = E.build_rank_index(s["t"].bitmap, 1024)
     plans_idx = [E.BatchPlan([s["t"] for s in g], [s["out"] for s in g], indices=[s["idx"] for s in g])

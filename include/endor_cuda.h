@@ -118,7 +118,7 @@ int endor_cuda_sync_status(void* ws, void* stream);
 int endor_cuda_decompress(const endor_tensor_view* t, void* dense_out, void* ws, size_t ws_bytes,
                           void* stream);
 
-/* decompress of up to 16 tensors of one dtype in two launches total (one
+/* decompress of up to 64 tensors of one dtype in two launches total (one
  * count, one persistent expand over all of their tiles) -- e.g. every weight
  * matrix of a decoder layer.  Bitmaps and outputs 16-byte aligned; the
  * workspace needs endor_cuda_workspace_bytes_batch(views, count) bytes.
@@ -176,7 +176,7 @@ int endor_cuda_decompress_chunked(const endor_tensor_view* t, uint64_t chunk_siz
                                   const uint64_t* prefix, uint64_t chunk_count, void* dense_out,
                                   void* ws, size_t ws_bytes, void* stream);
 
-/* decompress_chunked over up to 16 tensors.  With chunk_size == 1024 (the
+/* decompress_chunked over up to 64 tensors.  With chunk_size == 1024 (the
  * recommended load-time index: 8 bytes per 1024 elements) and 16-byte aligned
  * bitmaps and prefixes, the index supplies every sub-tile's value offset, so
  * the whole batch is ONE expand launch with no counting pass; like the
@@ -258,7 +258,7 @@ int endor_cuda_quantize_values(const void* values_f16, uint64_t nnz, void* q_out
 int endor_cuda_gemv(uint64_t rows, uint64_t cols, const void* w_f16, const void* x_f16,
                     float* y_f32, void* y_f16, void* stream);
 
-/* Batched dense GEMV: y_i = W_i x_i for up to 16 matrices (one decoder
+/* Batched dense GEMV: y_i = W_i x_i for up to 64 matrices (one decoder
  * layer) in one launch.  y_f32 / y_f16 arrays (and their entries) may be
  * NULL, not both for a matrix.  Same numerics as endor_cuda_gemv. */
 int endor_cuda_gemv_batch(const uint64_t* rows, const uint64_t* cols, const void* const* w_f16,
@@ -276,7 +276,7 @@ int endor_cuda_gemv_batch(const uint64_t* rows, const uint64_t* cols, const void
 int endor_cuda_gemv_compressed(const endor_tensor_view* t, const uint64_t* prefix1024, const void* x_f16,
                                float* y_f32, void* y_f16, void* ws, size_t ws_bytes, void* stream);
 
-/* Batched fused decompress -> GEMV: y_i = W_i x_i for up to 16 tensors (one
+/* Batched fused decompress -> GEMV: y_i = W_i x_i for up to 64 tensors (one
  * decoder layer's ops) in one persistent launch (+ one counting launch when
  * some prefix1024[i] is NULL, + one row-sum launch).  prefixes1024 may be
  * NULL (count every tensor); y_f32 / y_f16 arrays may be NULL, entries too.

@@ -472,7 +472,7 @@ def extract_cols(t: EndorTensor, cols) -> DenseMatrix:
 
 
 class BatchPlan:
-    """A prepared batch decompress of up to 16 same-dtype tensors (e.g. one
+    """A prepared batch decompress of up to 64 same-dtype tensors (e.g. one
     decoder layer's weights): two kernel launches for the whole batch."""
 
     def __init__(self, tensors, outs=None, indices=None):

@@ -227,7 +227,7 @@ int endor_cuda_decompress(const endor_tensor_view* t, void* dense_out, void* ws,
 static int plan_batch(const endor_tensor_view* views, void* const* outs, int count, Batch* b,
                       int* eb_out, uint64_t* nmax, size_t* bytes) {
     if (count < 0 || count > kMaxBatch || (count > 0 && !views))
-        return fail(ENDOR_ERR_INVALID_ARGUMENT, "batch must hold 0..16 tensors");
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "batch must hold 0..64 tensors");
     *b = Batch{};
     int eb = 0, st;
     uint64_t mx = 1;
@@ -363,7 +363,7 @@ int endor_cuda_gemv_compressed_batch(const endor_tensor_view* views, const uint6
                                      const void* const* x_f16, float* const* y_f32, void* const* y_f16,
                                      int count, void* ws, size_t ws_bytes, void* stream) {
     if (count < 0 || count > kMaxBatch || (count > 0 && (!views || !x_f16)))
-        return fail(ENDOR_ERR_INVALID_ARGUMENT, "batch must hold 0..16 tensors with x vectors");
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "batch must hold 0..64 tensors with x vectors");
     for (int i = 0; i < count; ++i) {
         const endor_tensor_view* t = &views[i];
         uint64_t n;
@@ -565,7 +565,7 @@ int endor_cuda_decompress_chunked_batch(const endor_tensor_view* views, const ui
                                         uint64_t cs, void* const* dense_outs, int count, void* ws,
                                         size_t ws_bytes, void* stream) {
     if (count < 0 || count > kMaxBatch || (count > 0 && (!views || !prefixes || !dense_outs)))
-        return fail(ENDOR_ERR_INVALID_ARGUMENT, "batch must hold 0..16 tensors with prefixes and outputs");
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "batch must hold 0..64 tensors with prefixes and outputs");
     bool fast = cs == uint64_t(kSubElems);
     for (int i = 0; i < count && fast; ++i) fast = aligned(views[i].bitmap, 16) && aligned(prefixes[i], 16);
     if (!fast) {  // general path, one tensor at a time (verifies every index entry)
@@ -740,7 +740,7 @@ int endor_cuda_gemv_batch(const uint64_t* rows, const uint64_t* cols, const void
                           const void* const* x_f16, float* const* y_f32, void* const* y_f16, int count,
                           void* stream) {
     if (count < 0 || count > kMaxBatch || (count > 0 && (!rows || !cols || !w_f16 || !x_f16)))
-        return fail(ENDOR_ERR_INVALID_ARGUMENT, "batch must hold 0..16 GEMVs");
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "batch must hold 0..64 GEMVs");
     GemvBatch gb{};
     for (int i = 0; i < count; ++i) {
         uint64_t n;

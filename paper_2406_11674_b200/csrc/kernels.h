@@ -49,7 +49,7 @@ struct ExpandArgs {
 // ---- the hot path: a batch of whole tensors (one layer's ops) -----------------
 // count_kernel + expand_tma_kernel take the batch by value (__grid_constant__),
 // so one launch of each covers every tensor with no descriptor upload.
-constexpr int kMaxBatch = 16;
+constexpr int kMaxBatch = 64;  // e.g. every row shard of 8 decoder layers (48 tensors) in one launch
 struct BatchTensor {
     const uint8_t* bitmap;  // 16-byte aligned, ceil(n/8) bytes
     const uint8_t* values;  // nnz*eb bytes, any alignment
