@@ -54,6 +54,19 @@ def env_dist():
     return world, rank, local
 
 
+def numa_pin(gpu: int) -> None:
+    """Bind this rank to the CPUs NVML reports as local to its GPU, so pinned
+    host buffers (first-touched by this process) sit on the GPU's NUMA node and
+    each rank's H2D uses its own socket's memory (north star (c): every GPU
+    streams its shards over its own PCIe link)."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        pynvml.nvmlDeviceSetCpuAffinity(pynvml.nvmlDeviceGetHandleByIndex(gpu))
+    except Exception:
+        pass
+
+
 def measured_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -174,6 +187,7 @@ def run_ours(args):
         local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    numa_pin(local)
     if world > 1:
         if share:
             dist.init_process_group("gloo")
