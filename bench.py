@@ -61,8 +61,11 @@ def numa_pin(gpu: int) -> None:
     streams its shards over its own PCIe link)."""
     try:
         import pynvml
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        ids = [v for v in vis.split(",") if v.strip()]
+        phys = int(ids[gpu]) if ids and gpu < len(ids) and ids[gpu].strip().isdigit() else gpu
         pynvml.nvmlInit()
-        pynvml.nvmlDeviceSetCpuAffinity(pynvml.nvmlDeviceGetHandleByIndex(gpu))
+        pynvml.nvmlDeviceSetCpuAffinity(pynvml.nvmlDeviceGetHandleByIndex(phys))
     except Exception:
         pass
 
