@@ -553,6 +553,29 @@ int endor_cuda_decompress_chunked(const endor_tensor_view* t, uint64_t cs, const
         const uint64_t* pres[1] = {prefix};
         return endor_cuda_decompress_chunked_batch(t, pres, cs, outs, 1, ws, ws_bytes, stream);
     }
+    if (cs > uint64_t(kSubElems) && aligned(t->bitmap, 16)) {
+        // coarser index (the reference's default 4096, codec.hpp:19): count the
+        // bitmap once, check every index entry against the count tables, then
+        // the persistent TMA expand over the count tables
+        Batch b{};
+        b.count = 1;
+        b.check_total = 1;
+        BatchTensor& T = b.t[0];
+        T.bitmap = static_cast<const uint8_t*>(t->bitmap);
+        T.values = static_cast<const uint8_t*>(t->values);
+        T.dst = static_cast<uint8_t*>(dense_out);
+        T.n = n;
+        T.nnz = t->nnz;
+        uint64_t sub_cap, blk_cap;
+        batch_plan(b, &sub_cap, &blk_cap, count_ctas());  // within ws_layout(n)'s capacities
+        b.tsub = L.tsub;
+        b.blk = L.blk;
+        b.hdr = L.hdr;
+        CK(launch_count(b, S(stream)));
+        CK(launch_verify_index(reinterpret_cast<const unsigned long long*>(prefix), chunks, cs, b, S(stream)));
+        CK(launch_expand_tma(b, eb, S(stream)));
+        return ENDOR_OK;
+    }
     ScanArgs a = scan_args(t->bitmap, n, 0, n, L);
     a.check_total = 1;
     a.expect_total = t->nnz;

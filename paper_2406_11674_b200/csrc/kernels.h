@@ -98,6 +98,10 @@ __host__ __device__ inline int batch_tensor_of_cblk(const Batch& b, uint32_t g) 
 // (ws_layout_caps capacities).
 void batch_plan(Batch& b, uint64_t* sub_total, uint64_t* blk_total, int count_ctas);
 cudaError_t launch_count(const Batch& b, cudaStream_t s);
+// check a caller's RankIndex (chunk cs > 1024, power of two) against the
+// count tables of b.t[0] (after launch_count); latches CORRUPTION
+cudaError_t launch_verify_index(const unsigned long long* idx, uint64_t chunks, uint64_t cs, const Batch& b,
+                                cudaStream_t s);
 cudaError_t launch_expand_tma(const Batch& b, int mode, cudaStream_t s);  // 1 i8, 2 f16, 3 dequant
 // fused decompress -> GEMV over a batch (f16, cols % 1024 == 0, part set per tensor),
 // then y[r] = sum of row r's cols/1024 segment partials in a fixed order

@@ -192,6 +192,29 @@ void batch_plan(Batch& b, uint64_t* sub_total, uint64_t* blk_total, int count_ct
     *blk_total = blk;
 }
 
+// A caller's RankIndex at a chunk size > 1024 (e.g. kDefaultChunkSize 4096,
+// codec.hpp:19) checked entry by entry against count_kernel's two-level
+// table: idx[k] must equal rank(k * cs) (bitmap.hpp:121-131).
+__global__ void __launch_bounds__(256) verify_index_kernel(const unsigned long long* __restrict__ idx,
+                                                           uint64_t chunks, uint64_t step,
+                                                           const unsigned long long* __restrict__ tsub,
+                                                           const unsigned long long* __restrict__ blk,
+                                                           uint64_t spc, WsHeader* hdr) {
+    const uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= chunks) return;
+    const uint64_t j = k * step;  // the chunk start's 1024-element sub-tile
+    if (idx[k] != blk[j / spc] + tsub[j]) latch_status(hdr, ENDOR_ERR_CORRUPTION);
+}
+
+cudaError_t launch_verify_index(const unsigned long long* idx, uint64_t chunks, uint64_t cs, const Batch& b,
+                                cudaStream_t s) {
+    if (chunks == 0) return cudaSuccess;
+    const BatchTensor& T = b.t[0];
+    verify_index_kernel<<<unsigned(ceil_div(chunks, 256)), 256, 0, s>>>(
+        idx, chunks, cs / kSubElems, b.tsub + T.sub0, b.blk + T.blk0, uint64_t(kCountSubs) * T.cbpc, b.hdr);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_count(const Batch& b, cudaStream_t s) {
     if (b.ncblk == 0) return cudaSuccess;
     constexpr int smem = 2 * kCountBlockWords * 4;  // two 32 KiB stages

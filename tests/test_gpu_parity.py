@@ -231,16 +231,40 @@ def test_chunked_1024_index_errors_are_safe(E):
     bad[-1] += 1
     with pytest.raises(E.CorruptionError):
         E.decompress_chunked(t, E.RankIndex(1024, bad))
-    # wildly wrong middle entries: never an illegal access; reported or garbage
-    for v in (10 ** 12, -5):
+    # wrong middle entries (check_index only tests the last one; here every entry
+    # is verified): small or wild, always CorruptionError, never an illegal access
+    for v in (3, 10 ** 12, -5):
         bad = good.prefix.clone()
-        bad[len(bad) // 2] = v
-        try:
+        bad[len(bad) // 2] = v if v != 3 else bad[len(bad) // 2] + 3
+        with pytest.raises(E.CorruptionError):
             E.decompress_chunked(t, E.RankIndex(1024, bad))
-        except E.CorruptionError:
-            pass
     # and the device is still healthy afterwards
     assert E.decompress_chunked(t, good).bytes() == w.tobytes()
+
+
+@pytest.mark.parametrize("cs", [2048, 4096, 8192, 65536])
+def test_chunked_coarse_index_fast_path(E, seeded_cases, cs):
+    """decompress_chunked at the reference's default chunk size (4096,
+    codec.hpp:19) and other coarse ones: count + per-entry index check + the TMA
+    expand; bit-exact, and any wrong entry raises CorruptionError."""
+    for i, c in enumerate(seeded_cases[:30]):
+        rows, cols, eb = c["rows"], c["cols"], c["eb"]
+        w = O.random_dense(rows, cols, eb, c["seed"], c["zero_fraction"])
+        bm, vals, nnz, _ = O.compress(w, rows, cols, eb)
+        t = make_tensor(E, rows, cols, eb, bm, vals, nnz, values_offset=(i % 4) * eb)
+        idx = E.build_rank_index(t.bitmap, cs)
+        assert E.decompress_chunked(t, idx).bytes() == w.tobytes()
+    rows, cols = 512, 1000
+    w = O.random_dense(rows, cols, 2, 8, 0.5)
+    bm, vals, nnz, _ = O.compress(w, rows, cols, 2)
+    t = make_tensor(E, rows, cols, 2, bm, vals, nnz)
+    good = E.build_rank_index(t.bitmap, cs)
+    assert E.decompress_chunked(t, good).bytes() == w.tobytes()
+    if good.chunk_count() > 2:
+        bad = good.prefix.clone()
+        bad[1] += 1
+        with pytest.raises(E.CorruptionError):
+            E.decompress_chunked(t, E.RankIndex(cs, bad))
 
 
 def test_chunks_any_order_and_isolation(E):
