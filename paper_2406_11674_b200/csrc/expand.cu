@@ -322,16 +322,7 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
                 if (T.idx) {  // a caller's index may be inconsistent: stay inside the staged window
                     const uint32_t wcount = lds32(stg + Stage<EB>::kSub + 68);
                     const uint32_t wtotal = __shfl_sync(0xffffffffu, excl + pc, 31);
-                    bool bad = sw < tp || wtotal > wcount || rel > wcount - wtotal;
-                    if (kWarpElems == kSubElems) {
-                        // every entry exact (a superset of check_index's tail test):
-                        // this sub-tile's popcount == next entry - this entry
-                        const int nx = sub + 1;
-                        const bool has = nx < kTileElems / kSubElems && t0 + uint64_t(nx) * kSubElems < T.n;
-                        const unsigned long long sn = has ? lds64(stg + Stage<EB>::kSub + 8 * nx) : tp + wcount;
-                        bad |= sn - sw != wtotal;
-                    }
-                    if (bad) {
+                    if (sw < tp || wtotal > wcount || rel > wcount - wtotal) {
                         if (lane == 0) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
                         rel = 0;
                         if (wtotal > wcount) word = 0;  // nothing valid to place
