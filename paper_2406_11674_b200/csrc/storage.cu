@@ -12,8 +12,9 @@
 //     link dependency: DMA from NVMe into HBM when nvidia-fs is loaded
 //     (cuFile's compatibility mode only on explicit request: its driver open
 //     hangs on this pool's boxes, which have no nvidia-fs);
-//   * POSIX: O_DIRECT reads of 4 KiB-aligned spans into two pinned bounce
-//     buffers, each chunk's cudaMemcpyAsync overlapping the next read.
+//   * POSIX: O_DIRECT reads of 4 KiB-aligned spans into four pinned bounce
+//     buffers, three reads in flight on worker threads, each chunk's
+//     cudaMemcpyAsync issued in order as its read lands.
 //
 // verify = 1 completes decode_endor's checks on the device copy: the CRC-32
 // of the whole file (header on the host; bitmap and values on the GPU: one
@@ -31,6 +32,7 @@
 
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -40,6 +42,8 @@
 using namespace endor_b200;
 
 namespace {
+
+constexpr int kBounce = 4;  // pinned bounce buffers of the POSIX engine (3 reads in flight)
 
 thread_local int g_format_kind = -1;
 
@@ -248,8 +252,8 @@ struct endor_reader {
     int device = 0;
     int mode = 0;
     size_t bounce_bytes = 0;
-    void* bounce[2] = {nullptr, nullptr};
-    cudaEvent_t done[2] = {nullptr, nullptr};
+    void* bounce[kBounce] = {};
+    cudaEvent_t done[kBounce] = {};
     uint32_t* crc_tab = nullptr;  // 8 x 256 slicing tables
     uint32_t* crc_scratch = nullptr;
     size_t crc_cap = 0;  // u32 entries
@@ -379,9 +383,9 @@ int endor_reader_create(int device, size_t bounce_bytes, int mode, endor_reader*
         }
     }
     r->mode = mode;
-    r->bounce_bytes = ((bounce_bytes ? bounce_bytes : (64u << 20)) + 4095) & ~size_t(4095);
+    r->bounce_bytes = ((bounce_bytes ? bounce_bytes : (16u << 20)) + 4095) & ~size_t(4095);
     if (e == cudaSuccess && mode == ENDOR_IO_POSIX)
-        for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+        for (int i = 0; i < kBounce && e == cudaSuccess; ++i) {
             e = cudaHostAlloc(&r->bounce[i], r->bounce_bytes + 4096, cudaHostAllocPortable);
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r->done[i], cudaEventDisableTiming);
         }
@@ -399,7 +403,7 @@ int endor_reader_create(int device, size_t bounce_bytes, int mode, endor_reader*
 int endor_reader_destroy(endor_reader* r) {
     if (!r) return ENDOR_OK;
     cudaSetDevice(r->device);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kBounce; ++i) {
         if (r->done[i]) cudaEventSynchronize(r->done[i]), cudaEventDestroy(r->done[i]);
         if (r->bounce[i]) cudaFreeHost(r->bounce[i]);
     }
@@ -420,30 +424,66 @@ int endor_reader_stats(const endor_reader* r, double* seconds, uint64_t* bytes) 
 }
 
 static int read_posix(endor_reader* r, int fd, uint64_t off, uint64_t len, uint8_t* dst, cudaStream_t s) {
-    // 4 KiB-aligned spans through two pinned bounce buffers; the H2D of one
-    // chunk overlaps the read of the next
-    uint64_t done = 0;
-    int k = 0;
-    while (done < len) {
-        const uint64_t want = len - done < r->bounce_bytes ? len - done : r->bounce_bytes;
-        const uint64_t a0 = (off + done) & ~uint64_t(4095), head = off + done - a0;
-        const uint64_t span = (head + want + 4095) & ~uint64_t(4095);
-        cudaError_t e = cudaEventSynchronize(r->done[k]);
+    // 4 KiB-aligned spans through kBounce pinned bounce buffers: up to
+    // kBounce - 1 O_DIRECT reads in flight on worker threads (the device queue
+    // wants depth), each chunk's H2D issued in order as its read completes
+    const uint64_t B = r->bounce_bytes, nch = (len + B - 1) / B;
+    struct Job {
+        std::thread th;
+        uint64_t want = 0, head = 0;
+        int err = 0;
+    };
+    std::vector<Job> jobs(kBounce);
+    int st = ENDOR_OK;
+    auto start = [&](uint64_t c) -> int {
+        Job& j = jobs[c % kBounce];
+        const int k = int(c % kBounce);
+        cudaError_t e = cudaEventSynchronize(r->done[k]);  // bounce k's previous H2D is done
         if (e != cudaSuccess) return set_last_error(ENDOR_ERR_CUDA, cudaGetErrorString(e));
-        uint8_t* b = static_cast<uint8_t*>(r->bounce[k]);
-        uint64_t got = 0;
-        while (got < head + want) {
-            const ssize_t n = pread(fd, b + got, size_t(span - got), off_t(a0 + got));
-            if (n <= 0) return set_last_error(ENDOR_ERR_IO, "short read from the container");
-            got += uint64_t(n);
+        const uint64_t pos = off + c * B;
+        j.want = len - c * B < B ? len - c * B : B;
+        const uint64_t a0 = pos & ~uint64_t(4095);
+        j.head = pos - a0;
+        const uint64_t span = (j.head + j.want + 4095) & ~uint64_t(4095);
+        uint8_t* buf = static_cast<uint8_t*>(r->bounce[k]);
+        j.err = 0;
+        j.th = std::thread([&j, fd, buf, a0, span]() {
+            uint64_t got = 0;
+            while (got < j.head + j.want) {
+                const ssize_t n = pread(fd, buf + got, size_t(span - got), off_t(a0 + got));
+                if (n <= 0) {
+                    j.err = 1;
+                    return;
+                }
+                got += uint64_t(n);
+            }
+        });
+        return ENDOR_OK;
+    };
+    uint64_t issued = 0;
+    for (; issued < nch && issued < uint64_t(kBounce - 1) && !st; ++issued) st = start(issued);
+    for (uint64_t c = 0; c < issued; ++c) {
+        Job& j = jobs[c % kBounce];
+        j.th.join();
+        if (st) continue;  // drain the remaining workers after an error
+        if (j.err) {
+            st = set_last_error(ENDOR_ERR_IO, "short read from the container");
+            continue;
         }
-        if ((e = cudaMemcpyAsync(dst + done, b + head, want, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
-            (e = cudaEventRecord(r->done[k], s)) != cudaSuccess)
-            return set_last_error(ENDOR_ERR_CUDA, cudaGetErrorString(e));
-        done += want;
-        k ^= 1;
+        const int k = int(c % kBounce);
+        cudaError_t e;
+        if ((e = cudaMemcpyAsync(dst + c * B, static_cast<uint8_t*>(r->bounce[k]) + j.head, j.want,
+                                 cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+            (e = cudaEventRecord(r->done[k], s)) != cudaSuccess) {
+            st = set_last_error(ENDOR_ERR_CUDA, cudaGetErrorString(e));
+            continue;
+        }
+        if (issued < nch) {
+            st = start(issued);
+            if (!st) ++issued;
+        }
     }
-    return ENDOR_OK;
+    return st;
 }
 
 int endor_reader_read(endor_reader* r, const char* path, const endor_file_info* f, void* bitmap_dev,
