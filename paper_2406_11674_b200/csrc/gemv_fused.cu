@@ -137,7 +137,10 @@ struct ItemCursor {
     __device__ uint64_t item() const { return col + j * segs; }
 };
 
-__global__ void __launch_bounds__(kGvThreads, 3) gemv_fused_kernel(const __grid_constant__ Batch b, uint64_t nitems) {
+#ifndef ENDOR_GV_MINB
+#define ENDOR_GV_MINB 3  // CTAs per SM the register budget is sized for
+#endif
+__global__ void __launch_bounds__(kGvThreads, ENDOR_GV_MINB) gemv_fused_kernel(const __grid_constant__ Batch b, uint64_t nitems) {
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t sbase = smem_u32(smem);
     const uint32_t full0 = sbase, empty0 = sbase + 8 * kGvStages;
