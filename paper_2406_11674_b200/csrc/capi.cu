@@ -7,7 +7,10 @@
 #include <string.h>
 
 #include <cstdio>
+#include <map>
+#include <mutex>
 #include <string>
+#include <utility>
 
 #include "common.cuh"
 #include "endor_cuda.h"
@@ -29,6 +32,28 @@ int fail(int code, const char* what) {
 int endor_b200::set_last_error(int code, const char* what) {
     g_last_error = what;
     return code;
+}
+
+cudaError_t endor_b200::kernel_slots(const void* fn, int threads, size_t smem, int* blocks_per_sm, int* sms) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, std::pair<int, int>> cache;  // (fn, dev) -> (bps, sms)
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find({fn, dev});
+    if (it == cache.end()) {
+        if (smem > 48 * 1024 &&
+            (e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) != cudaSuccess)
+            return e;
+        int n = 0, bps = 0;
+        if ((e = cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, threads, smem)) != cudaSuccess) return e;
+        it = cache.emplace(std::make_pair(fn, dev), std::make_pair(bps < 1 ? 1 : bps, n)).first;
+    }
+    if (blocks_per_sm) *blocks_per_sm = it->second.first;
+    if (sms) *sms = it->second.second;
+    return cudaSuccess;
 }
 
 namespace {

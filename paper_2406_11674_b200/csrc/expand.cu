@@ -426,19 +426,11 @@ cudaError_t launch_expand(const ExpandArgs& a, int mode, cudaStream_t s) {
 
 template <int MODE>
 static cudaError_t launch_tma_mode(const Batch& b, cudaStream_t s) {
-    static int blocks_per_sm = 0, sms = 0;
     constexpr uint32_t smem = tma_smem_bytes<mode_in(MODE)>();
-    if (!blocks_per_sm) {
-        cudaError_t e = cudaFuncSetAttribute(expand_tma_kernel<MODE>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (e != cudaSuccess) return e;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, expand_tma_kernel<MODE>,
-                                                      kTmaThreads, smem);
-        if (blocks_per_sm < 1) blocks_per_sm = 1;
-    }
+    int blocks_per_sm = 1, sms = 148;
+    cudaError_t e = kernel_slots(reinterpret_cast<const void*>(expand_tma_kernel<MODE>), kTmaThreads, smem,
+                                 &blocks_per_sm, &sms);
+    if (e != cudaSuccess) return e;
     const uint64_t grid = umin64(b.ntiles, uint64_t(blocks_per_sm) * sms);
     if (grid == 0) return cudaSuccess;
     expand_tma_kernel<MODE><<<unsigned(grid), kTmaThreads, smem, s>>>(b);

@@ -250,12 +250,10 @@ cudaError_t launch_extract_cols(const RankTable& rt, const uint8_t* values, uint
     if (rows == 0 || nsel == 0) return cudaSuccess;
     const size_t smem = 2 * sizeof(uint32_t) * ((cols + 31) / 32);
     if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(extract_cols_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(extract_cols_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
+    cudaError_t e = kernel_slots(eb == 2 ? reinterpret_cast<const void*>(extract_cols_kernel<2>)
+                                         : reinterpret_cast<const void*>(extract_cols_kernel<1>),
+                                 256, 200 * 1024, nullptr, nullptr);
+    if (e != cudaSuccess) return e;
     if (rows > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     if (eb == 2) extract_cols_kernel<2><<<unsigned(rows), 256, smem, s>>>(rt, values, nnz, cols, sel, nsel, out, hdr);
     else extract_cols_kernel<1><<<unsigned(rows), 256, smem, s>>>(rt, values, nnz, cols, sel, nsel, out, hdr);

@@ -331,15 +331,11 @@ cudaError_t launch_prune(uint8_t* w, uint64_t n, int eb, uint64_t target, const 
     cudaError_t e = cudaMemsetAsync(L.hist, 0, sizeof(unsigned long long) * kHistBins, s);
     if (e != cudaSuccess) return e;
     const size_t smem = sizeof(uint32_t) * kHistBins;
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaFuncSetAttribute(hist_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        cudaFuncSetAttribute(hist_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        attr_done = true;
-    }
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int sms = 148;
+    e = kernel_slots(eb == 2 ? reinterpret_cast<const void*>(hist_kernel<2>)
+                             : reinterpret_cast<const void*>(hist_kernel<1>),
+                     1024, smem, nullptr, &sms);
+    if (e != cudaSuccess) return e;
     const uint64_t want = ceil_div(n, 1024);
     const unsigned hg = unsigned(want < uint64_t(sms) ? want : uint64_t(sms));
     if (eb == 2) hist_kernel<2><<<hg, 1024, smem, s>>>(w, n, L.hist);

@@ -415,17 +415,10 @@ cudaError_t launch_gemv_fused(Batch& b, cudaStream_t s) {
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
-    static int blocks_per_sm = 0, sms = 0;
-    if (!blocks_per_sm) {
-        cudaError_t e = cudaFuncSetAttribute(gemv_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(kGvSmem));
-        if (e != cudaSuccess) return e;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, gemv_fused_kernel, kGvThreads, kGvSmem);
-        if (blocks_per_sm < 1) blocks_per_sm = 1;
-    }
+    int blocks_per_sm = 1, sms = 148;
+    cudaError_t e = kernel_slots(reinterpret_cast<const void*>(gemv_fused_kernel), kGvThreads, kGvSmem,
+                                 &blocks_per_sm, &sms);
+    if (e != cudaSuccess) return e;
     uint64_t items = 0;
     for (int k = 0; k < b.count; ++k) {
         BatchTensor& T = b.t[k];

@@ -11,6 +11,12 @@ namespace endor_b200 {
 // thread-local last-error detail of the C ABI (capi.cu); returns code
 int set_last_error(int code, const char* what);
 
+// One-time, per-device kernel setup (cudaFuncSetAttribute is per device):
+// raises the dynamic shared-memory limit of `fn` to `smem` on the current
+// device and returns its resident CTAs per SM at `threads` and the SM count.
+// Thread-safe; cached per (kernel, device).
+cudaError_t kernel_slots(const void* fn, int threads, size_t smem, int* blocks_per_sm, int* sms);
+
 struct ScanArgs {
     const uint8_t* bitmap;
     uint64_t nbytes;         // ceil(n/8): readable bitmap bytes

@@ -218,12 +218,8 @@ cudaError_t launch_verify_index(const unsigned long long* idx, uint64_t chunks, 
 cudaError_t launch_count(const Batch& b, cudaStream_t s) {
     if (b.ncblk == 0) return cudaSuccess;
     constexpr int smem = 2 * kCountBlockWords * 4;  // two 32 KiB stages
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    cudaError_t e = kernel_slots(reinterpret_cast<const void*>(count_kernel), kScanThreads, smem, nullptr, nullptr);
+    if (e != cudaSuccess) return e;
     count_kernel<<<b.ncblk, kScanThreads, smem, s>>>(b);
     return cudaGetLastError();
 }
