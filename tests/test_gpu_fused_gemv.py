@@ -142,3 +142,21 @@ def test_fused_gemv_nonfinite_weights_stay_in_their_rows(E):
     ok[0] = ok[5] = False
     tol = 1e-3 * ref[ok].abs().max().item() + 1e-6
     assert torch.isfinite(y[ok]).all() and (y[ok] - ref[ok]).abs().max().item() <= tol
+
+
+@pytest.mark.parametrize("offset", [2, 6, 10, 14])
+def test_fused_gemv_unaligned_values_buffer(E, offset):
+    """The packed values may start at any 2-byte offset (the .endor layout puts
+    them at 32 + ceil(n/8), file_io.hpp:32-36): the TMA windows' ragged ends are
+    copied bytewise; results equal the aligned case bitwise."""
+    rows, cols = 50, 3072
+    w = E.synth_weight(rows, cols, 4242, device="cuda")
+    E.magnitude_prune(w, 0.5, inplace=True)
+    t = E.compress(w)
+    vb = t.values.numel()
+    buf = torch.zeros(vb + 64, dtype=torch.uint8, device="cuda")
+    buf[offset:offset + vb].copy_(t.values)
+    tu = E.EndorTensor(rows, cols, E.Dtype.F16, t.bitmap, buf[offset:offset + vb], validate=False, nnz=t.nnz())
+    x = (torch.rand(cols, generator=torch.Generator().manual_seed(1)) * 2 - 1).half().cuda()
+    assert torch.equal(E.gemv_compressed(tu, x), E.gemv_compressed(t, x))
+    assert torch.equal(E.gemv_compressed(tu, x, index=E.build_rank_index(t.bitmap, 1024)), E.gemv_compressed(t, x))
