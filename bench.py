@@ -81,31 +81,64 @@ def measured_peak():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region: NVML polled
+    in-process every millisecond (a sub-10 ms region still gets samples), with
+    nvidia-smi as the fallback where NVML is unavailable."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, set(reasons), perf_counter time)
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            vis = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
+            phys = int(vis[gpu_index]) if vis and gpu_index < len(vis) and vis[gpu_index].strip().isdigit() \
+                else gpu_index
+            h = pynvml.nvmlDeviceGetHandleByIndex(phys)
+            bits = [pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap]
+            self._max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))  # ~3 ms per call
+            self._nvml = (pynvml, h, bits)
+            t = time.perf_counter()
+            self._sample()  # first queries are slow (driver-side setup): pay it here
+            self.nvml_sample_ms = round((time.perf_counter() - t) * 1e3, 3)
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        if self._nvml:
+            nv, h, bits = self._nvml
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            return (float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), self._max_mhz,
+                    {n for n, bit in zip(self.NAMES, bits) if r & bit}, time.perf_counter())
+        out = subprocess.run(["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + self.Q,
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip()
+        f = [x.strip() for x in out.split(",")]
+        return (float(f[0]), float(f[1]), {n for n, v in zip(self.NAMES, f[2:6]) if v.lower() == "active"},
+                time.perf_counter())
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + self.Q,
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                self.samples.append(self._sample())
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.001 if self._nvml else 0.2)
 
     def __enter__(self):
+        # the launching thread holds the GIL between its (GIL-releasing) CUDA
+        # calls; a short switch interval lets the poller run inside short regions
+        self._switch = sys.getswitchinterval()
+        sys.setswitchinterval(0.0002)
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
@@ -113,16 +146,15 @@ class ClockSampler:
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=6)
+        sys.setswitchinterval(self._switch)
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples),
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": sorted(set().union(*(s[2] for s in self.samples))),
+                "samples": len(self.samples), "source": "nvml" if self._nvml else "nvidia-smi",
                 "samples_in_timed_region": getattr(self, "in_region", len(self.samples))}
 
 
@@ -232,6 +264,9 @@ def run_ours(args):
     def timed(plans, sample_clocks=False):
         """warmup, then exactly `steps` steps between events on the launching stream;
         barrier + synchronize on both sides; max over ranks."""
+        clk = ClockSampler(local) if sample_clocks else None
+        if clk:
+            clk.__enter__()  # polling from before the warm-up: it is running when the region opens
         for _ in range(args.warmup):
             for p in plans:
                 p.launch(sp)
@@ -241,17 +276,16 @@ def run_ours(args):
         barrier()
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        clk = ClockSampler(local) if sample_clocks else None
-        if clk:
-            clk.__enter__()
+        t_open = time.perf_counter()
         ev0.record(stream)
         for _ in range(args.steps):
             for p in plans:
                 p.launch(sp)
         ev1.record(stream)
         torch.cuda.synchronize()
+        t_close = time.perf_counter()
         if clk:
-            clk.in_region = len(clk.samples)
+            clk.in_region = sum(1 for s in list(clk.samples) if t_open <= s[3] <= t_close)
             # a sub-second timed region yields few nvidia-smi samples: keep the same
             # load running (untimed) until at least 3 samples exist
             t_end = time.time() + 3.0
