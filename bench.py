@@ -90,8 +90,9 @@ class ClockSampler:
          "clocks_event_reasons.sw_power_cap")
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, gpu_index: int, period_s: float = 0.001):
         self.idx = gpu_index
+        self.period = period_s
         self.samples = []  # (sm_mhz, max_mhz, set(reasons), perf_counter time)
         self._stop = threading.Event()
         self._t = None
@@ -132,7 +133,7 @@ class ClockSampler:
                 self.samples.append(self._sample())
             except Exception:
                 pass
-            self._stop.wait(0.001 if self._nvml else 0.2)
+            self._stop.wait(self.period if self._nvml else 0.2)
 
     def __enter__(self):
         # the launching thread holds the GIL between its (GIL-releasing) CUDA
@@ -388,7 +389,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         barrier()
         ops_all = hops * args.steps
-        with ClockSampler(local) as clk2:
+        with ClockSampler(local, float(os.environ.get("ENDOR_E2E_POLL_S", "0.02"))) as clk2:
             pipe.run(ops_all, sync=True)
         st = pipe.stats()
         barrier()
