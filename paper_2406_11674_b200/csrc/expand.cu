@@ -33,102 +33,6 @@
 
 namespace endor_b200 {
 
-// Fused INT8 dequant + decompress (decompress(dequantize_values(t)),
-// codec.hpp:334-349 then :157): 8 output f16 slots per 16-byte chunk, each
-// set slot = f32_to_f16(float(q) * scale) (float16.hpp:35-73, RNE), unset = +0.
-// FAST (scale finite, sign bit clear): unset slots hold q = 0 -> +0 exactly,
-// and a finite product is converted with the hardware RNE (identical to the
-// reference's routine for every non-NaN input).  Otherwise the reference's
-// own bit routine runs per slot and unset slots are masked to +0.
-template <bool FAST>
-__device__ __forceinline__ uint4 gather_chunk_dequant(uint32_t m, uint32_t a, float scale) {
-    uint32_t o[4];
-#pragma unroll
-    for (int g = 0; g < 2; ++g) {
-        const uint32_t q = (m >> (4 * g)) & 15u;
-        const uint32_t al = a & ~3u, sh = a << 3;
-        const uint32_t x = __byte_perm(__funnelshift_r(lds32(al), lds32(al + 4), sh), 0u, g_lut8[q]);
-        float f[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) f[k] = __fmul_rn(float(int8_t(x >> (8 * k))), scale);
-        if constexpr (FAST) {
-            const __half2 h0 = __floats2half2_rn(f[0], f[1]), h1 = __floats2half2_rn(f[2], f[3]);
-            o[2 * g] = *reinterpret_cast<const uint32_t*>(&h0);
-            o[2 * g + 1] = *reinterpret_cast<const uint32_t*>(&h1);
-        } else {
-            // NaN products follow the x86 SSE rules the reference runs under: a NaN
-            // operand propagates quieted, 0 * inf gives the default NaN 0xFFC00000
-            // (the GPU would produce a canonical 0x7FFFFFFF instead)
-            const uint32_t sb = __float_as_uint(scale);
-            const bool snan = (sb & 0x7FFFFFFFu) > 0x7F800000u;
-            uint32_t h[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                float v = f[k];
-                if (v != v) v = __uint_as_float(snan ? (sb | 0x00400000u) : 0xFFC00000u);
-                h[k] = (q >> k) & 1u ? f32_to_f16_bits(v) : 0u;
-            }
-            o[2 * g] = h[0] | (h[1] << 16);
-            o[2 * g + 1] = h[2] | (h[3] << 16);
-        }
-        a += __popc(q);
-    }
-    return make_uint4(o[0], o[1], o[2], o[3]);
-}
-
-// Element modes of the expand kernels: bytes per packed value (IN) and per
-// dense output element (OUT).
-constexpr int kModeI8 = 1, kModeF16 = 2, kModeDequant = 3;
-__host__ __device__ constexpr int mode_in(int m) { return m == kModeF16 ? 2 : 1; }
-__host__ __device__ constexpr int mode_out(int m) { return m == kModeI8 ? 1 : 2; }
-
-template <int MODE>
-__device__ __forceinline__ uint4 gather_mode(uint32_t m, uint32_t a, float scale, bool fast) {
-    if constexpr (MODE == kModeDequant) {
-        return fast ? gather_chunk_dequant<true>(m, a, scale) : gather_chunk_dequant<false>(m, a, scale);
-    } else {
-        return gather_chunk<MODE>(m, a);
-    }
-}
-
-__device__ __forceinline__ void store_partial(uint8_t* p, uint4 q, uint32_t valid_bytes) {
-    const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-    for (uint32_t b = 0; b < 16; ++b)
-        if (b < valid_bytes) p[b] = uint8_t(qw[b >> 2] >> ((b & 3) * 8));
-}
-
-// Expand one warp's 1024-element sub-tile.  word/excl: this lane's bitmap word
-// (bits past the range already cleared) and its exclusive popcount within the
-// warp; vbase: shared address of the sub-tile's first packed value.  Lane l
-// writes chunks l, l+32, .. so every store instruction covers 512 contiguous
-// bytes.  FULL: all 1024 elements valid (no bounds checks).
-template <int MODE, bool FULL, int WE = 1024>
-__device__ __forceinline__ void expand_subtile(uint32_t word, uint32_t excl, uint32_t vbase,
-                                               uint8_t* out, int32_t valid_elems, int lane,
-                                               float scale = 1.f, bool fast = true) {
-    constexpr int IN = mode_in(MODE), OUT = mode_out(MODE);
-    constexpr int EPC = 16 / OUT;             // output elements per 16-byte chunk
-    constexpr int CPW = 32 / EPC;             // chunks per bitmap word (4 or 2)
-    constexpr int ITERS = WE / EPC / 32;      // chunks per lane
-    const uint32_t sh = (lane % CPW) * EPC;   // chunk position inside its word: lane-constant
-    const uint32_t low = (1u << sh) - 1u;
-    uint8_t* o = out + size_t(lane) * 16;
-#pragma unroll
-    for (int j = 0; j < ITERS; ++j) {
-        const int src = (32 * j + lane) / CPW;
-        const uint32_t wd = __shfl_sync(0xffffffffu, word, src);
-        const uint32_t pre = __shfl_sync(0xffffffffu, excl, src);
-        const uint32_t m = (wd >> sh) & ((1u << EPC) - 1u);
-        const uint32_t r = pre + __popc(wd & low);
-        const int e = (32 * j + lane) * EPC;
-        if (!FULL && e >= valid_elems) continue;
-        const uint4 q = gather_mode<MODE>(m, vbase + r * IN, scale, fast);
-        if (FULL || e + EPC <= valid_elems) *reinterpret_cast<uint4*>(o + j * 512) = q;
-        else store_partial(o + j * 512, q, uint32_t(valid_elems - e) * OUT);
-    }
-}
-
 // ---------------------------------------------------------------------------
 // persistent TMA kernel (batched over whole tensors)
 // ---------------------------------------------------------------------------

@@ -16,6 +16,7 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "gather.cuh"
 #include "kernels.h"
 
 namespace endor_b200 {
@@ -86,6 +87,7 @@ __global__ void __launch_bounds__(kExpandThreads) extract_rows_kernel(RankTable 
     __shared__ __align__(16) uint8_t s_vals[kTileElems * EB + 64];
     if (read_status(hdr)) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    init_luts(tid);  // published by the __syncthreads below
     const uint64_t i = blockIdx.x / tiles_per_row, j = blockIdx.x % tiles_per_row;
     const uint64_t row = sel[i];
     const uint64_t x0 = row * cols + j * kTileElems;
@@ -136,10 +138,20 @@ __global__ void __launch_bounds__(kExpandThreads) extract_rows_kernel(RankTable 
         *reinterpret_cast<uint4*>(s_vals + v * 16) = q;
     }
     __syncthreads();
-    // scatter_range semantics per element (codec.hpp:136-149): each thread
-    // writes its 32 elements; element-wise stores keep any row alignment legal
     const uint32_t sb = smem_u32(s_vals) + uint32_t(ws - as);
-    uint8_t* dst = out + (i * cols + j * kTileElems + uint64_t(tid) * 32) * EB;
+    uint8_t* dst = out + (i * cols + j * kTileElems) * EB;
+    if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+        // the expand kernels' gather: each warp places its 1024 elements with
+        // the PRMT selector tables and coalesced 16-byte stores
+        const int32_t wfirst = warp * kSubElems;
+        if (wfirst < int32_t(count))
+            expand_subtile<EB, false>(wv, incl - pc, sb + wexcl * EB, dst + size_t(wfirst) * EB,
+                                      min(int32_t(count) - wfirst, kSubElems), lane);
+        return;
+    }
+    // output rows not 16-byte aligned (cols * eb % 16 != 0): scatter_range
+    // semantics per element (codec.hpp:136-149), element-wise stores
+    dst += uint64_t(tid) * 32 * EB;
     uint32_t r = wexcl + incl - pc;
     const uint32_t nel = uint32_t(tid) * 32 < count ? min(32u, count - uint32_t(tid) * 32) : 0u;
     for (uint32_t e = 0; e < nel; ++e) {
@@ -215,9 +227,14 @@ __global__ void __launch_bounds__(256) extract_cols_kernel(RankTable rt, const u
         uint32_t v = 0;
         if ((word >> b) & 1u) {
             const uint64_t rk = base + s_pre[w] + __popc(word & ((1u << b) - 1u));
-            // byte loads: the packed values may sit at any alignment (file_io.hpp:32-36)
-            v = EB == 2 ? uint32_t(__ldg(values + rk * 2)) | (uint32_t(__ldg(values + rk * 2 + 1)) << 8)
-                        : uint32_t(__ldg(values + rk));
+            if constexpr (EB == 2) {
+                // the packed values may sit at any alignment (file_io.hpp:32-36)
+                v = (reinterpret_cast<uintptr_t>(values) & 1)
+                        ? uint32_t(__ldg(values + rk * 2)) | (uint32_t(__ldg(values + rk * 2 + 1)) << 8)
+                        : uint32_t(__ldg(reinterpret_cast<const uint16_t*>(values) + rk));
+            } else {
+                v = uint32_t(__ldg(values + rk));
+            }
         }
         if constexpr (EB == 2) reinterpret_cast<uint16_t*>(orow)[k] = uint16_t(v);
         else orow[k] = uint8_t(v);
