@@ -367,3 +367,37 @@ def test_gemv_matches_fp32_reference(E, rows, cols):
     y = E.gemv(Wd, x.cuda()).cpu()
     tol = 1e-3 * ref.abs().max().item() + 1e-6
     assert (y - ref).abs().max().item() <= tol
+
+
+def test_concurrent_host_threads_disjoint_chunks(E):
+    """SPEC.md:143-144 / codec.hpp:188-190: per-chunk calls into disjoint regions
+    may run concurrently.  Four host threads, each with its own stream and
+    workspace, decompress_chunk_into interleaved chunks of one tensor into one
+    buffer; the result is the reference's decompress."""
+    import threading
+    rows, cols = 257, 1031
+    w = O.random_dense(rows, cols, 2, 606, 0.45)
+    bm, vals, nnz, _ = O.compress(w, rows, cols, 2)
+    t = make_tensor(E, rows, cols, 2, bm, vals, nnz)
+    idx = E.build_rank_index(t.bitmap, 4096)
+    buf = torch.zeros(t.dense_bytes(), dtype=torch.uint8, device="cuda")
+    errs = []
+
+    def worker(r):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for k in range(r, idx.chunk_count(), 4):
+                    E.decompress_chunk_into(t, idx, k, buf)
+            s.synchronize()
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(4)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    torch.cuda.synchronize()
+    assert not errs
+    assert buf.cpu().numpy().tobytes() == w.tobytes()
