@@ -1,0 +1,101 @@
+"""Every kernel of the library once on small shapes, for compute-sanitizer
+(memcheck / racecheck / synccheck / initcheck).  Checks
+results against the oracle as it goes, so a sanitizer run is also a parity run.
+
+  compute-sanitizer --tool memcheck python tools/sanitize_smoke.py
+"""
+import os
+import sys
+import tempfile
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from oracle import oracle as O  # noqa: E402
+from paper_2406_11674_b200 import codec as E  # noqa: E402
+from paper_2406_11674_b200 import storage as S  # noqa: E402
+from paper_2406_11674_b200.pipeline import HostOp, OffloadPipeline, pinned_copy  # noqa: E402
+
+dev = torch.device("cuda", 0)
+
+
+def tensor(rows, cols, eb, seed, zf, offset=0):
+    w = O.random_dense(rows, cols, eb, seed, zf)
+    bm, vals, nnz, _ = O.compress(w, rows, cols, eb)
+    b = torch.zeros(len(bm) + 32, dtype=torch.uint8, device=dev)[: len(bm)]
+    b.copy_(torch.from_numpy(bm))
+    vb = torch.zeros(len(vals) + 64, dtype=torch.uint8, device=dev)[offset: offset + len(vals)]
+    if len(vals):
+        vb.copy_(torch.from_numpy(vals))
+    t = E.EndorTensor(rows, cols, E.Dtype.F16 if eb == 2 else E.Dtype.I8, E.Bitmap(rows * cols, data=b), vb,
+                      validate=False, nnz=nnz)
+    return w, t
+
+
+checks = 0
+for (rows, cols, eb, zf, off) in [(2, 2, 2, 0.5, 0), (37, 1000, 2, 0.5, 2), (64, 2048, 2, 0.3, 6),
+                                  (9, 4096, 1, 0.6, 1), (300, 1024, 2, 0.9, 10)]:
+    w, t = tensor(rows, cols, eb, rows + cols, zf, off)
+    assert E.decompress(t).bytes() == w.tobytes()                                  # count + TMA expand
+    for cs in (64, 1024, 4096):
+        idx = E.build_rank_index(t.bitmap, cs)                                     # scan_kernel
+        assert E.decompress_chunked(t, idx).bytes() == w.tobytes()                 # fallback / fast / coarse
+        buf = torch.zeros(t.dense_bytes(), dtype=torch.uint8, device=dev)
+        for k in range(idx.chunk_count()):
+            E.decompress_chunk_into(t, idx, k, buf)                                # partial-range expand
+        assert buf.cpu().numpy().tobytes() == w.tobytes()
+    sel = sorted({0, rows // 2, rows - 1})
+    assert E.extract_rows(t, sel).bytes() == w.reshape(rows, cols * eb)[sel].tobytes()
+    csel = sorted({0, cols // 3, cols - 1})
+    got = E.extract_cols(t, csel).bytes()
+    ref = w.view(np.uint16 if eb == 2 else np.uint8).reshape(rows, cols)[:, csel].tobytes()
+    assert got == ref
+    if eb == 2:
+        dw = E.decompress(t)
+        assert E.compress(dw).values.cpu().numpy().tobytes() == t.values.cpu().numpy().tobytes()
+        x = (torch.rand(cols, device=dev) * 2 - 1).half()
+        y = E.gemv(dw, x)                                                          # dense GEMV
+        ref = torch.from_numpy(w.view(np.float16).reshape(rows, cols).astype(np.float32)).to(dev) @ x.float()
+        assert (y - ref).abs().max().item() <= 1e-3 * ref.abs().max().item() + 1e-6
+        if cols % 1024 == 0:
+            yf = E.gemv_compressed(t, x)                                           # fused (count + flatten)
+            assert (yf - ref).abs().max().item() <= 1e-3 * ref.abs().max().item() + 1e-6
+            yi = E.gemv_compressed(t, x, index=E.build_rank_index(t.bitmap, 1024))
+            assert torch.equal(yf, yi)
+        q = E.quantize_values(t)                                                   # absmax + quantize
+        E.decompress_dequant(q)                                                    # fused dequant expand
+    checks += 1
+
+# batched paths
+ws = [tensor(40, 2048, 2, s, 0.5) for s in range(3)]
+outs = E.decompress_batch([t for _, t in ws])
+assert [o.bytes() for o in outs] == [w.tobytes() for w, _ in ws]
+xs = [(torch.rand(2048, device=dev) * 2 - 1).half() for _ in ws]
+E.gemv_compressed_batch([t for _, t in ws], xs)
+E.gemv_batch([E.decompress(t) for _, t in ws], xs)
+
+# fixtures
+sw = E.synth_weight(64, 1024, 5, device=dev)
+E.magnitude_prune(sw, 0.5, inplace=True)
+
+# storage (+ GPU CRC) and the pipeline, host- and file-sourced
+with tempfile.TemporaryDirectory() as d:
+    w, t = tensor(33, 2048, 2, 7, 0.5)
+    p = os.path.join(d, "t.endor")
+    S.write_endor_file(t, p)
+    got = S.read_endor_file(p, dev, verify=True)
+    assert E.decompress(got).bytes() == w.tobytes()
+    x = (torch.rand(2048, device=dev) * 2 - 1).half()
+    e0 = torch.empty(0, dtype=torch.uint8)
+    ops = [HostOp(33, 2048, 0, pinned_copy(t.bitmap.data), pinned_copy(t.values), t.nnz(), x=x,
+                  y=torch.empty(33, dtype=torch.float32, device=dev)),
+           HostOp(33, 2048, 0, e0, e0, t.nnz(), path=p, x=x, y=torch.empty(33, dtype=torch.float32, device=dev)),
+           HostOp(33, 2048, 0, pinned_copy(t.bitmap.data), pinned_copy(t.values), t.nnz(), x=x,
+                  y=torch.empty(33, dtype=torch.float32, device=dev), materialize=True)]
+    pipe = OffloadPipeline(0, 33 * 2048)
+    pipe.run(ops, sync=True)
+    pipe.close()
+    assert torch.equal(ops[0].y, ops[1].y)
+torch.cuda.synchronize()
+print(f"sanitize smoke ok ({checks} shapes)")
