@@ -1,7 +1,9 @@
 // Write-path variants for the expand kernel's 9:16 read:write mix (development aid):
 //   mode 0: 16-byte st.global (as the expand kernel)
 //   mode 1: stage 16 KiB per CTA in smem, then one cp.async.bulk S2G store
-//   mode 2: as 0 but with st.global.L1::no_allocate.v4 (default policy) -- plain
+//   mode 2: per-warp 2 KiB cp.async.bulk S2G stores
+//   mode 3: 32-byte st.global.v8 (sm_100 256-bit stores), .cs
+//   mode 4: 32-byte st.global.v8, default policy
 #include <cuda_runtime.h>
 #include <stdint.h>
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -47,6 +49,18 @@ __global__ void __launch_bounds__(256) mix2(const uint4* __restrict__ src, uint4
                              ::"l"(dst + blk * 1024 + w * 128), "r"(smem_u32(&buf[s][w * 128])), "r"(2048) : "memory");
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
+        } else if (MODE == 3 || MODE == 4) {  // 32-byte stores: thread t writes vectors 2t,2t+1 (+512)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                uint4* d = dst + blk * 1024 + 2 * threadIdx.x + 512 * j;
+                const uint4 a = v[2 * j], c = v[2 * j + 1];
+                if (MODE == 3)
+                    asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(d), "r"(a.x), "r"(a.y),
+                                 "r"(a.z), "r"(a.w), "r"(c.x), "r"(c.y), "r"(c.z), "r"(c.w) : "memory");
+                else
+                    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(d), "r"(a.x), "r"(a.y),
+                                 "r"(a.z), "r"(a.w), "r"(c.x), "r"(c.y), "r"(c.z), "r"(c.w) : "memory");
+            }
         } else {
 #pragma unroll
             for (int j = 0; j < 4; ++j) __stcs(dst + blk * 1024 + threadIdx.x + 256 * j, v[j]);
@@ -63,6 +77,8 @@ extern "C" float mix2_time(const void* src, void* dst, uint64_t nblk, int reps, 
         if (k == 2) cudaEventRecord(a);
         if (mode == 1) mix2<1><<<blocks, 256>>>((const uint4*)src, (uint4*)dst, nblk);
         else if (mode == 2) mix2<2><<<blocks, 256>>>((const uint4*)src, (uint4*)dst, nblk);
+        else if (mode == 3) mix2<3><<<blocks, 256>>>((const uint4*)src, (uint4*)dst, nblk);
+        else if (mode == 4) mix2<4><<<blocks, 256>>>((const uint4*)src, (uint4*)dst, nblk);
         else mix2<0><<<blocks, 256>>>((const uint4*)src, (uint4*)dst, nblk);
     }
     cudaEventRecord(b);
