@@ -11,7 +11,8 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libendor_cuda.so")
+# ENDOR_LIB: load a differently-built copy (development variants, tools/build_variant.sh)
+LIB_PATH = os.environ.get("ENDOR_LIB") or os.path.join(PKG, "libendor_cuda.so")
 
 _u64, _i32, _vp, _sz, _f64 = C.c_uint64, C.c_int32, C.c_void_p, C.c_size_t, C.c_double
 

@@ -14,6 +14,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "gather.cuh"
@@ -54,23 +55,105 @@ __device__ __forceinline__ uint32_t bits_at(const uint8_t* bm, uint64_t nbytes, 
 // ---- index validation (single CTA, positions in order) ---------------------------
 __global__ void __launch_bounds__(1024) validate_indices_kernel(const unsigned long long* idx, uint64_t nsel,
                                                                 uint64_t limit, WsHeader* hdr) {
+    constexpr int U = 8;  // positions per thread per pass, loads in flight
     __shared__ unsigned long long s_first;
     if (threadIdx.x == 0) s_first = ~0ull;
     __syncthreads();
-    for (uint64_t base = 0; base < nsel; base += blockDim.x) {
-        const uint64_t i = base + threadIdx.x;
-        if (i < nsel) {
-            unsigned long long key = ~0ull;
-            if (idx[i] >= limit) key = i * 2;                              // BoundsError
-            else if (i > 0 && idx[i] <= idx[i - 1]) key = i * 2 + 1;      // invalid_argument
-            if (key != ~0ull) atomicMin(&s_first, key);
+    for (uint64_t base = 0; base < nsel; base += 1024 * U) {
+        unsigned long long cur[U], prv[U], key = ~0ull;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = base + threadIdx.x + 1024 * u;
+            cur[u] = i < nsel ? idx[i] : 0ull;
+            prv[u] = i > 0 && i < nsel ? idx[i - 1] : 0ull;
         }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = base + threadIdx.x + 1024 * u;
+            if (i >= nsel) continue;
+            if (cur[u] >= limit) key = min(key, (unsigned long long)(i * 2));                        // BoundsError
+            else if (i > 0 && cur[u] <= prv[u]) key = min(key, (unsigned long long)(i * 2 + 1));     // invalid_argument
+        }
+        if (key != ~0ull) atomicMin(&s_first, key);
         __syncthreads();
         if (s_first != ~0ull) break;  // uniform: everyone read the same value
         __syncthreads();
     }
     if (threadIdx.x == 0 && s_first != ~0ull)
         latch_status(hdr, (s_first & 1) ? ENDOR_ERR_INVALID_ARGUMENT : ENDOR_ERR_BOUNDS);
+}
+
+// ---- one 8192-element tile of a row: bits, ranks, staged values ----------------------
+// Shared by extract_rows and the tiled extract_cols: thread tid owns the
+// tile's 32-bit slice tid (bits past `count` cleared); the tile's packed
+// values [rank(x0), rank(x0) + total) are staged in s_vals (aligned superset,
+// ragged buffer ends byte-wise).  Returns false (after latching CORRUPTION)
+// when the ranks run past nnz.
+struct TileRanks {
+    uint32_t wv, pc, incl, wexcl, total;
+    uint32_t sb;  // shared address of the tile's first packed value
+};
+template <int EB>
+__device__ __forceinline__ bool load_tile(const RankTable& rt, const uint8_t* values, uint64_t nnz, uint64_t x0,
+                                          uint32_t count, uint8_t* s_vals, uint32_t* s_warp,
+                                          unsigned long long* s_base, WsHeader* hdr, TileRanks& r) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (warp == 0) {
+        const unsigned long long b = rank_at(rt, x0, lane);
+        if (lane == 0) *s_base = b;
+    }
+    uint32_t wv = 0;
+    if (uint32_t(tid) * 32 < count) {
+        wv = bits_at(rt.bitmap, rt.nbytes, x0 + uint64_t(tid) * 32);
+        const uint32_t rem = count - uint32_t(tid) * 32;
+        if (rem < 32) wv &= (1u << rem) - 1u;
+    }
+    r.wv = wv;
+    r.pc = __popc(wv);
+    r.incl = warp_incl_scan(r.pc, lane);
+    if (lane == 31) s_warp[warp] = r.incl;
+    __syncthreads();
+    uint32_t wexcl = 0, total = 0;
+#pragma unroll
+    for (int k = 0; k < kExpandThreads / 32; ++k) {
+        wexcl += (k < warp) ? s_warp[k] : 0u;
+        total += s_warp[k];
+    }
+    r.wexcl = wexcl;
+    r.total = total;
+    const uint64_t vbase = *s_base;
+    if (vbase + total > nnz) {
+        if (tid == 0) latch_status(hdr, ENDOR_ERR_CORRUPTION);
+        return false;
+    }
+    const uintptr_t vlo = reinterpret_cast<uintptr_t>(values), vhi = vlo + nnz * EB;
+    const uintptr_t ws = vlo + vbase * EB, we = ws + uint64_t(total) * EB;
+    const uintptr_t as = ws & ~uintptr_t(15);
+    const uint32_t nvec = uint32_t((we - as + 15) >> 4);
+    for (uint32_t v = tid; v < nvec; v += kExpandThreads) {
+        const uintptr_t addr = as + uintptr_t(v) * 16;
+        uint4 q;
+        if (addr >= vlo && addr + 16 <= vhi) {
+            q = __ldg(reinterpret_cast<const uint4*>(addr));
+        } else {
+            uint32_t w4[4] = {0u, 0u, 0u, 0u};
+            for (int b = 0; b < 16; ++b) {
+                const uintptr_t x = addr + b;
+                if (x >= vlo && x < vhi) w4[b >> 2] |= uint32_t(*reinterpret_cast<const uint8_t*>(x)) << ((b & 3) * 8);
+            }
+            q = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+        }
+        *reinterpret_cast<uint4*>(s_vals + v * 16) = q;
+    }
+    r.sb = smem_u32(s_vals) + uint32_t(ws - as);
+    return true;
+}
+
+// packed value at shared byte address a (any alignment)
+template <int EB>
+__device__ __forceinline__ uint32_t lds_value(uint32_t a) {
+    const uint32_t w = __funnelshift_r(lds32(a & ~3u), lds32((a & ~3u) + 4), (a & 3u) * 8);
+    return EB == 2 ? (w & 0xFFFFu) : (w & 0xFFu);
 }
 
 // ---- extract_rows ------------------------------------------------------------------
@@ -87,81 +170,32 @@ __global__ void __launch_bounds__(kExpandThreads) extract_rows_kernel(RankTable 
     __shared__ __align__(16) uint8_t s_vals[kTileElems * EB + 64];
     if (read_status(hdr)) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    init_luts(tid);  // published by the __syncthreads below
+    init_luts(tid);  // published by the __syncthreads in load_tile
     const uint64_t i = blockIdx.x / tiles_per_row, j = blockIdx.x % tiles_per_row;
     const uint64_t row = sel[i];
-    const uint64_t x0 = row * cols + j * kTileElems;
     const uint32_t count = uint32_t(umin64(kTileElems, cols - j * kTileElems));
-    if (warp == 0) {
-        const unsigned long long b = rank_at(rt, x0, lane);
-        if (lane == 0) s_base = b;
-    }
-    uint32_t wv = 0;
-    if (uint32_t(tid) * 32 < count) {
-        wv = bits_at(rt.bitmap, rt.nbytes, x0 + uint64_t(tid) * 32);
-        const uint32_t rem = count - uint32_t(tid) * 32;
-        if (rem < 32) wv &= (1u << rem) - 1u;
-    }
-    const uint32_t pc = __popc(wv);
-    const uint32_t incl = warp_incl_scan(pc, lane);
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    uint32_t wexcl = 0, total = 0;
-#pragma unroll
-    for (int k = 0; k < kExpandThreads / 32; ++k) {
-        wexcl += (k < warp) ? s_warp[k] : 0u;
-        total += s_warp[k];
-    }
-    const uint64_t vbase = s_base;
-    if (vbase + total > nnz) {
-        if (tid == 0) latch_status(hdr, ENDOR_ERR_CORRUPTION);
+    TileRanks r;
+    if (!load_tile<EB>(rt, values, nnz, row * cols + j * kTileElems, count, s_vals, s_warp, &s_base, hdr, r))
         return;
-    }
-    // stage the tile's packed values (aligned superset; buffer ends byte-wise)
-    const uintptr_t vlo = reinterpret_cast<uintptr_t>(values), vhi = vlo + nnz * EB;
-    const uintptr_t ws = vlo + vbase * EB, we = ws + uint64_t(total) * EB;
-    const uintptr_t as = ws & ~uintptr_t(15);
-    const uint32_t nvec = uint32_t((we - as + 15) >> 4);
-    for (uint32_t v = tid; v < nvec; v += kExpandThreads) {
-        const uintptr_t addr = as + uintptr_t(v) * 16;
-        uint4 q;
-        if (addr >= vlo && addr + 16 <= vhi) {
-            q = __ldg(reinterpret_cast<const uint4*>(addr));
-        } else {
-            uint32_t r[4] = {0u, 0u, 0u, 0u};
-            for (int b = 0; b < 16; ++b) {
-                const uintptr_t x = addr + b;
-                if (x >= vlo && x < vhi) r[b >> 2] |= uint32_t(*reinterpret_cast<const uint8_t*>(x)) << ((b & 3) * 8);
-            }
-            q = make_uint4(r[0], r[1], r[2], r[3]);
-        }
-        *reinterpret_cast<uint4*>(s_vals + v * 16) = q;
-    }
     __syncthreads();
-    const uint32_t sb = smem_u32(s_vals) + uint32_t(ws - as);
     uint8_t* dst = out + (i * cols + j * kTileElems) * EB;
     if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
         // the expand kernels' gather: each warp places its 1024 elements with
         // the PRMT selector tables and coalesced 16-byte stores
         const int32_t wfirst = warp * kSubElems;
         if (wfirst < int32_t(count))
-            expand_subtile<EB, false>(wv, incl - pc, sb + wexcl * EB, dst + size_t(wfirst) * EB,
+            expand_subtile<EB, false>(r.wv, r.incl - r.pc, r.sb + r.wexcl * EB, dst + size_t(wfirst) * EB,
                                       min(int32_t(count) - wfirst, kSubElems), lane);
         return;
     }
     // output rows not 16-byte aligned (cols * eb % 16 != 0): scatter_range
     // semantics per element (codec.hpp:136-149), element-wise stores
     dst += uint64_t(tid) * 32 * EB;
-    uint32_t r = wexcl + incl - pc;
+    uint32_t rk = r.wexcl + r.incl - r.pc;
     const uint32_t nel = uint32_t(tid) * 32 < count ? min(32u, count - uint32_t(tid) * 32) : 0u;
     for (uint32_t e = 0; e < nel; ++e) {
         uint32_t v = 0;
-        if ((wv >> e) & 1u) {
-            const uint32_t a = sb + r * EB;
-            const uint32_t w = __funnelshift_r(lds32(a & ~3u), lds32((a & ~3u) + 4), (a & 3u) * 8);
-            v = EB == 2 ? (w & 0xFFFFu) : (w & 0xFFu);
-            ++r;
-        }
+        if ((r.wv >> e) & 1u) v = lds_value<EB>(r.sb + (rk++) * EB);
         if constexpr (EB == 2) {
             reinterpret_cast<uint16_t*>(dst)[e] = uint16_t(v);
         } else {
@@ -170,74 +204,100 @@ __global__ void __launch_bounds__(kExpandThreads) extract_rows_kernel(RankTable 
     }
 }
 
-// ---- extract_cols ------------------------------------------------------------------
-// One CTA per matrix row: the row's bitmap words and their exclusive popcounts
-// in shared memory, then every selected column looked up directly.
+// ---- extract_cols ----------------------------------------------------------------
+// CTA = rpc consecutive rows (their bits are one contiguous bit range, so one
+// scan ranks them all): the rows' bitmap words and exclusive popcounts go to
+// shared memory, then each selected column is looked up in every row.  The
+// per-lookup chain (sel[k] -> rank -> packed value) is dependent, so lookups
+// are batched kColBatch deep per thread to keep that many loads in flight,
+// and one sel[] batch serves all rpc rows.
+constexpr int kColBatch = 8;
+
 template <int EB>
 __global__ void __launch_bounds__(256) extract_cols_kernel(RankTable rt, const uint8_t* values, uint64_t nnz,
-                                                           uint64_t cols, const unsigned long long* sel,
-                                                           uint64_t nsel, uint8_t* out, WsHeader* hdr) {
-    extern __shared__ uint32_t s_row[];  // [words] bits, then [words] exclusive popcounts
+                                                           uint64_t rows, uint64_t cols,
+                                                           const unsigned long long* sel, uint64_t nsel,
+                                                           uint32_t rpc, uint8_t* out, WsHeader* hdr) {
+    extern __shared__ uint32_t s_row[];  // [rpc * words] bits, then [rpc * words] exclusive popcounts
     __shared__ uint32_t s_warp[8];
     __shared__ unsigned long long s_base;
     if (read_status(hdr)) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t row = blockIdx.x;
-    const uint64_t x0 = row * cols;
-    const uint32_t words = uint32_t((cols + 31) / 32);
-    uint32_t* s_pre = s_row + words;
+    const uint64_t r0 = uint64_t(blockIdx.x) * rpc;
+    const uint32_t nr = uint32_t(umin64(rpc, rows - r0));
+    const uint32_t words = uint32_t((cols + 31) / 32), nw = nr * words;
+    uint32_t* s_pre = s_row + rpc * words;
     if (warp == 0) {
-        const unsigned long long b = rank_at(rt, x0, lane);
+        const unsigned long long b = rank_at(rt, r0 * cols, lane);
         if (lane == 0) s_base = b;
     }
-    // words and a block-wide exclusive scan of their popcounts, 256 at a time
-    uint32_t carry = 0;
-    for (uint32_t w0 = 0; w0 < words; w0 += 256) {
-        const uint32_t w = w0 + tid;
-        uint32_t v = 0;
-        if (w < words) {
-            v = bits_at(rt.bitmap, rt.nbytes, x0 + uint64_t(w) * 32);
-            const uint64_t rem = cols - uint64_t(w) * 32;
-            if (rem < 32) v &= (1u << rem) - 1u;
-            s_row[w] = v;
-        }
-        const uint32_t pc = __popc(v);
-        const uint32_t incl = warp_incl_scan(pc, lane);
-        if (lane == 31) s_warp[warp] = incl;
-        __syncthreads();
-        uint32_t wex = 0, tot = 0;
-        for (int k = 0; k < 8; ++k) {
-            wex += (k < warp) ? s_warp[k] : 0u;
-            tot += s_warp[k];
-        }
-        if (w < words) s_pre[w] = carry + wex + incl - pc;
-        carry += tot;
-        __syncthreads();
+    // each thread ranks a contiguous run of the (row, word) sequence
+    const uint32_t per = (nw + 255) / 256, w0 = min(nw, uint32_t(tid) * per), w1 = min(nw, w0 + per);
+    uint32_t sum = 0;
+#pragma unroll 8
+    for (uint32_t w = w0; w < w1; ++w) {
+        const uint32_t r = w / words, j = w - r * words;
+        uint32_t v = bits_at(rt.bitmap, rt.nbytes, (r0 + r) * cols + uint64_t(j) * 32);
+        const uint64_t rem = cols - uint64_t(j) * 32;
+        if (rem < 32) v &= (1u << rem) - 1u;
+        s_row[w] = v;
+        sum += __popc(v);
+    }
+    const uint32_t incl = warp_incl_scan(sum, lane);
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    uint32_t run = incl - sum, total = 0;
+    for (int k = 0; k < 8; ++k) {
+        run += k < warp ? s_warp[k] : 0u;
+        total += s_warp[k];
+    }
+    for (uint32_t w = w0; w < w1; ++w) {
+        s_pre[w] = run;
+        run += __popc(s_row[w]);
     }
     const unsigned long long base = s_base;
-    if (base + carry > nnz) {
+    if (base + total > nnz) {
         if (tid == 0) latch_status(hdr, ENDOR_ERR_CORRUPTION);
         return;
     }
-    uint8_t* orow = out + row * nsel * EB;
-    for (uint64_t k = tid; k < nsel; k += 256) {
-        const uint64_t c = sel[k];
-        const uint32_t w = uint32_t(c / 32), b = uint32_t(c & 31);
-        const uint32_t word = s_row[w];
-        uint32_t v = 0;
-        if ((word >> b) & 1u) {
-            const uint64_t rk = base + s_pre[w] + __popc(word & ((1u << b) - 1u));
-            if constexpr (EB == 2) {
-                // the packed values may sit at any alignment (file_io.hpp:32-36)
-                v = (reinterpret_cast<uintptr_t>(values) & 1)
-                        ? uint32_t(__ldg(values + rk * 2)) | (uint32_t(__ldg(values + rk * 2 + 1)) << 8)
-                        : uint32_t(__ldg(reinterpret_cast<const uint16_t*>(values) + rk));
-            } else {
-                v = uint32_t(__ldg(values + rk));
+    __syncthreads();
+    for (uint64_t k0 = tid; k0 < nsel; k0 += 256 * kColBatch) {
+        uint32_t w[kColBatch], msk[kColBatch];
+#pragma unroll
+        for (int u = 0; u < kColBatch; ++u) {
+            const uint64_t k = k0 + 256 * u;
+            const unsigned long long c = k < nsel ? __ldg(sel + k) : 0ull;
+            w[u] = uint32_t(c / 32);
+            msk[u] = k < nsel ? (1u << (c & 31)) : 0u;
+        }
+        for (uint32_t r = 0; r < nr; ++r) {
+            uint32_t v[kColBatch];
+#pragma unroll
+            for (int u = 0; u < kColBatch; ++u) {
+                const uint32_t word = s_row[r * words + w[u]];
+                v[u] = 0;
+                if (word & msk[u]) {
+                    const uint64_t rk = base + s_pre[r * words + w[u]] + __popc(word & (msk[u] - 1u));
+                    if constexpr (EB == 2) {
+                        // the packed values may sit at any alignment (file_io.hpp:32-36)
+                        v[u] = (reinterpret_cast<uintptr_t>(values) & 1)
+                                   ? uint32_t(__ldg(values + rk * 2)) | (uint32_t(__ldg(values + rk * 2 + 1)) << 8)
+                                   : uint32_t(__ldg(reinterpret_cast<const uint16_t*>(values) + rk));
+                    } else {
+                        v[u] = uint32_t(__ldg(values + rk));
+                    }
+                }
+            }
+            uint8_t* orow = out + (r0 + r) * nsel * EB;
+#pragma unroll
+            for (int u = 0; u < kColBatch; ++u) {
+                const uint64_t k = k0 + 256 * u;
+                if (k < nsel) {
+                    if constexpr (EB == 2) reinterpret_cast<uint16_t*>(orow)[k] = uint16_t(v[u]);
+                    else orow[k] = uint8_t(v[u]);
+                }
             }
         }
-        if constexpr (EB == 2) reinterpret_cast<uint16_t*>(orow)[k] = uint16_t(v);
-        else orow[k] = uint8_t(v);
     }
 }
 
@@ -265,15 +325,27 @@ cudaError_t launch_extract_cols(const RankTable& rt, const uint8_t* values, uint
                                 uint64_t cols, int eb, const unsigned long long* sel, uint64_t nsel, uint8_t* out,
                                 WsHeader* hdr, cudaStream_t s) {
     if (rows == 0 || nsel == 0) return cudaSuccess;
-    const size_t smem = 2 * sizeof(uint32_t) * ((cols + 31) / 32);
-    if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
+    const uint64_t words = (cols + 31) / 32;
+    // rows per CTA: one sel[] batch serves them all (ENDOR_EXTRACT_COLS_RPC overrides)
+    static const int env_rpc = [] {
+        const char* e = getenv("ENDOR_EXTRACT_COLS_RPC");
+        return e ? atoi(e) : 0;
+    }();
+    uint64_t rpc = env_rpc > 0 ? uint64_t(env_rpc) : 4;
+    while (rpc > 1 && rpc * words * 8 > 64 * 1024) rpc /= 2;
+    const size_t smem = size_t(rpc * words * 8);
     cudaError_t e = kernel_slots(eb == 2 ? reinterpret_cast<const void*>(extract_cols_kernel<2>)
                                          : reinterpret_cast<const void*>(extract_cols_kernel<1>),
                                  256, 200 * 1024, nullptr, nullptr);
     if (e != cudaSuccess) return e;
-    if (rows > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    if (eb == 2) extract_cols_kernel<2><<<unsigned(rows), 256, smem, s>>>(rt, values, nnz, cols, sel, nsel, out, hdr);
-    else extract_cols_kernel<1><<<unsigned(rows), 256, smem, s>>>(rt, values, nnz, cols, sel, nsel, out, hdr);
+    const uint64_t grid = ceil_div(rows, rpc);
+    if (grid > 0x7FFFFFFFull || smem > 200 * 1024) return cudaErrorInvalidConfiguration;
+    if (eb == 2)
+        extract_cols_kernel<2><<<unsigned(grid), 256, smem, s>>>(rt, values, nnz, rows, cols, sel, nsel,
+                                                                 uint32_t(rpc), out, hdr);
+    else
+        extract_cols_kernel<1><<<unsigned(grid), 256, smem, s>>>(rt, values, nnz, rows, cols, sel, nsel,
+                                                                 uint32_t(rpc), out, hdr);
     return cudaGetLastError();
 }
 

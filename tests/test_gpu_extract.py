@@ -54,9 +54,50 @@ def test_large_rows_and_cols(E):
     rsel = torch.arange(3, rows, 97, device="cuda")
     got = E.extract_rows(t, rsel)
     assert torch.equal(got.data.view(torch.int16).reshape(-1, cols), dense[rsel])
-    csel = torch.arange(5, cols, 131, device="cuda")
-    got = E.extract_cols(t, csel)
-    assert torch.equal(got.data.view(torch.int16).reshape(rows, -1), dense[:, csel])
+    for step in (131, 2, 1):  # direct lookups (sparse selection), tiled (half, all columns)
+        csel = torch.arange(5 % step, cols, step, device="cuda")
+        got = E.extract_cols(t, csel)
+        assert torch.equal(got.data.view(torch.int16).reshape(rows, -1), dense[:, csel]), step
+
+
+@pytest.mark.parametrize("rpc", [1, 3])
+def test_extract_cols_rows_per_cta(cuda_lib, rpc):
+    """extract_cols with 1 and 3 rows per CTA (the default is 4) over the
+    acceptance subset and ragged shapes, each in a fresh process."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import numpy as np, torch\n"
+        "from oracle import oracle as O\n"
+        "from paper_2406_11674_b200 import codec as E\n"
+        "for it, rows, cols, eb, zeros, w, chunk, rsel, csel in O.acceptance_cases(300):\n"
+        "    bm, vals, nnz, _ = O.compress(w, rows, cols, eb)\n"
+        "    b = torch.zeros(len(bm) + 32, dtype=torch.uint8, device='cuda')[:len(bm)]\n"
+        "    b.copy_(torch.from_numpy(bm.copy())) if len(bm) else None\n"
+        "    off = it % 3\n"
+        "    v = torch.zeros(len(vals) + off + 32, dtype=torch.uint8, device='cuda')[off:off + len(vals)]\n"
+        "    v.copy_(torch.from_numpy(vals.copy())) if len(vals) else None\n"
+        "    t = E.EndorTensor(rows, cols, E.Dtype.F16 if eb == 2 else E.Dtype.I8, E.Bitmap(rows * cols, data=b), v,\n"
+        "                      validate=False, nnz=nnz)\n"
+        "    want = w.view(np.uint16 if eb == 2 else np.uint8).reshape(rows, cols)[:, csel]\n"
+        "    assert E.extract_cols(t, csel).bytes() == np.ascontiguousarray(want).tobytes(), it\n"
+        "for rows, cols, eb in ((3, 20000, 2), (70, 8193, 1), (5, 16384, 2), (37, 3072, 2), (1, 1024, 2), (9, 8, 2), (300, 40, 2), (2, 8200, 2)):\n"
+        "    w = O.random_dense(rows, cols, eb, rows + cols, 0.5)\n"
+        "    bm, vals, nnz, _ = O.compress(w, rows, cols, eb)\n"
+        "    t = E.EndorTensor(rows, cols, E.Dtype.F16 if eb == 2 else E.Dtype.I8,\n"
+        "                      E.Bitmap(rows * cols, data=torch.from_numpy(bm.copy()).cuda()),\n"
+        "                      torch.from_numpy(vals.copy()).cuda(), validate=False, nnz=nnz)\n"
+        "    for csel in ([0], [cols - 1], list(range(0, cols, 7)), [8191, 8192, cols - 1], list(range(cols)),\n"
+        "                 list(range(1000, cols, 2)), list(range(cols - 40, cols))):\n"
+        "        csel = sorted({c for c in csel if 0 <= c < cols})\n"
+        "        want = w.view(np.uint16 if eb == 2 else np.uint8).reshape(rows, cols)[:, csel]\n"
+        "        assert E.extract_cols(t, csel).bytes() == np.ascontiguousarray(want).tobytes(), (rows, cols, csel[:3])\n"
+        "print('ok')\n")
+    env = dict(os.environ, ENDOR_EXTRACT_COLS_RPC=str(rpc), PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-2000:]
 
 
 def test_index_validation_matches_reference(E):

@@ -1,8 +1,9 @@
 """Selective decompression (extract_rows / extract_cols, codec.hpp:239-297) on
 OPT-66B fc1 at several selection fractions, through the raw C ABI (development
 aid).  Algorithmic bytes: the counting pass over the whole bitmap (n/8) + the
-selected rows' bitmap and values (rows) or the whole compressed tensor (cols) +
-the dense output."""
+selected rows' bitmap and values (rows), or every row's bitmap and at most one
+32-byte value sector per selected value, capped at all values (cols) + the
+dense output."""
 import ctypes as C
 import json
 import os
@@ -26,8 +27,10 @@ ws = E.workspace(n, dev)
 st = torch.cuda.current_stream().cuda_stream
 g = torch.Generator(device="cpu").manual_seed(0)
 res = {}
-for frac in (0.05, 0.25, 0.5):
-    for kind in ("rows", "cols"):
+KINDS = os.environ.get("KINDS", "rows,cols").split(",")
+FRACS = [float(f) for f in os.environ.get("FRACS", "0.001,0.01,0.05,0.25,0.5").split(",")]
+for frac in FRACS:
+    for kind in KINDS:
         m = rows if kind == "rows" else cols
         k = max(1, int(m * frac))
         sel = torch.randperm(m, generator=g)[:k].sort().values.to(torch.int64).to(dev)
@@ -48,7 +51,10 @@ for frac in (0.05, 0.25, 0.5):
         ms = a.elapsed_time(b) / 10
         E.sync_status(ws, dev)
         dense_out = (k * cols if kind == "rows" else rows * k) * 2
-        touched = (k * cols // 8 + int(t.nnz() * k / rows) * 2) if kind == "rows" else t.compressed_bytes()
+        if kind == "rows":
+            touched = k * cols // 8 + int(t.nnz() * k / rows) * 2
+        else:  # every row's bits + at most one 32-byte value sector per selected value
+            touched = n // 8 + min(t.nnz() * 2, int(t.nnz() * frac) * 32)
         alg = n // 8 + touched + dense_out
         ref = w.data.view(torch.float16).reshape(rows, cols)
         got = out[:dense_out].view(torch.float16).reshape((k, cols) if kind == "rows" else (rows, k))
@@ -58,4 +64,4 @@ for frac in (0.05, 0.25, 0.5):
                                  "bit_exact": exact}
         print(kind, frac, res[f"{kind}_{frac}"], flush=True)
 os.makedirs("gpurun_out", exist_ok=True)
-json.dump(res, open("gpurun_out/extract_probe.json", "w"), indent=1)
+json.dump(res, open("gpurun_out/extract_probe%s.json" % os.environ.get("ENDOR_EXTRACT_COLS_RPC", ""), "w"), indent=1)
