@@ -60,6 +60,21 @@ def test_large_rows_and_cols(E):
         assert torch.equal(got.data.view(torch.int16).reshape(rows, -1), dense[:, csel]), step
 
 
+def test_extract_rows_expand_ring_shapes(E):
+    """extract_rows with cols % 1024 == 0 (the TMA expand ring over (row, tile)
+    items): odd 1024-chunk row starts (unaligned index entries), partial last
+    tiles, both dtypes, any value-buffer alignment, first / last / all rows."""
+    for rows, cols, eb, zf, voff in ((7, 3072, 2, 0.5, 1), (5, 9216, 2, 0.3, 0), (33, 1024, 1, 0.6, 3),
+                                     (4, 16384, 2, 0.9, 2), (3, 8192, 1, 0.0, 0), (2, 2048, 2, 1.0, 0)):
+        w = O.random_dense(rows, cols, eb, rows * 7 + cols, zf)
+        bm, vals, nnz, _ = O.compress(w, rows, cols, eb)
+        t = _tensor(E, rows, cols, eb, bm, vals, nnz, voff=voff)
+        full = w.reshape(rows, cols * eb)
+        for rsel in ([0], [rows - 1], list(range(rows)), list(range(1, rows, 2)), [0, rows - 1]):
+            rsel = sorted(set(rsel))
+            assert E.extract_rows(t, rsel).bytes() == full[rsel].tobytes(), (rows, cols, eb, rsel)
+
+
 @pytest.mark.parametrize("rpc", [1, 3])
 def test_extract_cols_rows_per_cta(cuda_lib, rpc):
     """extract_cols with 1 and 3 rows per CTA (the default is 4) over the
