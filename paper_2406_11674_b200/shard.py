@@ -96,6 +96,43 @@ def shard_tensor(t, shard: RowShard):
     return E.EndorTensor(shard.rows, shard.cols, t.dtype, bm, vals, validate=False, nnz=v1 - v0)
 
 
+def _gf2_times(mat: List[int], vec: int) -> int:
+    s, i = 0, 0
+    while vec:
+        if vec & 1:
+            s ^= mat[i]
+        vec >>= 1
+        i += 1
+    return s
+
+
+def crc32_combine(crc1: int, crc2: int, len2: int) -> int:
+    """CRC-32 (zlib) of A || B from crc(A), crc(B) and len(B): lets every rank
+    checksum its own row shard and rank 0 assemble the whole matrix's CRC
+    (compared with the reference's, tests/golden/large.json) without moving
+    the shards.  zlib's crc32_combine: apply len2 zero bytes to crc1 by
+    repeated squaring of the GF(2) shift operator."""
+    if len2 <= 0:
+        return crc1
+    odd = [0xEDB88320] + [1 << n for n in range(31)]  # operator for one zero bit
+    even = [_gf2_times(odd, odd[n]) for n in range(32)]  # two bits
+    odd = [_gf2_times(even, even[n]) for n in range(32)]  # four bits
+    while True:
+        even = [_gf2_times(odd, odd[n]) for n in range(32)]
+        if len2 & 1:
+            crc1 = _gf2_times(even, crc1)
+        len2 >>= 1
+        if not len2:
+            break
+        odd = [_gf2_times(even, even[n]) for n in range(32)]
+        if len2 & 1:
+            crc1 = _gf2_times(odd, crc1)
+        len2 >>= 1
+        if not len2:
+            break
+    return (crc1 ^ crc2) & 0xFFFFFFFF
+
+
 def all_gather_dense(shard_dense, full_rows: int, group=None):
     """Optional NCCL all-gather of dense row shards into the full matrix on
     every rank (only when one device needs the whole dense W).  Shards must be

@@ -71,3 +71,19 @@ def test_host_rank_matches_oracle():
     bm, _, _, _ = O.compress(w, 50, 40, 2)
     for end in (0, 1, 7, 8, 9, 63, 64, 65, 1000, 2000):
         assert S.host_rank(bm, end) == O.lib().or_rank_range(bm, 0, end)
+
+
+def test_crc32_combine_matches_zlib():
+    import zlib
+    rng = np.random.default_rng(5)
+    for la, lb in ((0, 0), (1, 0), (0, 7), (13, 1), (1000, 4097), (65536, 3)):
+        a = rng.integers(0, 256, la, dtype=np.uint8).tobytes()
+        b = rng.integers(0, 256, lb, dtype=np.uint8).tobytes()
+        assert S.crc32_combine(zlib.crc32(a), zlib.crc32(b), lb) == zlib.crc32(a + b)
+    # a matrix split into row shards, combined in order
+    m = rng.integers(0, 256, (37, 64), dtype=np.uint8)
+    c = 0
+    for sh in S.row_shards(37, 32, 5):
+        part = m[sh.r0:sh.r1].tobytes()
+        c = S.crc32_combine(c, zlib.crc32(part), len(part))
+    assert c == zlib.crc32(m.tobytes())
