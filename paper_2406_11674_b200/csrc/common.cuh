@@ -169,10 +169,21 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 }
 // 1-D TMA bulk copy global -> shared, completion counted on an mbarrier.
 // dst/src 16-byte aligned, bytes a multiple of 16.
+#ifndef ENDOR_BULK_EVICT_FIRST
+#define ENDOR_BULK_EVICT_FIRST 0
+#endif
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+#if ENDOR_BULK_EVICT_FIRST
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory");
+#else
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
         ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+#endif
 }
 
 // ---- device helpers ------------------------------------------------------------

@@ -8,6 +8,10 @@
 
 #include "common.cuh"
 
+#ifndef ENDOR_STORE_CS
+#define ENDOR_STORE_CS 0
+#endif
+
 namespace endor_b200 {
 
 // ---- selector tables ---------------------------------------------------------
@@ -169,7 +173,11 @@ __device__ __forceinline__ void expand_subtile(uint32_t word, uint32_t excl, uin
         const int e = (32 * j + lane) * EPC;
         if (!FULL && e >= valid_elems) continue;
         const uint4 q = gather_mode<MODE>(m, vbase + r * IN, scale, fast);
+#if ENDOR_STORE_CS
+        if (FULL || e + EPC <= valid_elems) __stcs(reinterpret_cast<uint4*>(o + j * 512), q);
+#else
         if (FULL || e + EPC <= valid_elems) *reinterpret_cast<uint4*>(o + j * 512) = q;
+#endif
         else store_partial(o + j * 512, q, uint32_t(valid_elems - e) * OUT);
     }
 }

@@ -4,6 +4,9 @@
 //   mode 2: per-warp 2 KiB cp.async.bulk S2G stores
 //   mode 3: 32-byte st.global.v8 (sm_100 256-bit stores), .cs
 //   mode 4: 32-byte st.global.v8, default policy
+//   mode 5: 16-byte st.global (default policy)
+//   mode 6: 16-byte st.global.L1::no_allocate
+//   mode 7: 16-byte st.global.L2::cache_hint (evict_first policy)
 #include <cuda_runtime.h>
 #include <stdint.h>
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -61,6 +64,21 @@ __global__ void __launch_bounds__(256) mix2(const uint4* __restrict__ src, uint4
                     asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(d), "r"(a.x), "r"(a.y),
                                  "r"(a.z), "r"(a.w), "r"(c.x), "r"(c.y), "r"(c.z), "r"(c.w) : "memory");
             }
+        } else if (MODE == 5) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dst[blk * 1024 + threadIdx.x + 256 * j] = v[j];
+        } else if (MODE == 6) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst + blk * 1024 + threadIdx.x + 256 * j),
+                             "r"(v[j].x), "r"(v[j].y), "r"(v[j].z), "r"(v[j].w) : "memory");
+        } else if (MODE == 7) {
+            uint64_t pol;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(dst + blk * 1024 + threadIdx.x + 256 * j),
+                             "r"(v[j].x), "r"(v[j].y), "r"(v[j].z), "r"(v[j].w), "l"(pol) : "memory");
         } else {
 #pragma unroll
             for (int j = 0; j < 4; ++j) __stcs(dst + blk * 1024 + threadIdx.x + 256 * j, v[j]);
@@ -79,6 +97,9 @@ extern "C" float mix2_time(const void* src, void* dst, uint64_t nblk, int reps, 
         else if (mode == 2) mix2<2><<<blocks, 256>>>((const uint4*)src, (uint4*)dst, nblk);
         else if (mode == 3) mix2<3><<<blocks, 256>>>((const uint4*)src, (uint4*)dst, nblk);
         else if (mode == 4) mix2<4><<<blocks, 256>>>((const uint4*)src, (uint4*)dst, nblk);
+        else if (mode == 5) mix2<5><<<blocks, 256>>>((const uint4*)src, (uint4*)dst, nblk);
+        else if (mode == 6) mix2<6><<<blocks, 256>>>((const uint4*)src, (uint4*)dst, nblk);
+        else if (mode == 7) mix2<7><<<blocks, 256>>>((const uint4*)src, (uint4*)dst, nblk);
         else mix2<0><<<blocks, 256>>>((const uint4*)src, (uint4*)dst, nblk);
     }
     cudaEventRecord(b);

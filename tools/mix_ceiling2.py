@@ -12,7 +12,8 @@ nblk = 2038431744 // 16384
 src = torch.empty(nblk * 576 * 16 + 4096, dtype=torch.uint8, device="cuda")
 dst = torch.empty(nblk * 16384, dtype=torch.uint8, device="cuda")
 byts = nblk * (16384 + 576 * 16)
-for mode in (0, 1, 2, 3, 4):
+MODES = [int(m) for m in os.environ.get("MODES", "0,1,2,3,4,5,6,7").split(",")]
+for mode in MODES:
     for blocks in (148 * 4, 148 * 8, 148 * 16):
         ms = L.mix2_time(src.data_ptr(), dst.data_ptr(), nblk, 10, mode, blocks)
         print(f"mode {mode} blocks {blocks}: {ms:.4f} ms {byts / ms / 1e6:.1f} GB/s", flush=True)
