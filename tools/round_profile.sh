@@ -25,4 +25,5 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemv
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemv_batch_kernel -c 1 \
     -o "$O/full_gemv" -f python tools/fused_bench.py > "$O/full_gemv.log" 2>&1
 timeout 300 python tools/fused_bench.py > "$O/fused_bench.log" 2>&1
+timeout 300 python tools/extract_probe.py > "$O/extract.log" 2>&1 && cp gpurun_out/extract_probe.json "$O/extract.json"
 echo done2
