@@ -225,6 +225,18 @@ int endor_cuda_decompress_chunk_into_host(uint64_t rows, uint64_t cols, int32_t 
 int endor_cuda_compress_host(uint64_t rows, uint64_t cols, int32_t dtype, const void* dense_host,
                              void* bitmap_host_out, void* values_host_out, uint64_t* nnz_out,
                              int32_t* negzero_out);
+/* extract_rows / extract_cols (codec.hpp:239-297) on host buffers (sync):
+ * out_host receives nsel*cols (rows) or rows*nsel (cols) elements. */
+int endor_cuda_extract_rows_host(uint64_t rows, uint64_t cols, int32_t dtype, const void* bitmap_host,
+                                 const void* values_host, uint64_t nnz, const uint64_t* rows_host, uint64_t nsel,
+                                 void* out_host);
+int endor_cuda_extract_cols_host(uint64_t rows, uint64_t cols, int32_t dtype, const void* bitmap_host,
+                                 const void* values_host, uint64_t nnz, const uint64_t* cols_host, uint64_t nsel,
+                                 void* out_host);
+/* quantize_values / dequantize_values (codec.hpp:306-349) of packed values on
+ * host buffers (sync). */
+int endor_cuda_quantize_values_host(const void* values_f16_host, uint64_t nnz, void* q_host_out, float* scale_out);
+int endor_cuda_dequantize_values_host(const void* q_host, uint64_t nnz, float scale, void* f16_host_out);
 
 /* ---- input producers (offline in the paper) ---------------- */
 
@@ -250,6 +262,12 @@ int endor_cuda_magnitude_prune(uint64_t n, int32_t dtype, double sparsity, void*
  * (absmax/127, 1.0 for all-zero) is returned through scale_out_host.  Sync. */
 int endor_cuda_quantize_values(const void* values_f16, uint64_t nnz, void* q_out, float* scale_out_host,
                                void* ws, size_t ws_bytes, void* stream);
+
+/* dequantize_values (codec.hpp:334-349) on device, bit-exact: out_f16[i] =
+ * f32_to_f16(float(q[i]) * scale) over the packed values (the bitmap is
+ * unchanged; float16.hpp:35-73 RNE, NaN products as on the reference's x86).
+ * Async on the stream. */
+int endor_cuda_dequantize_values(const void* q_i8, uint64_t nnz, float scale, void* out_f16, void* stream);
 
 /* ---- consumer ------------------------------------------------------------ */
 

@@ -7,6 +7,10 @@
 //     endor::decompress_chunk_into(...)    (codec.hpp:191)
 //     endor::build_rank_index(b, cs)       (bitmap.hpp:117)
 //     endor::compress(w)                   (codec.hpp:97)
+//     endor::extract_rows(t, rows)         (codec.hpp:239)
+//     endor::extract_cols(t, cols)         (codec.hpp:271)
+//     endor::quantize_values(t)            (codec.hpp:306)
+//     endor::dequantize_values(t)          (codec.hpp:334)
 // with the same calls in namespace endor::cuda.  Arguments, return types,
 // ownership (value semantics, caller-owned span for chunk_into) and the
 // exception types thrown (error.hpp) are the reference's.  Requires the
@@ -103,6 +107,48 @@ inline EndorTensor compress(const DenseMatrix& w) {
     vals.resize(nnz * elem_bytes(w.dtype()));
     return EndorTensor(w.rows(), w.cols(), w.dtype(), Bitmap::from_bytes(bm, n), std::move(vals),
                        std::nullopt, negzero != 0);
+}
+
+// extract_rows / extract_cols (codec.hpp:239-297): index checks in the
+// reference's order and exception types (check_sorted_unique, :224-232).
+inline DenseMatrix extract_rows(const EndorTensor& t, std::span<const std::size_t> rows) {
+    DenseMatrix out(rows.size(), t.cols(), t.dtype());
+    const auto bm = t.bitmap().to_bytes();
+    const std::vector<std::uint64_t> sel(rows.begin(), rows.end());
+    check(endor_cuda_extract_rows_host(t.rows(), t.cols(), dtype_code(t.dtype()), bm.data(), t.values().data(),
+                                       t.nnz(), sel.data(), sel.size(), out.bytes().data()));
+    return out;
+}
+
+inline DenseMatrix extract_cols(const EndorTensor& t, std::span<const std::size_t> cols) {
+    DenseMatrix out(t.rows(), cols.size(), t.dtype());
+    const auto bm = t.bitmap().to_bytes();
+    const std::vector<std::uint64_t> sel(cols.begin(), cols.end());
+    check(endor_cuda_extract_cols_host(t.rows(), t.cols(), dtype_code(t.dtype()), bm.data(), t.values().data(),
+                                       t.nnz(), sel.data(), sel.size(), out.bytes().data()));
+    return out;
+}
+
+// quantize_values (codec.hpp:306-331): symmetric absmax f16 -> i8 of the
+// packed values; the bitmap is shared.
+inline EndorTensor quantize_values(const EndorTensor& t) {
+    if (t.dtype() != Dtype::F16) throw std::invalid_argument("quantize_values requires an f16 tensor");
+    std::vector<std::byte> q(t.nnz());
+    float scale = 1.0f;
+    check(endor_cuda_quantize_values_host(t.values().data(), t.nnz(), q.data(), &scale));
+    return EndorTensor(t.rows(), t.cols(), Dtype::I8, t.bitmap(), std::move(q), scale,
+                       t.negative_zero_collapsed());
+}
+
+// dequantize_values (codec.hpp:334-349).  decompress(dequantize_values(t)) is
+// also available fused on device (endor_cuda_decompress_dequant).
+inline EndorTensor dequantize_values(const EndorTensor& t) {
+    if (t.dtype() != Dtype::I8 || !t.quant_scale())
+        throw std::invalid_argument("dequantize_values requires a quantized i8 tensor");
+    std::vector<std::byte> out(t.nnz() * 2);
+    check(endor_cuda_dequantize_values_host(t.values().data(), t.nnz(), *t.quant_scale(), out.data()));
+    return EndorTensor(t.rows(), t.cols(), Dtype::F16, t.bitmap(), std::move(out), std::nullopt,
+                       t.negative_zero_collapsed());
 }
 
 }  // namespace endor::cuda

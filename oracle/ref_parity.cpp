@@ -188,6 +188,46 @@ int main() {
         REQUIRE(t.values_bytes() == 339738624ull && t.bitmap_bytes() == 42467328ull);
         REQUIRE(cuda::decompress(t) == p);
     });
+    run("extract_rows / extract_cols == slices of decompress (acceptance.cpp:126-153)", [] {
+        std::mt19937_64 rng(99);
+        for (int iter = 0; iter < 40; ++iter) {
+            const std::size_t rows = 1 + rng() % 40, cols = 1 + rng() % 3000;
+            const Dtype dt = rng() % 2 ? Dtype::F16 : Dtype::I8;
+            const DenseMatrix w = random_dense(rows, cols, dt, rng(), static_cast<double>(rng() % 101) / 100.0);
+            const EndorTensor t = compress(w);
+            std::vector<std::size_t> rs, cs;
+            for (std::size_t r = 0; r < rows; ++r) if (rng() % 3 == 0) rs.push_back(r);
+            for (std::size_t c = 0; c < cols; ++c) if (rng() % 5 == 0) cs.push_back(c);
+            REQUIRE(cuda::extract_rows(t, rs) == extract_rows(t, rs));
+            REQUIRE(cuda::extract_cols(t, cs) == extract_cols(t, cs));
+        }
+        const EndorTensor t = compress(random_dense(6, 9, Dtype::F16, 3, 0.5));
+        const std::vector<std::size_t> oob{1, 6}, dup{2, 2}, oobc{0, 9}, uns{5, 1};
+        REQUIRE(throws_as<BoundsError>([&] { cuda::extract_rows(t, oob); }));
+        REQUIRE(throws_as<std::invalid_argument>([&] { cuda::extract_rows(t, dup); }));
+        REQUIRE(throws_as<BoundsError>([&] { cuda::extract_cols(t, oobc); }));
+        REQUIRE(throws_as<std::invalid_argument>([&] { cuda::extract_cols(t, uns); }));
+    });
+    run("quantize_values / dequantize_values bit-exact (test_codec.cpp:324-387)", [] {
+        std::mt19937_64 rng(5);
+        for (int iter = 0; iter < 30; ++iter) {
+            const DenseMatrix w = random_dense(1 + rng() % 50, 1 + rng() % 200, Dtype::F16, rng(),
+                                               static_cast<double>(rng() % 101) / 100.0);
+            const EndorTensor t = compress(w);
+            const EndorTensor qr = quantize_values(t), qc = cuda::quantize_values(t);
+            REQUIRE(qc.quant_scale() && *qc.quant_scale() == *qr.quant_scale());
+            REQUIRE(std::equal(qc.values().begin(), qc.values().end(), qr.values().begin(), qr.values().end()));
+            const EndorTensor dr = dequantize_values(qr), dc = cuda::dequantize_values(qr);
+            REQUIRE(std::equal(dc.values().begin(), dc.values().end(), dr.values().begin(), dr.values().end()));
+            REQUIRE(cuda::decompress(dc) == decompress(dr));
+        }
+        REQUIRE(throws_as<std::invalid_argument>([] {
+            cuda::quantize_values(compress(random_dense(2, 2, Dtype::I8, 1, 0.0)));
+        }));
+        REQUIRE(throws_as<std::invalid_argument>([] {
+            cuda::dequantize_values(compress(random_dense(2, 2, Dtype::F16, 1, 0.0)));
+        }));
+    });
     std::printf("%d failure(s)\n", g_fail);
     return g_fail;
 }

@@ -87,6 +87,11 @@ SIGNATURES = {
     "endor_cuda_compress": (C.c_int, [_u64, _u64, _i32, _vp, _vp, _vp, C.POINTER(_u64),
                                       C.POINTER(_i32), _vp, _sz, _vp]),
     "endor_cuda_quantize_values": (C.c_int, [_vp, _u64, _vp, C.POINTER(C.c_float), _vp, _sz, _vp]),
+    "endor_cuda_dequantize_values": (C.c_int, [_vp, _u64, C.c_float, _vp, _vp]),
+    "endor_cuda_extract_rows_host": (C.c_int, [_u64, _u64, _i32, _vp, _vp, _u64, _vp, _u64, _vp]),
+    "endor_cuda_extract_cols_host": (C.c_int, [_u64, _u64, _i32, _vp, _vp, _u64, _vp, _u64, _vp]),
+    "endor_cuda_quantize_values_host": (C.c_int, [_vp, _u64, _vp, C.POINTER(C.c_float)]),
+    "endor_cuda_dequantize_values_host": (C.c_int, [_vp, _u64, C.c_float, _vp]),
     "endor_cuda_synth_weight": (C.c_int, [_u64, _u64, _i32, _u64, _u64, _u64, _vp, _vp]),
     "endor_cuda_magnitude_prune": (C.c_int, [_u64, _i32, _f64, _vp, _vp, _sz, _vp]),
     "endor_cuda_gemv": (C.c_int, [_u64, _u64, _vp, _vp, _vp, _vp, _vp]),

@@ -443,6 +443,20 @@ def quantize_values(t: EndorTensor) -> EndorTensor:
                        negative_zero_collapsed=t.negative_zero_collapsed(), validate=False, nnz=t.nnz())
 
 
+def dequantize_values(t: EndorTensor) -> EndorTensor:
+    """codec.hpp:334-349 on the device: i8 packed values + scale -> f16 values
+    (bit-exact f32_to_f16 RNE); the bitmap is shared.  decompress_dequant fuses
+    this with the expand."""
+    if t.dtype != Dtype.I8 or t.quant_scale is None:
+        raise InvalidArgument("dequantize_values requires a quantized i8 tensor")
+    dev = t.device
+    out = _alloc(t.nnz() * 2, dev)
+    check(_lib.lib().endor_cuda_dequantize_values(_ptr(t.values), t.nnz(), float(t.quant_scale), _ptr(out),
+                                                  _stream_ptr(dev)))
+    return EndorTensor(t.rows, t.cols, Dtype.F16, t.bitmap, out,
+                       negative_zero_collapsed=t.negative_zero_collapsed(), validate=False, nnz=t.nnz())
+
+
 def _index_list(idx, dev) -> torch.Tensor:
     t = torch.as_tensor(idx, dtype=torch.int64) if not isinstance(idx, torch.Tensor) else idx
     return t.to(device=dev, dtype=torch.int64).contiguous().reshape(-1)

@@ -743,6 +743,12 @@ int endor_cuda_quantize_values(const void* values_f16, uint64_t nnz, void* q_out
     return ENDOR_OK;
 }
 
+int endor_cuda_dequantize_values(const void* q_i8, uint64_t nnz, float scale, void* out_f16, void* stream) {
+    if (nnz && (!q_i8 || !out_f16 || !aligned(out_f16, 2))) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null or misaligned buffer");
+    CK(launch_dequant_values(q_i8, nnz, scale, out_f16, S(stream)));
+    return ENDOR_OK;
+}
+
 int endor_cuda_synth_weight(uint64_t rows, uint64_t cols, int32_t dtype, uint64_t seed,
                             uint64_t row0, uint64_t nrows, void* out, void* stream) {
     uint64_t n;
@@ -1009,6 +1015,65 @@ int endor_cuda_compress_host(uint64_t rows, uint64_t cols, int32_t dtype, const 
                            s->ws.p, s->ws.cap, nullptr));
     CK(cudaMemcpy(bitmap_host_out, s->bm.p, bmb, cudaMemcpyDeviceToHost));
     if (*nnz_out) CK(cudaMemcpy(values_host_out, s->vals.p, *nnz_out * eb, cudaMemcpyDeviceToHost));
+    return ENDOR_OK;
+}
+
+// extract_rows / extract_cols (codec.hpp:239-297) on host buffers: index
+// validation order and exceptions as check_sorted_unique (codec.hpp:224-232).
+static int extract_host(uint64_t rows, uint64_t cols, int32_t dtype, const void* bitmap_host,
+                        const void* values_host, uint64_t nnz, const uint64_t* sel_host, uint64_t nsel,
+                        void* out_host, bool by_rows) {
+    HostSession* s;
+    endor_tensor_view v;
+    uint64_t n;
+    ST(session(&s, 1));
+    ST(upload(s, rows, cols, dtype, bitmap_host, values_host, nnz, &v, &n));
+    ST(session(&s, n ? n : 1));
+    const uint64_t out_elems = by_rows ? nsel * cols : rows * nsel;
+    const size_t ob = out_elems * eb_of(dtype);
+    if (nsel && !sel_host) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null index list");
+    CK(s->prefix.need(nsel * 8 + 16));
+    CK(s->dense.need(ob + 16));
+    if (nsel) CK(cudaMemcpy(s->prefix.p, sel_host, nsel * 8, cudaMemcpyHostToDevice));
+    ST((by_rows ? endor_cuda_extract_rows : endor_cuda_extract_cols)(&v, static_cast<const uint64_t*>(s->prefix.p),
+                                                                      nsel, s->dense.p, s->ws.p, s->ws.cap, nullptr));
+    ST(endor_cuda_sync_status(s->ws.p, nullptr));
+    if (ob) CK(cudaMemcpy(out_host, s->dense.p, ob, cudaMemcpyDeviceToHost));
+    return ENDOR_OK;
+}
+
+int endor_cuda_extract_rows_host(uint64_t rows, uint64_t cols, int32_t dtype, const void* bitmap_host,
+                                 const void* values_host, uint64_t nnz, const uint64_t* rows_host, uint64_t nsel,
+                                 void* out_host) {
+    return extract_host(rows, cols, dtype, bitmap_host, values_host, nnz, rows_host, nsel, out_host, true);
+}
+
+int endor_cuda_extract_cols_host(uint64_t rows, uint64_t cols, int32_t dtype, const void* bitmap_host,
+                                 const void* values_host, uint64_t nnz, const uint64_t* cols_host, uint64_t nsel,
+                                 void* out_host) {
+    return extract_host(rows, cols, dtype, bitmap_host, values_host, nnz, cols_host, nsel, out_host, false);
+}
+
+int endor_cuda_quantize_values_host(const void* values_f16_host, uint64_t nnz, void* q_host_out,
+                                    float* scale_out) {
+    HostSession* s;
+    ST(session(&s, 1));
+    CK(s->vals.need(nnz * 2 + 16));
+    CK(s->dense.need(nnz + 16));
+    if (nnz) CK(cudaMemcpy(s->vals.p, values_f16_host, nnz * 2, cudaMemcpyHostToDevice));
+    ST(endor_cuda_quantize_values(s->vals.p, nnz, s->dense.p, scale_out, s->ws.p, s->ws.cap, nullptr));
+    if (nnz) CK(cudaMemcpy(q_host_out, s->dense.p, nnz, cudaMemcpyDeviceToHost));
+    return ENDOR_OK;
+}
+
+int endor_cuda_dequantize_values_host(const void* q_host, uint64_t nnz, float scale, void* f16_host_out) {
+    HostSession* s;
+    ST(session(&s, 1));
+    CK(s->vals.need(nnz + 16));
+    CK(s->dense.need(nnz * 2 + 16));
+    if (nnz) CK(cudaMemcpy(s->vals.p, q_host, nnz, cudaMemcpyHostToDevice));
+    ST(endor_cuda_dequantize_values(s->vals.p, nnz, scale, s->dense.p, nullptr));
+    if (nnz) CK(cudaMemcpy(f16_host_out, s->dense.p, nnz * 2, cudaMemcpyDeviceToHost));
     return ENDOR_OK;
 }
 

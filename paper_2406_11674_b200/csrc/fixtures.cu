@@ -317,6 +317,27 @@ static unsigned grid_for(uint64_t work, unsigned threads, unsigned cap = 148 * 3
     return unsigned(g < 1 ? 1 : (g > cap ? cap : g));
 }
 
+// dequantize_values (codec.hpp:334-349): f16 = f32_to_f16(float(q) * scale)
+// per packed value, RNE (float16.hpp:35-73); NaN products follow the x86 SSE
+// rules the reference runs under (see gather_chunk_dequant).
+__global__ void __launch_bounds__(256) dequant_values_kernel(const int8_t* q, uint64_t nnz, float scale,
+                                                             uint16_t* out) {
+    const uint32_t sb = __float_as_uint(scale);
+    const bool snan = (sb & 0x7FFFFFFFu) > 0x7F800000u;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nnz; i += uint64_t(gridDim.x) * blockDim.x) {
+        float v = __fmul_rn(float(q[i]), scale);
+        if (v != v) v = __uint_as_float(snan ? (sb | 0x00400000u) : 0xFFC00000u);
+        out[i] = f32_to_f16_bits(v);
+    }
+}
+
+cudaError_t launch_dequant_values(const void* q, uint64_t nnz, float scale, void* out, cudaStream_t s) {
+    if (nnz == 0) return cudaSuccess;
+    const unsigned g = unsigned(umin64(ceil_div(nnz, 256), 148ull * 16));
+    dequant_values_kernel<<<g, 256, 0, s>>>(static_cast<const int8_t*>(q), nnz, scale, static_cast<uint16_t*>(out));
+    return cudaGetLastError();
+}
+
 cudaError_t launch_synth(uint64_t i0, uint64_t count, int eb, uint64_t seed, void* out,
                          cudaStream_t s) {
     if (count == 0) return cudaSuccess;

@@ -134,6 +134,7 @@ cudaError_t launch_extract_cols(const RankTable& rt, const uint8_t* values, uint
 
 cudaError_t launch_scan(const ScanArgs& a, cudaStream_t s);
 cudaError_t launch_expand(const ExpandArgs& a, int mode, cudaStream_t s);  // mode 1 i8, 2 f16, 3 dequant
+cudaError_t launch_dequant_values(const void* q, uint64_t nnz, float scale, void* out, cudaStream_t s);
 cudaError_t launch_synth(uint64_t i0, uint64_t count, int eb, uint64_t seed, void* out,
                          cudaStream_t s);
 cudaError_t launch_prune(uint8_t* w, uint64_t n, int eb, uint64_t target, const WsLayout& L,

@@ -72,6 +72,23 @@ def test_every_int8_value_every_edge_scale(E, scale):
     assert got == want.tobytes()
 
 
+@pytest.mark.parametrize("scale", SCALES)
+def test_dequantize_values_every_int8_value(E, scale):
+    """dequantize_values (codec.hpp:334-349) of the packed values alone: all
+    256 i8 values at every edge scale == the oracle's f32_to_f16 restatement,
+    and decompress(dequantize_values(t)) == the fused dequant expand."""
+    nnz = 256 * 3
+    q = (np.arange(nnz) * 101 % 256).astype(np.uint8)
+    want = np.zeros(nnz, np.uint16)
+    O.lib().or_dequantize_values(q, nnz, np.float32(scale), want)
+    bits = np.ones(nnz, bool)
+    bm = np.packbits(bits, bitorder="little")
+    t = _i8_tensor(E, 3, 256, bm, q, nnz, float(np.float32(scale)), values_offset=1)
+    d = E.dequantize_values(t)
+    assert d.dtype == E.Dtype.F16 and d.values.cpu().numpy().tobytes() == want.tobytes()
+    assert E.decompress(d).bytes() == E.decompress_dequant(t).bytes()
+
+
 def test_dequant_large_layer_shape(E):
     """fc1-sized: 9216 x 36864 @ 50%, GPU-generated, quantized on the host
     oracle, fused dequant+decompress == oracle chain (CRC)."""
@@ -115,6 +132,8 @@ def test_dequant_errors(E):
     t = E.EndorTensor(10, 10, E.Dtype.F16, E.Bitmap(100, data=_dev(bm)), _dev(vals))
     with pytest.raises(E.InvalidArgument):  # f16 tensor: codec.hpp:335-337
         E.decompress_dequant(t)
+    with pytest.raises(E.InvalidArgument):
+        E.dequantize_values(t)
     q, scale = O.quantize_values(vals, nnz)
     bad = _i8_tensor(E, 10, 10, bm, q[:-1], nnz - 1, scale)
     with pytest.raises(E.CorruptionError):  # popcount != nnz
