@@ -437,7 +437,10 @@ def quantize_values(t: EndorTensor) -> EndorTensor:
     q = _alloc(t.nnz(), dev)
     scale = C.c_float(0.0)
     ws = workspace(1, dev)
-    check(_lib.lib().endor_cuda_quantize_values(_ptr(t.values), t.nnz(), _ptr(q), C.byref(scale), ws.data_ptr(),
+    vals = t.values
+    if vals.numel() and _ptr(vals) % 2:  # the kernel reads f16 words: realign on the device
+        vals = _alloc(vals.numel(), dev).copy_(vals)
+    check(_lib.lib().endor_cuda_quantize_values(_ptr(vals), t.nnz(), _ptr(q), C.byref(scale), ws.data_ptr(),
                                                 ws.numel(), _stream_ptr(dev)))
     return EndorTensor(t.rows, t.cols, Dtype.I8, t.bitmap, q, quant_scale=scale.value,
                        negative_zero_collapsed=t.negative_zero_collapsed(), validate=False, nnz=t.nnz())
