@@ -3,7 +3,7 @@ oracle (development aid; test infrastructure like tests/, it imports oracle/).
 
   python tools/fuzz.py [seconds] [seed]
 
-Shapes 1..6000 x 1..6000 (capped at 4M elements), both dtypes, zero fractions
+Shapes up to FUZZ_MAX_ELEMS elements (default 4M; 1..6000 per side), both dtypes, zero fractions
 0..1 incl. the extremes, block-structured masks, odd value/bitmap offsets,
 and every API: decompress, decompress_chunked (chunk 64..8192), chunk_into,
 build_rank_index, extract_rows/cols, compress, fused GEMV (f16, cols % 1024
@@ -30,14 +30,18 @@ def dev_bytes(a, off):
     return v
 
 
+MAX_ELEMS = int(os.environ.get("FUZZ_MAX_ELEMS", "4000000"))
+
+
 def make(rng):
     eb = int(rng.choice([1, 2]))
     if rng.random() < 0.25:
         cols = int(rng.choice([1024, 2048, 3072, 8192, 9216]))
-        rows = int(rng.integers(1, max(2, 4_000_000 // cols)))
+        rows = int(rng.integers(1, max(2, MAX_ELEMS // cols)))
     else:
-        rows, cols = int(rng.integers(1, 6000)), int(rng.integers(1, 6000))
-        while rows * cols > 4_000_000:
+        side = int(MAX_ELEMS ** 0.5 * 3)
+        rows, cols = int(rng.integers(1, side)), int(rng.integers(1, side))
+        while rows * cols > MAX_ELEMS:
             rows = max(1, rows // 2)
     zf = float(rng.choice([0.0, 1.0, rng.random()]))
     w = O.random_dense(rows, cols, eb, int(rng.integers(1 << 62)), zf)
