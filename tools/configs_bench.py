@@ -220,17 +220,53 @@ def cfg5(out, G):
             "note": "per-GPU share on this box's PCIe link (G GPUs would each stream their own shards)"}
 
 
+def cfg_structured(out):
+    """SURVEY.md 8(d) cross-check: per-tile density made uneven or structured.
+    fc1 shape with the reference's N:M pruning (nm_prune 2:4 and 1:4, restated
+    in the oracle, weight_gen.hpp:118-141) and with whole-row bands pruned
+    (every other block of 64 rows empty, the rest 80 % dense)."""
+    import numpy as np
+    from oracle import oracle as O
+    rows, cols = 9216, 36864
+    w = E.synth_weight(rows, cols, catalog.FC1_SEED, device=DEV)
+    host = w.data.view(torch.uint8).cpu().numpy()
+    res = []
+    for keep, m in ((2, 4), (1, 4)):
+        pr = np.zeros_like(host)
+        assert O.lib().or_nm_prune(rows, cols, 2, keep, m, host, pr) == 0
+        d = E.DenseMatrix(rows, cols, E.Dtype.F16, torch.from_numpy(pr).to(DEV))
+        res.append(decomp_stats([E.compress(d)], f"fc1 nm_prune {keep}:{m}"))
+        print(json.dumps(res[-1]), flush=True)
+    wb = E.synth_weight(rows, cols, catalog.FC1_SEED, device=DEV)
+    E.magnitude_prune(wb, 0.2, inplace=True)
+    band = wb.data.view(torch.uint8).reshape(rows, cols * 2)
+    for r0 in range(0, rows, 128):
+        band[r0: r0 + 64] = 0
+    res.append(decomp_stats([E.compress(wb)], "fc1 64-row bands alternately empty / 80 % dense"))
+    print(json.dumps(res[-1]), flush=True)
+    out["structured_sparsity_fc1"] = res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01", "configs.json"))
     ap.add_argument("--skip-pass", action="store_true")
+    ap.add_argument("--only", default="", help="comma list of: structured (write only these keys)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     out = {"device": torch.cuda.get_device_name(0), "hbm_peak_gbs": PEAK, "host_threads": os.cpu_count()}
+    if args.only:
+        if "structured" in args.only:
+            cfg_structured(out)
+        os.makedirs(os.path.dirname(args.out), exist_ok=True)
+        with open(args.out, "w") as f:
+            json.dump(out, f, indent=1)
+        return
     cfg1(out)
     print(json.dumps(out["config1_fc1_round_trip"]), flush=True)
     cfg3(out)
     cfg4(out)
+    cfg_structured(out)
     if not args.skip_pass:
         out["config5_opt66b_64_layer_pass"] = [cfg5(out, 8), cfg5(out, 1)]
         torch.cuda.empty_cache()
