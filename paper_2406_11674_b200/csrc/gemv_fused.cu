@@ -11,20 +11,25 @@
 //  * work item t = 8 consecutive 1024-element sub-tiles [8t, 8t+8) of the
 //    flattened matrix (the RankIndex chunks): one contiguous bitmap kilobyte
 //    and one contiguous packed-value window, so one producer warp moves an
-//    item with three 1-D TMA bulk copies (bitmap, the 8 index entries,
-//    values) into a 4-stage smem ring (cp.async.bulk + mbarrier complete_tx);
+//    item with two 1-D TMA bulk copies (bitmap, values) into a 4-stage smem
+//    ring (cp.async.bulk + mbarrier complete_tx).  The item's nine index
+//    entries are fetched 32 items ahead (one per lane), validated (monotone,
+//    within [0, nnz], at most 1024 apart) and written to the stage as 32-bit
+//    offsets relative to the value window;
 //  * consumer warp w takes sub-tile 8t + w, i.e. column segment
 //    (8t + w) % segs.  A CTA walks items t0, t0 + segs, t0 + 2 segs, ..
 //    (the same 8 segments one 8-row band further down each time), so every
 //    warp's x segment (1024 f16 = 16 registers per lane) stays in registers
 //    for the whole run;
-//  * lane l expands nibbles l, l+32, .. of the sub-tile (4 weights each):
-//    neighbouring lanes read neighbouring bytes, so each LDS is one
-//    conflict-free wavefront; PRMT selector gathers (gather.cuh) place the
-//    packed values and FHFMA (fp32 += f16*f16, one instruction per weight)
-//    accumulates; the fp32 partial of each sub-tile goes to the workspace and
-//    a second tiny kernel sums each row's partials in a fixed order
-//    (deterministic, no atomics).
+//  * lane l expands bitmap bytes l, l+32, .. of the sub-tile (8 weights, two
+//    nibbles each; ENDOR_GV_BYTE_LANES=0 selects nibble lanes, conflict-free
+//    LDS but twice the shuffles -- measured slower): PRMT selector gathers
+//    (gather.cuh) place the packed values and FHFMA (fp32 += f16*f16, one
+//    instruction per weight, predicated for unset slots) accumulates; the
+//    fp32 partial of each sub-tile goes to the workspace and a second tiny
+//    kernel sums each row's partials in a fixed order (deterministic, no
+//    atomics).  ~300 warp-instructions per 1024 weights: issue-bound (ncu
+//    71 % issue, 78 % L1), independent of the density.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
