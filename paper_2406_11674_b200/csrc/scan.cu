@@ -2,7 +2,8 @@
 // serial value cursor and of build_rank_index (bitmap.hpp:117-132).
 //
 //   count_kernel   hot path.  Two-level, no inter-CTA waiting: every CTA
-//                  popcounts 131072 bits (16 expand tiles), writes the
+//                  popcounts a contiguous range of 262144-bit count blocks
+//                  (streamed through a 2-stage TMA bulk ring), writes the
 //                  CTA-local exclusive offset of each 1024-bit sub-tile and
 //                  its aggregate; the last CTA to finish scans the aggregates
 //                  into per-CTA bases and checks the total against nnz
