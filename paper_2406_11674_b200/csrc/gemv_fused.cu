@@ -33,6 +33,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "gather.cuh"
@@ -46,6 +47,7 @@ constexpr int kGvThreads = (kGvWarps + 1) * 32;   // + 1 producer warp
 #define ENDOR_GV_STAGES 4
 #endif
 constexpr int kGvStages = ENDOR_GV_STAGES;
+constexpr uint64_t kGvSparseDensity10 = 2;  // set-bit consumer at density <= 0.2 (tools/fused_sweep.py)
 // lane granularity of the gather: 1 = byte lanes (two nibbles per step, one
 // shuffle pair per 8 weights), 0 = nibble lanes (conflict-free LDS)
 #ifndef ENDOR_GV_BYTE_LANES
@@ -57,6 +59,14 @@ constexpr uint32_t kGvMeta = kGvWarps * 128;                   // 9 u32 sub-tile
 constexpr uint32_t kGvVals = kGvMeta + 48;                     // packed-value window
 constexpr uint32_t kGvStage = kGvVals + kGvWarps * kSubElems * 2 + 32 + 64;  // + alignment slack + over-read pad
 constexpr uint32_t kGvSmem = 256 + kGvStages * kGvStage;
+// SPARSE consumer (s >= ~0.7): each lane walks the set bits of its own bitmap
+// word -- cost per set value, not per slot.  x (1024 f16 per warp) lives in
+// shared memory transposed (column 32 l + b at b * 32 + l: at most 2-way bank
+// conflicts for any per-lane bit), so one stage fewer keeps 3 CTAs per SM.
+template <bool SPARSE>
+constexpr int gv_stages() { return SPARSE ? kGvStages - 1 : kGvStages; }
+template <bool SPARSE>
+constexpr uint32_t gv_smem() { return 256 + gv_stages<SPARSE>() * kGvStage + (SPARSE ? kGvWarps * kSubElems * 2 : 0); }
 
 // inclusive warp prefix sum: shfl.up's in-range predicate guards each add
 __device__ __forceinline__ uint32_t warp_incl_scan_p(uint32_t v) {
@@ -145,7 +155,9 @@ struct ItemCursor {
 #ifndef ENDOR_GV_MINB
 #define ENDOR_GV_MINB 3  // CTAs per SM the register budget is sized for
 #endif
+template <bool SPARSE>
 __global__ void __launch_bounds__(kGvThreads, ENDOR_GV_MINB) gemv_fused_kernel(const __grid_constant__ Batch b, uint64_t nitems) {
+    constexpr int kGvStages = gv_stages<SPARSE>();
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t sbase = smem_u32(smem);
     const uint32_t full0 = sbase, empty0 = sbase + 8 * kGvStages;
@@ -281,7 +293,25 @@ __global__ void __launch_bounds__(kGvThreads, ENDOR_GV_MINB) gemv_fused_kernel(c
     const BatchTensor* T = &b.t[cur.ti];
     for (uint32_t i = 0; i < m; ++i) {
         const bool ok = k < nsub;
-        if (ok && run != xrun) {  // x stays in registers along a column
+        if (SPARSE && ok && run != xrun) {  // x segment -> this warp's smem, transposed
+            const uint32_t xs = st0 + kGvStages * kGvStage + warp * (kSubElems * 2);
+            const uint4* src = static_cast<const uint4*>(T->x) + (k % cur.segs) * (kSubElems / 8) + lane * 4;
+            __syncwarp();  // the previous run's reads are done
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint4 v = __ldg(src + q);
+                const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int h = 0; h < 8; ++h) {  // column 32 lane + 8 q + h
+                    const uint32_t bcol = 8 * q + h;
+                    asm volatile("st.shared.u16 [%0], %1;" ::"r"(xs + 2 * (bcol * 32 + lane)),
+                                 "h"(uint16_t(w4[h >> 1] >> (16 * (h & 1)))) : "memory");
+                }
+            }
+            __syncwarp();
+            xrun = run;
+        }
+        if (!SPARSE && ok && run != xrun) {  // x stays in registers along a column
 #if ENDOR_GV_BYTE_LANES
             const uint4* xs = static_cast<const uint4*>(T->x) + (k % cur.segs) * (kSubElems / 8);
 #pragma unroll
@@ -321,6 +351,35 @@ __global__ void __launch_bounds__(kGvThreads, ENDOR_GV_MINB) gemv_fused_kernel(c
                 wbase = stg + kGvVals;
             }
             float acc0 = 0.f, acc1 = 0.f;
+            if constexpr (SPARSE) {
+                // lane l: the set bits of word l, values from its exclusive rank on
+                const uint32_t xs = st0 + kGvStages * kGvStage + warp * (kSubElems * 2) + 2 * lane;
+                uint32_t a = wbase;  // this word's first packed value
+                uint32_t w = word;
+                if ((a & 1) == 0) {
+                    while (w) {
+                        const uint32_t bit = __ffs(w) - 1;
+                        w &= w - 1;
+                        uint16_t v, xv;
+                        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+                        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(xv) : "r"(xs + 64 * bit));
+                        asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(acc0) : "h"(v), "h"(xv));
+                        a += 2;
+                    }
+                } else {  // an odd values buffer (any alignment is allowed): two byte loads
+                    while (w) {
+                        const uint32_t bit = __ffs(w) - 1;
+                        w &= w - 1;
+                        uint16_t v0, v1, xv;
+                        asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v0) : "r"(a));
+                        asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v1) : "r"(a + 1));
+                        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(xv) : "r"(xs + 64 * bit));
+                        const uint16_t v = uint16_t(v0 | (v1 << 8));
+                        asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(acc0) : "h"(v), "h"(xv));
+                        a += 2;
+                    }
+                }
+            } else {
 #if ENDOR_GV_BYTE_LANES
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -358,6 +417,7 @@ __global__ void __launch_bounds__(kGvThreads, ENDOR_GV_MINB) gemv_fused_kernel(c
                 acc1 = fma_f16x2_if<4u, 8u>(prmt(x, y, sel >> 16), xr[2 * q + 1], acc1, nib);  // slots 2, 3
             }
 #endif
+            }
             float a = acc0 + acc1;
 #pragma unroll
             for (int d = 16; d > 0; d >>= 1) a += __shfl_xor_sync(0xffffffffu, a, d);
@@ -421,8 +481,21 @@ cudaError_t launch_gemv_fused(Batch& b, cudaStream_t s) {
         if (e != cudaSuccess) return e;
     }
     int blocks_per_sm = 1, sms = 148;
-    cudaError_t e = kernel_slots(reinterpret_cast<const void*>(gemv_fused_kernel), kGvThreads, kGvSmem,
-                                 &blocks_per_sm, &sms);
+    // per-batch consumer choice by density (ENDOR_GV_SPARSE=0/1 forces one)
+    uint64_t n_all = 0, nnz_all = 0;
+    for (int k = 0; k < b.count; ++k) {
+        n_all += b.t[k].n;
+        nnz_all += b.t[k].nnz;
+    }
+    static const int env_sparse = [] {
+        const char* e = getenv("ENDOR_GV_SPARSE");
+        return e ? atoi(e) : -1;
+    }();
+    const bool sparse = env_sparse >= 0 ? env_sparse != 0 : nnz_all * 10 <= n_all * kGvSparseDensity10;
+    const void* fn = sparse ? reinterpret_cast<const void*>(gemv_fused_kernel<true>)
+                            : reinterpret_cast<const void*>(gemv_fused_kernel<false>);
+    const uint32_t smem = sparse ? gv_smem<true>() : gv_smem<false>();
+    cudaError_t e = kernel_slots(fn, kGvThreads, smem, &blocks_per_sm, &sms);
     if (e != cudaSuccess) return e;
     uint64_t items = 0;
     for (int k = 0; k < b.count; ++k) {
@@ -432,7 +505,8 @@ cudaError_t launch_gemv_fused(Batch& b, cudaStream_t s) {
     }
     const uint64_t grid = umin64(items, uint64_t(blocks_per_sm) * sms);
     if (grid == 0) return cudaSuccess;
-    gemv_fused_kernel<<<unsigned(grid), kGvThreads, kGvSmem, s>>>(b, items);
+    if (sparse) gemv_fused_kernel<true><<<unsigned(grid), kGvThreads, smem, s>>>(b, items);
+    else gemv_fused_kernel<false><<<unsigned(grid), kGvThreads, smem, s>>>(b, items);
     return cudaGetLastError();
 }
 

@@ -19,7 +19,7 @@ def E(cuda_lib):
 
 
 @pytest.mark.parametrize("rows,cols,s", [(1, 1024, 0.5), (37, 2048, 0.0), (300, 9216, 0.5), (64, 36864, 0.9),
-                                         (1024, 8192, 0.3)])
+                                         (1024, 8192, 0.3), (300, 9216, 0.85), (7, 1024, 0.97), (40, 4096, 0.999)])
 def test_fused_gemv_matches_fp32_reference(E, rows, cols, s):
     w = E.synth_weight(rows, cols, rows * 31 + cols, device="cuda")
     if s > 0:
@@ -160,3 +160,21 @@ def test_fused_gemv_unaligned_values_buffer(E, offset):
     x = (torch.rand(cols, generator=torch.Generator().manual_seed(1)) * 2 - 1).half().cuda()
     assert torch.equal(E.gemv_compressed(tu, x), E.gemv_compressed(t, x))
     assert torch.equal(E.gemv_compressed(tu, x, index=E.build_rank_index(t.bitmap, 1024)), E.gemv_compressed(t, x))
+
+
+@pytest.mark.parametrize("mode", ["0", "1"])
+def test_every_fused_case_under_each_consumer(cuda_lib, mode):
+    """This file again with the consumer forced (ENDOR_GV_SPARSE=0: byte
+    lanes, =1: set-bit walk) -- the library otherwise picks by density."""
+    import os
+    import subprocess
+    import sys
+    if os.environ.get("ENDOR_GV_SPARSE") is not None:
+        pytest.skip("already forced")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, ENDOR_GV_SPARSE=mode)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_gpu_fused_gemv.py"),
+                        os.path.join(root, "tests", "test_gpu_density.py")],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
