@@ -11,6 +11,7 @@
 // When the caller only wants y = W x (no dense_dev), the op runs as one fused
 // decompress -> GEMV (gemv_fused.cu): the dense W never touches HBM.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for nsys / ncu timelines
 #include <stdint.h>
 
 #include <new>
@@ -130,8 +131,17 @@ int endor_pipeline_destroy(endor_pipeline* p) {
 
 void* endor_pipeline_stream(endor_pipeline* p) { return p ? p->compute : nullptr; }
 
+namespace {
+// NVTX range for the enqueue of one pipeline stage (no-ops without a tool attached)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+
 int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops, int sync) {
     if (!p || (nops > 0 && !ops)) return ENDOR_ERR_INVALID_ARGUMENT;
+    NvtxRange run_range("endor_pipeline_run");
     PK(cudaSetDevice(p->device));
     int st = ensure_events(p, nops);
     if (st) return st;
@@ -149,6 +159,7 @@ int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops
         auto& slot = p->slots[i % p->depth];
         const size_t bmb = (n + 7) / 8, vb = op.nnz * eb;
         // copy stream: wait until the slot's previous occupant was decompressed
+        NvtxRange h2d_range(op.path ? "endor op: storage -> HBM" : "endor op: H2D compressed");
         PK(cudaStreamWaitEvent(p->copy, slot.free_ev, 0));
         PK(cudaEventRecord(p->h2d_beg[i], p->copy));
         if (op.path) {
@@ -166,6 +177,7 @@ int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops
         }
         PK(cudaEventRecord(p->h2d_end[i], p->copy));
         // compute stream: decompress into the dense ring (or the caller's buffer), then GEMV
+        NvtxRange compute_range("endor op: decompress + GEMV");
         PK(cudaStreamWaitEvent(p->compute, p->h2d_end[i], 0));
         PK(cudaEventRecord(p->dec_beg[i], p->compute));
         endor_tensor_view v{op.rows, op.cols, op.dtype, 0, slot.bitmap, slot.values, op.nnz};
