@@ -96,3 +96,17 @@ def test_product_has_no_cpu_fallback():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"(from|import)\s+oracle|liboracle|libendor_ref|ref_shim", src), f
+
+
+def test_integration_snippets_type_check():
+    """INTEGRATION.md's C calls (tests/c/integration_example.c) compile against
+    include/endor_cuda.h: the documented boundary is the shipped one."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no gcc")
+    r = subprocess.run([gcc, "-std=c11", "-Wall", "-Werror", "-Wno-missing-field-initializers", "-fsyntax-only",
+                        "-I", os.path.join(ROOT, "include"), os.path.join(ROOT, "tests", "c", "integration_example.c")],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
