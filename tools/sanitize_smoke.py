@@ -67,6 +67,15 @@ for (rows, cols, eb, zf, off) in [(2, 2, 2, 0.5, 0), (37, 1000, 2, 0.5, 2), (64,
         E.decompress_dequant(q)                                                    # fused dequant expand
     checks += 1
 
+# the fused GEMV's set-bit consumer (density <= 0.2), odd value offset
+w9, t9 = tensor(48, 4096, 2, 99, 0.9, 3)
+x9 = (torch.rand(4096, device=dev) * 2 - 1).half()
+y9 = E.gemv_compressed(t9, x9)
+ref9 = torch.from_numpy(w9.view(np.float16).reshape(48, 4096).astype(np.float32)).to(dev) @ x9.float()
+assert (y9 - ref9).abs().max().item() <= 1e-3 * ref9.abs().max().item() + 1e-6
+d9 = E.dequantize_values(E.quantize_values(t9))
+assert d9.nnz() == t9.nnz()
+
 # batched paths
 ws = [tensor(40, 2048, 2, s, 0.5) for s in range(3)]
 outs = E.decompress_batch([t for _, t in ws])
