@@ -58,8 +58,7 @@ constexpr uint32_t kGvMeta = kGvWarps * 128;                   // 9 u32 sub-tile
                                                                // window, then the window's byte offset
 constexpr uint32_t kGvVals = kGvMeta + 48;                     // packed-value window
 constexpr uint32_t kGvStage = kGvVals + kGvWarps * kSubElems * 2 + 32 + 64;  // + alignment slack + over-read pad
-constexpr uint32_t kGvSmem = 256 + kGvStages * kGvStage;
-// SPARSE consumer (s >= ~0.7): each lane walks the set bits of its own bitmap
+// SPARSE consumer (density <= 0.2): each lane walks the set bits of its own bitmap
 // word -- cost per set value, not per slot.  x (1024 f16 per warp) lives in
 // shared memory transposed (column 32 l + b at b * 32 + l: at most 2-way bank
 // conflicts for any per-lane bit), so one stage fewer keeps 3 CTAs per SM.

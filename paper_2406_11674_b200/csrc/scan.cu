@@ -28,7 +28,6 @@ namespace endor_b200 {
 // count_kernel (batched)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kScanThreads) count_kernel(const __grid_constant__ Batch b) {
-    __shared__ unsigned long long s_warp[kScanThreads / 32];
     __shared__ uint32_t s_sub[kCountSubs];
     __shared__ int s_last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
