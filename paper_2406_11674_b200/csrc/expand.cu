@@ -50,6 +50,12 @@ struct Stage {
     static constexpr uint32_t kBytes = kVals + kTileElems * EB + 64;
 };
 
+// A caller's RankIndex is validated by the producer (monotone, within
+// [0, nnz], <= 1024 values per sub-tile), so sub-tile k starts at most 1024 k
+// values into the tile's window and no consumer read can leave the stage's
+// 8192-value window buffer.  A middle entry that passes but disagrees with the
+// bitmap yields garbage -- the reference's check_index does not look at middle
+// entries either (codec.hpp:170-184) -- never an out-of-bounds access.
 template <int EB>
 constexpr uint32_t tma_smem_bytes() {
     return 256 /* 2*kStages mbarriers */ + kStages * Stage<EB>::kBytes;
@@ -101,44 +107,57 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
                 if (lane == 0 && T.idx[last] + tail != T.nnz) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
             }
         }
-        // absolute [start, end) value offsets of global tile t: the caller's
-        // RankIndex, or count_kernel's two levels
-        auto window = [&](uint64_t t, unsigned long long& s0, unsigned long long& s1) {
+        // Global tile t's absolute value window [s0, s1) and its nine sub-tile
+        // starts relative to s0 (rel[8] = s1 - s0): the caller's RankIndex --
+        // validated here, so the consumers need no checks -- or count_kernel's
+        // two levels (a tile never straddles two count CTAs' ranges).
+        auto entries = [&](uint64_t t, unsigned long long& s0, uint32_t* rel) {
             const BatchTensor& T = b.t[batch_tensor_of_tile(b, t)];
-            const uint64_t lt = t - T.tile0, nsub = ceil_div(T.n, kSubElems);
-            const uint64_t a = lt * 8, e = lt * 8 + 8;
+            const uint64_t lt = t - T.tile0, nsub = ceil_div(T.n, kSubElems), a = lt * 8;
+            unsigned long long e[9];
             if (T.idx) {
-                s0 = T.idx[a];
-                s1 = e >= nsub ? T.nnz : T.idx[e];
-                // memory safety only: an inconsistent index yields garbage like the
-                // reference, but never a read outside the values buffer
-                const unsigned long long c0 = s0 < T.nnz ? s0 : T.nnz;
-                const unsigned long long c1 = s1 < c0 ? c0 : (s1 < T.nnz ? s1 : T.nnz);
-                if (c0 != s0 || c1 != s1 || c1 - c0 > kTileElems) {
-                    latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
-                    s0 = c0;
-                    s1 = c1 - c0 > kTileElems ? c0 + kTileElems : c1;
+#pragma unroll
+                for (int k = 0; k <= 8; ++k) e[k] = a + k < nsub ? T.idx[a + k] : T.nnz;
+                // monotone, within [0, nnz], at most 1024 values per sub-tile: clamp
+                // and latch (memory safety; an entry that passes but disagrees with
+                // the bitmap yields garbage like the reference)
+                bool bad = false;
+                unsigned long long lo = 0;
+#pragma unroll
+                for (int k = 0; k <= 8; ++k) {
+                    unsigned long long v = e[k] < lo ? lo : (e[k] > T.nnz ? T.nnz : e[k]);
+                    if (k > 0 && v - lo > kSubElems) v = lo + kSubElems;
+                    bad |= v != e[k];
+                    e[k] = lo = v;
                 }
-                return;
+                if (bad) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
+            } else {
+                const uint64_t spc = uint64_t(kSubsPerBlk) * T.cbpc;  // one count CTA's range
+                const unsigned long long* blk = b.blk + T.blk0;
+                const unsigned long long* tsub = b.tsub + T.sub0;
+                const unsigned long long base = blk[a / spc];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) e[k] = a + k < nsub ? base + tsub[a + k] : blk[T.ncta];
+                e[8] = a + 8 >= nsub ? blk[T.ncta] : blk[(a + 8) / spc] + tsub[a + 8];
             }
-            const uint64_t subs_per_cta = uint64_t(kSubsPerBlk) * T.cbpc;  // one count CTA's range
-            const unsigned long long* blk = b.blk + T.blk0;
-            const unsigned long long* tsub = b.tsub + T.sub0;
-            s0 = blk[a / subs_per_cta] + tsub[a];
-            s1 = e >= nsub ? blk[T.ncta] : blk[e / subs_per_cta] + tsub[e];
+            s0 = e[0];
+#pragma unroll
+            for (int k = 0; k <= 8; ++k) rel[k] = uint32_t(e[k] - e[0]);
         };
-        unsigned long long tp_l = 0, te_l = 0;  // lane k: window of this CTA's tile i+k
+        unsigned long long tp_l = 0;  // lane k: tile i+k's window start ..
+        uint32_t rel_l[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // .. and its relative sub-tile starts
         int i = 0, ti = 0;
         for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
             const int s = i % kStages;
             const uint32_t stg = st0 + s * Stage<EB>::kBytes;
             const uint32_t full = full0 + 8 * s;
-            if ((i & 31) == 0) {  // one round trip fetches the next 32 tiles' windows
+            if ((i & 31) == 0) {  // one round trip fetches the next 32 tiles' entries
                 const uint64_t tl = t + uint64_t(lane) * gridDim.x;
-                if (tl < ntiles) window(tl, tp_l, te_l);
+                if (tl < ntiles) entries(tl, tp_l, rel_l);
             }
-            const unsigned long long tp = __shfl_sync(0xffffffffu, tp_l, i & 31);
-            const unsigned long long te = __shfl_sync(0xffffffffu, te_l, i & 31);
+            const int own = i & 31;  // the lane holding this tile's entries
+            const unsigned long long tp = __shfl_sync(0xffffffffu, tp_l, own);
+            const unsigned long long te = tp + __shfl_sync(0xffffffffu, rel_l[8], own);
             while (ti + 1 < b.count && t >= b.t[ti + 1].tile0) ++ti;
             const BatchTensor& T = b.t[ti];
             const uint64_t lt = t - T.tile0;
@@ -154,20 +173,17 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
             const uintptr_t as = ws & ~uintptr_t(15), ae = (we + 15) & ~uintptr_t(15);
             const uintptr_t bs = as > vlo16 ? as : vlo16, be = ae < vhi16 ? ae : vhi16;
             const uint32_t vbulk = be > bs ? uint32_t(be - bs) : 0u;
-            // the 8 sub-tile offsets: bulk-copied, except a caller index's ragged
-            // last tile (fewer than 8 entries exist past lt*8)
-            const uint64_t nsub_t = ceil_div(T.n, kSubElems);
-            const bool sub_bulk = !T.idx || lt * 8 + 8 <= nsub_t;
-            const unsigned long long* subsrc = T.idx ? T.idx + lt * 8 : b.tsub + T.sub0 + lt * 8;
             if (lane == 0) {
-                mbar_arrive_expect_tx(full, bm_bulk + (sub_bulk ? 64u : 0u) + vbulk);
+                mbar_arrive_expect_tx(full, bm_bulk + vbulk);
                 if (bm_bulk) bulk_g2s(stg + Stage<EB>::kBm, T.bitmap + t0 / 8, bm_bulk, full);
-                if (sub_bulk) bulk_g2s(stg + Stage<EB>::kSub, subsrc, 64, full);
                 if (vbulk) bulk_g2s(stg + Stage<EB>::kVals + uint32_t(bs - as), reinterpret_cast<const void*>(bs), vbulk, full);
             }
-            if (!sub_bulk && lane < 8 && lt * 8 + lane < nsub_t)
-                asm volatile("st.shared.u64 [%0], %1;" ::"r"(stg + Stage<EB>::kSub + 8 * lane),
-                             "l"(subsrc[lane]) : "memory");
+            if (lane == own) {  // the 8 sub-tile starts, relative to the window start
+                asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(stg + Stage<EB>::kSub), "r"(rel_l[0]),
+                             "r"(rel_l[1]), "r"(rel_l[2]), "r"(rel_l[3]) : "memory");
+                asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(stg + Stage<EB>::kSub + 16),
+                             "r"(rel_l[4]), "r"(rel_l[5]), "r"(rel_l[6]), "r"(rel_l[7]) : "memory");
+            }
             // edge bytes the bulk copies cannot move (ends of the buffers)
             for (uint32_t x = bm_bulk + lane; x < bm_bytes; x += 32)
                 sts8(stg + Stage<EB>::kBm + x, __ldg(T.bitmap + t0 / 8 + x));
@@ -179,12 +195,9 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
                         sts8(stg + Stage<EB>::kVals + x, *reinterpret_cast<const uint8_t*>(p));
                 }
             }
-            if (lane == 0) {  // smem byte offset of the window start, and its value count
+            if (lane == 0)  // smem byte offset of the window start
                 asm volatile("st.shared.u32 [%0], %1;" ::"r"(stg + Stage<EB>::kSub + 64),
                              "r"(uint32_t(ws - as)) : "memory");
-                asm volatile("st.shared.u32 [%0], %1;" ::"r"(stg + Stage<EB>::kSub + 68),
-                             "r"(uint32_t(te - tp)) : "memory");
-            }
             __syncwarp();
             if (lane == 0) mbar_arrive(full);
         }
@@ -210,11 +223,9 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
                 }
                 const uint32_t pc = __popc(word);
                 const uint32_t excl = warp_excl_scan_small(pc);
-                const unsigned long long tp = lds64(stg + Stage<EB>::kSub);
                 const int sub = wfirst / kSubElems;  // this warp's 1024-element offset entry
-                const unsigned long long sw = lds64(stg + Stage<EB>::kSub + 8 * sub);
                 const uint32_t off = lds32(stg + Stage<EB>::kSub + 64);
-                uint32_t rel = uint32_t(sw - tp);
+                uint32_t rel = lds32(stg + Stage<EB>::kSub + 4 * sub);  // validated by the producer
                 if (kWarpElems < kSubElems && (wfirst % kSubElems)) {
                     // second half of a 1024-element entry: skip the values of the first half
                     // (its words precede ours and are always complete)
@@ -222,15 +233,6 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
                     for (int k = lane; k < (wfirst % kSubElems) / 32; k += 32)
                         pw += __popc(lds32(stg + Stage<EB>::kBm + (sub * 32 + k) * 4));
                     rel += __reduce_add_sync(0xffffffffu, pw);
-                }
-                if (T.idx) {  // a caller's index may be inconsistent: stay inside the staged window
-                    const uint32_t wcount = lds32(stg + Stage<EB>::kSub + 68);
-                    const uint32_t wtotal = __shfl_sync(0xffffffffu, excl + pc, 31);
-                    if (sw < tp || wtotal > wcount || rel > wcount - wtotal) {
-                        if (lane == 0) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
-                        rel = 0;
-                        if (wtotal > wcount) word = 0;  // nothing valid to place
-                    }
                 }
                 const uint32_t vbase = stg + Stage<EB>::kVals + off + rel * EB;
                 uint8_t* out = T.dst + (t0 + wfirst) * OB;

@@ -242,6 +242,19 @@ def test_chunked_1024_index_errors_are_safe(E):
             E.decompress_chunked(t, E.RankIndex(1024, bad))
         except E.CorruptionError:
             pass
+    # adversarial but validation-passing indices: monotone, <= 1024 values per
+    # sub-tile, last entry right -- wrong starts inside / past the windows read
+    # garbage (as the reference would) but never outside the staged buffers
+    rng = np.random.default_rng(3)
+    for trial in range(20):
+        bad = good.prefix.clone().cpu().numpy().astype(np.int64)
+        for k in range(1, len(bad) - 1):
+            lo, hi = bad[k - 1], min(bad[k - 1] + 1024, bad[k + 1])
+            bad[k] = int(rng.integers(lo, hi + 1))
+        try:
+            E.decompress_chunked(t, E.RankIndex(1024, torch.from_numpy(bad).cuda()))
+        except E.CorruptionError:
+            pass
     # and the device is still healthy afterwards
     assert E.decompress_chunked(t, good).bytes() == w.tobytes()
 

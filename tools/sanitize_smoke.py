@@ -67,6 +67,19 @@ for (rows, cols, eb, zf, off) in [(2, 2, 2, 0.5, 0), (37, 1000, 2, 0.5, 2), (64,
         E.decompress_dequant(q)                                                    # fused dequant expand
     checks += 1
 
+# adversarial, validation-passing 1024 indices (garbage allowed, out-of-bounds not)
+wa, ta = tensor(64, 4096, 2, 5, 0.5, 2)
+ga = E.build_rank_index(ta.bitmap, 1024).prefix.cpu().numpy().astype(np.int64)
+rng = np.random.default_rng(0)
+for _ in range(5):
+    bad = ga.copy()
+    for k in range(1, len(bad) - 1):
+        bad[k] = int(rng.integers(bad[k - 1], min(bad[k - 1] + 1024, bad[k + 1]) + 1))
+    try:
+        E.decompress_chunked(ta, E.RankIndex(1024, torch.from_numpy(bad).to(dev)))
+    except E.CorruptionError:
+        pass
+
 # the fused GEMV's set-bit consumer (density <= 0.2), odd value offset
 w9, t9 = tensor(48, 4096, 2, 99, 0.9, 3)
 x9 = (torch.rand(4096, device=dev) * 2 - 1).half()
