@@ -37,7 +37,7 @@ namespace endor_b200 {
 // persistent TMA kernel (batched over whole tensors)
 // ---------------------------------------------------------------------------
 #ifndef ENDOR_TMA_STAGES
-#define ENDOR_TMA_STAGES 6  // 6 x 17.6 KB ring = 2 CTAs/SM; measured best of 2..12 (profiles/r01)
+#define ENDOR_TMA_STAGES 5  // 5 x 17.6 KB ring = 2 CTAs/SM; re-measured after the consumer-check removal: 4 / 5 / 6 / 7 stages -> 3590 / 3950 / 3904 / 3115 dense-GB/s
 #endif
 constexpr int kStages = ENDOR_TMA_STAGES;
 constexpr int kTmaThreads = (kConsumerWarps + 1) * 32;  // consumers + 1 producer warp
