@@ -13,12 +13,14 @@
 //   branch-free, for any byte alignment of the values stream.
 //
 // expand_tma_kernel (the hot path): persistent, warp-specialised.  One
-// producer warp streams each 8192-element tile's bitmap (1 KiB), its eight
-// sub-tile offsets and its packed-values window into a 6-stage shared-memory
-// ring with 1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx); eight
-// consumer warps each expand one 1024-element sub-tile per tile, fully
-// independently, and write dense rows with coalesced 16-byte stores.  HBM
-// traffic per element: 1/8 (bitmap) + (1-s)*eb (values) read, eb written.
+// producer warp streams each 8192-element tile's bitmap (1 KiB) and its
+// packed-values window into a 5-stage shared-memory ring with 1-D TMA bulk
+// copies (cp.async.bulk + mbarrier complete_tx), and stages the tile's eight
+// sub-tile starts (validated, relative to the window); eight consumer warps
+// each expand one 1024-element sub-tile per tile, fully independently and
+// with no checks on their critical path, and write dense rows with coalesced
+// 16-byte stores.  HBM traffic per element: 1/8 (bitmap) + (1-s)*eb (values)
+// read, eb written.
 //
 // expand_kernel (fallback): one CTA per tile, plain loads; used for
 // decompress_chunk_into's partial ranges and bitmaps that are not 16-byte
