@@ -44,6 +44,7 @@ sys.path.insert(0, ROOT)
 METRIC = "Endor decompress dense-GB/s/GPU; offloaded OPT-66B layer ms at 1-8 B200"
 UNIT = "GB/s"
 SPARSITY = 0.5
+WORKLOAD = "opt-66b decoder layer (q,k,v,out 9216^2; fc1 9216x36864; fc2 36864x9216) f16 @50% unstructured"
 PCIE_GEN5_X16_GBS = 63.0
 
 
@@ -164,21 +165,25 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 def build_shards(E, catalog, rank, world, dev):
-    """Generate this rank's row shards of layers 0..world-1 on the device with
-    the bit-exact synth/prune/compress kernels.  Returns a list of dicts."""
+    """This rank's row shards of layers 0..world-1: every whole matrix is
+    generated and compressed on the device (bit-exact synth/prune/compress
+    kernels), then the rank's shard is SLICED out of the compressed tensor --
+    bitmap bits [r0 C, r1 C), values [rank(r0 C), rank(r1 C)) -- into its own
+    buffers, as the per-GPU transfer of that slice would deliver it
+    (shard.shard_tensor; no re-compression).  Returns a list of dicts."""
     import torch
     from paper_2406_11674_b200 import shard as S
     spec = catalog.model_catalog("opt-66b")
     out = []
     for layer in range(world):
         for oi, op in enumerate(spec.ops):
+            sh = S.row_shard(op.rows, op.cols, rank, world)
             w = E.synth_weight(op.rows, op.cols, catalog.op_seed(layer, oi), device=dev)
             E.magnitude_prune(w, SPARSITY, inplace=True)
-            sh = S.row_shard(op.rows, op.cols, rank, world)
-            part = E.DenseMatrix(sh.rows, op.cols, E.Dtype.F16,
-                                 w.data[sh.r0 * op.cols * 2: sh.r1 * op.cols * 2])
-            t = E.compress(part)
-            del w, part
+            t = E.compress(w)
+            del w
+            if world > 1:
+                t = S.shard_tensor(t, sh, copy=True)
             out.append({"name": f"L{layer}.{op.name}[{sh.r0}:{sh.r1}]", "t": t, "rows": sh.rows,
                         "cols": op.cols, "n": sh.rows * op.cols, "nnz": t.nnz()})
         torch.cuda.empty_cache()
@@ -618,7 +623,7 @@ def run_ours(args):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16",
                 "data": "synthetic: reference synth_weight + magnitude_prune(0.5) (bit-exact on GPU), seeds 1000*layer+op",
-                "config": {"workload": "opt-66b decoder layer (q,k,v,out 9216^2; fc1 9216x36864; fc2 36864x9216) f16 @50% unstructured",
+                "config": {"workload": WORKLOAD,
                            "layers_per_step": world, "sharding": f"row-block x{world}",
                            "per_gpu_dense_bytes_per_step": dense_rank,
                            "per_gpu_compressed_bytes_per_step": comp_rank,
@@ -742,7 +747,7 @@ def run_reference(args):
     line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f16", "data": "synthetic (reference synth_weight + magnitude_prune 0.5)",
-            "config": {"workload": "opt-66b decoder layer f16 @50% unstructured", "layers_per_step": 1,
+            "config": {"workload": WORKLOAD, "layers_per_step": 1,
                        "parallelism": f"{threads} host threads"},
             "impl": "reference",
             "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads, "kind": kind,
@@ -752,6 +757,22 @@ def run_reference(args):
         if o["h"]:
             R.ref_tensor_free(o["h"])
     print(json.dumps(line), flush=True)
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(n: int, argv) -> int:
+    """Re-run this script as N ranks under torch.distributed.run (the same
+    launch the driver uses for N>1) and return the launcher's exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *argv]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.run(cmd, env=env).returncode
 
 
 def main():
@@ -764,8 +785,16 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the INT8 pipeline and fused-GEMV side measurements")
     args = ap.parse_args()
-    if args.warmup < 3 and args.impl == "ours":
-        pass  # the driver passes W >= 3; smaller values are allowed for profiling runs
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `bench.py --gpus N` outside a launcher: become the launcher -- one
+        # process per GPU under torchrun (NCCL rendezvous on 127.0.0.1); rank 0
+        # prints the single JSON line
+        sys.exit(relaunch(args.gpus, sys.argv[1:]))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        ap.error(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     if args.impl == "reference":
         run_reference(args)
     else:

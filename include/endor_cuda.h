@@ -169,9 +169,10 @@ int endor_cuda_popcount(const void* bitmap, uint64_t n, uint64_t* total_out, voi
 
 /* decompress_chunked (codec.hpp:205-216) with a device-resident RankIndex.
  * chunk_count must equal ceil(n/cs) (else CORRUPTION, codec.hpp:174-176).
- * cs == 1024: single-launch fast path, check_index semantics (see
- * endor_cuda_decompress_chunked_batch).  Other sizes: every prefix entry is
- * verified on device (a superset of check_index). */
+ * Any nonzero chunk size is accepted, as by the reference's RankIndex
+ * constructor (bitmap.hpp:104).  cs == 1024: single-launch fast path,
+ * check_index semantics (see endor_cuda_decompress_chunked_batch).  Other
+ * sizes: every prefix entry is verified on device (a superset of check_index). */
 int endor_cuda_decompress_chunked(const endor_tensor_view* t, uint64_t chunk_size,
                                   const uint64_t* prefix, uint64_t chunk_count, void* dense_out,
                                   void* ws, size_t ws_bytes, void* stream);
@@ -192,7 +193,9 @@ int endor_cuda_decompress_chunked_batch(const endor_tensor_view* views, const ui
 /* decompress_chunk_into (codec.hpp:191-201): writes exactly and only chunk
  * k's byte range of dense_out (which must hold the full dense matrix,
  * dense_out_bytes == n*eb, else INVALID_ARGUMENT; k >= chunk_count ->
- * BOUNDS).  Like check_index, verifies prefix[last] + tail popcount == nnz. */
+ * BOUNDS).  Like check_index, verifies prefix[last] + tail popcount == nnz.
+ * Any nonzero chunk size (chunk ranges may start and end inside a bitmap
+ * word; the neighbouring elements are never written). */
 int endor_cuda_decompress_chunk_into(const endor_tensor_view* t, uint64_t chunk_size,
                                      const uint64_t* prefix, uint64_t chunk_count, uint64_t k,
                                      void* dense_out, uint64_t dense_out_bytes, void* ws,

@@ -560,17 +560,17 @@ int endor_cuda_decompress_chunked(const endor_tensor_view* t, uint64_t cs, const
     uint64_t n;
     int eb, st;
     if ((st = check_view(t, &n, &eb))) return st;
-    // check_index (codec.hpp:170-176): the index must cover the bitmap
+    // check_index (codec.hpp:170-176): the index must cover the bitmap; any
+    // nonzero chunk size is a valid RankIndex (bitmap.hpp:104)
     const uint64_t chunks = (n == 0 || cs == 0) ? 0 : ceil_div(n, cs);
     if (cs == 0 || chunk_count != chunks) return fail(ENDOR_ERR_CORRUPTION, "rank index does not cover the bitmap");
-    if (!is_pow2_ge64(cs))
-        return fail(ENDOR_ERR_INVALID_ARGUMENT, "device RankIndex chunk sizes must be powers of two >= 64");
     if (n == 0) return ENDOR_OK;
     if (!prefix) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null prefix");
     if (!dense_out || !aligned(dense_out, 16))
         return fail(ENDOR_ERR_INVALID_ARGUMENT, "dense output must be non-null and 16-byte aligned");
     WsLayout L;
     if ((st = check_ws(ws, ws_bytes, n, &L))) return st;
+    const auto* idx = reinterpret_cast<const unsigned long long*>(prefix);
     if (cs == uint64_t(kSubElems) && aligned(t->bitmap, 16) && aligned(prefix, 16)) {
         // fast path: the index supplies every sub-tile offset -> one expand launch,
         // check_index's tail test inside it (codec.hpp:177-183)
@@ -578,10 +578,10 @@ int endor_cuda_decompress_chunked(const endor_tensor_view* t, uint64_t cs, const
         const uint64_t* pres[1] = {prefix};
         return endor_cuda_decompress_chunked_batch(t, pres, cs, outs, 1, ws, ws_bytes, stream);
     }
-    if (cs > uint64_t(kSubElems) && aligned(t->bitmap, 16)) {
-        // coarser index (the reference's default 4096, codec.hpp:19): count the
-        // bitmap once, check every index entry against the count tables, then
-        // the persistent TMA expand over the count tables
+    if (aligned(t->bitmap, 16)) {
+        // any other chunk size (the reference's default 4096, codec.hpp:19):
+        // count the bitmap once (total == nnz covers the tail test), check every
+        // index entry against the count tables, then the persistent TMA expand
         Batch b{};
         b.count = 1;
         b.check_total = 1;
@@ -597,16 +597,23 @@ int endor_cuda_decompress_chunked(const endor_tensor_view* t, uint64_t cs, const
         b.blk = L.blk;
         b.hdr = L.hdr;
         CK(launch_count(b, S(stream)));
-        CK(launch_verify_index(reinterpret_cast<const unsigned long long*>(prefix), chunks, cs, b, S(stream)));
+        CK(launch_verify_index(idx, chunks, cs, T.bitmap, n, b.tsub + T.sub0, b.blk + T.blk0,
+                               uint64_t(kCountSubs) * T.cbpc, b.hdr, S(stream)));
         CK(launch_expand_tma(b, eb, S(stream)));
         return ENDOR_OK;
     }
+    // bitmap not 16-byte aligned: general rank scan (tile offsets + flat
+    // 1024-element sub-tile ranks, total == nnz), entry check, plain expand
     ScanArgs a = scan_args(t->bitmap, n, 0, n, L);
     a.check_total = 1;
     a.expect_total = t->nnz;
-    a.cs = cs;
-    a.idx_in = reinterpret_cast<const unsigned long long*>(prefix);
-    return full_expand(t, n, eb, dense_out, L, a, S(stream));
+    a.tprefix = L.tprefix;
+    a.tsub = L.tsub;
+    CK(launch_scan(a, S(stream)));
+    CK(launch_verify_index(idx, chunks, cs, static_cast<const uint8_t*>(t->bitmap), n, L.tsub, nullptr, 0, L.hdr,
+                           S(stream)));
+    CK(launch_expand(expand_args(t, n, 0, n, dense_out, L), eb, S(stream)));
+    return ENDOR_OK;
 }
 
 int endor_cuda_decompress_chunked_batch(const endor_tensor_view* views, const uint64_t* const* prefixes,
@@ -652,6 +659,30 @@ int endor_cuda_decompress_chunked_batch(const endor_tensor_view* views, const ui
     return ENDOR_OK;
 }
 
+// Range [b, e) of a tensor with its first value at *base_dev: scan (masking
+// bits below b; b need not be word aligned) + the plain expand, writing
+// exactly the elements of [b, e).  check: verify base + popcount == nnz.
+static int range_expand(const endor_tensor_view* t, uint64_t n, int eb, uint64_t b, uint64_t e,
+                        const unsigned long long* base_dev, bool check, void* dst, const WsLayout& L,
+                        cudaStream_t s) {
+    const uint64_t b0 = b & ~uint64_t(31);
+    ScanArgs a = scan_args(t->bitmap, n, b0, e, L);
+    a.lo = b;
+    a.p0_ptr = base_dev;
+    a.tprefix = dst ? L.tprefix : nullptr;
+    if (check) {
+        a.check_total = 1;
+        a.expect_total = t->nnz;
+    }
+    CK(launch_scan(a, s));
+    if (dst) {
+        ExpandArgs x = expand_args(t, n, b0, e, dst, L);
+        x.lo = b;
+        CK(launch_expand(x, eb, s));
+    }
+    return ENDOR_OK;
+}
+
 int endor_cuda_decompress_chunk_into(const endor_tensor_view* t, uint64_t cs, const uint64_t* prefix,
                                      uint64_t chunk_count, uint64_t k, void* dense_out,
                                      uint64_t dense_out_bytes, void* ws, size_t ws_bytes,
@@ -664,34 +695,18 @@ int endor_cuda_decompress_chunk_into(const endor_tensor_view* t, uint64_t cs, co
     if (k >= chunk_count) return fail(ENDOR_ERR_BOUNDS, "chunk index out of range");  // codec.hpp:194
     if (dense_out_bytes != n * uint64_t(eb))  // codec.hpp:195-197
         return fail(ENDOR_ERR_INVALID_ARGUMENT, "destination buffer must hold the full dense matrix");
-    if (!is_pow2_ge64(cs))
-        return fail(ENDOR_ERR_INVALID_ARGUMENT, "device RankIndex chunk sizes must be powers of two >= 64");
     if (!prefix) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null prefix");
     if (!dense_out || !aligned(dense_out, 16))
         return fail(ENDOR_ERR_INVALID_ARGUMENT, "dense output must be non-null and 16-byte aligned");
     WsLayout L;
     if ((st = check_ws(ws, ws_bytes, n, &L))) return st;
     const auto* pre = reinterpret_cast<const unsigned long long*>(prefix);
-    const uint64_t last = chunk_count - 1;
+    const uint64_t last = chunk_count - 1;  // chunk_count >= 1 here (k < chunk_count)
     // check_index tail (codec.hpp:177-183): prefix[last] + popcount(last chunk) == nnz
-    if (k != last) {
-        ScanArgs c = scan_args(t->bitmap, n, last * cs, n, L);
-        c.p0_ptr = pre + last;
-        c.check_total = 1;
-        c.expect_total = t->nnz;
-        CK(launch_scan(c, S(stream)));
-    }
+    if (k != last && (st = range_expand(t, n, eb, last * cs, n, pre + last, true, nullptr, L, S(stream))))
+        return st;
     const uint64_t b = k * cs, e = (b + cs < n) ? b + cs : n;
-    ScanArgs a = scan_args(t->bitmap, n, b, e, L);
-    a.p0_ptr = pre + k;
-    a.tprefix = L.tprefix;
-    if (k == last) {
-        a.check_total = 1;
-        a.expect_total = t->nnz;
-    }
-    CK(launch_scan(a, S(stream)));
-    CK(launch_expand(expand_args(t, n, b, e, dense_out, L), eb, S(stream)));
-    return ENDOR_OK;
+    return range_expand(t, n, eb, b, e, pre + k, k == last, dense_out, L, S(stream));
 }
 
 int endor_cuda_compress(uint64_t rows, uint64_t cols, int32_t dtype, const void* dense,
@@ -963,18 +978,13 @@ int endor_cuda_decompress_chunk_into_host(uint64_t rows, uint64_t cols, int32_t 
     // check_index first (codec.hpp:193), exactly as the reference orders it
     const uint64_t chunks = (n == 0 || cs == 0) ? 0 : ceil_div(n, cs);
     if (cs == 0 || chunk_count != chunks) return fail(ENDOR_ERR_CORRUPTION, "rank index does not cover the bitmap");
-    if (!is_pow2_ge64(cs))
-        return fail(ENDOR_ERR_INVALID_ARGUMENT, "device RankIndex chunk sizes must be powers of two >= 64");
-    CK(s->prefix.need(chunk_count * 8 + 8));
-    CK(cudaMemcpy(s->prefix.p, prefix_host, chunk_count * 8, cudaMemcpyHostToDevice));
-    const uint64_t last = chunk_count - 1;
-    {
-        WsLayout L = ws_layout(s->ws.p, n);
-        ScanArgs c = scan_args(v.bitmap, n, last * cs, n, L);
-        c.p0_ptr = static_cast<const unsigned long long*>(s->prefix.p) + last;
-        c.check_total = 1;
-        c.expect_total = nnz;
-        CK(launch_scan(c, nullptr));
+    if (chunk_count) {  // the tail test runs only when there are chunks (codec.hpp:177)
+        if (!prefix_host) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null prefix");
+        CK(s->prefix.need(chunk_count * 8 + 8));
+        CK(cudaMemcpy(s->prefix.p, prefix_host, chunk_count * 8, cudaMemcpyHostToDevice));
+        const uint64_t last = chunk_count - 1;
+        ST(range_expand(&v, n, eb, last * cs, n, static_cast<const unsigned long long*>(s->prefix.p) + last, true,
+                        nullptr, ws_layout(s->ws.p, n), nullptr));
         ST(endor_cuda_sync_status(s->ws.p, nullptr));
     }
     if (k >= chunk_count) return fail(ENDOR_ERR_BOUNDS, "chunk index out of range");

@@ -167,6 +167,12 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
         "@!P bra WAIT_%=;\n}" ::"r"(bar), "r"(parity) : "memory");
 }
+// Orders this thread's generic-proxy shared-memory writes before later
+// async-proxy (TMA) accesses of the same bytes: the producers patch buffer
+// edges with st.shared into stage buffers a later cp.async.bulk overwrites.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 // 1-D TMA bulk copy global -> shared, completion counted on an mbarrier.
 // dst/src 16-byte aligned, bytes a multiple of 16.
 #ifndef ENDOR_BULK_EVICT_FIRST
@@ -206,6 +212,14 @@ __device__ __forceinline__ void latch_status(WsHeader* hdr, uint32_t code) {
 
 __device__ __forceinline__ uint32_t read_status(const WsHeader* hdr) {
     return *reinterpret_cast<const volatile uint32_t*>(&hdr->status);
+}
+
+// CTA-uniform view of the latched status: thread 0 reads it once and one
+// barrier broadcasts the answer, so a latch landing mid-read can never split
+// a CTA (warp-specialised kernels would otherwise leave a producer or its
+// consumers waiting on an mbarrier forever).  Call from every thread.
+__device__ __forceinline__ bool cta_error_latched(const WsHeader* hdr) {
+    return __syncthreads_or(threadIdx.x == 0 && read_status(hdr) != 0) != 0;
 }
 
 template <typename T>

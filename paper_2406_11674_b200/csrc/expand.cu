@@ -23,7 +23,8 @@
 // read, eb written.
 //
 // expand_kernel (fallback): one CTA per tile, plain loads; used for
-// decompress_chunk_into's partial ranges and bitmaps that are not 16-byte
+// decompress_chunk_into's partial ranges (which may start and end inside a
+// bitmap word at arbitrary chunk sizes) and bitmaps that are not 16-byte
 // aligned.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -73,7 +74,7 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t ntiles = b.ntiles;
 
-    if (read_status(b.hdr)) return;  // a latched error: write nothing
+    if (cta_error_latched(b.hdr)) return;  // a latched error: write nothing
     init_luts(tid);
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -200,6 +201,7 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
             if (lane == 0)  // smem byte offset of the window start
                 asm volatile("st.shared.u32 [%0], %1;" ::"r"(stg + Stage<EB>::kSub + 64),
                              "r"(uint32_t(ws - as)) : "memory");
+            if (bm_bulk != bm_bytes || vbulk != win) fence_proxy_async_smem();  // st.shared edges vs later TMA
             __syncwarp();
             if (lane == 0) mbar_arrive(full);
         }
@@ -260,7 +262,7 @@ __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandArgs a) {
     __shared__ uint32_t s_warp[kExpandThreads / 32];
     __shared__ __align__(16) uint8_t s_vals[kTileElems * EB + 64];
 
-    if (read_status(a.hdr)) return;  // a latched error: write nothing
+    if (cta_error_latched(a.hdr)) return;  // a latched error: write nothing
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     init_luts(tid);
     const uint64_t t0 = a.e0 + uint64_t(blockIdx.x) * kTileElems;
@@ -272,6 +274,8 @@ __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandArgs a) {
         wv = load_word32(a.bitmap, t0 / 32 + tid, a.nbytes);
         const int32_t rem = count - tid * 32;
         if (rem < 32) wv &= (1u << rem) - 1u;
+        const uint64_t bit0 = t0 + uint64_t(tid) * 32;
+        if (bit0 < a.lo) wv &= ~0u << (a.lo - bit0);  // bits before the range (scan masked them too)
     }
     const uint32_t pc = __popc(wv);
     const uint32_t incl = warp_incl_scan(pc, lane);
@@ -317,8 +321,9 @@ __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandArgs a) {
     if (wfirst < count) {
         const uint32_t off = uint32_t(wstart - astart);
         const uint32_t vb = smem_u32(s_vals) + off + (wexcl * EB);
+        const int32_t head = a.lo > t0 + wfirst ? int32_t(a.lo - (t0 + wfirst)) : 0;  // < 32
         expand_subtile<MODE, false>(wv, incl - pc, vb, a.dst + (t0 + wfirst) * OB,
-                                  min(count - wfirst, kSubElems), lane, a.scale, a.deq_fast != 0);
+                                  min(count - wfirst, kSubElems), lane, a.scale, a.deq_fast != 0, head);
     }
 }
 

@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kExpandThreads) extract_rows_kernel(RankTable 
     __shared__ uint32_t s_warp[kExpandThreads / 32];
     __shared__ unsigned long long s_base;
     __shared__ __align__(16) uint8_t s_vals[kTileElems * EB + 64];
-    if (read_status(hdr)) return;
+    if (cta_error_latched(hdr)) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     init_luts(tid);  // published by the __syncthreads in load_tile
     const uint64_t i = blockIdx.x / tiles_per_row, j = blockIdx.x % tiles_per_row;
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(256) extract_cols_kernel(RankTable rt, const u
     extern __shared__ uint32_t s_row[];  // [rpc * words] bits, then [rpc * words] exclusive popcounts
     __shared__ uint32_t s_warp[8];
     __shared__ unsigned long long s_base;
-    if (read_status(hdr)) return;
+    if (cta_error_latched(hdr)) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t r0 = uint64_t(blockIdx.x) * rpc;
     const uint32_t nr = uint32_t(umin64(rpc, rows - r0));

@@ -140,22 +140,25 @@ __device__ __forceinline__ uint4 gather_mode(uint32_t m, uint32_t a, float scale
     }
 }
 
-__device__ __forceinline__ void store_partial(uint8_t* p, uint4 q, uint32_t valid_bytes) {
+// bytes [lo_bytes, hi_bytes) of a 16-byte chunk (range ends)
+__device__ __forceinline__ void store_partial(uint8_t* p, uint4 q, uint32_t hi_bytes, uint32_t lo_bytes = 0) {
     const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
     for (uint32_t b = 0; b < 16; ++b)
-        if (b < valid_bytes) p[b] = uint8_t(qw[b >> 2] >> ((b & 3) * 8));
+        if (b >= lo_bytes && b < hi_bytes) p[b] = uint8_t(qw[b >> 2] >> ((b & 3) * 8));
 }
 
 // Expand one warp's 1024-element sub-tile.  word/excl: this lane's bitmap word
 // (bits past the range already cleared) and its exclusive popcount within the
 // warp; vbase: shared address of the sub-tile's first packed value.  Lane l
 // writes chunks l, l+32, .. so every store instruction covers 512 contiguous
-// bytes.  FULL: all 1024 elements valid (no bounds checks).
+// bytes.  FULL: all 1024 elements valid (no bounds checks).  head_elems:
+// leading elements that belong to another range (a chunk starting inside a
+// bitmap word, decompress_chunk_into at an arbitrary chunk size): not written.
 template <int MODE, bool FULL, int WE = 1024>
 __device__ __forceinline__ void expand_subtile(uint32_t word, uint32_t excl, uint32_t vbase,
                                                uint8_t* out, int32_t valid_elems, int lane,
-                                               float scale = 1.f, bool fast = true) {
+                                               float scale = 1.f, bool fast = true, int32_t head_elems = 0) {
     constexpr int IN = mode_in(MODE), OUT = mode_out(MODE);
     constexpr int EPC = 16 / OUT;             // output elements per 16-byte chunk
     constexpr int CPW = 32 / EPC;             // chunks per bitmap word (4 or 2)
@@ -171,14 +174,15 @@ __device__ __forceinline__ void expand_subtile(uint32_t word, uint32_t excl, uin
         const uint32_t m = (wd >> sh) & ((1u << EPC) - 1u);
         const uint32_t r = pre + __popc(wd & low);
         const int e = (32 * j + lane) * EPC;
-        if (!FULL && e >= valid_elems) continue;
+        if (!FULL && (e >= valid_elems || e + EPC <= head_elems)) continue;
         const uint4 q = gather_mode<MODE>(m, vbase + r * IN, scale, fast);
 #if ENDOR_STORE_CS
-        if (FULL || e + EPC <= valid_elems) __stcs(reinterpret_cast<uint4*>(o + j * 512), q);
+        if (FULL || (e + EPC <= valid_elems && e >= head_elems)) __stcs(reinterpret_cast<uint4*>(o + j * 512), q);
 #else
-        if (FULL || e + EPC <= valid_elems) *reinterpret_cast<uint4*>(o + j * 512) = q;
+        if (FULL || (e + EPC <= valid_elems && e >= head_elems)) *reinterpret_cast<uint4*>(o + j * 512) = q;
 #endif
-        else store_partial(o + j * 512, q, uint32_t(valid_elems - e) * OUT);
+        else store_partial(o + j * 512, q, uint32_t(min(valid_elems - e, EPC)) * OUT,
+                           uint32_t(max(head_elems - e, 0)) * OUT);
     }
 }
 

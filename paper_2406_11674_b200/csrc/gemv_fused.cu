@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kGvThreads, ENDOR_GV_MINB) gemv_fused_kernel(c
     const uint32_t st0 = sbase + 256;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-    if (read_status(b.hdr)) return;  // a latched error: write nothing
+    if (cta_error_latched(b.hdr)) return;  // a latched error: write nothing
     init_luts(tid);
     if (tid == 0) {
         for (int s = 0; s < kGvStages; ++s) {
@@ -270,6 +270,7 @@ __global__ void __launch_bounds__(kGvThreads, ENDOR_GV_MINB) gemv_fused_kernel(c
                     sts8(stg + kGvVals + uint32_t(p - as), *reinterpret_cast<const uint8_t*>(p));
                 for (uintptr_t p = (e1 > ws ? e1 : ws) + lane; p < we; p += 32)
                     sts8(stg + kGvVals + uint32_t(p - as), *reinterpret_cast<const uint8_t*>(p));
+                fence_proxy_async_smem();  // st.shared edges vs the TMA that later reuses the stage
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(full);

@@ -21,7 +21,9 @@ struct ScanArgs {
     const uint8_t* bitmap;
     uint64_t nbytes;         // ceil(n/8): readable bitmap bytes
     uint64_t n;              // tensor element count (padding check)
-    uint64_t e0, e1;         // bit range [e0, e1), e0 % 64 == 0
+    uint64_t e0, e1;         // bit range [e0, e1), e0 % 32 == 0
+    uint64_t lo;             // first counted bit (e0 <= lo < e0 + 32): bits below are masked out
+                             // (chunk ranges at arbitrary RankIndex chunk sizes); 0 = e0
     const unsigned long long* p0_ptr;  // base offset = *p0_ptr if set, else p0
     uint64_t p0;
     unsigned long long* tprefix;       // per-tile (relative to e0) offsets, or null
@@ -42,7 +44,8 @@ struct ExpandArgs {
     uint64_t nbytes;
     const uint8_t* values;
     uint64_t nnz;
-    uint64_t e0, e1;
+    uint64_t e0, e1;                    // tiles start at e0 (e0 % 32 == 0)
+    uint64_t lo;                        // first element written (e0 <= lo < e0 + 32); 0 = e0
     const unsigned long long* tprefix;  // per-tile offsets (fallback kernel)
     const unsigned long long* tsub;     // CTA-local sub-tile offsets from count_kernel (TMA kernel)
     const unsigned long long* blk;      // count-CTA bases, total at [nblk] (TMA kernel)
@@ -104,10 +107,13 @@ __host__ __device__ inline int batch_tensor_of_cblk(const Batch& b, uint32_t g) 
 // (ws_layout_caps capacities).
 void batch_plan(Batch& b, uint64_t* sub_total, uint64_t* blk_total, int count_ctas);
 cudaError_t launch_count(const Batch& b, cudaStream_t s);
-// check a caller's RankIndex (chunk cs > 1024, power of two) against the
-// count tables of b.t[0] (after launch_count); latches CORRUPTION
-cudaError_t launch_verify_index(const unsigned long long* idx, uint64_t chunks, uint64_t cs, const Batch& b,
-                                cudaStream_t s);
+// check every entry of a caller's RankIndex (any chunk size cs >= 1) against
+// ranks from a 1024-element sub-tile table: rank(1024 j) = (blk ? blk[j / spc]
+// : 0) + tsub[j] (count_kernel's two levels, or scan_kernel's flat tsub), plus
+// the popcount of the bits from the sub-tile start; latches CORRUPTION
+cudaError_t launch_verify_index(const unsigned long long* idx, uint64_t chunks, uint64_t cs, const uint8_t* bitmap,
+                                uint64_t n, const unsigned long long* tsub, const unsigned long long* blk,
+                                uint64_t spc, WsHeader* hdr, cudaStream_t s);
 cudaError_t launch_expand_tma(const Batch& b, int mode, cudaStream_t s);  // 1 i8, 2 f16, 3 dequant
 // fused decompress -> GEMV over a batch (f16, cols % 1024 == 0, part set per tensor),
 // then y[r] = sum of row r's cols/1024 segment partials in a fixed order

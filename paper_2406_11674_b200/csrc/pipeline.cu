@@ -46,12 +46,12 @@ struct endor_pipeline {
 };
 
 namespace {
-thread_local std::string p_err;
-
+// CUDA and argument errors go through the C ABI's last-error slot
+// (endor_cuda_last_error_string), like every other entry point
 int perr(cudaError_t e, const char* where) {
-    p_err = std::string(where) + ": " + cudaGetErrorString(e);
-    return ENDOR_ERR_CUDA;
+    return set_last_error(ENDOR_ERR_CUDA, (std::string(where) + ": " + cudaGetErrorString(e)).c_str());
 }
+int pbad(const char* what) { return set_last_error(ENDOR_ERR_INVALID_ARGUMENT, what); }
 #define PK(expr)                                             \
     do {                                                     \
         cudaError_t e_ = (expr);                             \
@@ -81,7 +81,7 @@ extern "C" {
 
 int endor_pipeline_create(int device_ordinal, uint64_t max_op_elems, int ring_depth,
                           endor_pipeline** out) {
-    if (!out || max_op_elems == 0) return ENDOR_ERR_INVALID_ARGUMENT;
+    if (!out || max_op_elems == 0) return pbad("null output or zero max_op_elems");
     auto* p = new (std::nothrow) endor_pipeline();
     if (!p) return ENDOR_ERR_CUDA;
     p->device = device_ordinal;
@@ -140,7 +140,7 @@ struct NvtxRange {
 }  // namespace
 
 int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops, int sync) {
-    if (!p || (nops > 0 && !ops)) return ENDOR_ERR_INVALID_ARGUMENT;
+    if (!p || (nops > 0 && !ops)) return pbad("null pipeline or ops");
     NvtxRange run_range("endor_pipeline_run");
     PK(cudaSetDevice(p->device));
     int st = ensure_events(p, nops);
@@ -152,10 +152,16 @@ int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops
         const int eb = op.dtype == ENDOR_DTYPE_F16 ? 2 : 1;     // packed-value bytes (H2D)
         const bool deq = (op.flags & 1) != 0;                    // i8 values -> f16 W
         const int ob = (op.dtype == ENDOR_DTYPE_F16 || deq) ? 2 : 1;  // dense bytes
-        if (n > p->max_elems || (op.dtype != ENDOR_DTYPE_F16 && op.dtype != ENDOR_DTYPE_I8) ||
-            (deq && op.dtype != ENDOR_DTYPE_I8))
-            return ENDOR_ERR_INVALID_ARGUMENT;
-        if ((op.x_dev || op.y_dev) && ob != 2) return ENDOR_ERR_INVALID_ARGUMENT;
+        if (op.rows && op.cols > UINT64_MAX / op.rows)
+            return set_last_error(ENDOR_ERR_SIZE, "matrix dimensions overflow the addressable element count");
+        if (n > p->max_elems) return pbad("op larger than the pipeline's max_op_elems");
+        if ((op.dtype != ENDOR_DTYPE_F16 && op.dtype != ENDOR_DTYPE_I8) || (deq && op.dtype != ENDOR_DTYPE_I8))
+            return pbad("unknown dtype, or dequant flag on a non-i8 op");
+        // values length vs bitmap size (codec.hpp:34-39) BEFORE any copy is
+        // enqueued: the staging slot holds at most max_op_elems values
+        if (op.nnz > n) return set_last_error(ENDOR_ERR_CORRUPTION, "values length does not match bitmap popcount");
+        if ((op.x_dev || op.y_dev) && ob != 2) return pbad("GEMV ops need an f16 (or dequantized) W");
+        if (!op.path && ((n && !op.bitmap_host) || (op.nnz && !op.values_host))) return pbad("null host buffer");
         auto& slot = p->slots[i % p->depth];
         const size_t bmb = (n + 7) / 8, vb = op.nnz * eb;
         // copy stream: wait until the slot's previous occupant was decompressed
@@ -167,7 +173,7 @@ int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops
             endor_file_info fi;
             if ((st = endor_file_probe(op.path, &fi))) return st;
             if (fi.rows != op.rows || fi.cols != op.cols || fi.dtype != op.dtype || fi.nnz != op.nnz)
-                return ENDOR_ERR_INVALID_ARGUMENT;
+                return pbad("op shape / dtype / nnz disagree with the file header");
             if (!p->reader && (st = endor_reader_create(p->device, 0, ENDOR_IO_AUTO, &p->reader))) return st;
             if ((st = endor_reader_read(p->reader, op.path, &fi, slot.bitmap, slot.values, 0, nullptr, 0, p->copy)))
                 return st;
@@ -224,7 +230,7 @@ int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops
 }
 
 int endor_pipeline_stats_get(endor_pipeline* p, endor_pipeline_stats* out) {
-    if (!p || !out) return ENDOR_ERR_INVALID_ARGUMENT;
+    if (!p || !out) return pbad("null pipeline or output");
     PK(cudaSetDevice(p->device));
     PK(cudaStreamSynchronize(p->compute));
     PK(cudaStreamSynchronize(p->copy));

@@ -192,26 +192,33 @@ void batch_plan(Batch& b, uint64_t* sub_total, uint64_t* blk_total, int count_ct
     *blk_total = blk;
 }
 
-// A caller's RankIndex at a chunk size > 1024 (e.g. kDefaultChunkSize 4096,
-// codec.hpp:19) checked entry by entry against count_kernel's two-level
-// table: idx[k] must equal rank(k * cs) (bitmap.hpp:121-131).
+// A caller's RankIndex at any chunk size (kDefaultChunkSize 4096,
+// codec.hpp:19, or any nonzero size the RankIndex constructor accepts,
+// bitmap.hpp:104) checked entry by entry: idx[k] must equal rank(k * cs)
+// (bitmap.hpp:121-131), read from a 1024-element sub-tile rank table plus the
+// popcount of the (< 1024) bits between the sub-tile start and k * cs.
 __global__ void __launch_bounds__(256) verify_index_kernel(const unsigned long long* __restrict__ idx,
-                                                           uint64_t chunks, uint64_t step,
+                                                           uint64_t chunks, uint64_t cs,
+                                                           const uint8_t* __restrict__ bitmap, uint64_t nbytes,
                                                            const unsigned long long* __restrict__ tsub,
                                                            const unsigned long long* __restrict__ blk,
                                                            uint64_t spc, WsHeader* hdr) {
     const uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (k >= chunks) return;
-    const uint64_t j = k * step;  // the chunk start's 1024-element sub-tile
-    if (idx[k] != blk[j / spc] + tsub[j]) latch_status(hdr, ENDOR_ERR_CORRUPTION);
+    const uint64_t p = k * cs, j = p / kSubElems;  // p < n: whole words below p exist
+    unsigned long long r = tsub[j] + (blk ? blk[j / spc] : 0ull);
+    uint64_t w = j * 32;
+    for (; (w + 1) * 32 <= p; ++w) r += __popc(load_word32(bitmap, w, nbytes));
+    if (p & 31) r += __popc(load_word32(bitmap, w, nbytes) & ((1u << (p & 31)) - 1u));
+    if (idx[k] != r) latch_status(hdr, ENDOR_ERR_CORRUPTION);
 }
 
-cudaError_t launch_verify_index(const unsigned long long* idx, uint64_t chunks, uint64_t cs, const Batch& b,
-                                cudaStream_t s) {
+cudaError_t launch_verify_index(const unsigned long long* idx, uint64_t chunks, uint64_t cs, const uint8_t* bitmap,
+                                uint64_t n, const unsigned long long* tsub, const unsigned long long* blk,
+                                uint64_t spc, WsHeader* hdr, cudaStream_t s) {
     if (chunks == 0) return cudaSuccess;
-    const BatchTensor& T = b.t[0];
-    verify_index_kernel<<<unsigned(ceil_div(chunks, 256)), 256, 0, s>>>(
-        idx, chunks, cs / kSubElems, b.tsub + T.sub0, b.blk + T.blk0, uint64_t(kCountSubs) * T.cbpc, b.hdr);
+    verify_index_kernel<<<unsigned(ceil_div(chunks, 256)), 256, 0, s>>>(idx, chunks, cs, bitmap, (n + 7) / 8, tsub,
+                                                                       blk, spc ? spc : 1, hdr);
     return cudaGetLastError();
 }
 
@@ -250,6 +257,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(ScanArgs a) {
         if (wi < wend) {
             v = load_word32(a.bitmap, wi, a.nbytes);
             const uint64_t bit0 = wi * 32;
+            if (bit0 < a.lo) v &= ~0u << (a.lo - bit0);  // below the range start (0 < lo - bit0 < 32)
             if (bit0 + 32 > a.e1) {
                 const uint32_t keep = uint32_t(a.e1 - bit0);  // 1..31
                 // Padding bits of the final byte must be zero (bitmap.hpp:78-84).

@@ -340,11 +340,17 @@ int endor_file_probe(const char* path, endor_file_info* out) {
         else {
             f.header_bytes = hdr;
             f.bitmap_offset = hdr;
-            f.bitmap_bytes = (f.rows * f.cols + 7) / 8;
+            const uint64_t n = f.rows * f.cols;
+            f.bitmap_bytes = n / 8 + ((n & 7) != 0);  // ceil(n/8) without the n + 7 wrap
             f.values_offset = hdr + f.bitmap_bytes;
-            f.values_bytes = f.nnz * eb;
-            f.file_bytes = f.values_offset + f.values_bytes + 4;
-            if (size < f.file_bytes) st = fmt_fail(ENDOR_FMT_TRUNCATED, "file shorter than declared layout");
+            // the declared layout must be addressable: an overflowing size can
+            // only describe a file longer than any file (the reference's cursor
+            // runs off the end: Truncated)
+            const bool wraps = f.nnz > UINT64_MAX / eb || f.values_offset < hdr ||
+                               f.nnz * eb > UINT64_MAX - f.values_offset - 4;
+            f.values_bytes = wraps ? 0 : f.nnz * eb;
+            f.file_bytes = wraps ? UINT64_MAX : f.values_offset + f.values_bytes + 4;
+            if (wraps || size < f.file_bytes) st = fmt_fail(ENDOR_FMT_TRUNCATED, "file shorter than declared layout");
             else if (size > f.file_bytes)
                 st = fmt_fail(ENDOR_FMT_MALFORMED, "trailing bytes after declared layout");
             else {

@@ -6,7 +6,7 @@ the same order; codec.hpp:21-23, bitmap.hpp:14-17) that row block is
 
   * a contiguous bitmap bit range [r0*C, r1*C) -- byte aligned when C % 8 == 0,
     4-byte aligned (what the kernels require) when C % 32 == 0 (every catalog
-    shape: C in {8192, 9216, 28672, 36864});
+    shape: C in {8192, 9216, 28672, 36864}); other widths are re-packed;
   * a contiguous values range [rank(r0*C), rank(r1*C)), rank = Bitmap::rank
     (bitmap.hpp:41).
 
@@ -75,25 +75,70 @@ def host_shard_slices(bitmap: np.ndarray, values: np.ndarray, eb: int, shard: Ro
     return bitmap[b0:b1], values[v0 * eb: v1 * eb], v1 - v0
 
 
-def shard_tensor(t, shard: RowShard):
-    """Device view of one row shard of an EndorTensor (codec.EndorTensor):
-    bitmap/values are slices of t's device buffers, value offsets come from
-    device popcounts of the bitmap prefix."""
+def device_rank(bitmap, bit: int) -> int:
+    """Bitmap::rank(bit) (bitmap.hpp:41) of a device bitmap (codec.Bitmap):
+    the device popcount of the whole bytes below `bit` plus the low bits of
+    the byte it falls in."""
+    import torch
+    from . import codec as E
+    if bit < 0 or bit > bitmap.size():
+        raise E.BoundsError("rank position past the bitmap")
+    full, rem = divmod(bit, 8)
+    r = E.Bitmap(full * 8, data=bitmap.data[:full]).count() if full else 0
+    if rem:
+        r += int(torch.bitwise_and(bitmap.data[full], (1 << rem) - 1).item()).bit_count()
+    return r
+
+
+def _bit_slice(data, b0: int, b1: int):
+    """Bits [b0, b1) of an LSB-first device byte array, re-packed from bit 0
+    (zero padding bits), for row shards whose bit range is not byte aligned."""
+    import torch
+    n = b1 - b0
+    lo, hi = b0 // 8, (b1 + 7) // 8
+    sh = torch.arange(8, device=data.device, dtype=torch.uint8)
+    bits = ((data[lo:hi].unsqueeze(1) >> sh) & 1).reshape(-1)[b0 - 8 * lo: b0 - 8 * lo + n]
+    pad = (-n) % 8
+    if pad:
+        bits = torch.cat([bits, torch.zeros(pad, dtype=torch.uint8, device=data.device)])
+    return (bits.reshape(-1, 8) << sh).sum(dim=1, dtype=torch.uint8) if n else bits[:0]
+
+
+def shard_tensor(t, shard: RowShard, copy: bool = False):
+    """One row shard of a device EndorTensor (codec.EndorTensor): its bitmap
+    bit range [r0*C, r1*C) and its values [rank(r0*C), rank(r1*C))
+    (bitmap.hpp:41, codec.hpp:21-23), sliced out of the whole compressed
+    tensor -- never recompressed.
+
+    copy=False returns views into t's buffers where the kernels accept them
+    (bitmap byte-aligned and 4-byte aligned; a view that is not 16-byte
+    aligned runs the plain fallback expand); copy=True (or a bit range that is
+    not byte aligned) gives the shard its own buffers, as a per-GPU transfer
+    of the slice would."""
     from . import codec as E
     if shard.cols != t.cols:
         raise ValueError("shard/tensor column mismatch")
-    b0, b1 = shard.bitmap_byte_range()
     eb = E.elem_bytes(t.dtype)
-
-    def rank(bit):
-        if bit == 0:
-            return 0
-        return E.Bitmap(bit, data=t.bitmap.data[: (bit + 7) // 8]).count() if bit % 8 == 0 else None
-
-    v0, v1 = rank(shard.bit_begin), rank(shard.bit_end)
-    bm = E.Bitmap(shard.bit_end - shard.bit_begin, data=t.bitmap.data[b0:b1])
-    vals = t.values[v0 * eb: v1 * eb]
-    return E.EndorTensor(shard.rows, shard.cols, t.dtype, bm, vals, validate=False, nnz=v1 - v0)
+    b0, b1 = shard.bit_begin, shard.bit_end
+    v0 = device_rank(t.bitmap, b0)
+    v1 = device_rank(t.bitmap, b1)
+    nbytes = (b1 - b0 + 7) // 8
+    byte_ok = b0 % 8 == 0
+    if byte_ok and not copy and (t.bitmap.data.data_ptr() + b0 // 8) % 4 == 0:
+        bm_data = t.bitmap.data[b0 // 8: b0 // 8 + nbytes]
+        if (b1 - b0) % 8:  # the last byte also holds the next shard's bits: clear them
+            bm_data = bm_data.clone()
+            bm_data[-1] &= (1 << ((b1 - b0) % 8)) - 1
+        vals = t.values[v0 * eb: v1 * eb]
+    else:
+        bm_data = E._alloc(nbytes, t.device)
+        bm_data.copy_(_bit_slice(t.bitmap.data, b0, b1) if not byte_ok or (b1 - b0) % 8
+                      else t.bitmap.data[b0 // 8: b0 // 8 + nbytes])
+        vals = E._alloc((v1 - v0) * eb, t.device)
+        vals.copy_(t.values[v0 * eb: v1 * eb])
+    bm = E.Bitmap(b1 - b0, data=bm_data)
+    return E.EndorTensor(shard.rows, shard.cols, t.dtype, bm, vals, validate=False, nnz=v1 - v0,
+                         negative_zero_collapsed=t.negative_zero_collapsed())
 
 
 def _gf2_times(mat: List[int], vec: int) -> int:
@@ -133,17 +178,40 @@ def crc32_combine(crc1: int, crc2: int, len2: int) -> int:
     return (crc1 ^ crc2) & 0xFFFFFFFF
 
 
+def _gather_into(out, inp, group):
+    """all_gather_into_tensor; under gloo (CPU collectives, e.g. ranks sharing
+    one GPU) CUDA buffers are staged through host memory."""
+    import torch.distributed as dist
+    if out.is_cuda and dist.get_backend(group) == "gloo":
+        o = out.cpu()
+        dist.all_gather_into_tensor(o, inp.cpu(), group=group)
+        out.copy_(o)
+    else:
+        dist.all_gather_into_tensor(out, inp, group=group)
+    return out
+
+
 def all_gather_dense(shard_dense, full_rows: int, group=None):
-    """Optional NCCL all-gather of dense row shards into the full matrix on
-    every rank (only when one device needs the whole dense W).  Shards must be
-    equal-sized (R % world == 0) for all_gather_into_tensor."""
+    """Optional all-gather (NCCL over NVLink) of dense row shards into the full
+    matrix on every rank -- only when one device needs the whole dense W
+    (SURVEY.md 8(e)).  Ragged shards (R % world != 0) are padded to the largest
+    shard for the collective and trimmed after.  Returns uint8 row-major bytes."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
-    out = torch.empty(full_rows * shard_dense.cols * (2 if int(shard_dense.dtype) == 0 else 1),
-                      dtype=torch.uint8, device=shard_dense.data.device)
-    dist.all_gather_into_tensor(out, shard_dense.data.contiguous(), group=group)
-    return out
+    row_bytes = shard_dense.cols * (2 if int(shard_dense.dtype) == 0 else 1)
+    shards = row_shards(full_rows, 1, world)
+    width = max(sh.rows for sh in shards) * row_bytes
+    dev = shard_dense.data.device
+    mine = shard_dense.data.reshape(-1)
+    if mine.numel() != width:
+        buf = torch.zeros(width, dtype=torch.uint8, device=dev)
+        buf[: mine.numel()] = mine
+        mine = buf
+    out = _gather_into(torch.empty(width * world, dtype=torch.uint8, device=dev), mine.contiguous(), group)
+    if all(sh.rows * row_bytes == width for sh in shards):
+        return out
+    return torch.cat([out[g * width: g * width + sh.rows * row_bytes] for g, sh in enumerate(shards)])
 
 
 def all_gather_y(y_shard, full_rows: int, group=None):
@@ -158,6 +226,5 @@ def all_gather_y(y_shard, full_rows: int, group=None):
     width = max(sh.rows for sh in shards)
     buf = torch.zeros(width, dtype=y_shard.dtype, device=y_shard.device)
     buf[: y_shard.numel()] = y_shard
-    out = torch.empty(width * world, dtype=y_shard.dtype, device=y_shard.device)
-    dist.all_gather_into_tensor(out, buf, group=group)
+    out = _gather_into(torch.empty(width * world, dtype=y_shard.dtype, device=y_shard.device), buf, group)
     return torch.cat([out[g * width: g * width + sh.rows] for g, sh in enumerate(shards)])

@@ -414,3 +414,68 @@ def test_concurrent_host_threads_disjoint_chunks(E):
     torch.cuda.synchronize()
     assert not errs
     assert buf.cpu().numpy().tobytes() == w.tobytes()
+
+
+def _host_prefix(bm, n, cs):
+    """RankIndex(cs, prefix) for ANY nonzero chunk size (the reference's
+    RankIndex constructor accepts it, bitmap.hpp:104; check_index and
+    scatter_range work with it, codec.hpp:132-216)."""
+    bits = np.unpackbits(np.asarray(bm, dtype=np.uint8), bitorder="little")[:n].astype(np.int64)
+    cum = np.concatenate([[0], np.cumsum(bits)])
+    return cum[np.arange(0, n, cs)]
+
+
+@pytest.mark.parametrize("cs", [1, 3, 31, 100, 1000, 1500, 2048, 4095, 5000, 9999])
+@pytest.mark.parametrize("eb", [1, 2])
+def test_arbitrary_chunk_sizes(E, cs, eb):
+    """decompress_chunked / decompress_chunk_into at chunk sizes that are not
+    powers of two (chunk ranges start and end inside bitmap words): output
+    == the reference's, every chunk writes exactly its own range (0xAB
+    sentinel, test_codec.cpp:181-200), a corrupted middle entry is rejected."""
+    rows, cols = 37, 613 if cs > 64 else 41
+    w = O.random_dense(rows, cols, eb, 900 + cs, 0.45)
+    bm, vals, nnz, _ = O.compress(w, rows, cols, eb)
+    t = make_tensor(E, rows, cols, eb, bm, vals, nnz)
+    n = rows * cols
+    pre = _host_prefix(bm, n, cs)
+    idx = E.RankIndex(cs, torch.from_numpy(pre).cuda())
+    assert E.decompress_chunked(t, idx).bytes() == w.tobytes()
+    # unaligned bitmap (plain scan + expand path)
+    ub = torch.zeros(len(bm) + 20, dtype=torch.uint8, device="cuda")[4:4 + len(bm)]
+    ub.copy_(torch.from_numpy(bm.copy()))
+    tu = E.EndorTensor(rows, cols, t.dtype, E.Bitmap(n, data=ub), t.values, validate=False, nnz=nnz)
+    assert E.decompress_chunked(tu, idx).bytes() == w.tobytes()
+    ks = list(range(idx.chunk_count()))
+    for k in (ks if len(ks) <= 24 else ks[:8] + ks[len(ks) // 2: len(ks) // 2 + 4] + ks[-8:]):
+        buf = torch.full((t.dense_bytes(),), 0xAB, dtype=torch.uint8, device="cuda")
+        E.decompress_chunk_into(t, idx, k, buf)
+        got = buf.cpu().numpy()
+        b, e = k * cs * eb, min((k + 1) * cs, n) * eb
+        assert (got[b:e] == w[b:e]).all(), k
+        assert (got[:b] == 0xAB).all() and (got[e:] == 0xAB).all(), k
+    full = torch.zeros(t.dense_bytes(), dtype=torch.uint8, device="cuda")
+    for k in reversed(ks):
+        E.decompress_chunk_into(t, idx, k, full)
+    assert full.cpu().numpy().tobytes() == w.tobytes()
+    if len(pre) > 2:
+        bad = pre.copy()
+        bad[len(pre) // 2] += 1
+        with pytest.raises(E.CorruptionError):
+            E.decompress_chunked(t, E.RankIndex(cs, torch.from_numpy(bad).cuda()))
+        bad_last = pre.copy()
+        bad_last[-1] += 1
+        with pytest.raises(E.CorruptionError):
+            E.decompress_chunk_into(t, E.RankIndex(cs, torch.from_numpy(bad_last).cuda()), 0, full)
+
+
+def test_empty_tensor_chunk_into_host_bounds(E):
+    """an empty tensor through the host-buffer chunk_into must raise
+    BoundsError (check_index passes with 0 chunks, codec.hpp:172-177,194), not
+    read before the prefix allocation."""
+    import ctypes as C
+    L = E._lib.lib()
+    dst = (C.c_uint8 * 1)()
+    st = L.endor_cuda_decompress_chunk_into_host(0, 5, 0, None, None, 0, 64, None, 0, 0, dst, 0)
+    assert st == 3, L.endor_cuda_last_error_string()  # ENDOR_ERR_BOUNDS
+    st = L.endor_cuda_decompress_chunk_into_host(4, 0, 1, None, None, 0, 4096, None, 0, 2, dst, 0)
+    assert st == 3

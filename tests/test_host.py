@@ -87,3 +87,26 @@ def test_crc32_combine_matches_zlib():
         part = m[sh.r0:sh.r1].tobytes()
         c = S.crc32_combine(c, zlib.crc32(part), len(part))
     assert c == zlib.crc32(m.tobytes())
+
+
+def test_bit_slice_repacks_any_offset():
+    """shard._bit_slice (rows whose bit range is not byte aligned, cols % 8 != 0):
+    bits [b0, b1) re-packed LSB-first from bit 0 with zero padding bits."""
+    import numpy as np
+    import torch
+    from paper_2406_11674_b200 import shard as S
+    rng = np.random.default_rng(3)
+    raw = rng.integers(0, 256, 200, dtype=np.uint8)
+    bits = np.unpackbits(raw, bitorder="little")
+    for b0, b1 in [(0, 0), (0, 13), (3, 3), (5, 77), (8, 64), (13, 1599), (1590, 1600), (7, 8)]:
+        got = S._bit_slice(torch.from_numpy(raw), b0, b1).numpy()
+        want = np.packbits(bits[b0:b1], bitorder="little")
+        assert got.tobytes() == want.tobytes(), (b0, b1)
+
+
+def test_row_shards_cover_rows_exactly():
+    from paper_2406_11674_b200 import shard as S
+    for rows, world in [(1, 8), (5, 8), (9216, 8), (1023, 3)]:
+        sh = S.row_shards(rows, 7, world)
+        assert sh[0].r0 == 0 and sh[-1].r1 == rows
+        assert all(a.r1 == b.r0 for a, b in zip(sh, sh[1:]))

@@ -94,6 +94,19 @@ def test_probe_rejects_each_header_corruption(L, tmp_path, mutate, kind):
     assert st == 7 and k == KIND[kind]
 
 
+def test_probe_rejects_layout_sizes_that_wrap(L, tmp_path):
+    """rows=2^31, cols=2^32, nnz=2^63-2^59 (quantized f16) makes
+    header + bitmap + values + crc wrap to 40 bytes; the reference's cursor
+    runs off the end (Truncated).  The probe must not report ~2^60-byte
+    sections for a 40-byte file."""
+    import struct
+    rows, cols, nnz = 1 << 31, 1 << 32, (1 << 63) - (1 << 59)
+    hdr = b"ENDR" + struct.pack("<HBB", 1, 0, 1) + struct.pack("<QQQ", rows, cols, nnz) + struct.pack("<f", 1.0)
+    for tail in (b"\0\0\0\0", b"\0" * 8):
+        st, k, info = probe_kind(L, tmp_path, hdr + tail)
+        assert st == 7 and k == KIND["Truncated"]
+
+
 # ---------------------------------------------------------------------------- GPU
 
 torch = pytest.importorskip("torch")
