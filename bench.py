@@ -413,8 +413,7 @@ def run_ours(args):
         ref_dense = shards[-1]["dense"][: shards[-1]["n"] * 2].view(torch.float16).reshape(shards[-1]["rows"], -1)
         E.decompress(shards[-1]["t"], out=E.DenseMatrix(shards[-1]["rows"], shards[-1]["cols"], E.Dtype.F16,
                                                         shards[-1]["dense"][: shards[-1]["n"] * 2]))
-        yref = (ref_dense.float() @ hops[-1].x.float()).cpu()
-        gemv_err = float((hops[-1].y_host - yref).abs().max() / (yref.abs().max() + 1e-12))
+        gemv_err = gemv_errors(hops[-1].y_host, ref_dense, hops[-1].x)
         torch.cuda.synchronize()
         barrier()
         ops_all = hops * args.steps
@@ -464,7 +463,7 @@ def run_ours(args):
                                   "gemv_ms_per_step": round(sm_["gemv_ms"] / args.steps, 4),
                                   "exposed_compute_ms_per_run": round(mat_exposed, 4),
                                   "note": "decompress to a dense W ring, then dense GEMV (flags bit1)"},
-               "gemv_max_rel_err": gemv_err,
+               "gemv_error": gemv_err,
                "api": "endor_pipeline_run (C ABI), pinned host buffers; each op y = W x by the fused "
                       "decompress -> GEMV kernel (W never in HBM)",
                "clocks": clk2.summary()}
@@ -604,14 +603,14 @@ def run_ours(args):
                  "note": "y = W x for the layer's six shards; fused (one batched call, load-time 1024 RankIndex) "
                          "never writes W: 1/8 + 2(1-s) B per weight read vs 5.125 for decompress + GEMV"}
         E.check(L.endor_cuda_sync_status(fws.data_ptr(), sp))
-        # the fused y must equal the split path's y within fp32 rounding
+        # the fused y, element-wise against a float64 GEMV over each (bit-exact) dense shard
         run_fused()
         torch.cuda.synchronize()
-        ysplit = [y.clone() for y in ys]
-        run_split()
-        torch.cuda.synchronize()
-        fused["max_rel_diff_vs_split"] = max(float((a - b).abs().max() / (b.abs().max() + 1e-12))
-                                             for a, b in zip(ysplit, ys))
+        errs = [gemv_errors(y, s["out"].data.view(torch.float16).reshape(s["rows"], s["cols"]), x)
+                for s, x, y in zip(shards, xs, ys)]
+        fused["gemv_error"] = {"max_err_over_sum_abs": max(e["max_err_over_sum_abs"] for e in errs),
+                               "max_rel_err_well_conditioned": max(e["max_rel_err_well_conditioned"] for e in errs),
+                               "within_1e-3": all(e["within_1e-3"] for e in errs), "tensors": len(errs)}
 
     # ---- CPU baseline (rank 0, N == 1): the reference's own decompress ---------------------
     cpu = None
@@ -637,6 +636,23 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def gemv_errors(y, W, x):
+    """North star GEMV tolerance, element-wise: per row |y - y_ref| / sum_j
+    |W_ij x_j| and, on rows not dominated by cancellation (|y_ref| >= 0.1 of
+    that sum), |y - y_ref| / |y_ref|; y_ref in float64 on the device."""
+    import torch
+    Wd, xd = W.double(), x.double().to(W.device)
+    ref = Wd @ xd
+    mag = Wd.abs() @ xd.abs()
+    err = (y.to(W.device).double() - ref).abs()
+    good = ref.abs() >= 0.1 * mag
+    out = {"max_err_over_sum_abs": float((err / mag.clamp_min(1e-30)).max()),
+           "max_rel_err_well_conditioned": float((err[good] / ref[good].abs()).max()) if bool(good.any()) else 0.0,
+           "rows": int(ref.numel()), "well_conditioned_rows": int(good.sum())}
+    out["within_1e-3"] = out["max_err_over_sum_abs"] <= 1e-3 and out["max_rel_err_well_conditioned"] <= 1e-3
+    return out
 
 
 def cpu_baseline_from_device(shards):

@@ -54,3 +54,30 @@ def cuda_lib():
         pytest.skip("no CUDA device")
     from paper_2406_11674_b200 import _lib
     return _lib.lib()
+
+
+def gemv_check(y, W, x, tol=1e-3):
+    """North star GEMV tolerance, element-wise:
+    every row r satisfies |y_r - y_ref_r| <= tol * sum_j |W_rj x_j| (the
+    conditioning of that dot product), and rows whose |y_ref_r| is not
+    dominated by cancellation (|y_ref_r| >= 0.1 sum_j |W_rj x_j|) also satisfy
+    the plain relative bound |y_r - y_ref_r| <= tol * |y_ref_r|.  y_ref is the
+    float64 product over the same f16 W and x.  Returns (max error/mag,
+    max relative error over well-conditioned rows)."""
+    import torch
+    y = y.detach().double().cpu().reshape(-1)
+    Wd = W.detach().cpu().double()
+    xd = x.detach().cpu().double().reshape(-1)
+    ref = Wd @ xd
+    mag = Wd.abs() @ xd.abs()
+    err = (y - ref).abs()
+    finite = torch.isfinite(ref)
+    assert torch.equal(torch.isfinite(y), finite), "non-finite pattern differs from the reference"
+    err, ref, mag = err[finite], ref[finite], mag[finite]
+    bound = tol * mag + 1e-30
+    bad = err > bound
+    assert not bad.any(), f"{int(bad.sum())} rows exceed {tol} * sum|W x|; worst {float((err / bound).max())}"
+    good = ref.abs() >= 0.1 * mag
+    rel = (err[good] / ref[good].abs()).max().item() if good.any() else 0.0
+    assert rel <= tol, f"per-element relative error {rel} > {tol}"
+    return float((err / (mag + 1e-30)).max()) if err.numel() else 0.0, rel

@@ -9,10 +9,12 @@ density ramp 0 -> 100 %, and a single set element.  Each is checked
 bit-exact for decompress (count + TMA expand), decompress_chunked at chunk
 1024 (single launch) and 4096 (coarse index), extract_rows / extract_cols,
 and the fused decompress -> GEMV against an fp32 GEMV over the dense matrix
-(north star tolerance 1e-3 relative).
+(north star tolerance 1e-3 relative, element-wise: conftest.gemv_check).
 """
 import numpy as np
 import pytest
+
+from conftest import gemv_check  # noqa: E402
 
 torch = pytest.importorskip("torch")
 
@@ -77,7 +79,5 @@ def test_density_pattern(cuda_lib, name, w):
     csel = sorted({0, 1, 8191, 8192, COLS // 3, COLS - 1} | set(range(100, COLS, 97)))
     assert E.extract_cols(t, csel).bytes() == np.ascontiguousarray(w[:, csel]).tobytes(), name
     x = (torch.rand(COLS, device="cuda", generator=torch.Generator("cuda").manual_seed(2)) * 2 - 1).half()
-    dense = torch.from_numpy(w.view(np.float16).astype(np.float32)).cuda()
-    ref = dense @ x.float()
     y = E.gemv_compressed(t, x)
-    assert (y - ref).abs().max().item() <= 1e-3 * ref.abs().max().item() + 1e-6, name
+    gemv_check(y, torch.from_numpy(np.ascontiguousarray(w).view(np.float16)), x)

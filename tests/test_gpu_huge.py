@@ -75,9 +75,13 @@ def test_f16_past_2p32(cuda_lib):
 
     x = (torch.rand(COLS, device="cuda", generator=torch.Generator("cuda").manual_seed(3)) * 2 - 1).half()
     y = E.gemv_compressed(t, x)
-    ref = E.gemv(w, x)
-    tol = 1e-3 * ref.abs().max().item() + 1e-6
-    assert (y - ref.float()).abs().max().item() <= tol
+    ref = E.gemv(w, x)  # the dense kernel over the same W: agree within fp32 rounding, per row
+    wabs = E.DenseMatrix(ROWS, COLS, E.Dtype.F16, w.data.view(torch.float16).abs().view(torch.uint8))
+    mag = E.gemv(wabs, x.abs())  # sum_j |W_ij x_j| (the row's conditioning), element-wise bound
+    assert ((y - ref).abs() <= 1e-3 * mag).all()
+    good = ref.abs() >= 0.1 * mag
+    assert ((y - ref)[good].abs() <= 1e-3 * ref[good].abs()).all()
+    del wabs, mag
     del w, t, wb
     torch.cuda.empty_cache()
 
