@@ -647,7 +647,7 @@ def gemv_errors(y, W, x):
     ref = Wd @ xd
     mag = Wd.abs() @ xd.abs()
     err = (y.to(W.device).double() - ref).abs()
-    good = ref.abs() >= 0.1 * mag
+    good = (ref.abs() >= 0.1 * mag) & (mag > 0)
     out = {"max_err_over_sum_abs": float((err / mag.clamp_min(1e-30)).max()),
            "max_rel_err_well_conditioned": float((err[good] / ref[good].abs()).max()) if bool(good.any()) else 0.0,
            "rows": int(ref.numel()), "well_conditioned_rows": int(good.sum())}

@@ -4,6 +4,7 @@
 // fixtures.cu and gemv.cu.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <cstdio>
@@ -32,6 +33,14 @@ int fail(int code, const char* what) {
 int endor_b200::set_last_error(int code, const char* what) {
     g_last_error = what;
     return code;
+}
+
+bool endor_b200::pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("ENDOR_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
 }
 
 cudaError_t endor_b200::kernel_slots(const void* fn, int threads, size_t smem, int* blocks_per_sm, int* sms) {

@@ -23,9 +23,18 @@ constexpr int kScanWarpWords = 32 * kScanWordsPerLane;                   // 512
 constexpr int kScanBlockWords = (kScanThreads / 32) * kScanWarpWords;    // 4096
 constexpr uint64_t kScanBlockBits = uint64_t(kScanBlockWords) * 32;     // 131072
 
-// count_kernel (hot path): 32 KiB count blocks = 256 sub-tiles of 1024 bits.
-constexpr int kCountBlockWords = 8192;
-constexpr int kCountSubs = kCountBlockWords / 32;  // 256
+// count_kernel (hot path): count blocks of kCountBlockWords u32 words
+// (16 KiB = 128 sub-tiles of 1024 bits), streamed through a kCountStages-deep
+// TMA ring per CTA (3 blocks in flight while one is counted).
+#ifndef ENDOR_COUNT_BLOCK_WORDS
+#define ENDOR_COUNT_BLOCK_WORDS 4096
+#endif
+#ifndef ENDOR_COUNT_STAGES
+#define ENDOR_COUNT_STAGES 4
+#endif
+constexpr int kCountBlockWords = ENDOR_COUNT_BLOCK_WORDS;
+constexpr int kCountSubs = kCountBlockWords / 32;  // sub-tiles per count block
+constexpr int kCountStages = ENDOR_COUNT_STAGES;
 
 // ---- workspace ---------------------------------------------------------------
 // [0,256)                 WsHeader
@@ -41,6 +50,7 @@ struct WsHeader {
     unsigned long long total;   // last scan total (p0 + popcount of range)
     unsigned long long aux[4];
 };
+static_assert(sizeof(WsHeader) <= 256, "the workspace header occupies the first 256 bytes");
 
 struct WsLayout {
     WsHeader* hdr;
@@ -191,6 +201,17 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
         ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 #endif
 }
+
+// ---- programmatic dependent launch (PDL) ------------------------------------------
+// The hot-path kernels (count -> expand / fused GEMV -> row sum) are launched
+// with cudaLaunchAttributeProgrammaticStreamSerialization: a dependent grid's
+// CTAs start (launch latency, mbarrier / LUT prologue) while the previous
+// kernel drains, and block in pdl_wait() -- which returns once the previous
+// grid has completed and its memory is visible -- before reading anything it
+// produced (workspace tables, the latched status).  Without the attribute both
+// are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ---- device helpers ------------------------------------------------------------
 // Little-endian u32 bitmap word `w`; bytes at or past `nbytes` read as zero

@@ -39,11 +39,31 @@ namespace endor_b200 {
 // ---------------------------------------------------------------------------
 // persistent TMA kernel (batched over whole tensors)
 // ---------------------------------------------------------------------------
-#ifndef ENDOR_TMA_STAGES
-#define ENDOR_TMA_STAGES 5  // 5 x 17.6 KB ring = 2 CTAs/SM; re-measured after the consumer-check removal: 4 / 5 / 6 / 7 stages -> 3590 / 3950 / 3904 / 3115 dense-GB/s
+// One CTA per SM holding kPipes independent pipelines (a producer warp + 8
+// consumer warps + a kStages-deep ring each).  The SM's tiles -- tile
+// blockIdx.x + j * gridDim.x for j = 0, 1, .. -- are claimed one at a time
+// from a shared-memory counter by whichever producer is ready, so the two
+// pipelines finish within a few tiles of each other.  (Two independent CTAs
+// per SM with a fixed half of the tiles each did not: the warp scheduler
+// favours the older CTA, which finished at 0.75x of the kernel time while
+// its neighbour ran alone for the rest, tools/cta_timing.py.)
+#ifndef ENDOR_TMA_PIPES
+#define ENDOR_TMA_PIPES 2
 #endif
+#ifndef ENDOR_TMA_STAGES
+#define ENDOR_TMA_STAGES 5  // per pipe: 5 x 17.6 KB (f16); 4 / 5 / 6 / 7 measured 3590 / 3950 / 3904 / 3115 dense-GB/s in r1
+#endif
+#ifndef ENDOR_TMA_BATCH
+#define ENDOR_TMA_BATCH 4  // tiles per claim (the two pipes end within about one claim of each other)
+#endif
+#ifndef ENDOR_TMA_LOOKAHEAD
+#define ENDOR_TMA_LOOKAHEAD 2  // claims in flight per producer: their index loads land meanwhile
+#endif
+constexpr int kPipes = ENDOR_TMA_PIPES;
 constexpr int kStages = ENDOR_TMA_STAGES;
-constexpr int kTmaThreads = (kConsumerWarps + 1) * 32;  // consumers + 1 producer warp
+constexpr int kLook = ENDOR_TMA_LOOKAHEAD;
+constexpr int kBatch = ENDOR_TMA_BATCH;
+constexpr int kTmaThreads = kPipes * (kConsumerWarps + 1) * 32;  // warps [0, kPipes) are the producers
 
 template <int EB>
 struct Stage {
@@ -59,38 +79,71 @@ struct Stage {
 // 8192-value window buffer.  A middle entry that passes but disagrees with the
 // bitmap yields garbage -- the reference's check_index does not look at middle
 // entries either (codec.hpp:170-184) -- never an out-of-bounds access.
+// header: [0, 256) mbarriers + claim counter; then per pipe kLook claims x
+// kBatch tile slots of 12 u64 (a claimed tile's index entries, via cp.async)
+constexpr uint32_t kSlotBytes = 12 * 8;
+constexpr uint32_t kTmaHeader = 256 + ((kPipes * kLook * kBatch * kSlotBytes + 127) & ~127u);
 template <int EB>
 constexpr uint32_t tma_smem_bytes() {
-    return 256 /* 2*kStages mbarriers */ + kStages * Stage<EB>::kBytes;
+    return kTmaHeader + kPipes * kStages * Stage<EB>::kBytes;
 }
+static_assert(2 * kPipes * kStages * 8 + 8 <= 256, "mbarrier area");
+static_assert(256 + kPipes * kLook * kSlotBytes <= kTmaHeader, "claim slot area");
+
+#ifdef ENDOR_CTA_TIMING  // development aid (tools/cta_timing.py): per-CTA start / end globaltimer
+__device__ unsigned long long g_cta_times[3 * 4096];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
 
 template <int MODE>
-__global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_constant__ Batch b) {
+__global__ void __launch_bounds__(kTmaThreads, 1) expand_tma_kernel(const __grid_constant__ Batch b) {
+#ifdef ENDOR_CTA_TIMING
+    if (threadIdx.x == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_cta_times[3 * blockIdx.x] = gtimer();
+        g_cta_times[3 * blockIdx.x + 2] = smid;
+    }
+#endif
     constexpr int EB = mode_in(MODE), OB = mode_out(MODE);  // packed-value / dense-element bytes
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t sbase = smem_u32(smem);
-    const uint32_t full0 = sbase, empty0 = sbase + 8 * kStages;
-    const uint32_t st0 = sbase + 256;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // pipe p: producer warp p, consumer warps kPipes + 8 p .. +7
+    const int pipe = warp < kPipes ? warp : (warp - kPipes) / kConsumerWarps;
+    const uint32_t full0 = sbase + 16 * kStages * pipe, empty0 = full0 + 8 * kStages;
+    const uint32_t claim = sbase + 16 * kStages * kPipes;  // shared u32 tile-claim counter
+    const uint32_t st0 = sbase + kTmaHeader + pipe * kStages * Stage<EB>::kBytes;
+    const uint32_t slot0 = sbase + 256 + pipe * kLook * kBatch * kSlotBytes;  // this pipe's claim slots
     const uint64_t ntiles = b.ntiles;
+    // this CTA's tiles: blockIdx.x + j * gridDim.x, j < nj
+    const uint32_t nj = blockIdx.x < ntiles ? uint32_t((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0u;
 
-    if (cta_error_latched(b.hdr)) return;  // a latched error: write nothing
     init_luts(tid);
     if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(full0 + 8 * s, 2);                // producer: expect_tx arrive + fix-up arrive
-            mbar_init(empty0 + 8 * s, kConsumerWarps);  // one arrive per consumer warp
+        for (int s = 0; s < kPipes * kStages; ++s) {
+            mbar_init(sbase + 16 * kStages * (s / kStages) + 8 * (s % kStages), 2);  // expect_tx + fix-up
+            mbar_init(sbase + 16 * kStages * (s / kStages) + 8 * kStages + 8 * (s % kStages), kConsumerWarps);
         }
+        asm volatile("st.shared.u32 [%0], 0;" ::"r"(claim) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncthreads();
+    pdl_wait();  // the prologue above overlapped the previous kernel's tail
+    // a latched error: write nothing (the barrier inside also publishes the
+    // LUTs, the claim counter and the mbarrier initialisation)
+    if (cta_error_latched(b.hdr)) return;
+    pdl_launch_dependents();
 
-    if (warp == kConsumerWarps) {
-        // ================= producer warp =================
-        constexpr uint32_t kSubsPerBlk = kCountSubs;  // 256 sub-tiles per count block
+    if (warp < kPipes) {
+        // ================= producer warp of pipe `pipe` =================
+        constexpr uint32_t kSubsPerBlk = kCountSubs;  // sub-tiles per count block
         // check_index's tail test (codec.hpp:177-183) for caller-indexed tensors:
         // idx[last] + popcount(last chunk) == nnz, plus the padding bits
-        if (blockIdx.x == 0) {
+        if (blockIdx.x == 0 && pipe == 0) {
             for (int k = 0; k < b.count; ++k) {
                 const BatchTensor& T = b.t[k];
                 if (!T.idx) continue;
@@ -110,17 +163,44 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
                 if (lane == 0 && T.idx[last] + tail != T.nnz) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
             }
         }
-        // Global tile t's absolute value window [s0, s1) and its nine sub-tile
-        // starts relative to s0 (rel[8] = s1 - s0): the caller's RankIndex --
-        // validated here, so the consumers need no checks -- or count_kernel's
-        // two levels (a tile never straddles two count CTAs' ranges).
-        auto entries = [&](uint64_t t, unsigned long long& s0, uint32_t* rel) {
+        // Tile t's absolute value window [s0, s1) and its nine sub-tile starts
+        // relative to s0 (rel[8] = s1 - s0): the caller's RankIndex -- validated
+        // here, so the consumers need no checks -- or count_kernel's two levels
+        // (a tile never straddles two count CTAs' ranges).
+        //
+        // Tiles are claimed kBatch at a time (SM-local indices j, tile =
+        // blockIdx.x + j * gridDim.x) from the shared counter; lane k < kBatch
+        // fetches tile k's index entries with cp.async (global -> shared, no
+        // registers: register scoreboards are per warp, so loads into one
+        // register for successive claims would serialise on each other) into
+        // its slot of the claim, one commit group per claim, and the claim is
+        // issued kLook claims later after cp.async.wait_group(kLook - 1).
+        auto tile_of = [&](uint32_t j) -> uint64_t { return j < nj ? blockIdx.x + uint64_t(j) * gridDim.x : ntiles; };
+        auto fetch = [&](uint32_t slot, uint64_t t) {  // one lane per tile; t < ntiles
+            const BatchTensor& T = b.t[batch_tensor_of_tile(b, t)];
+            const uint64_t lt = t - T.tile0, nsub = ceil_div(T.n, kSubElems), a = lt * 8;
+            auto cp8 = [&](int k, const unsigned long long* src) {
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(slot + 8 * k), "l"(src) : "memory");
+            };
+            if (T.idx) {
+#pragma unroll
+                for (int k = 0; k <= 8; ++k)
+                    if (a + k < nsub) cp8(k, T.idx + a + k);
+            } else {
+                const uint64_t spc = uint64_t(kSubsPerBlk) * T.cbpc;  // one count CTA's range
+#pragma unroll
+                for (int k = 0; k <= 8; ++k)
+                    if (a + k < nsub) cp8(k, b.tsub + T.sub0 + a + k);
+                cp8(9, b.blk + T.blk0 + a / spc);                           // base of entries 0..7
+                if (a + 8 < nsub) cp8(10, b.blk + T.blk0 + (a + 8) / spc);  // base of entry 8
+                cp8(11, b.blk + T.blk0 + T.ncta);                           // total
+            }
+        };
+        auto finish = [&](uint32_t slot, uint64_t t, unsigned long long& s0, uint32_t* rel) {  // one lane per tile
             const BatchTensor& T = b.t[batch_tensor_of_tile(b, t)];
             const uint64_t lt = t - T.tile0, nsub = ceil_div(T.n, kSubElems), a = lt * 8;
             unsigned long long e[9];
             if (T.idx) {
-#pragma unroll
-                for (int k = 0; k <= 8; ++k) e[k] = a + k < nsub ? T.idx[a + k] : T.nnz;
                 // monotone, within [0, nnz], at most 1024 values per sub-tile: clamp
                 // and latch (memory safety; an entry that passes but disagrees with
                 // the bitmap yields garbage like the reference)
@@ -128,39 +208,55 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
                 unsigned long long lo = 0;
 #pragma unroll
                 for (int k = 0; k <= 8; ++k) {
-                    unsigned long long v = e[k] < lo ? lo : (e[k] > T.nnz ? T.nnz : e[k]);
+                    const unsigned long long r = a + k < nsub ? lds64(slot + 8 * k) : T.nnz;
+                    unsigned long long v = r < lo ? lo : (r > T.nnz ? T.nnz : r);
                     if (k > 0 && v - lo > kSubElems) v = lo + kSubElems;
-                    bad |= v != e[k];
+                    bad |= v != r;
                     e[k] = lo = v;
                 }
                 if (bad) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
             } else {
-                const uint64_t spc = uint64_t(kSubsPerBlk) * T.cbpc;  // one count CTA's range
-                const unsigned long long* blk = b.blk + T.blk0;
-                const unsigned long long* tsub = b.tsub + T.sub0;
-                const unsigned long long base = blk[a / spc];
+                const unsigned long long b0 = lds64(slot + 72), tot = lds64(slot + 88);
 #pragma unroll
-                for (int k = 0; k < 8; ++k) e[k] = a + k < nsub ? base + tsub[a + k] : blk[T.ncta];
-                e[8] = a + 8 >= nsub ? blk[T.ncta] : blk[(a + 8) / spc] + tsub[a + 8];
+                for (int k = 0; k < 8; ++k) e[k] = a + k < nsub ? b0 + lds64(slot + 8 * k) : tot;
+                e[8] = a + 8 < nsub ? lds64(slot + 80) + lds64(slot + 64) : tot;
             }
             s0 = e[0];
 #pragma unroll
             for (int k = 0; k <= 8; ++k) rel[k] = uint32_t(e[k] - e[0]);
         };
-        unsigned long long tp_l = 0;  // lane k: tile i+k's window start ..
-        uint32_t rel_l[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // .. and its relative sub-tile starts
+        auto claim_batch = [&](uint32_t c) -> uint32_t {  // claim c's first j (lane-uniform), fetch its tiles
+            uint32_t j = 0;
+            if (lane == 0) asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(j) : "r"(claim), "n"(kBatch) : "memory");
+            j = __shfl_sync(0xffffffffu, j, 0);
+            const uint64_t t = tile_of(j + lane);
+            if (lane < kBatch && t < ntiles) fetch(slot0 + ((c % kLook) * kBatch + lane) * kSlotBytes, t);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            return j;
+        };
+        uint32_t qj[kLook];  // first j of the claims in flight, oldest first
+#pragma unroll
+        for (int k = 0; k < kLook; ++k) qj[k] = claim_batch(k);
         int i = 0, ti = 0;
-        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        for (uint32_t c = 0; qj[0] < nj; ++c) {
+            asm volatile("cp.async.wait_group %0;" ::"n"(kLook - 1) : "memory");
+            __syncwarp();
+            unsigned long long tp_l = 0;
+            uint32_t rel_l[9] = {};
+            const uint64_t tl = tile_of(qj[0] + lane);
+            if (lane < kBatch && tl < ntiles) finish(slot0 + ((c % kLook) * kBatch + lane) * kSlotBytes, tl, tp_l, rel_l);
+            __syncwarp();  // the slots are read before the claim below refills them
+#pragma unroll
+            for (int k = 0; k + 1 < kLook; ++k) qj[k] = qj[k + 1];
+            qj[kLook - 1] = claim_batch(c + kLook);
+            for (uint32_t own = 0; own < uint32_t(kBatch); ++own, ++i) {
+            const uint64_t t = __shfl_sync(0xffffffffu, tl, own);
+            if (t >= ntiles) break;
+            const unsigned long long tp = __shfl_sync(0xffffffffu, tp_l, own);
+            const unsigned long long te = tp + __shfl_sync(0xffffffffu, rel_l[8], own);
             const int s = i % kStages;
             const uint32_t stg = st0 + s * Stage<EB>::kBytes;
             const uint32_t full = full0 + 8 * s;
-            if ((i & 31) == 0) {  // one round trip fetches the next 32 tiles' entries
-                const uint64_t tl = t + uint64_t(lane) * gridDim.x;
-                if (tl < ntiles) entries(tl, tp_l, rel_l);
-            }
-            const int own = i & 31;  // the lane holding this tile's entries
-            const unsigned long long tp = __shfl_sync(0xffffffffu, tp_l, own);
-            const unsigned long long te = tp + __shfl_sync(0xffffffffu, rel_l[8], own);
             while (ti + 1 < b.count && t >= b.t[ti + 1].tile0) ++ti;
             const BatchTensor& T = b.t[ti];
             const uint64_t lt = t - T.tile0;
@@ -180,6 +276,9 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
                 mbar_arrive_expect_tx(full, bm_bulk + vbulk);
                 if (bm_bulk) bulk_g2s(stg + Stage<EB>::kBm, T.bitmap + t0 / 8, bm_bulk, full);
                 if (vbulk) bulk_g2s(stg + Stage<EB>::kVals + uint32_t(bs - as), reinterpret_cast<const void*>(bs), vbulk, full);
+                asm volatile("st.shared.u32 [%0], %1;" ::"r"(stg + Stage<EB>::kSub + 64),  // window start
+                             "r"(uint32_t(ws - as)) : "memory");
+                asm volatile("st.shared.u64 [%0], %1;" ::"r"(stg + Stage<EB>::kSub + 72), "l"(t) : "memory");
             }
             if (lane == own) {  // the 8 sub-tile starts, relative to the window start
                 asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(stg + Stage<EB>::kSub), "r"(rel_l[0]),
@@ -187,42 +286,57 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
                 asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(stg + Stage<EB>::kSub + 16),
                              "r"(rel_l[4]), "r"(rel_l[5]), "r"(rel_l[6]), "r"(rel_l[7]) : "memory");
             }
-            // edge bytes the bulk copies cannot move (ends of the buffers)
+            // edge bytes the bulk copies cannot move (the ends of the bitmap and of
+            // the values buffer): only the bytes outside [bs, be) are visited
+            bool edges = bm_bulk != bm_bytes;
             for (uint32_t x = bm_bulk + lane; x < bm_bytes; x += 32)
                 sts8(stg + Stage<EB>::kBm + x, __ldg(T.bitmap + t0 / 8 + x));
-            const uint32_t win = uint32_t(ae - as);
-            if (vbulk != win) {
-                for (uint32_t x = lane; x < win; x += 32) {
-                    const uintptr_t p = as + x;
-                    if (p >= vlo && p < vhi && !(p >= bs && p < be))
-                        sts8(stg + Stage<EB>::kVals + x, *reinterpret_cast<const uint8_t*>(p));
-                }
+            if (bs > ws || be < we) {
+                edges = true;
+                const uintptr_t h1 = vbulk ? bs : we, t1 = vbulk ? be : we;  // head [ws, h1), tail [t1, we)
+                for (uintptr_t p = ws + lane; p < h1 && p < we; p += 32)
+                    sts8(stg + Stage<EB>::kVals + uint32_t(p - as), *reinterpret_cast<const uint8_t*>(p));
+                for (uintptr_t p = (t1 > ws ? t1 : ws) + lane; p < we; p += 32)
+                    sts8(stg + Stage<EB>::kVals + uint32_t(p - as), *reinterpret_cast<const uint8_t*>(p));
             }
-            if (lane == 0)  // smem byte offset of the window start
-                asm volatile("st.shared.u32 [%0], %1;" ::"r"(stg + Stage<EB>::kSub + 64),
-                             "r"(uint32_t(ws - as)) : "memory");
-            if (bm_bulk != bm_bytes || vbulk != win) fence_proxy_async_smem();  // st.shared edges vs later TMA
+            if (edges) fence_proxy_async_smem();  // st.shared edges vs the TMA that later reuses the stage
             __syncwarp();
             if (lane == 0) mbar_arrive(full);
+            }
         }
-    } else {
-        // ================= consumer warps =================
-        int i = 0, ti = 0;
-        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        // end of work: a sentinel tile id releases the consumers
+        {
             const int s = i % kStages;
             const uint32_t stg = st0 + s * Stage<EB>::kBytes;
-            while (ti + 1 < b.count && t >= b.t[ti + 1].tile0) ++ti;  // tiles only move forward
+            if (i >= kStages) mbar_wait(empty0 + 8 * s, ((i / kStages) - 1) & 1);
+            if (lane == 0) {
+                asm volatile("st.shared.u64 [%0], %1;" ::"r"(stg + Stage<EB>::kSub + 72), "l"(~0ull) : "memory");
+                mbar_arrive(full0 + 8 * s);
+                mbar_arrive(full0 + 8 * s);
+            }
+        }
+    } else {
+        // ================= consumer warps of pipe `pipe` =================
+        const int cw = (warp - kPipes) % kConsumerWarps;
+        int ti = 0;
+        for (int i = 0;; ++i) {
+            const int s = i % kStages;
+            const uint32_t stg = st0 + s * Stage<EB>::kBytes;
+            mbar_wait(full0 + 8 * s, (i / kStages) & 1);
+            const uint64_t t = lds64(stg + Stage<EB>::kSub + 72);
+            if (t >= ntiles) break;  // the producer's end-of-work sentinel
+            while (ti + 1 < b.count && t >= b.t[ti + 1].tile0) ++ti;  // a pipe's tiles only move forward
             const BatchTensor& T = b.t[ti];
             const uint64_t t0 = (t - T.tile0) * kTileElems;
             const int32_t count = int32_t(umin64(kTileElems, T.n - t0));
-            mbar_wait(full0 + 8 * s, (i / kStages) & 1);
-            const int32_t wfirst = warp * kWarpElems;
+            const int32_t wfirst = cw * kWarpElems;
             if (wfirst < count) {
                 const int32_t valid = min(count - wfirst, kWarpElems);
                 const int32_t lbit = lane * 32;
                 uint32_t word = 0;
                 if (lane < kWarpWords && lbit < valid) {
-                    word = lds32(stg + Stage<EB>::kBm + (warp * kWarpWords + lane) * 4);
+                    word = lds32(stg + Stage<EB>::kBm + (cw * kWarpWords + lane) * 4);
                     if (valid - lbit < 32) word &= (1u << (valid - lbit)) - 1u;
                 }
                 const uint32_t pc = __popc(word);
@@ -251,6 +365,10 @@ __global__ void __launch_bounds__(kTmaThreads) expand_tma_kernel(const __grid_co
             if (lane == 0) mbar_arrive(empty0 + 8 * s);
         }
     }
+#ifdef ENDOR_CTA_TIMING
+    __syncthreads();
+    if (threadIdx.x == 0) g_cta_times[3 * blockIdx.x + 1] = gtimer();
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -328,6 +446,12 @@ __global__ void __launch_bounds__(kExpandThreads) expand_kernel(ExpandArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+#ifdef ENDOR_CTA_TIMING
+extern "C" int endor_debug_cta_times(unsigned long long* host_out, int n) {
+    return int(cudaMemcpyFromSymbol(host_out, g_cta_times, sizeof(unsigned long long) * 3 * n));
+}
+#endif
+
 cudaError_t launch_expand(const ExpandArgs& a, int mode, cudaStream_t s) {
     const uint64_t ntiles = ceil_div(a.e1 - a.e0, kTileElems);
     if (ntiles == 0) return cudaSuccess;
@@ -346,8 +470,7 @@ static cudaError_t launch_tma_mode(const Batch& b, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     const uint64_t grid = umin64(b.ntiles, uint64_t(blocks_per_sm) * sms);
     if (grid == 0) return cudaSuccess;
-    expand_tma_kernel<MODE><<<unsigned(grid), kTmaThreads, smem, s>>>(b);
-    return cudaGetLastError();
+    return launch_pdl(expand_tma_kernel<MODE>, dim3(unsigned(grid)), dim3(kTmaThreads), smem, s, b);
 }
 
 // Whole-tensor expand of a batch through the TMA ring (needs count_kernel's

@@ -163,7 +163,6 @@ __global__ void __launch_bounds__(kGvThreads, ENDOR_GV_MINB) gemv_fused_kernel(c
     const uint32_t st0 = sbase + 256;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-    if (cta_error_latched(b.hdr)) return;  // a latched error: write nothing
     init_luts(tid);
     if (tid == 0) {
         for (int s = 0; s < kGvStages; ++s) {
@@ -172,7 +171,9 @@ __global__ void __launch_bounds__(kGvThreads, ENDOR_GV_MINB) gemv_fused_kernel(c
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncthreads();
+    pdl_wait();
+    if (cta_error_latched(b.hdr)) return;  // a latched error: write nothing (+ publishes the prologue)
+    pdl_launch_dependents();
     // this CTA's contiguous range of the column-major item order
     const uint64_t u0 = nitems * blockIdx.x / gridDim.x, u1 = nitems * (blockIdx.x + 1) / gridDim.x;
     if (u0 >= u1) return;
@@ -452,6 +453,8 @@ struct FlattenBatch {
 };
 
 __global__ void __launch_bounds__(256) flatten_kernel(const __grid_constant__ FlattenBatch f) {
+    pdl_wait();
+    pdl_launch_dependents();
     const uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (g >= f.sub0[f.count]) return;
     int k = 0;
@@ -476,8 +479,7 @@ cudaError_t launch_gemv_fused(Batch& b, cudaStream_t s) {
     }
     f.sub0[f.count] = nflat;
     if (nflat) {
-        flatten_kernel<<<unsigned(ceil_div(nflat, 256)), 256, 0, s>>>(f);
-        cudaError_t e = cudaGetLastError();
+        cudaError_t e = launch_pdl(flatten_kernel, dim3(unsigned(ceil_div(nflat, 256))), dim3(256), 0, s, f);
         if (e != cudaSuccess) return e;
     }
     int blocks_per_sm = 1, sms = 148;
@@ -505,9 +507,8 @@ cudaError_t launch_gemv_fused(Batch& b, cudaStream_t s) {
     }
     const uint64_t grid = umin64(items, uint64_t(blocks_per_sm) * sms);
     if (grid == 0) return cudaSuccess;
-    if (sparse) gemv_fused_kernel<true><<<unsigned(grid), kGvThreads, smem, s>>>(b, items);
-    else gemv_fused_kernel<false><<<unsigned(grid), kGvThreads, smem, s>>>(b, items);
-    return cudaGetLastError();
+    if (sparse) return launch_pdl(gemv_fused_kernel<true>, dim3(unsigned(grid)), dim3(kGvThreads), smem, s, b, items);
+    return launch_pdl(gemv_fused_kernel<false>, dim3(unsigned(grid)), dim3(kGvThreads), smem, s, b, items);
 }
 
 // y[r] = sum over the row's segment partials in segment order (deterministic)
@@ -521,6 +522,8 @@ struct ReduceBatch {
 };
 
 __global__ void __launch_bounds__(256) row_reduce_kernel(const __grid_constant__ ReduceBatch rb) {
+    pdl_wait();
+    pdl_launch_dependents();
     const uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (g >= rb.row0[rb.count]) return;
     int k = 0;
@@ -547,8 +550,7 @@ cudaError_t launch_row_reduce_batch(const Batch& b, float* const* y32, void* con
     }
     rb.row0[b.count] = rows;
     if (rows == 0) return cudaSuccess;
-    row_reduce_kernel<<<unsigned(ceil_div(rows, 256)), 256, 0, s>>>(rb);
-    return cudaGetLastError();
+    return launch_pdl(row_reduce_kernel, dim3(unsigned(ceil_div(rows, 256))), dim3(256), 0, s, rb);
 }
 
 }  // namespace endor_b200

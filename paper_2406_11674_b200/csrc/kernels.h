@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "common.cuh"
 
 namespace endor_b200 {
@@ -16,6 +18,26 @@ int set_last_error(int code, const char* what);
 // device and returns its resident CTAs per SM at `threads` and the SM count.
 // Thread-safe; cached per (kernel, device).
 cudaError_t kernel_slots(const void* fn, int threads, size_t smem, int* blocks_per_sm, int* sms);
+
+// Launch with programmatic dependent launch (see pdl_wait in common.cuh):
+// the kernel must call pdl_wait() before touching global memory that the
+// previous kernel in the stream may write.  ENDOR_PDL=0 launches plainly.
+bool pdl_enabled();
+template <typename... Params, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(Params...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 struct ScanArgs {
     const uint8_t* bitmap;

@@ -28,8 +28,12 @@ namespace endor_b200 {
 // count_kernel (batched)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kScanThreads) count_kernel(const __grid_constant__ Batch b) {
-    __shared__ uint32_t s_sub[kCountSubs];
+    constexpr int kVecPerThread = kCountBlockWords / 4 / kScanThreads;  // uint4 per thread per block
+    static_assert(kVecPerThread * kScanThreads * 4 == kCountBlockWords, "block / thread geometry");
+    __shared__ uint32_t s_sub[2][kCountSubs];  // double-buffered: one barrier per block
     __shared__ int s_last;
+    __shared__ __align__(8) unsigned long long s_full[kCountStages];
+    extern __shared__ __align__(128) uint4 s_blk[];  // [kCountStages][kCountBlockWords / 4]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ti = batch_tensor_of_cblk(b, blockIdx.x);
     const BatchTensor& T = b.t[ti];
@@ -39,47 +43,48 @@ __global__ void __launch_bounds__(kScanThreads) count_kernel(const __grid_consta
     const uint64_t nblocks = ceil_div(nwords, kCountBlockWords);
     const uint64_t cb0 = uint64_t(lc) * T.cbpc, cb1 = umin64(nblocks, cb0 + T.cbpc);
     const uint64_t nsubs = (nwords + 31) / 32;
-    // 2-stage ring of 32 KiB blocks filled by 1-D TMA bulk copies: block cb+1 is
-    // in flight while block cb is counted, so HBM never idles between blocks
-    extern __shared__ __align__(128) uint4 s_blk[];  // [2][kCountBlockWords / 4]
-    __shared__ __align__(8) unsigned long long s_full[2];
+    // kCountStages-deep ring of count blocks filled by 1-D TMA bulk copies:
+    // blocks cb+1 .. cb+S-1 are in flight while block cb is counted
     const uint32_t full0 = smem_u32(&s_full[0]);
     auto full_block = [&](uint64_t cb) { return cb < cb1 && (cb + 1) * kCountBlockWords * 32 <= n; };
-    auto issue = [&](uint64_t cb, int s) {  // thread 0 only
-        const uint32_t bar = full0 + 8 * s;
+    auto issue = [&](uint64_t cb, int st) {  // thread 0 only
+        const uint32_t bar = full0 + 8 * st;
         mbar_arrive_expect_tx(bar, kCountBlockWords * 4);
-        bulk_g2s(smem_u32(s_blk + s * (kCountBlockWords / 4)), T.bitmap + cb * kCountBlockWords * 4,
+        bulk_g2s(smem_u32(s_blk + st * (kCountBlockWords / 4)), T.bitmap + cb * kCountBlockWords * 4,
                  kCountBlockWords * 4, bar);
     };
     if (tid == 0) {
-        mbar_init(full0, 1);
-        mbar_init(full0 + 8, 1);
+        for (int st = 0; st < kCountStages; ++st) mbar_init(full0 + 8 * st, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        if (full_block(cb0)) issue(cb0, 0);
     }
     __syncthreads();
+    pdl_wait();  // every global access below may depend on the previous kernel
+    pdl_launch_dependents();
+    if (tid == 0)
+        for (int st = 0; st < kCountStages; ++st)
+            if (full_block(cb0 + st)) issue(cb0 + st, st);
 
-    // stream this CTA's range of 262144-bit count blocks; sub-tile offsets are
-    // relative to the range start, whose base comes from the last-CTA scan
+    // stream this CTA's range of count blocks; sub-tile offsets are relative
+    // to the range start, whose base comes from the last-CTA scan
     unsigned long long running = 0;
     int it = 0;
     for (uint64_t cb = cb0; cb < cb1; ++cb, ++it) {
         const uint64_t w0 = cb * kCountBlockWords;
-        const int s = it & 1;
-        if (tid == 0 && full_block(cb + 1)) issue(cb + 1, s ^ 1);  // stage s^1 freed by the last sync
+        const int st = it % kCountStages;
+        uint32_t* sub = s_sub[it & 1];
         if (full_block(cb)) {
             // full block: 8 consecutive lanes (128 B) = one 1024-bit sub-tile
-            mbar_wait(full0 + 8 * s, (it >> 1) & 1);
-            uint4 v[8];
+            mbar_wait(full0 + 8 * st, (it / kCountStages) & 1);
+            uint4 v[kVecPerThread];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) v[j] = s_blk[s * (kCountBlockWords / 4) + j * kScanThreads + tid];
+            for (int j = 0; j < kVecPerThread; ++j) v[j] = s_blk[st * (kCountBlockWords / 4) + j * kScanThreads + tid];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < kVecPerThread; ++j) {
                 uint32_t c = __popc(v[j].x) + __popc(v[j].y) + __popc(v[j].z) + __popc(v[j].w);
                 c += __shfl_xor_sync(0xffffffffu, c, 1);
                 c += __shfl_xor_sync(0xffffffffu, c, 2);
                 c += __shfl_xor_sync(0xffffffffu, c, 4);
-                if ((lane & 7) == 0) s_sub[32 * j + tid / 8] = c;
+                if ((lane & 7) == 0) sub[32 * j + tid / 8] = c;
             }
         } else {
             // ragged last block: word loads with the tail masked and padding checked
@@ -101,28 +106,32 @@ __global__ void __launch_bounds__(kScanThreads) count_kernel(const __grid_consta
                     }
                 }
                 const uint32_t c = __reduce_add_sync(0xffffffffu, __popc(wv));
-                if (lane == 0) s_sub[s] = c;
+                if (lane == 0) sub[s] = c;
             }
         }
-        __syncthreads();
-        if (warp == 0) {  // exclusive offsets of the block's 256 sub-tiles (8 per lane)
-            uint32_t cs[8], sum = 0;
+        __syncthreads();  // block cb read by every thread, sub[] complete
+        // stage st is free again: refill it with the block kCountStages ahead
+        if (tid == 0 && full_block(cb + kCountStages)) issue(cb + kCountStages, st);
+        if (warp == 0) {  // exclusive offsets of the block's sub-tiles (kCountSubs / 32 per lane)
+            constexpr int kPer = kCountSubs / 32;
+            uint32_t cs[kPer], sum = 0;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                cs[k] = s_sub[8 * lane + k];
+            for (int k = 0; k < kPer; ++k) {
+                cs[k] = sub[kPer * lane + k];
                 sum += cs[k];
             }
             const uint32_t incl = warp_incl_scan(sum, lane);
             unsigned long long e = running + (incl - sum);
-            const uint64_t sub = w0 / 32 + 8 * lane;
+            const uint64_t s0 = w0 / 32 + kPer * lane;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                if (sub + k < nsubs) b.tsub[T.sub0 + sub + k] = e;
+            for (int k = 0; k < kPer; ++k) {
+                if (s0 + k < nsubs) b.tsub[T.sub0 + s0 + k] = e;
                 e += cs[k];
             }
             running += __shfl_sync(0xffffffffu, incl, 31);
         }
-        __syncthreads();  // s_sub is rewritten by the next block
+        // (no second barrier: the next block writes the other sub[] buffer, and
+        // warp 0 finishes this scan before it reaches the next barrier)
     }
     if (tid == 0) {
         b.blk[T.blk0 + lc] = running;  // warp 0's lane 0 holds the range aggregate
@@ -224,11 +233,10 @@ cudaError_t launch_verify_index(const unsigned long long* idx, uint64_t chunks, 
 
 cudaError_t launch_count(const Batch& b, cudaStream_t s) {
     if (b.ncblk == 0) return cudaSuccess;
-    constexpr int smem = 2 * kCountBlockWords * 4;  // two 32 KiB stages
+    constexpr int smem = kCountStages * kCountBlockWords * 4;  // the TMA ring
     cudaError_t e = kernel_slots(reinterpret_cast<const void*>(count_kernel), kScanThreads, smem, nullptr, nullptr);
     if (e != cudaSuccess) return e;
-    count_kernel<<<b.ncblk, kScanThreads, smem, s>>>(b);
-    return cudaGetLastError();
+    return launch_pdl(count_kernel, dim3(b.ncblk), dim3(kScanThreads), smem, s, b);
 }
 
 __global__ void __launch_bounds__(kScanThreads) scan_kernel(ScanArgs a) {

@@ -77,7 +77,7 @@ def gemv_check(y, W, x, tol=1e-3):
     bound = tol * mag + 1e-30
     bad = err > bound
     assert not bad.any(), f"{int(bad.sum())} rows exceed {tol} * sum|W x|; worst {float((err / bound).max())}"
-    good = ref.abs() >= 0.1 * mag
+    good = (ref.abs() >= 0.1 * mag) & (mag > 0)
     rel = (err[good] / ref[good].abs()).max().item() if good.any() else 0.0
     assert rel <= tol, f"per-element relative error {rel} > {tol}"
     return float((err / (mag + 1e-30)).max()) if err.numel() else 0.0, rel
