@@ -21,6 +21,8 @@
  *   endor_cuda_magnitude_prune       <- magnitude_prune        weight_gen.hpp:96-113
  *   endor_cuda_gemv                  <- (absent; the consumer is modelled as a
  *                                        constant compute time, sim.hpp:227)
+ *   endor_cuda_gemm_compressed       <- (absent; prefill / batched consumer,
+ *                                        sim.hpp:30,256: fused tcgen05 GEMM)
  *   endor_pipeline_*                 <- the Endor offload stages, modelled
  *                                        only analytically at sim.hpp:196-224
  *   endor_cuda_decompress_host       <- decompress() end to end over host
@@ -305,6 +307,24 @@ int endor_cuda_gemv_compressed(const endor_tensor_view* t, const uint64_t* prefi
 int endor_cuda_gemv_compressed_batch(const endor_tensor_view* views, const uint64_t* const* prefixes1024,
                                      const void* const* x_f16, float* const* y_f32, void* const* y_f16,
                                      int count, void* ws, size_t ws_bytes, void* stream);
+
+/* Fused decompress -> GEMM on the tcgen05 tensor cores (north star (b): the
+ * prefill / batched-decode consumer; the reference models it only as a
+ * constant, sim.hpp:30,256):  Y[t, r] = sum_c W[r, c] X[t, c]  for t < tokens,
+ * i.e. Y = X W^T with W the decompressed tensor (codec.hpp:157) -- which is
+ * never written to HBM: each CTA expands its 128-row W tile into shared
+ * memory as the MMA's A operand.  f16 W (any rows / cols), X f16
+ * [tokens][x_ld] row-major (16-byte aligned, x_ld >= cols, x_ld % 8 == 0),
+ * fp32 accumulation; Y [tokens][rows] as y_f32 and/or y_f16.  prefix1024
+ * (optional, device): the tensor's RankIndex at chunk 1024 -- when given no
+ * counting pass runs.  Errors as decompress (popcount != nnz, padding bits,
+ * an inconsistent index: CorruptionError via endor_cuda_sync_status).
+ * Deterministic (split-K partials are summed in a fixed order).  Workspace:
+ * endor_cuda_gemm_workspace_bytes(rows, cols, tokens). */
+size_t endor_cuda_gemm_workspace_bytes(uint64_t rows, uint64_t cols, uint64_t tokens);
+int endor_cuda_gemm_compressed(const endor_tensor_view* t, const uint64_t* prefix1024, const void* x_f16,
+                               uint64_t tokens, uint64_t x_ld, float* y_f32, void* y_f16, void* ws, size_t ws_bytes,
+                               void* stream);
 
 /* ---- storage: .endor containers straight to the GPU ---- */
 /* The EndorDirect mode (SsdToGpu, sim.hpp:205-214), executed

@@ -64,6 +64,9 @@ SIGNATURES = {
     "endor_cuda_decompress_chunked_batch": (C.c_int, [C.POINTER(TensorView), C.POINTER(_vp), _u64,
                                                       C.POINTER(_vp), C.c_int, _vp, _sz, _vp]),
     "endor_cuda_decompress_dequant": (C.c_int, [C.POINTER(TensorView), C.c_float, _vp, _vp, _sz, _vp]),
+    "endor_cuda_gemm_workspace_bytes": (_sz, [_u64, _u64, _u64]),
+    "endor_cuda_gemm_compressed": (C.c_int, [C.POINTER(TensorView), _vp, _vp, _u64, _u64, _vp, _vp, _vp, _sz,
+                                             _vp]),
     "endor_cuda_gemv_compressed": (C.c_int, [C.POINTER(TensorView), _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "endor_cuda_gemv_compressed_batch": (C.c_int, [C.POINTER(TensorView), C.POINTER(_vp), C.POINTER(_vp),
                                                    C.POINTER(_vp), C.POINTER(_vp), C.c_int, _vp, _sz, _vp]),

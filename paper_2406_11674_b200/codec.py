@@ -392,6 +392,42 @@ def gemv_compressed(t: EndorTensor, x: torch.Tensor, index: Optional[RankIndex] 
     return y
 
 
+def gemm_compressed(t: EndorTensor, x: torch.Tensor, index: Optional[RankIndex] = None,
+                    out_dtype: torch.dtype = torch.float32) -> torch.Tensor:
+    """Y = X W^T straight from the compressed W (fused decompress -> tcgen05
+    GEMM; the dense W is never written): x f16 [tokens, cols] -> Y [tokens,
+    rows] in fp32 (or f16) with fp32 accumulation."""
+    dev = t.device
+    if t.dtype != Dtype.F16 or x.dtype != torch.float16 or x.dim() != 2 or x.shape[1] != t.cols:
+        raise InvalidArgument("gemm_compressed needs an f16 W [rows, cols] and f16 X [tokens, cols]")
+    tokens = x.shape[0]
+    ld = (t.cols + 7) // 8 * 8
+    if x.stride(1) == 1 and x.stride(0) == ld and x.data_ptr() % 16 == 0:
+        xc = x
+    else:  # TMA rows must be 16-byte strided: pad each row to a multiple of 8 elements
+        xc = torch.zeros((tokens, ld), dtype=torch.float16, device=dev)
+        xc[:, :t.cols] = x
+    y = torch.empty((tokens, t.rows), dtype=out_dtype, device=dev)
+    if out_dtype not in (torch.float32, torch.float16):
+        raise InvalidArgument("gemm_compressed: out_dtype must be float32 or float16")
+    L = _lib.lib()
+    ws = workspace(t.element_count(), dev)
+    need = L.endor_cuda_gemm_workspace_bytes(t.rows, t.cols, tokens)
+    if ws.numel() < need:
+        ws = torch.zeros(need, dtype=torch.uint8, device=dev)
+    pre = None
+    if index is not None:
+        if index.chunk_size != 1024:
+            raise InvalidArgument("gemm_compressed takes a RankIndex at chunk size 1024")
+        pre = index.prefix.to(device=dev, dtype=torch.int64).contiguous()
+    v = t.view()
+    y32, y16 = (y, None) if out_dtype == torch.float32 else (None, y)
+    check(L.endor_cuda_gemm_compressed(C.byref(v), _ptr(pre), _ptr(xc), tokens, ld, _ptr(y32), _ptr(y16),
+                                       ws.data_ptr(), ws.numel(), _stream_ptr(dev)))
+    sync_status(ws, dev)
+    return y
+
+
 def gemv_compressed_batch(tensors: Sequence[EndorTensor], xs: Sequence[torch.Tensor],
                           indices: Optional[Sequence[Optional[RankIndex]]] = None) -> List[torch.Tensor]:
     """y_i = W_i x_i for a batch (e.g. one decoder layer's ops) in one fused

@@ -451,6 +451,87 @@ int endor_cuda_gemv_compressed_batch(const endor_tensor_view* views, const uint6
     return ENDOR_OK;
 }
 
+size_t endor_cuda_gemm_workspace_bytes(uint64_t rows, uint64_t cols, uint64_t tokens) {
+    uint64_t n;
+    if (!checked_n(rows, cols, &n)) return 0;
+    const GemmPlan p = gemm_plan(rows, cols, tokens, count_ctas() / 3);
+    return ws_layout(nullptr, n).bytes + align256(p.part_bytes);
+}
+
+int endor_cuda_gemm_compressed(const endor_tensor_view* t, const uint64_t* prefix1024, const void* x_f16,
+                               uint64_t tokens, uint64_t x_ld, float* y_f32, void* y_f16, void* ws, size_t ws_bytes,
+                               void* stream) {
+    uint64_t n;
+    int eb, st;
+    if ((st = check_view(t, &n, &eb))) return st;
+    if (t->dtype != ENDOR_DTYPE_F16) return fail(ENDOR_ERR_INVALID_ARGUMENT, "fused GEMM needs an f16 tensor");
+    if (!y_f32 && !y_f16) return fail(ENDOR_ERR_INVALID_ARGUMENT, "y must be given");
+    if ((y_f32 && !aligned(y_f32, 4)) || (y_f16 && !aligned(y_f16, 2)))
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "misaligned y");
+    if (tokens == 0 || t->rows == 0) return ENDOR_OK;
+    if (t->cols == 0) {  // empty reduction: Y = 0
+        if (y_f32) CK(cudaMemsetAsync(y_f32, 0, tokens * t->rows * 4, S(stream)));
+        if (y_f16) CK(cudaMemsetAsync(y_f16, 0, tokens * t->rows * 2, S(stream)));
+        return ENDOR_OK;
+    }
+    if (!x_f16 || !aligned(x_f16, 16) || x_ld < t->cols || x_ld % 8)
+        return fail(ENDOR_ERR_INVALID_ARGUMENT,
+                    "x must be a 16-byte aligned f16 [tokens][x_ld] with x_ld >= cols and x_ld % 8 == 0");
+    if (t->cols > 0x7FFFFFFFull || tokens > 0x7FFFFFFFull || x_ld > (uint64_t(1) << 38))
+        return fail(ENDOR_ERR_SIZE, "fused GEMM: cols and tokens must fit the TMA coordinate range (< 2^31)");
+    if (prefix1024 && !aligned(prefix1024, 8)) return fail(ENDOR_ERR_INVALID_ARGUMENT, "misaligned prefix");
+    WsLayout L;
+    if ((st = check_ws(ws, ws_bytes, n, &L))) return st;
+    const GemmPlan p = gemm_plan(t->rows, t->cols, tokens, count_ctas() / 3);
+    if (ws_bytes < L.bytes + align256(p.part_bytes))
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "workspace too small (endor_cuda_gemm_workspace_bytes)");
+    const unsigned long long* idx = reinterpret_cast<const unsigned long long*>(prefix1024);
+    if (!idx) {
+        // rank table of the reference's decompress (codec.hpp:157-160): counts,
+        // checks popcount == nnz and the padding bits, flat absolute offsets
+        if (aligned(t->bitmap, 16)) {
+            Batch b{};
+            b.count = 1;
+            b.check_total = 1;
+            b.t[0].bitmap = static_cast<const uint8_t*>(t->bitmap);
+            b.t[0].values = static_cast<const uint8_t*>(t->values);
+            b.t[0].n = n;
+            b.t[0].nnz = t->nnz;
+            uint64_t sub_cap, blk_cap;
+            batch_plan(b, &sub_cap, &blk_cap, count_ctas());
+            b.tsub = L.tsub;
+            b.blk = L.blk;
+            b.hdr = L.hdr;
+            CK(launch_count(b, S(stream)));
+            CK(launch_flatten(L.tsub, L.blk + b.t[0].blk0, uint64_t(kCountSubs) * b.t[0].cbpc, ceil_div(n, kSubElems),
+                              S(stream)));
+        } else {
+            ScanArgs a = scan_args(t->bitmap, n, 0, n, L);
+            a.tsub = L.tsub;
+            a.check_total = 1;
+            a.expect_total = t->nnz;
+            CK(launch_scan(a, S(stream)));
+        }
+        idx = L.tsub;
+    }
+    GemmLaunch g{};
+    g.bitmap = static_cast<const uint8_t*>(t->bitmap);
+    g.values = static_cast<const uint8_t*>(t->values);
+    g.nnz = t->nnz;
+    g.rows = t->rows;
+    g.cols = t->cols;
+    g.tokens = tokens;
+    g.idx = idx;
+    g.x = x_f16;
+    g.x_ld = x_ld;
+    g.part = reinterpret_cast<float*>(static_cast<char*>(ws) + L.bytes);
+    g.y32 = y_f32;
+    g.y16 = y_f16;
+    g.hdr = L.hdr;
+    CK(launch_gemm_fused(p, g, S(stream)));
+    return ENDOR_OK;
+}
+
 // extract_rows / extract_cols (codec.hpp:239-297): validation of the index
 // list (check_sorted_unique, codec.hpp:224-232), a count pass for ranks, then
 // the gather.  Errors are device-latched (endor_cuda_sync_status).

@@ -463,6 +463,19 @@ __global__ void __launch_bounds__(256) flatten_kernel(const __grid_constant__ Fl
     f.tsub[k][j] += f.blk[k][j / f.spc[k]];
 }
 
+cudaError_t launch_flatten(unsigned long long* tsub, const unsigned long long* blk, uint64_t spc, uint64_t count,
+                           cudaStream_t s) {
+    if (!count) return cudaSuccess;
+    FlattenBatch f{};
+    f.tsub[0] = tsub;
+    f.blk[0] = blk;
+    f.spc[0] = spc;
+    f.sub0[0] = 0;
+    f.sub0[1] = count;
+    f.count = 1;
+    return launch_pdl(flatten_kernel, dim3(unsigned(ceil_div(count, 256))), dim3(256), 0, s, f);
+}
+
 cudaError_t launch_gemv_fused(Batch& b, cudaStream_t s) {
     FlattenBatch f{};
     uint64_t nflat = 0;

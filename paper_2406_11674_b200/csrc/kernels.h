@@ -187,4 +187,34 @@ cudaError_t launch_gemv_batch(GemvBatch& gb, cudaStream_t s);
 cudaError_t launch_quantize(const void* vals, uint64_t nnz, void* q, float* scale_dev, unsigned int* amax,
                             cudaStream_t s);
 
+
+// ---- fused decompress -> GEMM (gemm_fused.cu, tcgen05) ------------------------
+// Y[t, r] = sum_c W[r, c] X[t, c]: f16 W (Endor format) and X [tokens][x_ld],
+// fp32 accumulation in TMEM; 128-row W tiles x bn tokens, K split so the grid
+// fills the SMs (split partials summed in order by a second kernel).
+struct GemmPlan {
+    int bn;                       // UMMA N: 64, 128 or 256
+    uint32_t m_tiles, n_tiles, ksplit, sps;
+    uint64_t nspans;              // 128-column spans per row
+    uint64_t part_bytes;          // split-K partials (0 when ksplit == 1)
+};
+GemmPlan gemm_plan(uint64_t rows, uint64_t cols, uint64_t tokens, int sms);
+struct GemmLaunch {
+    const uint8_t* bitmap;
+    const uint8_t* values;
+    uint64_t nnz, rows, cols, tokens;
+    const unsigned long long* idx;  // flat RankIndex at chunk 1024 (absolute)
+    const void* x;                  // f16 [tokens][x_ld], 16-byte aligned, x_ld * 2 % 16 == 0
+    uint64_t x_ld;
+    float* part;                    // plan.part_bytes of workspace
+    float* y32;                     // [tokens][rows], or null
+    void* y16;                      // [tokens][rows] f16, or null
+    WsHeader* hdr;
+};
+cudaError_t launch_gemm_fused(const GemmPlan& p, const GemmLaunch& g, cudaStream_t s);
+// count_kernel's two-level offsets -> a flat absolute 1024-chunk table, in place
+// (tsub[j] += blk[j / spc] for j < count)
+cudaError_t launch_flatten(unsigned long long* tsub, const unsigned long long* blk, uint64_t spc, uint64_t count,
+                           cudaStream_t s);
+
 }  // namespace endor_b200

@@ -81,3 +81,26 @@ def gemv_check(y, W, x, tol=1e-3):
     rel = (err[good] / ref[good].abs()).max().item() if good.any() else 0.0
     assert rel <= tol, f"per-element relative error {rel} > {tol}"
     return float((err / (mag + 1e-30)).max()) if err.numel() else 0.0, rel
+
+
+def gemm_check(y, W, X, tol=1e-3):
+    """gemv_check for Y = X W^T ([tokens, rows]), element-wise, in float64 on
+    Y's device: |Y_tr - ref_tr| <= tol * sum_j |X_tj W_rj| everywhere, and
+    <= tol * |ref_tr| where ref_tr is not dominated by cancellation.  Returns
+    (max error/mag, max relative error over well-conditioned entries)."""
+    import torch
+    dev = y.device
+    Wd = W.to(dev).double()
+    Xd = X.to(dev).double()
+    ref = Xd @ Wd.T
+    mag = Xd.abs() @ Wd.abs().T
+    yd = y.double()
+    assert yd.shape == ref.shape, (yd.shape, ref.shape)
+    err = (yd - ref).abs()
+    bound = tol * mag + 1e-30
+    bad = err > bound
+    assert not bad.any(), f"{int(bad.sum())} entries exceed {tol} * sum|X W|; worst {float((err / bound).max())}"
+    good = (ref.abs() >= 0.1 * mag) & (mag > 0)
+    rel = (err[good] / ref[good].abs()).max().item() if good.any() else 0.0
+    assert rel <= tol, f"per-element relative error {rel} > {tol}"
+    return float((err / (mag + 1e-30)).max()) if err.numel() else 0.0, rel
