@@ -10,10 +10,12 @@
 //
 // Tile: 128 W rows (UMMA M) x BN tokens (UMMA N) x the CTA's K range, fp32
 // accumulator in TMEM (BN columns).  Per CTA (384 threads, 1 per SM):
-//   warp 0      raw producer: per 128-column span, the span's bitmap (16 bytes
-//               per row; 2-D TMA when cols % 128 == 0) and every row's packed
-//               values window (one 1-D bulk copy per row, 16-byte aligned
-//               superset) into a raw ring; row value cursors advance by popc
+//   warps 0, 3  raw producers (64 rows each): per 128-column span, the span's
+//               bitmap (16 bytes per row, cp.async a few spans ahead) and every
+//               row's packed-values window (16-byte aligned superset, copied
+//               by 8 lanes per row with 16-byte cp.async) into a raw ring; row
+//               value cursors advance by popc.  (One 1-D bulk copy per row
+//               window -- 128 per span -- was TMA-issue-bound: 0.08 of roofline.)
 //   warp 1      X producer: 2-D TMA (128-byte swizzle) of each 64-column
 //               k-block's BN x 64 X tile
 //   warp 2      TMEM allocator + MMA issuer (one elected lane): 4 x
@@ -41,36 +43,46 @@
 #include "gather.cuh"
 #include "kernels.h"
 
+// development switch (tools/build_variant.sh): bit 0 no MMA, bit 1 no gather
+// (A left stale), bit 2 no value copies -- isolates the pipeline's limiter
+#ifndef ENDOR_GEMM_SKIP
+#define ENDOR_GEMM_SKIP 0
+#endif
+
 namespace endor_b200 {
 
 constexpr int kGmRows = 128;                        // UMMA M
 constexpr int kGmKB = 64;                           // k-block: 64 f16 = one 128-byte swizzle row
-constexpr int kGmSpan = 128;                        // raw stage: 2 k-blocks, 16 bitmap bytes per row
-constexpr int kGmSlotRow = 272;                     // <= 128 values + 16-byte alignment slack
-constexpr int kGmRawHdr = kGmRows * 4;              // per-row byte offset of the first value
-constexpr int kGmRawBytes = kGmRawHdr + kGmRows * kGmSlotRow;  // 35328
-constexpr int kGmBmpBytes = kGmRows * 16;           // 2048
+constexpr int kGmSpan = 128;                        // bitmap span: 2 k-blocks, 16 bytes per row
+constexpr int kGmWin = 144;                         // per-thread values window: <= 64 values + 16-byte slack
 constexpr int kGmExpandWarps = 8;
+constexpr int kGmExpandThreads = kGmExpandWarps * 32;
+constexpr int kGmRawBytes = kGmExpandThreads * kGmWin;  // one span's windows: 36 KiB
+constexpr int kGmBmpBytes = kGmRows * 16;           // 2048
 constexpr int kGmThreads = (4 + kGmExpandWarps) * 32;  // 384
+constexpr int kGmLook = 2;                          // spans of value copies in flight per thread
+constexpr int kGmRaw = kGmLook + 1;                 // private window slots per thread
+constexpr int kGmBmp = 8;                           // bitmap ring (spans)
+
+constexpr int kGmAS = 4;                           // A stages, in TMEM (32 columns each)
 
 template <int BN>
 struct GmCfg {
-    static constexpr int kAB = BN == 256 ? 3 : 4;                 // A/B stages
-    static constexpr int kRaw = BN == 64 ? 3 : 2;                 // raw (values) stages
-    static constexpr int kBmp = BN == 256 ? 4 : 8;                // bitmap stages (lookahead kBmp - kRaw spans)
-    static constexpr uint32_t kA = 0;                             // A tiles, 16 KiB each (1024-aligned)
-    static constexpr uint32_t kB = kA + kAB * 16384;              // X tiles, BN x 128 bytes
-    static constexpr uint32_t kRawOff = kB + kAB * BN * 128;
-    static constexpr uint32_t kBmpOff = kRawOff + kRaw * kGmRawBytes;
-    static constexpr uint32_t kBar = kBmpOff + kBmp * kGmBmpBytes;
-    // full[kAB] empty[kAB] raw_full[kRaw] raw_empty[kRaw] bmp_full[kBmp] tmem_full, tmem addr
-    static constexpr uint32_t kTmemSlot = kBar + 8 * (2 * kAB + 2 * kRaw + kBmp + 1);
+    static constexpr int kXS = BN == 64 ? 8 : (BN == 128 ? 6 : 3);  // X stages (TMA ring in smem)
+    static constexpr uint32_t kTmemCols = BN + 32 * kGmAS <= 256 ? 256 : 512;  // accumulator + A stages
+    static constexpr uint32_t kB = 0;                             // X tiles, BN x 128 bytes (1024-aligned)
+    static constexpr uint32_t kRawOff = kB + kXS * BN * 128;
+    static constexpr uint32_t kBmpOff = kRawOff + kGmRaw * kGmRawBytes;
+    static constexpr uint32_t kBar = kBmpOff + kGmBmp * kGmBmpBytes;
+    // xfull[kXS] xempty[kXS] afull[kAS] aempty[kAS] bmp_full[kBmp] bmp_empty[kBmp] tmem_full, tmem addr
+    static constexpr uint32_t kTmemSlot = kBar + 8 * (2 * kXS + 2 * kGmAS + 2 * kGmBmp + 1);
     static constexpr uint32_t kRank = (kTmemSlot + 4 + 15) & ~15u;  // u64 start[128], end[128]
     static constexpr uint32_t kEnd = kRank + 2 * 8 * kGmRows + 16;  // + gather over-read pad
     static constexpr uint32_t kSmem = kEnd + 1024;                  // + alignment of the dynamic base
 };
-static_assert(GmCfg<256>::kSmem <= 232448 && GmCfg<128>::kSmem <= 232448 && GmCfg<64>::kSmem <= 232448,
-              "GEMM shared-memory plan exceeds 227 KiB");
+static_assert(GmCfg<256>::kSmem + 1024 <= 232448 && GmCfg<128>::kSmem + 1024 <= 232448 &&
+                  GmCfg<64>::kSmem + 1024 <= 232448,
+              "GEMM shared-memory plan exceeds 227 KiB (incl. 1 KiB static)");
 
 struct GemmArgs {
     const uint8_t* bitmap;
@@ -85,7 +97,7 @@ struct GemmArgs {
     float* y32;                              // ksplit == 1
     __half* y16;
     WsHeader* hdr;
-    int bmp_tma;                             // bitmap via the 2-D tensor map
+    int bmp_async;                           // cols % 128 == 0 and 16-byte aligned bitmap: cp.async rows
 };
 
 // ---- tcgen05 / TMA wrappers -------------------------------------------------------
@@ -106,6 +118,27 @@ __device__ __forceinline__ void umma_f16(uint32_t tmem, uint64_t ad, uint64_t bd
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
         ::"r"(tmem), "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
+}
+// A from TMEM (lane = M row, K elements packed 2 per 32-bit column), B from shared memory
+__device__ __forceinline__ void umma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bd, uint32_t idesc,
+                                            uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "r"(tmem_a), "l"(bd), "r"(idesc), "r"(acc) : "memory");
+}
+// this warp's 32 TMEM lanes, 32 consecutive 32-bit columns from 8 x uint4 per thread
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint4 (&v)[8]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+        ::"r"(taddr), "r"(v[0].x), "r"(v[0].y), "r"(v[0].z), "r"(v[0].w), "r"(v[1].x), "r"(v[1].y), "r"(v[1].z),
+          "r"(v[1].w), "r"(v[2].x), "r"(v[2].y), "r"(v[2].z), "r"(v[2].w), "r"(v[3].x), "r"(v[3].y), "r"(v[3].z),
+          "r"(v[3].w), "r"(v[4].x), "r"(v[4].y), "r"(v[4].z), "r"(v[4].w), "r"(v[5].x), "r"(v[5].y), "r"(v[5].z),
+          "r"(v[5].w), "r"(v[6].x), "r"(v[6].y), "r"(v[6].z), "r"(v[6].w), "r"(v[7].x), "r"(v[7].y), "r"(v[7].z),
+          "r"(v[7].w)
+        : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
@@ -146,8 +179,7 @@ __device__ __forceinline__ unsigned long long warp_rank(const GemmArgs& a, uint6
 
 template <int BN>
 __global__ void __launch_bounds__(kGmThreads, 1)
-    gemm_fused_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap bmap,
-                      const __grid_constant__ GemmArgs a) {
+    gemm_fused_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ GemmArgs a) {
     using C = GmCfg<BN>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t sraw = smem_u32(smem_raw);
@@ -155,9 +187,9 @@ __global__ void __launch_bounds__(kGmThreads, 1)
     uint8_t* const smem = smem_raw + (sb - sraw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-    const uint32_t full0 = sb + C::kBar, empty0 = full0 + 8 * C::kAB;
-    const uint32_t rfull0 = empty0 + 8 * C::kAB, rempty0 = rfull0 + 8 * C::kRaw;
-    const uint32_t bfull0 = rempty0 + 8 * C::kRaw, tfull = bfull0 + 8 * C::kBmp;
+    const uint32_t xfull0 = sb + C::kBar, xempty0 = xfull0 + 8 * C::kXS;
+    const uint32_t afull0 = xempty0 + 8 * C::kXS, aempty0 = afull0 + 8 * kGmAS;
+    const uint32_t bfull0 = aempty0 + 8 * kGmAS, bempty0 = bfull0 + 8 * kGmBmp, tfull = bempty0 + 8 * kGmBmp;
     unsigned long long* const rstart = reinterpret_cast<unsigned long long*>(smem + C::kRank);
     unsigned long long* const rend = rstart + kGmRows;
 
@@ -175,29 +207,31 @@ __global__ void __launch_bounds__(kGmThreads, 1)
 
     init_luts(tid);
     if (tid == 0) {
-        for (int s = 0; s < C::kAB; ++s) {
-            mbar_init(full0 + 8 * s, 1 + kGmExpandWarps);  // X expect_tx + the expand warps
-            mbar_init(empty0 + 8 * s, 1);                 // tcgen05.commit
+        for (int s = 0; s < C::kXS; ++s) {
+            mbar_init(xfull0 + 8 * s, 1);                     // X expect_tx
+            mbar_init(xempty0 + 8 * s, 1);                    // tcgen05.commit
         }
-        for (int s = 0; s < C::kRaw; ++s) {
-            mbar_init(rfull0 + 8 * s, 32);                // every producer lane (expect_tx)
-            mbar_init(rempty0 + 8 * s, kGmExpandWarps);
+        for (int s = 0; s < kGmAS; ++s) {
+            mbar_init(afull0 + 8 * s, kGmExpandWarps / 2);    // the 4 warps of a k-block parity
+            mbar_init(aempty0 + 8 * s, 1);                    // tcgen05.commit
         }
-        for (int s = 0; s < C::kBmp; ++s) mbar_init(bfull0 + 8 * s, 1);
+        for (int s = 0; s < kGmBmp; ++s) {
+            mbar_init(bfull0 + 8 * s, 32);                    // bitmap producer lanes
+            mbar_init(bempty0 + 8 * s, kGmExpandWarps);
+        }
         mbar_init(tfull, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
-        if (a.bmp_tma) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&bmap)) : "memory");
     }
     pdl_wait();  // idx (count + flatten) and the latched status come from the previous kernels
     if (cta_error_latched(a.hdr)) return;
     pdl_launch_dependents();
     if (warp == 2) {  // TMEM accumulator: BN fp32 columns x 128 lanes
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sb + C::kTmemSlot),
-                     "r"(uint32_t(BN)) : "memory");
+                     "r"(C::kTmemCols) : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     // row value cursors at the split's range ends (every warp takes rows)
@@ -220,38 +254,23 @@ __global__ void __launch_bounds__(kGmThreads, 1)
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + C::kTmemSlot);
 
     if (warp == 0) {
-        // ===== raw producer: bitmap spans + per-row value windows =====
-        constexpr int kLookBmp = C::kBmp - C::kRaw;  // bitmap spans in flight beyond the raw ring
-        const uint64_t vlo = reinterpret_cast<uint64_t>(a.values), vhi = vlo + a.nnz * 2;
-        const uint64_t safe_lo = (vlo + 15) & ~uint64_t(15), safe_hi = vhi & ~uint64_t(15);
-        unsigned long long cur[4];
-        bool bad = false;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            cur[i] = rstart[lane + 32 * i];
-            bad |= cur[i] > rend[lane + 32 * i] || rend[lane + 32 * i] > a.nnz;
-        }
-        if (a.bmp_tma && lane == 0)
-            for (uint32_t s = 0; s < nsp && s < uint32_t(kLookBmp); ++s) {
-                mbar_arrive_expect_tx(bfull0 + 8 * s, kGmBmpBytes);
-                tma_load_2d(sb + C::kBmpOff + s * kGmBmpBytes, &bmap, int((sp0 + s) * 16), int(m0), bfull0 + 8 * s);
-            }
-        for (uint32_t s = 0; s < nsp; ++s) {
-            const uint32_t rs = s % C::kRaw, bs = s % C::kBmp;
-            mbar_wait(rempty0 + 8 * rs, ((s / C::kRaw) & 1) ^ 1);
+        // ===== bitmap producer: 16 bytes per row per 128-column span, kGmBmp spans ahead =====
+        for (uint32_t sn = 0; sn < nsp; ++sn) {
+            const uint32_t bs = sn % kGmBmp;
+            mbar_wait(bempty0 + 8 * bs, ((sn / kGmBmp) & 1) ^ 1);
             const uint32_t bslot = sb + C::kBmpOff + bs * kGmBmpBytes;
-            if (a.bmp_tma) {
-                const uint32_t sn = s + kLookBmp;
-                if (lane == 0 && sn < nsp) {
-                    const uint32_t bn = sn % C::kBmp;
-                    mbar_arrive_expect_tx(bfull0 + 8 * bn, kGmBmpBytes);
-                    tma_load_2d(sb + C::kBmpOff + bn * kGmBmpBytes, &bmap, int((sp0 + sn) * 16), int(m0),
-                                bfull0 + 8 * bn);
+            const uint64_t kc = k0 + uint64_t(sn) * kGmSpan;
+            if (a.bmp_async) {  // cols % 128 == 0, 16-byte aligned bitmap: 16 aligned bytes per row
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int r = lane + 32 * i;
+                    const bool live = m0 + r < a.rows;
+                    const uint8_t* src = a.bitmap + (live ? ((m0 + r) * a.cols + kc) / 8 : 0);
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(bslot + r * 16), "l"(src),
+                                 "r"(live ? 16 : 0) : "memory");
                 }
-                mbar_wait(bfull0 + 8 * bs, (s / C::kBmp) & 1);
-            } else {
-                // generic: any cols -- 128 bits from bit (gr*cols + k), funnel-shifted, masked to the range
-                const uint64_t kc = k0 + uint64_t(s) * kGmSpan;
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bfull0 + 8 * bs) : "memory");
+            } else {  // any cols: 128 bits from bit (gr*cols + kc), funnel-shifted, masked to the range
                 const uint32_t valid = uint32_t(umin64(kGmSpan, k1 - kc));
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
@@ -275,117 +294,121 @@ __global__ void __launch_bounds__(kGmThreads, 1)
                     }
                     sts128(bslot + r * 16, q);
                 }
+                mbar_arrive(bfull0 + 8 * bs);
             }
-            const uint32_t raw = sb + C::kRawOff + rs * kGmRawBytes;
-            uint32_t bytes = 0;
-            uint64_t src[4];
-            uint32_t len[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int r = lane + 32 * i;
-                const uint4 q = lds128(bslot + r * 16);
-                const uint32_t pc = __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
-                unsigned long long c0 = cur[i], c1 = c0 + pc;
-                if (c1 > a.nnz) {
-                    bad = true;
-                    c1 = a.nnz;
-                    c0 = c0 < c1 ? c0 : c1;
-                }
-                cur[i] = c1;
-                const uint64_t a0 = vlo + 2 * c0, a1 = vlo + 2 * c1;
-                const uint64_t A0 = a0 & ~uint64_t(15), A1 = (a1 + 15) & ~uint64_t(15);
-                asm volatile("st.shared.u32 [%0], %1;" ::"r"(raw + 4 * r), "r"(uint32_t(a0 - A0)) : "memory");
-                src[i] = A0;
-                len[i] = 0;
-                if (c1 > c0) {
-                    if (A0 >= safe_lo && A1 <= safe_hi) {
-                        len[i] = uint32_t(A1 - A0);
-                        bytes += len[i];
-                    } else {  // a window touching a ragged end of the values buffer: bytewise
-                        const uint32_t dst = raw + kGmRawHdr + r * kGmSlotRow;
-                        for (uint64_t p = a0; p < a1; ++p)
-                            sts8(dst + uint32_t(p - A0), *reinterpret_cast<const uint8_t*>(p));
-                        fence_proxy_async_smem();  // a later bulk copy overwrites these bytes
-                    }
-                }
-            }
-            mbar_arrive_expect_tx(rfull0 + 8 * rs, bytes);
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-                if (len[i])
-                    bulk_g2s(raw + kGmRawHdr + (lane + 32 * i) * kGmSlotRow, reinterpret_cast<const void*>(src[i]),
-                             len[i], rfull0 + 8 * rs);
         }
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-            if (m0 + lane + 32 * i < a.rows) bad |= cur[i] != rend[lane + 32 * i];
-        if (bad) latch_status(a.hdr, ENDOR_ERR_CORRUPTION);
     } else if (warp == 1) {
         // ===== X producer =====
         if (lane == 0)
             for (uint32_t kb = 0; kb < nkb; ++kb) {
-                const uint32_t st = kb % C::kAB;
-                mbar_wait(empty0 + 8 * st, ((kb / C::kAB) & 1) ^ 1);
-                mbar_arrive_expect_tx(full0 + 8 * st, BN * 128);
+                const uint32_t st = kb % C::kXS;
+                mbar_wait(xempty0 + 8 * st, ((kb / C::kXS) & 1) ^ 1);
+                mbar_arrive_expect_tx(xfull0 + 8 * st, BN * 128);
                 tma_load_2d(sb + C::kB + st * (BN * 128), &xmap, int(k0 + uint64_t(kb) * kGmKB), int(n0),
-                            full0 + 8 * st);
+                            xfull0 + 8 * st);
             }
     } else if (warp == 2) {
-        // ===== MMA issuer =====
+        // ===== MMA issuer: A (the expanded W rows) from TMEM, X from shared memory =====
         // kind::f16: D f32 (bit 4), A = B = f16, both K-major, N >> 3 at bit 17, M >> 4 at bit 24
         constexpr uint32_t idesc = (1u << 4) | (uint32_t(BN >> 3) << 17) | (uint32_t(kGmRows >> 4) << 24);
         for (uint32_t kb = 0; kb < nkb; ++kb) {
-            const uint32_t st = kb % C::kAB;
-            mbar_wait(full0 + 8 * st, (kb / C::kAB) & 1);
+            const uint32_t sx = kb % C::kXS, sa = kb % kGmAS;
+            mbar_wait(xfull0 + 8 * sx, (kb / C::kXS) & 1);
+            mbar_wait(afull0 + 8 * sa, (kb / kGmAS) & 1);
             tc_fence_after();
             if (lane == 0) {
-                const uint64_t ad = umma_desc_sw128(sb + C::kA + st * 16384);
-                const uint64_t bd = umma_desc_sw128(sb + C::kB + st * (BN * 128));
+                const uint32_t at = tmem + BN + 32 * sa;  // A stage: lane = W row, 2 f16 per column
+                const uint64_t bd = umma_desc_sw128(sb + C::kB + sx * (BN * 128));
 #pragma unroll
-                for (int k = 0; k < kGmKB / 16; ++k)  // +32 bytes per K = 16 step inside the swizzle atom
-                    umma_f16(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
-                umma_commit(empty0 + 8 * st);
+                for (int k = 0; k < kGmKB / 16; ++k)  // K = 16: 8 A columns, +32 bytes of X per step
+                    if (!(ENDOR_GEMM_SKIP & 1)) umma_f16_ts(tmem, at + 8 * k, bd + 2 * k, idesc, (kb | k) != 0);
+                umma_commit(xempty0 + 8 * sx);
+                umma_commit(aempty0 + 8 * sa);
                 if (kb + 1 == nkb) umma_commit(tfull);
             }
             __syncwarp();
         }
     } else if (warp >= 4) {
-        // ===== expand into the A stage, then the epilogue =====
+        // ===== expand: thread (row r, k-block parity h) fills row r of every
+        // k-block 2s + h.  It copies its own values window of span s + kGmLook
+        // (16-byte cp.async into a private slot) while expanding span s, so no
+        // other thread touches its raw bytes. =====
         const int q = warp & 3;           // TMEM lane quadrant this warp may access
-        const int h = (warp - 4) >> 2;    // which 4 of the k-block's 8 chunks
+        const int h = (warp - 4) >> 2;    // k-block parity: 0 = even, 1 = odd k-blocks
         const int r = 32 * q + lane;      // W row within the tile
-        const uint32_t sw = uint32_t(r & 7);
-        for (uint32_t s = 0; s < nsp; ++s) {
-            const uint32_t rs = s % C::kRaw;
-            mbar_wait(rfull0 + 8 * rs, (s / C::kRaw) & 1);
-            const uint32_t raw = sb + C::kRawOff + rs * kGmRawBytes;
-            const uint4 bits = lds128(sb + C::kBmpOff + (s % C::kBmp) * kGmBmpBytes + r * 16);
-            uint32_t va = raw + kGmRawHdr + r * kGmSlotRow + lds32(raw + 4 * r);
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const uint32_t kb = 2 * s + j;
-                if (kb >= nkb) break;
-                const uint32_t lo = j ? bits.z : bits.x, hi = j ? bits.w : bits.y;
-                const uint32_t st = kb % C::kAB;
-                const uint32_t m32 = h ? hi : lo;
-                uint32_t ca = va + (h ? 2 * __popc(lo) : 0);
-                va += 2 * (__popc(lo) + __popc(hi));
-                mbar_wait(empty0 + 8 * st, ((kb / C::kAB) & 1) ^ 1);
-                const uint32_t arow = sb + C::kA + st * 16384 + r * 128;
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const uint32_t m = (m32 >> (8 * c)) & 0xFFu;
-                    const uint4 v = gather_chunk<2>(m, ca);
-                    ca += 2 * __popc(m);
-                    sts128(arow + ((uint32_t(4 * h + c) ^ sw) << 4), v);
-                }
-                fence_proxy_async_smem();  // generic-proxy A writes -> the tensor core's async-proxy reads
-                __syncwarp();
-                if (lane == 0) mbar_arrive(full0 + 8 * st);
+        const int et = tid - 4 * 32;      // expand thread 0..255
+        const uint64_t vlo = reinterpret_cast<uint64_t>(a.values), vhi = vlo + a.nnz * 2;
+        const uint64_t safe_lo = (vlo + 15) & ~uint64_t(15), safe_hi = vhi & ~uint64_t(15);
+        const uint32_t win0 = sb + C::kRawOff + et * kGmWin;  // + slot * kGmRawBytes
+        unsigned long long icur = rstart[r], gcur = icur;      // issue / gather cursors (value index)
+        const unsigned long long iend = rend[r];
+        bool bad = icur > iend || iend > a.nnz;
+        // copy this thread's window of span sn (its k-block's values) into slot sn % kGmRaw
+        auto issue = [&](uint32_t sn) {
+            const uint32_t bs = sn % kGmBmp;
+            mbar_wait(bfull0 + 8 * bs, (sn / kGmBmp) & 1);
+            const uint4 bits = lds128(sb + C::kBmpOff + bs * kGmBmpBytes + r * 16);
+            const uint32_t p0 = __popc(bits.x) + __popc(bits.y), p1 = __popc(bits.z) + __popc(bits.w);
+            unsigned long long c0 = icur + (h ? p0 : 0), c1 = c0 + (h ? p1 : p0);
+            icur += p0 + p1;
+            if (c1 > a.nnz) {
+                bad = true;
+                c1 = a.nnz;
+                c0 = c0 < c1 ? c0 : c1;
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(rempty0 + 8 * rs);
+            if (c1 <= c0) return;
+            const uint64_t a0 = vlo + 2 * c0, a1 = vlo + 2 * c1;
+            const uint64_t A0 = a0 & ~uint64_t(15), A1 = (a1 + 15) & ~uint64_t(15);
+            const uint32_t dst = win0 + (sn % kGmRaw) * kGmRawBytes;
+            if (ENDOR_GEMM_SKIP & 4) return;
+            if (A0 >= safe_lo && A1 <= safe_hi) {
+                for (uint64_t p = A0; p < A1; p += 16)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + uint32_t(p - A0)), "l"(p)
+                                 : "memory");
+            } else {  // a window touching a ragged end of the values buffer: bytewise
+                for (uint64_t p = a0; p < a1; ++p) sts8(dst + uint32_t(p - A0), *reinterpret_cast<const uint8_t*>(p));
+            }
+        };
+        for (uint32_t sn = 0; sn < uint32_t(kGmLook); ++sn) {
+            if (sn < nsp) issue(sn);
+            asm volatile("cp.async.commit_group;" ::: "memory");
         }
+        for (uint32_t s = 0; s < nsp; ++s) {
+            if (s + kGmLook < nsp) issue(s + kGmLook);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            asm volatile("cp.async.wait_group %0;" ::"n"(kGmLook) : "memory");  // span s's copies landed
+            const uint32_t bs = s % kGmBmp;
+            const uint4 bits = lds128(sb + C::kBmpOff + bs * kGmBmpBytes + r * 16);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bempty0 + 8 * bs);  // this warp is done with span s's bitmap
+            const uint32_t kb = 2 * s + h;
+            const uint32_t lo = h ? bits.z : bits.x, hi = h ? bits.w : bits.y;
+            const unsigned long long c0 = gcur + (h ? __popc(bits.x) + __popc(bits.y) : 0);
+            gcur += __popc(bits.x) + __popc(bits.y) + __popc(bits.z) + __popc(bits.w);
+            if (kb >= nkb) continue;  // ragged last span: no odd k-block
+            const uint32_t sa = kb % kGmAS;
+            uint32_t ca = win0 + (s % kGmRaw) * kGmRawBytes + uint32_t((vlo + 2 * c0) & 15);
+            // all eight gathers first (their LDS issue back to back), then one TMEM store
+            uint4 v[8];
+            if (!(ENDOR_GEMM_SKIP & 2))
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const uint32_t m = ((c < 4 ? lo : hi) >> (8 * (c & 3))) & 0xFFu;
+                v[c] = gather_chunk<2>(m, ca);
+                ca += 2 * __popc(m);
+            }
+            if (ENDOR_GEMM_SKIP & 2)
+                for (int c = 0; c < 8; ++c) v[c] = make_uint4(lo, hi, ca, c);
+            mbar_wait(aempty0 + 8 * sa, ((kb / kGmAS) & 1) ^ 1);
+            tc_fence_after();
+            tmem_st32(tmem + (uint32_t(32 * q) << 16) + BN + 32 * sa, v);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(afull0 + 8 * sa);
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        if (m0 + r < a.rows && icur != iend) bad = true;
+        if (bad) latch_status(a.hdr, ENDOR_ERR_CORRUPTION);
         // ---- epilogue: TMEM -> registers -> Y (or the split's fp32 partial) ----
         mbar_wait(tfull, 0);
         tc_fence_after();
@@ -416,7 +439,7 @@ __global__ void __launch_bounds__(kGmThreads, 1)
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(uint32_t(BN)) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::kTmemCols) : "memory");
     }
 }
 
@@ -480,21 +503,19 @@ EncodeTiled encode_fn() {
 }  // namespace
 
 template <int BN>
-static cudaError_t launch_bn(const GemmPlan& p, const GemmLaunch& g, const CUtensorMap& xm, const CUtensorMap& bm,
-                             const GemmArgs& a, cudaStream_t s) {
+static cudaError_t launch_bn(const GemmPlan& p, const CUtensorMap& xm, const GemmArgs& a, cudaStream_t s) {
     int bps = 1, sms = 148;
     cudaError_t e = kernel_slots(reinterpret_cast<const void*>(gemm_fused_kernel<BN>), kGmThreads, GmCfg<BN>::kSmem,
                                  &bps, &sms);
     if (e != cudaSuccess) return e;
     const uint64_t units = uint64_t(p.m_tiles) * p.n_tiles * p.ksplit;
-    (void)g;
-    return launch_pdl(gemm_fused_kernel<BN>, dim3(unsigned(units)), dim3(kGmThreads), GmCfg<BN>::kSmem, s, xm, bm, a);
+    return launch_pdl(gemm_fused_kernel<BN>, dim3(unsigned(units)), dim3(kGmThreads), GmCfg<BN>::kSmem, s, xm, a);
 }
 
 cudaError_t launch_gemm_fused(const GemmPlan& p, const GemmLaunch& g, cudaStream_t s) {
     EncodeTiled enc = encode_fn();
     if (!enc) return cudaErrorNotSupported;
-    CUtensorMap xm{}, bm{};
+    CUtensorMap xm{};
     {
         const cuuint64_t dims[2] = {g.cols, g.tokens};
         const cuuint64_t strides[1] = {g.x_ld * 2};
@@ -504,16 +525,7 @@ cudaError_t launch_gemm_fused(const GemmPlan& p, const GemmLaunch& g, cudaStream
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return cudaErrorInvalidValue;
     }
-    const bool bmp_tma = g.cols % kGmSpan == 0 && (reinterpret_cast<uintptr_t>(g.bitmap) & 15) == 0;
-    if (bmp_tma) {
-        const cuuint64_t dims[2] = {g.cols / 8, g.rows};
-        const cuuint64_t strides[1] = {g.cols / 8};
-        const cuuint32_t box[2] = {16, uint32_t(kGmRows)}, es[2] = {1, 1};
-        if (enc(&bm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(g.bitmap), dims, strides, box, es,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-            return cudaErrorInvalidValue;
-    }
+    const bool bmp_async = g.cols % kGmSpan == 0 && (reinterpret_cast<uintptr_t>(g.bitmap) & 15) == 0;
     GemmArgs a{};
     a.bitmap = g.bitmap;
     a.nbytes = (g.rows * g.cols + 7) / 8;
@@ -532,10 +544,10 @@ cudaError_t launch_gemm_fused(const GemmPlan& p, const GemmLaunch& g, cudaStream
     a.y32 = g.y32;
     a.y16 = reinterpret_cast<__half*>(g.y16);
     a.hdr = g.hdr;
-    a.bmp_tma = bmp_tma ? 1 : 0;
-    cudaError_t e = p.bn == 64    ? launch_bn<64>(p, g, xm, bm, a, s)
-                    : p.bn == 128 ? launch_bn<128>(p, g, xm, bm, a, s)
-                                  : launch_bn<256>(p, g, xm, bm, a, s);
+    a.bmp_async = bmp_async ? 1 : 0;
+    cudaError_t e = p.bn == 64    ? launch_bn<64>(p, xm, a, s)
+                    : p.bn == 128 ? launch_bn<128>(p, xm, a, s)
+                                  : launch_bn<256>(p, xm, a, s);
     if (e != cudaSuccess || p.ksplit <= 1) return e;
     const uint64_t count = g.tokens * g.rows;
     const unsigned blocks = unsigned(umin64(ceil_div(count, 256), 148 * 8));
