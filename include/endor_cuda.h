@@ -322,6 +322,18 @@ int endor_cuda_gemv_compressed_batch(const endor_tensor_view* views, const uint6
  * Deterministic (split-K partials are summed in a fixed order).  Workspace:
  * endor_cuda_gemm_workspace_bytes(rows, cols, tokens). */
 size_t endor_cuda_gemm_workspace_bytes(uint64_t rows, uint64_t cols, uint64_t tokens);
+/* (Above ENDOR_GEMM_TWO_PASS_TOKENS tokens, default 384, gemm_compressed
+ * decompresses W once into the workspace -- included in the size above -- and
+ * runs the dense GEMM below: the fused kernel would re-expand each W tile once
+ * per 256-token tile.) */
+
+/* Dense GEMM consumer on tcgen05 (no cuBLAS): Y[t, r] = sum_c W[r, c] X[t, c]
+ * with W a dense f16 [rows][cols] (16-byte aligned, cols % 8 == 0), X as in
+ * endor_cuda_gemm_compressed, fp32 accumulation, Y [tokens][rows] as y_f32
+ * and/or y_f16.  Workspace: endor_cuda_gemm_workspace_bytes(rows, cols,
+ * tokens) bytes (split-K partials; zero-initialised once). */
+int endor_cuda_gemm(uint64_t rows, uint64_t cols, const void* w_f16, const void* x_f16, uint64_t tokens,
+                    uint64_t x_ld, float* y_f32, void* y_f16, void* ws, size_t ws_bytes, void* stream);
 int endor_cuda_gemm_compressed(const endor_tensor_view* t, const uint64_t* prefix1024, const void* x_f16,
                                uint64_t tokens, uint64_t x_ld, float* y_f32, void* y_f16, void* ws, size_t ws_bytes,
                                void* stream);

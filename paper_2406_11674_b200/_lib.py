@@ -65,6 +65,7 @@ SIGNATURES = {
                                                       C.POINTER(_vp), C.c_int, _vp, _sz, _vp]),
     "endor_cuda_decompress_dequant": (C.c_int, [C.POINTER(TensorView), C.c_float, _vp, _vp, _sz, _vp]),
     "endor_cuda_gemm_workspace_bytes": (_sz, [_u64, _u64, _u64]),
+    "endor_cuda_gemm": (C.c_int, [_u64, _u64, _vp, _vp, _u64, _u64, _vp, _vp, _vp, _sz, _vp]),
     "endor_cuda_gemm_compressed": (C.c_int, [C.POINTER(TensorView), _vp, _vp, _u64, _u64, _vp, _vp, _vp, _sz,
                                              _vp]),
     "endor_cuda_gemv_compressed": (C.c_int, [C.POINTER(TensorView), _vp, _vp, _vp, _vp, _vp, _sz, _vp]),

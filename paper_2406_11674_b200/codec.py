@@ -151,11 +151,12 @@ def _alloc(nbytes: int, device: torch.device, pad: int = 16) -> torch.Tensor:
 _WS: Dict[Tuple[int, int], torch.Tensor] = {}
 
 
-def workspace(n: int, device: torch.device) -> torch.Tensor:
-    """Zero-initialised workspace for tensors of up to n elements, one per
-    (device, stream) -- the library leaves it zeroed after every call."""
+def workspace(n: int, device: torch.device, min_bytes: int = 0) -> torch.Tensor:
+    """Zero-initialised workspace for tensors of up to n elements (and at
+    least min_bytes), one per (device, stream), grown on demand -- the library
+    leaves it zeroed after every call."""
     key = (device.index, _stream_ptr(device))
-    need = _lib.lib().endor_cuda_workspace_bytes(max(n, 1), 1)
+    need = max(_lib.lib().endor_cuda_workspace_bytes(max(n, 1), 1), min_bytes)
     ws = _WS.get(key)
     if ws is None or ws.numel() < need:
         ws = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=device)
@@ -411,10 +412,7 @@ def gemm_compressed(t: EndorTensor, x: torch.Tensor, index: Optional[RankIndex] 
     if out_dtype not in (torch.float32, torch.float16):
         raise InvalidArgument("gemm_compressed: out_dtype must be float32 or float16")
     L = _lib.lib()
-    ws = workspace(t.element_count(), dev)
-    need = L.endor_cuda_gemm_workspace_bytes(t.rows, t.cols, tokens)
-    if ws.numel() < need:
-        ws = torch.zeros(need, dtype=torch.uint8, device=dev)
+    ws = workspace(t.element_count(), dev, L.endor_cuda_gemm_workspace_bytes(t.rows, t.cols, tokens))
     pre = None
     if index is not None:
         if index.chunk_size != 1024:
@@ -424,6 +422,27 @@ def gemm_compressed(t: EndorTensor, x: torch.Tensor, index: Optional[RankIndex] 
     y32, y16 = (y, None) if out_dtype == torch.float32 else (None, y)
     check(L.endor_cuda_gemm_compressed(C.byref(v), _ptr(pre), _ptr(xc), tokens, ld, _ptr(y32), _ptr(y16),
                                        ws.data_ptr(), ws.numel(), _stream_ptr(dev)))
+    sync_status(ws, dev)
+    return y
+
+
+def gemm(w: DenseMatrix, x: torch.Tensor, out_dtype: torch.dtype = torch.float32) -> torch.Tensor:
+    """Y = X W^T for a dense f16 W [rows, cols] (cols % 8 == 0) on the tcgen05
+    tensor cores (no cuBLAS): x f16 [tokens, cols] -> Y [tokens, rows]."""
+    dev = w.data.device
+    rows, cols = w.rows, w.cols
+    if w.dtype != Dtype.F16 or x.dtype != torch.float16 or x.dim() != 2 or x.shape[1] != cols:
+        raise InvalidArgument("gemm needs an f16 W [rows, cols] and f16 X [tokens, cols]")
+    if out_dtype not in (torch.float32, torch.float16):
+        raise InvalidArgument("gemm: out_dtype must be float32 or float16")
+    tokens = x.shape[0]
+    xc = x.contiguous()
+    y = torch.empty((tokens, rows), dtype=out_dtype, device=dev)
+    L = _lib.lib()
+    ws = workspace(1, dev, L.endor_cuda_gemm_workspace_bytes(rows, cols, tokens))
+    y32, y16 = (y, None) if out_dtype == torch.float32 else (None, y)
+    check(L.endor_cuda_gemm(rows, cols, _ptr(w.data), _ptr(xc), tokens, cols, _ptr(y32), _ptr(y16), ws.data_ptr(),
+                            ws.numel(), _stream_ptr(dev)))
     sync_status(ws, dev)
     return y
 

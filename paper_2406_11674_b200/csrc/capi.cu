@@ -455,7 +455,43 @@ size_t endor_cuda_gemm_workspace_bytes(uint64_t rows, uint64_t cols, uint64_t to
     uint64_t n;
     if (!checked_n(rows, cols, &n)) return 0;
     const GemmPlan p = gemm_plan(rows, cols, tokens, count_ctas() / 3);
-    return ws_layout(nullptr, n).bytes + align256(p.part_bytes);
+    return ws_layout(nullptr, n).bytes + align256(p.part_bytes) + (p.two_pass ? align256(n * 2) : 0);
+}
+
+int endor_cuda_gemm(uint64_t rows, uint64_t cols, const void* w_f16, const void* x_f16, uint64_t tokens,
+                    uint64_t x_ld, float* y_f32, void* y_f16, void* ws, size_t ws_bytes, void* stream) {
+    uint64_t n;
+    if (!checked_n(rows, cols, &n)) return fail(ENDOR_ERR_SIZE, "matrix dimensions overflow the addressable element count");
+    if (!y_f32 && !y_f16) return fail(ENDOR_ERR_INVALID_ARGUMENT, "y must be given");
+    if (tokens == 0 || rows == 0) return ENDOR_OK;
+    if (cols == 0) {
+        if (y_f32) CK(cudaMemsetAsync(y_f32, 0, tokens * rows * 4, S(stream)));
+        if (y_f16) CK(cudaMemsetAsync(y_f16, 0, tokens * rows * 2, S(stream)));
+        return ENDOR_OK;
+    }
+    if (!w_f16 || !aligned(w_f16, 16) || cols % 8)
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "W must be a 16-byte aligned f16 [rows][cols] with cols % 8 == 0");
+    if (!x_f16 || !aligned(x_f16, 16) || x_ld < cols || x_ld % 8)
+        return fail(ENDOR_ERR_INVALID_ARGUMENT,
+                    "x must be a 16-byte aligned f16 [tokens][x_ld] with x_ld >= cols and x_ld % 8 == 0");
+    if (cols > 0x7FFFFFFFull || tokens > 0x7FFFFFFFull || rows > 0x7FFFFFFFull)
+        return fail(ENDOR_ERR_SIZE, "GEMM: rows, cols and tokens must fit the TMA coordinate range (< 2^31)");
+    GemmPlan p = gemm_plan(rows, cols, tokens, count_ctas() / 3);
+    if (!ws || !aligned(ws, 256) || ws_bytes < 256 + align256(p.part_bytes))
+        return fail(ENDOR_ERR_INVALID_ARGUMENT, "workspace too small (endor_cuda_gemm_workspace_bytes)");
+    GemmLaunch g{};
+    g.rows = rows;
+    g.cols = cols;
+    g.tokens = tokens;
+    g.x = x_f16;
+    g.x_ld = x_ld;
+    g.part = reinterpret_cast<float*>(static_cast<char*>(ws) + 256);
+    g.y32 = y_f32;
+    g.y16 = y_f16;
+    g.hdr = static_cast<WsHeader*>(ws);
+    g.w_dense = w_f16;
+    CK(launch_gemm_fused(p, g, S(stream)));
+    return ENDOR_OK;
 }
 
 int endor_cuda_gemm_compressed(const endor_tensor_view* t, const uint64_t* prefix1024, const void* x_f16,
@@ -483,10 +519,45 @@ int endor_cuda_gemm_compressed(const endor_tensor_view* t, const uint64_t* prefi
     WsLayout L;
     if ((st = check_ws(ws, ws_bytes, n, &L))) return st;
     const GemmPlan p = gemm_plan(t->rows, t->cols, tokens, count_ctas() / 3);
-    if (ws_bytes < L.bytes + align256(p.part_bytes))
+    if (ws_bytes < L.bytes + align256(p.part_bytes) + (p.two_pass ? align256(n * 2) : 0))
         return fail(ENDOR_ERR_INVALID_ARGUMENT, "workspace too small (endor_cuda_gemm_workspace_bytes)");
     const unsigned long long* idx = reinterpret_cast<const unsigned long long*>(prefix1024);
-    if (!idx) {
+    void* wd = p.two_pass ? static_cast<char*>(ws) + L.bytes + align256(p.part_bytes) : nullptr;
+    if (p.two_pass) {
+        // decompress W once into the workspace (the hot path: count + TMA expand,
+        // or one expand launch with the caller's index), then the dense GEMM
+        Batch b{};
+        b.count = 1;
+        b.check_total = 1;
+        b.t[0].bitmap = static_cast<const uint8_t*>(t->bitmap);
+        b.t[0].values = static_cast<const uint8_t*>(t->values);
+        b.t[0].dst = static_cast<uint8_t*>(wd);
+        b.t[0].n = n;
+        b.t[0].nnz = t->nnz;
+        b.t[0].idx = idx;
+        uint64_t sub_cap, blk_cap;
+        batch_plan(b, &sub_cap, &blk_cap, count_ctas());
+        b.tsub = L.tsub;
+        b.blk = L.blk;
+        b.hdr = L.hdr;
+        if (aligned(t->bitmap, 16)) {
+            CK(launch_count(b, S(stream)));  // no-op for an indexed tensor
+            CK(launch_expand_tma(b, 2, S(stream)));
+        } else {
+            ScanArgs a = scan_args(t->bitmap, n, 0, n, L);
+            a.check_total = 1;
+            a.expect_total = t->nnz;
+            if (idx) {
+                a.cs = kSubElems;
+                a.idx_in = idx;
+            }
+            ExpandArgs x = expand_args(t, n, 0, n, wd, L);
+            a.tprefix = L.tprefix;
+            CK(launch_scan(a, S(stream)));
+            CK(launch_expand(x, 2, S(stream)));
+        }
+        idx = nullptr;
+    } else if (!idx) {
         // rank table of the reference's decompress (codec.hpp:157-160): counts,
         // checks popcount == nnz and the padding bits, flat absolute offsets
         if (aligned(t->bitmap, 16)) {
@@ -528,6 +599,7 @@ int endor_cuda_gemm_compressed(const endor_tensor_view* t, const uint64_t* prefi
     g.y32 = y_f32;
     g.y16 = y_f16;
     g.hdr = L.hdr;
+    g.w_dense = wd;
     CK(launch_gemm_fused(p, g, S(stream)));
     return ENDOR_OK;
 }

@@ -37,6 +37,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -54,25 +55,25 @@ namespace endor_b200 {
 constexpr int kGmRows = 128;                        // UMMA M
 constexpr int kGmKB = 64;                           // k-block: 64 f16 = one 128-byte swizzle row
 constexpr int kGmSpan = 128;                        // bitmap span: 2 k-blocks, 16 bytes per row
-constexpr int kGmWin = 144;                         // per-thread values window: <= 64 values + 16-byte slack
-constexpr int kGmExpandWarps = 8;
+constexpr int kGmWin = 80;                          // per-thread values window: <= 32 values + 16-byte slack
+constexpr int kGmExpandWarps = 16;
 constexpr int kGmExpandThreads = kGmExpandWarps * 32;
-constexpr int kGmRawBytes = kGmExpandThreads * kGmWin;  // one span's windows: 36 KiB
+constexpr int kGmRawBytes = kGmExpandThreads * kGmWin;  // one span's windows: 40 KiB
 constexpr int kGmBmpBytes = kGmRows * 16;           // 2048
-constexpr int kGmThreads = (4 + kGmExpandWarps) * 32;  // 384
-constexpr int kGmLook = 2;                          // spans of value copies in flight per thread
-constexpr int kGmRaw = kGmLook + 1;                 // private window slots per thread
+constexpr int kGmThreads = (4 + kGmExpandWarps) * 32;  // 640
 constexpr int kGmBmp = 8;                           // bitmap ring (spans)
 
-constexpr int kGmAS = 4;                           // A stages, in TMEM (32 columns each)
+constexpr int kGmAS = 8;                           // A stages, in TMEM (32 columns each)
 
 template <int BN>
 struct GmCfg {
-    static constexpr int kXS = BN == 64 ? 8 : (BN == 128 ? 6 : 3);  // X stages (TMA ring in smem)
+    static constexpr int kXS = BN == 64 ? 8 : (BN == 128 ? 5 : 3);  // X stages (TMA ring in smem)
+    static constexpr int kLook = BN == 256 ? 1 : 2;                 // spans of value copies in flight per thread
+    static constexpr int kRaw = kLook + 1;                          // private window slots per thread
     static constexpr uint32_t kTmemCols = BN + 32 * kGmAS <= 256 ? 256 : 512;  // accumulator + A stages
     static constexpr uint32_t kB = 0;                             // X tiles, BN x 128 bytes (1024-aligned)
     static constexpr uint32_t kRawOff = kB + kXS * BN * 128;
-    static constexpr uint32_t kBmpOff = kRawOff + kGmRaw * kGmRawBytes;
+    static constexpr uint32_t kBmpOff = kRawOff + kRaw * kGmRawBytes;
     static constexpr uint32_t kBar = kBmpOff + kGmBmp * kGmBmpBytes;
     // xfull[kXS] xempty[kXS] afull[kAS] aempty[kAS] bmp_full[kBmp] bmp_empty[kBmp] tmem_full, tmem addr
     static constexpr uint32_t kTmemSlot = kBar + 8 * (2 * kXS + 2 * kGmAS + 2 * kGmBmp + 1);
@@ -137,6 +138,15 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint4 (&v)[8]) {
           "r"(v[3].w), "r"(v[4].x), "r"(v[4].y), "r"(v[4].z), "r"(v[4].w), "r"(v[5].x), "r"(v[5].y), "r"(v[5].z),
           "r"(v[5].w), "r"(v[6].x), "r"(v[6].y), "r"(v[6].z), "r"(v[6].w), "r"(v[7].x), "r"(v[7].y), "r"(v[7].z),
           "r"(v[7].w)
+        : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint4 (&v)[4]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+        ::"r"(taddr), "r"(v[0].x), "r"(v[0].y), "r"(v[0].z), "r"(v[0].w), "r"(v[1].x), "r"(v[1].y), "r"(v[1].z),
+          "r"(v[1].w), "r"(v[2].x), "r"(v[2].y), "r"(v[2].z), "r"(v[2].w), "r"(v[3].x), "r"(v[3].y), "r"(v[3].z),
+          "r"(v[3].w)
         : "memory");
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
@@ -212,7 +222,7 @@ __global__ void __launch_bounds__(kGmThreads, 1)
             mbar_init(xempty0 + 8 * s, 1);                    // tcgen05.commit
         }
         for (int s = 0; s < kGmAS; ++s) {
-            mbar_init(afull0 + 8 * s, kGmExpandWarps / 2);    // the 4 warps of a k-block parity
+            mbar_init(afull0 + 8 * s, kGmExpandWarps / 2);    // the 8 warps of a k-block parity
             mbar_init(aempty0 + 8 * s, 1);                    // tcgen05.commit
         }
         for (int s = 0; s < kGmBmp; ++s) {
@@ -329,28 +339,37 @@ __global__ void __launch_bounds__(kGmThreads, 1)
             __syncwarp();
         }
     } else if (warp >= 4) {
-        // ===== expand: thread (row r, k-block parity h) fills row r of every
-        // k-block 2s + h.  It copies its own values window of span s + kGmLook
-        // (16-byte cp.async into a private slot) while expanding span s, so no
-        // other thread touches its raw bytes. =====
+        // ===== expand: thread (row r, k-block parity h, half c2) fills 32
+        // columns of row r of every k-block 2s + h.  It copies its own values
+        // window of span s + kLook (16-byte cp.async into a private slot) while
+        // expanding span s, so no other thread touches its raw bytes. =====
+        const int ew = warp - 4;          // expand warp 0..15
         const int q = warp & 3;           // TMEM lane quadrant this warp may access
-        const int h = (warp - 4) >> 2;    // k-block parity: 0 = even, 1 = odd k-blocks
+        const int h = (ew >> 2) & 1;      // k-block parity: 0 = even, 1 = odd k-blocks
+        const int c2 = ew >> 3;           // which 32 columns of the k-block
+        const int wsel = 2 * h + c2;      // bitmap word of the span (32 columns each)
         const int r = 32 * q + lane;      // W row within the tile
-        const int et = tid - 4 * 32;      // expand thread 0..255
+        const int et = tid - 4 * 32;      // expand thread 0..511
         const uint64_t vlo = reinterpret_cast<uint64_t>(a.values), vhi = vlo + a.nnz * 2;
         const uint64_t safe_lo = (vlo + 15) & ~uint64_t(15), safe_hi = vhi & ~uint64_t(15);
         const uint32_t win0 = sb + C::kRawOff + et * kGmWin;  // + slot * kGmRawBytes
         unsigned long long icur = rstart[r], gcur = icur;      // issue / gather cursors (value index)
         const unsigned long long iend = rend[r];
         bool bad = icur > iend || iend > a.nnz;
-        // copy this thread's window of span sn (its k-block's values) into slot sn % kGmRaw
+        auto word = [](const uint4& b, int i) { return i == 0 ? b.x : (i == 1 ? b.y : (i == 2 ? b.z : b.w)); };
+        auto before = [&](const uint4& b) {  // set bits of the span ahead of this thread's 32 columns
+            uint32_t n = 0;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) n += i < wsel ? __popc(word(b, i)) : 0u;
+            return n;
+        };
+        // copy this thread's window of span sn into slot sn % kRaw
         auto issue = [&](uint32_t sn) {
             const uint32_t bs = sn % kGmBmp;
             mbar_wait(bfull0 + 8 * bs, (sn / kGmBmp) & 1);
             const uint4 bits = lds128(sb + C::kBmpOff + bs * kGmBmpBytes + r * 16);
-            const uint32_t p0 = __popc(bits.x) + __popc(bits.y), p1 = __popc(bits.z) + __popc(bits.w);
-            unsigned long long c0 = icur + (h ? p0 : 0), c1 = c0 + (h ? p1 : p0);
-            icur += p0 + p1;
+            unsigned long long c0 = icur + before(bits), c1 = c0 + __popc(word(bits, wsel));
+            icur += __popc(bits.x) + __popc(bits.y) + __popc(bits.z) + __popc(bits.w);
             if (c1 > a.nnz) {
                 bad = true;
                 c1 = a.nnz;
@@ -359,7 +378,7 @@ __global__ void __launch_bounds__(kGmThreads, 1)
             if (c1 <= c0) return;
             const uint64_t a0 = vlo + 2 * c0, a1 = vlo + 2 * c1;
             const uint64_t A0 = a0 & ~uint64_t(15), A1 = (a1 + 15) & ~uint64_t(15);
-            const uint32_t dst = win0 + (sn % kGmRaw) * kGmRawBytes;
+            const uint32_t dst = win0 + (sn % C::kRaw) * kGmRawBytes;
             if (ENDOR_GEMM_SKIP & 4) return;
             if (A0 >= safe_lo && A1 <= safe_hi) {
                 for (uint64_t p = A0; p < A1; p += 16)
@@ -369,39 +388,39 @@ __global__ void __launch_bounds__(kGmThreads, 1)
                 for (uint64_t p = a0; p < a1; ++p) sts8(dst + uint32_t(p - A0), *reinterpret_cast<const uint8_t*>(p));
             }
         };
-        for (uint32_t sn = 0; sn < uint32_t(kGmLook); ++sn) {
+        for (uint32_t sn = 0; sn < uint32_t(C::kLook); ++sn) {
             if (sn < nsp) issue(sn);
             asm volatile("cp.async.commit_group;" ::: "memory");
         }
         for (uint32_t s = 0; s < nsp; ++s) {
-            if (s + kGmLook < nsp) issue(s + kGmLook);
+            if (s + C::kLook < nsp) issue(s + C::kLook);
             asm volatile("cp.async.commit_group;" ::: "memory");
-            asm volatile("cp.async.wait_group %0;" ::"n"(kGmLook) : "memory");  // span s's copies landed
+            asm volatile("cp.async.wait_group %0;" ::"n"(C::kLook) : "memory");  // span s's copies landed
             const uint32_t bs = s % kGmBmp;
             const uint4 bits = lds128(sb + C::kBmpOff + bs * kGmBmpBytes + r * 16);
             __syncwarp();
             if (lane == 0) mbar_arrive(bempty0 + 8 * bs);  // this warp is done with span s's bitmap
             const uint32_t kb = 2 * s + h;
-            const uint32_t lo = h ? bits.z : bits.x, hi = h ? bits.w : bits.y;
-            const unsigned long long c0 = gcur + (h ? __popc(bits.x) + __popc(bits.y) : 0);
+            const uint32_t m32 = word(bits, wsel);
+            const unsigned long long c0 = gcur + before(bits);
             gcur += __popc(bits.x) + __popc(bits.y) + __popc(bits.z) + __popc(bits.w);
             if (kb >= nkb) continue;  // ragged last span: no odd k-block
             const uint32_t sa = kb % kGmAS;
-            uint32_t ca = win0 + (s % kGmRaw) * kGmRawBytes + uint32_t((vlo + 2 * c0) & 15);
-            // all eight gathers first (their LDS issue back to back), then one TMEM store
-            uint4 v[8];
+            uint32_t ca = win0 + (s % C::kRaw) * kGmRawBytes + uint32_t((vlo + 2 * c0) & 15);
+            // all four gathers first (their LDS issue back to back), then one TMEM store
+            uint4 v[4];
             if (!(ENDOR_GEMM_SKIP & 2))
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const uint32_t m = ((c < 4 ? lo : hi) >> (8 * (c & 3))) & 0xFFu;
+            for (int c = 0; c < 4; ++c) {
+                const uint32_t m = (m32 >> (8 * c)) & 0xFFu;
                 v[c] = gather_chunk<2>(m, ca);
                 ca += 2 * __popc(m);
             }
             if (ENDOR_GEMM_SKIP & 2)
-                for (int c = 0; c < 8; ++c) v[c] = make_uint4(lo, hi, ca, c);
+                for (int c = 0; c < 4; ++c) v[c] = make_uint4(m32, ca, c, 0);
             mbar_wait(aempty0 + 8 * sa, ((kb / kGmAS) & 1) ^ 1);
             tc_fence_after();
-            tmem_st32(tmem + (uint32_t(32 * q) << 16) + BN + 32 * sa, v);
+            tmem_st16(tmem + (uint32_t(32 * q) << 16) + BN + 32 * sa + 16 * c2, v);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(afull0 + 8 * sa);
@@ -413,15 +432,16 @@ __global__ void __launch_bounds__(kGmThreads, 1)
         mbar_wait(tfull, 0);
         tc_fence_after();
         const uint64_t gr = m0 + r;
-        constexpr int kHalf = BN / 2;
+        constexpr int kQuarter = BN / 4;  // columns per expand warp of this lane quadrant
+        const int col0 = (ew >> 2) * kQuarter;
 #pragma unroll 1
-        for (int c0 = 0; c0 < kHalf; c0 += 16) {
+        for (int c0 = 0; c0 < kQuarter; c0 += 16) {
             uint32_t v[16];
-            tmem_ld16(tmem + (uint32_t(32 * q) << 16) + uint32_t(h * kHalf + c0), v);
+            tmem_ld16(tmem + (uint32_t(32 * q) << 16) + uint32_t(col0 + c0), v);
             if (gr < a.rows) {
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
-                    const uint64_t n = uint64_t(n0) + h * kHalf + c0 + i;
+                    const uint64_t n = uint64_t(n0) + col0 + c0 + i;
                     if (n < a.tokens) {
                         const float f = __uint_as_float(v[i]);
                         if (a.ksplit > 1) {
@@ -438,6 +458,127 @@ __global__ void __launch_bounds__(kGmThreads, 1)
     }
     __syncthreads();
     if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::kTmemCols) : "memory");
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// Dense GEMM consumer (the two-pass path for large token counts, and
+// endor_cuda_gemm): Y = X W^T with W already decompressed in HBM.  A canonical
+// tcgen05 pipeline: one TMA warp loads each k-block's 128 x 64 W tile and BN x 64
+// X tile (128-byte swizzle) into a kDS-deep ring, one elected lane issues 4 SS
+// MMAs per k-block into a TMEM accumulator, four epilogue warps drain it.
+// ---------------------------------------------------------------------------------
+constexpr int kGdThreads = 256;
+template <int BN>
+struct GdCfg {
+    static constexpr int kStage = 16384 + BN * 128;
+    static constexpr int kDS = (200 * 1024) / kStage;             // 4 (BN 256), 6 (128), 8 (64)
+    static constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
+    static constexpr uint32_t kBar = kDS * kStage;
+    static constexpr uint32_t kTmemSlot = kBar + 8 * (2 * kDS + 1);
+    static constexpr uint32_t kSmem = kTmemSlot + 16 + 1024;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(kGdThreads, 1)
+    gemm_dense_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap xmap,
+                      const __grid_constant__ GemmArgs a) {
+    using C = GdCfg<BN>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t sraw = smem_u32(smem_raw);
+    const uint32_t sb = (sraw + 1023u) & ~1023u;
+    uint8_t* const smem = smem_raw + (sb - sraw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t full0 = sb + C::kBar, empty0 = full0 + 8 * C::kDS, tfull = empty0 + 8 * C::kDS;
+    uint32_t u = blockIdx.x;
+    const uint32_t nt = u % a.n_tiles;
+    u /= a.n_tiles;
+    const uint32_t ks = u % a.ksplit, mt = u / a.ksplit;
+    const uint64_t m0 = uint64_t(mt) * kGmRows;
+    const uint32_t n0 = nt * BN;
+    const uint64_t sp0 = uint64_t(ks) * a.sps;
+    const uint32_t nsp = uint32_t(umin64(a.nspans, sp0 + a.sps) - sp0);
+    const uint64_t k0 = sp0 * kGmSpan, k1 = umin64(a.cols, k0 + uint64_t(nsp) * kGmSpan);
+    const uint32_t nkb = uint32_t((k1 - k0 + kGmKB - 1) / kGmKB);
+    if (tid == 0) {
+        for (int s = 0; s < C::kDS; ++s) {
+            mbar_init(full0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, 1);
+        }
+        mbar_init(tfull, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&wmap)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
+    }
+    pdl_wait();  // W comes from the decompress launch before this one
+    if (cta_error_latched(a.hdr)) return;
+    pdl_launch_dependents();
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sb + C::kTmemSlot),
+                     "r"(C::kTmemCols) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + C::kTmemSlot);
+    if (warp == 0) {
+        if (lane == 0)
+            for (uint32_t kb = 0; kb < nkb; ++kb) {
+                const uint32_t st = kb % C::kDS;
+                mbar_wait(empty0 + 8 * st, ((kb / C::kDS) & 1) ^ 1);
+                mbar_arrive_expect_tx(full0 + 8 * st, C::kStage);
+                const int kc = int(k0 + uint64_t(kb) * kGmKB);
+                tma_load_2d(sb + st * C::kStage, &wmap, kc, int(m0), full0 + 8 * st);
+                tma_load_2d(sb + st * C::kStage + 16384, &xmap, kc, int(n0), full0 + 8 * st);
+            }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc = (1u << 4) | (uint32_t(BN >> 3) << 17) | (uint32_t(kGmRows >> 4) << 24);
+        for (uint32_t kb = 0; kb < nkb; ++kb) {
+            const uint32_t st = kb % C::kDS;
+            mbar_wait(full0 + 8 * st, (kb / C::kDS) & 1);
+            tc_fence_after();
+            if (lane == 0) {
+                const uint64_t ad = umma_desc_sw128(sb + st * C::kStage);
+                const uint64_t bd = umma_desc_sw128(sb + st * C::kStage + 16384);
+#pragma unroll
+                for (int k = 0; k < kGmKB / 16; ++k) umma_f16(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+                umma_commit(empty0 + 8 * st);
+                if (kb + 1 == nkb) umma_commit(tfull);
+            }
+            __syncwarp();
+        }
+    } else if (warp >= 4) {
+        const int q = warp & 3, r = 32 * q + lane;
+        const uint64_t gr = m0 + r;
+        mbar_wait(tfull, 0);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+            uint32_t v[16];
+            tmem_ld16(tmem + (uint32_t(32 * q) << 16) + uint32_t(c0), v);
+            if (gr < a.rows) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const uint64_t n = uint64_t(n0) + c0 + i;
+                    if (n < a.tokens) {
+                        const float f = __uint_as_float(v[i]);
+                        if (a.ksplit > 1) {
+                            a.part[(uint64_t(ks) * a.tokens + n) * a.rows + gr] = f;
+                        } else {
+                            if (a.y32) a.y32[n * a.rows + gr] = f;
+                            if (a.y16) a.y16[n * a.rows + gr] = __float2half_rn(f);
+                        }
+                    }
+                }
+            }
+        }
+        tc_fence_before();
+    }
+    __syncthreads();
+    if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::kTmemCols) : "memory");
     }
@@ -481,6 +622,15 @@ GemmPlan gemm_plan(uint64_t rows, uint64_t cols, uint64_t tokens, int sms) {
     p.sps = uint32_t(ceil_div(p.nspans, best));
     p.ksplit = uint32_t(ceil_div(p.nspans, p.sps));
     p.part_bytes = p.ksplit > 1 ? p.ksplit * tokens * rows * 4 : 0;
+    // Large token counts: the fused kernel re-expands each W tile once per
+    // 256-token n-tile, so past ~384 tokens decompressing W once into HBM (at
+    // the copy roofline) and running the dense tcgen05 GEMM wins (fc1: fused
+    // 0.52 vs 0.45 ms at 512 tokens, 1.91 vs 1.12 ms at 2048; profiles/r02).
+    static const uint64_t two_pass_tokens = [] {
+        const char* e = getenv("ENDOR_GEMM_TWO_PASS_TOKENS");
+        return e ? uint64_t(strtoull(e, nullptr, 10)) : uint64_t(384);
+    }();
+    p.two_pass = tokens > two_pass_tokens && cols % 8 == 0;
     return p;
 }
 
@@ -510,6 +660,17 @@ static cudaError_t launch_bn(const GemmPlan& p, const CUtensorMap& xm, const Gem
     if (e != cudaSuccess) return e;
     const uint64_t units = uint64_t(p.m_tiles) * p.n_tiles * p.ksplit;
     return launch_pdl(gemm_fused_kernel<BN>, dim3(unsigned(units)), dim3(kGmThreads), GmCfg<BN>::kSmem, s, xm, a);
+}
+
+template <int BN>
+static cudaError_t launch_dense(const GemmPlan& p, const CUtensorMap& wm, const CUtensorMap& xm, const GemmArgs& a,
+                                cudaStream_t s) {
+    int bps = 1, sms = 148;
+    cudaError_t e = kernel_slots(reinterpret_cast<const void*>(gemm_dense_kernel<BN>), kGdThreads, GdCfg<BN>::kSmem,
+                                 &bps, &sms);
+    if (e != cudaSuccess) return e;
+    const uint64_t units = uint64_t(p.m_tiles) * p.n_tiles * p.ksplit;
+    return launch_pdl(gemm_dense_kernel<BN>, dim3(unsigned(units)), dim3(kGdThreads), GdCfg<BN>::kSmem, s, wm, xm, a);
 }
 
 cudaError_t launch_gemm_fused(const GemmPlan& p, const GemmLaunch& g, cudaStream_t s) {
@@ -545,9 +706,24 @@ cudaError_t launch_gemm_fused(const GemmPlan& p, const GemmLaunch& g, cudaStream
     a.y16 = reinterpret_cast<__half*>(g.y16);
     a.hdr = g.hdr;
     a.bmp_async = bmp_async ? 1 : 0;
-    cudaError_t e = p.bn == 64    ? launch_bn<64>(p, xm, a, s)
-                    : p.bn == 128 ? launch_bn<128>(p, xm, a, s)
-                                  : launch_bn<256>(p, xm, a, s);
+    cudaError_t e;
+    if (g.w_dense) {
+        CUtensorMap wm{};
+        const cuuint64_t dims[2] = {g.cols, g.rows};
+        const cuuint64_t strides[1] = {g.cols * 2};
+        const cuuint32_t box[2] = {uint32_t(kGmKB), uint32_t(kGmRows)}, es[2] = {1, 1};
+        if (enc(&wm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(g.w_dense), dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+        e = p.bn == 64    ? launch_dense<64>(p, wm, xm, a, s)
+            : p.bn == 128 ? launch_dense<128>(p, wm, xm, a, s)
+                          : launch_dense<256>(p, wm, xm, a, s);
+    } else {
+        e = p.bn == 64    ? launch_bn<64>(p, xm, a, s)
+            : p.bn == 128 ? launch_bn<128>(p, xm, a, s)
+                          : launch_bn<256>(p, xm, a, s);
+    }
     if (e != cudaSuccess || p.ksplit <= 1) return e;
     const uint64_t count = g.tokens * g.rows;
     const unsigned blocks = unsigned(umin64(ceil_div(count, 256), 148 * 8));

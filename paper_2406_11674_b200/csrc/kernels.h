@@ -197,6 +197,7 @@ struct GemmPlan {
     uint32_t m_tiles, n_tiles, ksplit, sps;
     uint64_t nspans;              // 128-column spans per row
     uint64_t part_bytes;          // split-K partials (0 when ksplit == 1)
+    bool two_pass;                // decompress W to HBM, then the dense tcgen05 GEMM (large token counts)
 };
 GemmPlan gemm_plan(uint64_t rows, uint64_t cols, uint64_t tokens, int sms);
 struct GemmLaunch {
@@ -210,6 +211,7 @@ struct GemmLaunch {
     float* y32;                     // [tokens][rows], or null
     void* y16;                      // [tokens][rows] f16, or null
     WsHeader* hdr;
+    const void* w_dense;            // set: W already dense in HBM (f16 [rows][cols], cols % 8 == 0) -> dense kernel
 };
 cudaError_t launch_gemm_fused(const GemmPlan& p, const GemmLaunch& g, cudaStream_t s);
 // count_kernel's two-level offsets -> a flat absolute 1024-chunk table, in place

@@ -136,3 +136,34 @@ def test_gemm_opt66b_shapes(E, rows, cols, tokens):
     X = _x(tokens, cols, tokens)
     y = E.gemm_compressed(t, X, index=E.build_rank_index(t.bitmap, 1024))
     gemm_check(y, W, X)
+
+
+@pytest.mark.parametrize("rows,cols,tokens", [(128, 64, 16), (300, 1000, 70), (256, 4096, 256), (129, 2048, 600),
+                                              (1024, 9216, 1000)])
+def test_dense_gemm_matches_fp64_reference(E, rows, cols, tokens):
+    """the cuBLAS-free dense consumer (and the second pass of large-token GEMMs)"""
+    g = torch.Generator(device="cpu").manual_seed(rows + cols)
+    W = ((torch.rand(rows, cols, generator=g) * 2 - 1).half()).cuda()
+    X = _x(tokens, cols, tokens)
+    w = E.DenseMatrix(rows, cols, E.Dtype.F16, W.reshape(-1).view(torch.uint8).clone())
+    y = E.gemm(w, X)
+    gemm_check(y, W, X)
+    assert torch.equal(y, E.gemm(w, X))
+
+
+@pytest.mark.parametrize("rows,cols,tokens,s", [(300, 1024, 500, 0.5), (512, 9216, 1024, 0.5), (96, 1000, 900, 0.3)])
+def test_gemm_two_pass_large_tokens(E, rows, cols, tokens, s):
+    """tokens > 384: gemm_compressed decompresses W once into the workspace and
+    runs the dense tcgen05 GEMM; same contract (and same errors) as the fused path"""
+    if cols % 128:
+        t, W = _oracle_tensor(E, rows, cols, s, rows + cols, values_offset=2)
+    else:
+        t, W = _synth(E, rows, cols, s, rows + cols)
+    X = _x(tokens, cols, cols)
+    y = E.gemm_compressed(t, X)
+    gemm_check(y, W, X)
+    y2 = E.gemm_compressed(t, X, index=E.build_rank_index(t.bitmap, 1024))
+    assert torch.equal(y, y2)
+    bad = E.EndorTensor(rows, cols, E.Dtype.F16, t.bitmap, t.values[:-2], validate=False)
+    with pytest.raises(E.CorruptionError):
+        E.gemm_compressed(bad, X)
