@@ -59,7 +59,7 @@
 extern "C" {
 #endif
 
-#define ENDOR_CUDA_ABI_VERSION 2
+#define ENDOR_CUDA_ABI_VERSION 3
 
 typedef enum endor_status {
     ENDOR_OK = 0,
@@ -415,6 +415,14 @@ typedef struct endor_pipeline_op {
                                 (EndorDirect, SsdToGpu sim.hpp:205-214) through the pipeline's
                                 endor_reader instead of bitmap_host / values_host; rows, cols,
                                 dtype, nnz must match its header */
+    uint64_t tokens;         /* 0 or 1: GEMV as above.  > 1: GEMM (prefill / batched decode):
+                                x_dev is f16 [tokens][cols] (cols % 8 == 0), y_dev f32
+                                [tokens][rows], y_host (optional) the same size;
+                                endor_cuda_gemm_compressed on the compute stream */
+    const uint64_t* prefix1024_host; /* optional pinned RankIndex at chunk 1024 (ceil(n/1024)
+                                u64, built once at load time like the compression): copied
+                                with the op, so the decompress / fused GEMV / GEMM run no
+                                counting pass */
 } endor_pipeline_op;
 
 typedef struct endor_pipeline_stats {

@@ -28,7 +28,8 @@ class PipelineOp(C.Structure):
     _fields_ = [("rows", _u64), ("cols", _u64), ("dtype", _i32), ("flags", _i32),
                 ("bitmap_host", _vp), ("values_host", _vp), ("nnz", _u64),
                 ("x_dev", _vp), ("y_dev", _vp), ("dense_dev", _vp), ("y_host", _vp),
-                ("quant_scale", C.c_float), ("reserved2", _i32), ("path", C.c_char_p)]
+                ("quant_scale", C.c_float), ("reserved2", _i32), ("path", C.c_char_p),
+                ("tokens", _u64), ("prefix1024_host", _vp)]
 
 
 class PipelineStats(C.Structure):

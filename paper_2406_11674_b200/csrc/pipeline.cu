@@ -32,6 +32,7 @@ struct endor_pipeline {
     struct Slot {
         uint8_t* bitmap = nullptr;  // ceil(max/8) rounded up
         uint8_t* values = nullptr;  // max*2 bytes
+        uint64_t* prefix = nullptr; // ceil(max/1024) u64: the op's optional RankIndex at chunk 1024
         cudaEvent_t free_ev = nullptr;
     };
     std::vector<Slot> slots;
@@ -96,6 +97,7 @@ int endor_pipeline_create(int device_ordinal, uint64_t max_op_elems, int ring_de
     for (auto& s : p->slots) {
         PK(cudaMalloc(&s.bitmap, bmb));
         PK(cudaMalloc(&s.values, vb));
+        PK(cudaMalloc(&s.prefix, align256((max_op_elems + 1023) / 1024 * 8 + 8)));
         PK(cudaEventCreateWithFlags(&s.free_ev, cudaEventDisableTiming));
         PK(cudaEventRecord(s.free_ev, p->compute));
     }
@@ -116,6 +118,7 @@ int endor_pipeline_destroy(endor_pipeline* p) {
     for (auto& s : p->slots) {
         cudaFree(s.bitmap);
         cudaFree(s.values);
+        cudaFree(s.prefix);
         cudaEventDestroy(s.free_ev);
     }
     for (auto& d : p->dense) cudaFree(d);
@@ -145,6 +148,22 @@ int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops
     PK(cudaSetDevice(p->device));
     int st = ensure_events(p, nops);
     if (st) return st;
+    // GEMM ops (tokens > 1) need split-K partials (and, past the two-pass
+    // threshold, a dense W) in the workspace: grow it once, before enqueueing
+    size_t need = p->ws_bytes;
+    for (int i = 0; i < nops; ++i)
+        if (ops[i].tokens > 1) {
+            const size_t b = endor_cuda_gemm_workspace_bytes(ops[i].rows, ops[i].cols, ops[i].tokens);
+            need = b > need ? b : need;
+        }
+    if (need > p->ws_bytes) {
+        PK(cudaStreamSynchronize(p->compute));
+        PK(cudaFree(p->ws));
+        p->ws = nullptr;
+        PK(cudaMalloc(&p->ws, need));
+        p->ws_bytes = need;
+        PK(cudaMemsetAsync(p->ws, 0, need, p->compute));
+    }
     uint64_t h2d = 0, dense = 0, launches = 0;
     for (int i = 0; i < nops; ++i) {
         const endor_pipeline_op& op = ops[i];
@@ -161,9 +180,13 @@ int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops
         // enqueued: the staging slot holds at most max_op_elems values
         if (op.nnz > n) return set_last_error(ENDOR_ERR_CORRUPTION, "values length does not match bitmap popcount");
         if ((op.x_dev || op.y_dev) && ob != 2) return pbad("GEMV ops need an f16 (or dequantized) W");
+        const bool gemm = op.tokens > 1 && op.x_dev && op.y_dev;
+        if (gemm && (deq || op.dtype != ENDOR_DTYPE_F16 || op.cols % 8 || op.dense_dev))
+            return pbad("GEMM ops need an f16 W with cols % 8 == 0 and no dense_dev");
         if (!op.path && ((n && !op.bitmap_host) || (op.nnz && !op.values_host))) return pbad("null host buffer");
         auto& slot = p->slots[i % p->depth];
         const size_t bmb = (n + 7) / 8, vb = op.nnz * eb;
+        const size_t pb = op.prefix1024_host ? (n + 1023) / 1024 * 8 : 0;
         // copy stream: wait until the slot's previous occupant was decompressed
         NvtxRange h2d_range(op.path ? "endor op: storage -> HBM" : "endor op: H2D compressed");
         PK(cudaStreamWaitEvent(p->copy, slot.free_ev, 0));
@@ -181,6 +204,8 @@ int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops
             PK(cudaMemcpyAsync(slot.bitmap, op.bitmap_host, bmb, cudaMemcpyHostToDevice, p->copy));
             if (vb) PK(cudaMemcpyAsync(slot.values, op.values_host, vb, cudaMemcpyHostToDevice, p->copy));
         }
+        if (pb) PK(cudaMemcpyAsync(slot.prefix, op.prefix1024_host, pb, cudaMemcpyHostToDevice, p->copy));
+        const uint64_t* pre = pb ? slot.prefix : nullptr;
         PK(cudaEventRecord(p->h2d_end[i], p->copy));
         // compute stream: decompress into the dense ring (or the caller's buffer), then GEMV
         NvtxRange compute_range("endor op: decompress + GEMV");
@@ -191,19 +216,29 @@ int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops
         // (no dense W in HBM) unless flags bit1 asks for the materialised path
         const bool fused = op.x_dev && op.y_dev && !op.dense_dev && !deq && op.dtype == ENDOR_DTYPE_F16 &&
                            op.cols % 1024 == 0 && !(op.flags & 2);
-        if (fused) {
-            st = endor_cuda_gemv_compressed(&v, nullptr, op.x_dev, op.y_dev, nullptr, p->ws, p->ws_bytes,
-                                            p->compute);
+        if (gemm) {
+            // Y = X W^T from the compressed W (fused tcgen05 GEMM; past the
+            // two-pass threshold: decompress into the workspace + dense GEMM)
+            st = endor_cuda_gemm_compressed(&v, pre, op.x_dev, op.tokens, op.cols, op.y_dev, nullptr, p->ws,
+                                            p->ws_bytes, p->compute);
             if (st) return st;
-            launches += 4;  // count, flatten, fused GEMV, row sum
+            launches += pre ? 2 : 4;
+            PK(cudaEventRecord(p->dec_end[i], p->compute));
+            PK(cudaEventRecord(slot.free_ev, p->compute));
+        } else if (fused) {
+            st = endor_cuda_gemv_compressed(&v, pre, op.x_dev, op.y_dev, nullptr, p->ws, p->ws_bytes, p->compute);
+            if (st) return st;
+            launches += pre ? 2 : 4;  // (count, flatten,) fused GEMV, row sum
             PK(cudaEventRecord(p->dec_end[i], p->compute));
             PK(cudaEventRecord(slot.free_ev, p->compute));
         } else {
             void* dst = op.dense_dev ? op.dense_dev : p->dense[i & 1];
-            st = deq ? endor_cuda_decompress_dequant(&v, op.quant_scale, dst, p->ws, p->ws_bytes, p->compute)
-                     : endor_cuda_decompress(&v, dst, p->ws, p->ws_bytes, p->compute);
+            st = deq   ? endor_cuda_decompress_dequant(&v, op.quant_scale, dst, p->ws, p->ws_bytes, p->compute)
+                 : pre ? endor_cuda_decompress_chunked(&v, 1024, pre, (n + 1023) / 1024, dst, p->ws, p->ws_bytes,
+                                                       p->compute)
+                       : endor_cuda_decompress(&v, dst, p->ws, p->ws_bytes, p->compute);
             if (st) return st;
-            launches += 2;
+            launches += pre ? 1 : 2;
             PK(cudaEventRecord(p->dec_end[i], p->compute));
             PK(cudaEventRecord(slot.free_ev, p->compute));
             if (op.x_dev && op.y_dev) {
@@ -213,9 +248,10 @@ int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops
             }
         }
         if (op.x_dev && op.y_dev && op.y_host)
-            PK(cudaMemcpyAsync(op.y_host, op.y_dev, op.rows * sizeof(float), cudaMemcpyDeviceToHost, p->compute));
+            PK(cudaMemcpyAsync(op.y_host, op.y_dev, op.rows * sizeof(float) * (gemm ? op.tokens : 1),
+                               cudaMemcpyDeviceToHost, p->compute));
         PK(cudaEventRecord(p->op_end[i], p->compute));
-        h2d += bmb + vb;
+        h2d += bmb + vb + pb;
         dense += n * ob;
     }
     p->last_nops = nops;

@@ -38,13 +38,16 @@ class HostOp:
     quant_scale: Optional[float] = None    # i8 values dequantized to f16 W (INT8 + Endor)
     materialize: bool = False              # decompress W, then dense GEMV (default: fused when possible)
     path: Optional[str] = None             # EndorDirect: read bitmap + values from this .endor file
+    tokens: int = 0                        # > 1: GEMM, x f16 [tokens, cols] -> y f32 [tokens, rows]
+    prefix1024: Optional[torch.Tensor] = None  # pinned int64 RankIndex at chunk 1024 (no counting pass)
 
     @property
     def compressed_bytes(self) -> int:
         if self.path is not None:
             eb = 2 if self.dtype == 0 else 1
             return (self.rows * self.cols + 7) // 8 + self.nnz * eb
-        return self.bitmap.numel() + self.values.numel()
+        pb = (self.rows * self.cols + 1023) // 1024 * 8 if self.prefix1024 is not None else 0
+        return self.bitmap.numel() + self.values.numel() + pb
 
     @property
     def dense_bytes(self) -> int:
@@ -86,7 +89,8 @@ class OffloadPipeline:
             arr[i] = _lib.PipelineOp(o.rows, o.cols, o.dtype, flags, _p(o.bitmap), _p(o.values), o.nnz,
                                      _p(o.x), _p(o.y), _p(o.dense), _p(o.y_host),
                                      float(o.quant_scale) if deq else 0.0, 0,
-                                     os.fsencode(o.path) if o.path is not None else None)
+                                     os.fsencode(o.path) if o.path is not None else None,
+                                     int(o.tokens), _p(o.prefix1024))
         self._keep = (arr, ops)
         check(self._lib.endor_pipeline_run(self._h, arr, len(ops), 1 if sync else 0))
 

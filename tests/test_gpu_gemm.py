@@ -167,3 +167,42 @@ def test_gemm_two_pass_large_tokens(E, rows, cols, tokens, s):
     bad = E.EndorTensor(rows, cols, E.Dtype.F16, t.bitmap, t.values[:-2], validate=False)
     with pytest.raises(E.CorruptionError):
         E.gemm_compressed(bad, X)
+
+
+def _pinned_prefix(E, t):
+    idx = E.build_rank_index(t.bitmap, 1024)
+    h = torch.empty(idx.prefix.numel(), dtype=torch.int64, pin_memory=True)
+    h.copy_(idx.prefix.to(torch.int64))
+    return h
+
+
+@pytest.mark.parametrize("tokens", [16, 500])
+def test_pipeline_gemm_ops(E, tokens):
+    """endor_pipeline_op.tokens > 1: the offload pipeline streams each op's
+    compressed W from pinned host memory and runs the GEMM consumer on it
+    (fused below the two-pass threshold, decompress + dense GEMM above);
+    with and without a pinned load-time RankIndex (prefix1024_host)."""
+    from paper_2406_11674_b200.pipeline import HostOp, OffloadPipeline, pinned_copy
+    shapes = [(256, 2048), (128, 1024), (96, 1000)]
+    ts, Ws = [], []
+    for i, (r, c) in enumerate(shapes):
+        if c % 128:
+            t, W = _oracle_tensor(E, r, c, 0.5, 77 + i)
+        else:
+            t, W = _synth(E, r, c, 0.5, 77 + i)
+        ts.append(t)
+        Ws.append(W)
+    Xs = [_x(tokens, t.cols, i) for i, t in enumerate(ts)]
+    for with_prefix in (False, True):
+        ops = [HostOp(t.rows, t.cols, 0, pinned_copy(t.bitmap.data), pinned_copy(t.values), t.nnz(), x=X,
+                      y=torch.empty(tokens, t.rows, dtype=torch.float32, device="cuda"),
+                      y_host=torch.empty(tokens * t.rows, dtype=torch.float32, pin_memory=True), tokens=tokens,
+                      prefix1024=_pinned_prefix(E, t) if with_prefix else None)
+               for t, X in zip(ts, Xs)]
+        p = OffloadPipeline(0, max(t.element_count() for t in ts))
+        p.run(ops, sync=True)
+        st = p.stats()
+        p.close()
+        for o, W, X in zip(ops, Ws, Xs):
+            gemm_check(o.y_host.reshape(tokens, -1).cuda(), W, X)
+        assert st["h2d_bytes"] == sum(o.compressed_bytes for o in ops)
