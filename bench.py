@@ -559,7 +559,7 @@ def run_ours(args):
             e0 = torch.empty(0, dtype=torch.uint8)
             for i, s in enumerate(shards):
                 pth = os.path.join(d, f"op{i}.endor")
-                fbytes += ST.write_endor_file(s["t"], pth)
+                fbytes += ST.write_endor_file(s["t"], pth, version=2)  # 4 KiB-aligned sections
                 x = ((torch.rand(s["cols"], generator=g) * 2 - 1).half()).to(dev)
                 fops.append(HostOp(s["rows"], s["cols"], 0, e0, e0, s["nnz"], path=pth, x=x,
                                    y=torch.empty(s["rows"], dtype=torch.float32, device=dev),
@@ -578,7 +578,7 @@ def run_ours(args):
             storage = {"value": round(world * dense_rank / (s_ms * 1e-3) / 1e9, 2), "unit": UNIT,
                        "layer_ms": round(s_ms / world, 3), "layers_per_step": world, "reps": sreps,
                        "storage_gbs_per_gpu": round(sf["h2d_bytes"] / (sf["h2d_ms"] * 1e-3) / 1e9, 3),
-                       "io_mode": mode,
+                       "io_mode": mode, "container": "v2 (4 KiB-aligned sections, endor_file_encode_v2)",
                        "gds": "nvidia-fs not loaded on this box: O_DIRECT reads + pinned bounce buffers "
                               "(cuFile compatibility mode hangs in cuFileDriverOpen here)" if mode != "gds" else "GDS",
                        "file_bytes_per_gpu": fbytes,

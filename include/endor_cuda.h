@@ -350,13 +350,17 @@ typedef struct endor_file_info {
     float quant_scale;             /* flags bit0 */
     uint32_t crc;                  /* stored CRC-32 (IEEE, zlib) of every preceding byte */
     uint32_t header_crc;           /* CRC-32 of the header bytes alone */
-    uint32_t reserved;
+    uint32_t gap_bytes;            /* v2: zero fill between the bitmap and values sections */
     uint64_t header_bytes, bitmap_offset, bitmap_bytes, values_offset, values_bytes, file_bytes;
 } endor_file_info;
 
 /* Parse and validate the header and the declared layout in decode_endor's
  * order (magic, version, dtype, flags, fields, rows*cols, nnz, size:
- * file_io.hpp:212-252).  ENDOR_ERR_FORMAT + endor_cuda_last_format_kind(). */
+ * file_io.hpp:212-252).  ENDOR_ERR_FORMAT + endor_cuda_last_format_kind().
+ * Accepts version 1 (the reference's layout) and version 2 (endor_file_encode_v2:
+ * the same fields with the bitmap at byte 4096 and the values at the next 4 KiB
+ * boundary, zero fill in between, CRC-32 over every preceding byte -- aligned
+ * file offsets, which a GPUDirect Storage DMA needs; nonzero fill is Malformed). */
 int endor_file_probe(const char* path, endor_file_info* out);
 int endor_cuda_last_format_kind(void);
 
@@ -364,12 +368,18 @@ int endor_cuda_last_format_kind(void);
  * size (out == NULL: just the size; 0 on bad arguments / short out_cap). */
 size_t endor_file_encode(uint64_t rows, uint64_t cols, int32_t dtype, int32_t flags, float quant_scale,
                          const void* bitmap, const void* values, uint64_t nnz, void* out, size_t out_cap);
+/* The version-2 (4 KiB-aligned sections) container of the same tensor; an
+ * extension the reference does not read (its decode_endor accepts version 1). */
+size_t endor_file_encode_v2(uint64_t rows, uint64_t cols, int32_t dtype, int32_t flags, float quant_scale,
+                            const void* bitmap, const void* values, uint64_t nnz, void* out, size_t out_cap);
 
 #define ENDOR_IO_AUTO 0          /* GDS if nvidia-fs is loaded, else POSIX */
 #define ENDOR_IO_GDS 1           /* cuFile with nvidia-fs: NVMe -> HBM DMA */
-#define ENDOR_IO_CUFILE_COMPAT 2 /* cuFile compatibility mode (POSIX inside cuFile); only with
-                                    ENDOR_ALLOW_CUFILE_COMPAT=1 -- its driver open hangs without
-                                    nvidia-fs on this pool's boxes */
+#define ENDOR_IO_CUFILE_COMPAT 2 /* cuFile compatibility mode (POSIX inside cuFile).  Its driver
+                                    open hangs without nvidia-fs on this pool's boxes: it runs
+                                    under a watchdog (ENDOR_CUFILE_OPEN_TIMEOUT_S, default 10 s)
+                                    and a timeout returns ENDOR_ERR_IO instead of hanging;
+                                    ENDOR_ALLOW_CUFILE_COMPAT=0 forbids the mode */
 #define ENDOR_IO_POSIX 3         /* O_DIRECT reads into two pinned bounce buffers + async H2D */
 typedef struct endor_reader endor_reader;
 int endor_reader_create(int device_ordinal, size_t bounce_bytes, int mode, endor_reader** out);

@@ -43,7 +43,7 @@ class FileInfo(C.Structure):
     """endor_file_info."""
     _fields_ = [("rows", _u64), ("cols", _u64), ("nnz", _u64), ("dtype", _i32), ("flags", _i32),
                 ("quant_scale", C.c_float), ("crc", C.c_uint32), ("header_crc", C.c_uint32),
-                ("reserved", C.c_uint32), ("header_bytes", _u64), ("bitmap_offset", _u64),
+                ("gap_bytes", C.c_uint32), ("header_bytes", _u64), ("bitmap_offset", _u64),
                 ("bitmap_bytes", _u64), ("values_offset", _u64), ("values_bytes", _u64), ("file_bytes", _u64)]
 
 
@@ -110,6 +110,7 @@ SIGNATURES = {
     "endor_cuda_last_format_kind": (C.c_int, []),
     "endor_file_probe": (C.c_int, [C.c_char_p, C.POINTER(FileInfo)]),
     "endor_file_encode": (_sz, [_u64, _u64, _i32, _i32, C.c_float, _vp, _vp, _u64, _vp, _sz]),
+    "endor_file_encode_v2": (_sz, [_u64, _u64, _i32, _i32, C.c_float, _vp, _vp, _u64, _vp, _sz]),
     "endor_reader_create": (C.c_int, [C.c_int, _sz, C.c_int, C.POINTER(_vp)]),
     "endor_reader_destroy": (C.c_int, [_vp]),
     "endor_reader_mode": (C.c_int, [_vp]),

@@ -30,6 +30,10 @@
 #include <time.h>
 #include <unistd.h>
 
+#include <chrono>
+#include <condition_variable>
+#include <cstdlib>
+#include <mutex>
 #include <new>
 #include <string>
 #include <thread>
@@ -44,6 +48,7 @@ using namespace endor_b200;
 namespace {
 
 constexpr int kBounce = 4;  // pinned bounce buffers of the POSIX engine (3 reads in flight)
+constexpr uint64_t kV2Align = 4096;  // v2 container: bitmap and values start at 4 KiB boundaries
 
 thread_local int g_format_kind = -1;
 
@@ -211,9 +216,9 @@ struct CuFile {
     // this pool's boxes (profiles/r01/storage_probe.txt), so the driver is only
     // opened for real GDS, or when ENDOR_ALLOW_CUFILE_COMPAT=1 asks for it.
     static bool gds_present() { return access("/proc/driver/nvidia-fs/version", F_OK) == 0; }
-    static bool compat_allowed() {
+    static bool compat_allowed() {  // the watchdog bounds the driver open; =0 forbids the mode
         const char* e = getenv("ENDOR_ALLOW_CUFILE_COMPAT");
-        return e && e[0] == '1';
+        return !(e && e[0] == '0');
     }
     void open_driver() {
         if (ok || lib) return;
@@ -225,8 +230,38 @@ struct CuFile {
         handle_deregister = reinterpret_cast<void (*)(void*)>(dlsym(lib, "cuFileHandleDeregister"));
         read = reinterpret_cast<ssize_t (*)(void*, void*, size_t, off_t, off_t)>(dlsym(lib, "cuFileRead"));
         if (!driver_open || !handle_register || !handle_deregister || !read) return;
-        ok = driver_open().err == 0;
+        // watchdog: without nvidia-fs cuFileDriverOpen was measured to block
+        // forever on this pool's boxes; give it ENDOR_CUFILE_OPEN_TIMEOUT_S
+        // (default 10 s) on a helper thread, and on timeout leave it parked
+        // (detached) and report the engine unusable instead of hanging
+        struct Open {
+            std::mutex mu;
+            std::condition_variable cv;
+            bool done = false;
+            int err = -1;
+        };
+        auto* o = new Open();  // leaked if the driver never returns
+        auto fn = driver_open;
+        std::thread([o, fn]() {
+            const int e = fn().err;
+            std::lock_guard<std::mutex> g(o->mu);
+            o->err = e;
+            o->done = true;
+            o->cv.notify_all();
+        }).detach();
+        const char* te = getenv("ENDOR_CUFILE_OPEN_TIMEOUT_S");
+        const double tmo = te ? atof(te) : 10.0;
+        std::unique_lock<std::mutex> lk(o->mu);
+        const bool done = o->cv.wait_for(lk, std::chrono::duration<double>(tmo), [o] { return o->done; });
+        if (!done) {
+            timed_out = true;
+            return;  // o stays alive for the parked thread
+        }
+        ok = o->err == 0;
+        lk.unlock();
+        delete o;
     }
+    bool timed_out = false;
 };
 
 CuFile& cufile() {
@@ -266,21 +301,31 @@ extern "C" {
 
 int endor_cuda_last_format_kind(void) { return g_format_kind; }
 
-size_t endor_file_encode(uint64_t rows, uint64_t cols, int32_t dtype, int32_t flags, float quant_scale,
-                         const void* bitmap, const void* values, uint64_t nnz, void* out, size_t out_cap) {
+}  // extern "C"
+
+// v1 (file_io.hpp:187-210, byte-identical) and v2 (the same fields, sections at
+// 4 KiB boundaries, zero fill between them: a GDS DMA target needs aligned file
+// offsets; the reference reads v1 only)
+static size_t encode_container(int version, uint64_t rows, uint64_t cols, int32_t dtype, int32_t flags,
+                               float quant_scale, const void* bitmap, const void* values, uint64_t nnz, void* out,
+                               size_t out_cap) {
     const int eb = dtype == ENDOR_DTYPE_F16 ? 2 : (dtype == ENDOR_DTYPE_I8 ? 1 : 0);
     if (!eb || (rows && cols > UINT64_MAX / rows) || nnz > rows * cols) return 0;
     const bool q = flags & 1;
     const uint64_t n = rows * cols, bm = (n + 7) / 8, vb = nnz * eb;
-    const size_t hdr = 32 + (q ? 4 : 0), total = hdr + bm + vb + 4;
+    const size_t hdr = 32 + (q ? 4 : 0);
+    const size_t boff = version == 2 ? kV2Align : hdr;
+    const size_t voff = version == 2 ? boff + ((bm + kV2Align - 1) & ~uint64_t(kV2Align - 1)) : boff + bm;
+    const size_t total = voff + vb + 4;
     if (!out) return total;
     if (out_cap < total || (bm && !bitmap) || (vb && !values)) return 0;
     uint8_t* o = static_cast<uint8_t*>(out);
+    if (version == 2) memset(o, 0, voff);  // zero fill of the header page and the bitmap's last page
     memcpy(o, "ENDR", 4);
     auto put = [&](size_t at, uint64_t v, int nb) {
         for (int i = 0; i < nb; ++i) o[at + i] = uint8_t(v >> (8 * i));
     };
-    put(4, 1, 2);  // file_io.hpp:189-199
+    put(4, uint64_t(version), 2);  // file_io.hpp:189-199
     o[6] = uint8_t(dtype);
     o[7] = uint8_t(flags & 3);
     put(8, rows, 8);
@@ -291,10 +336,22 @@ size_t endor_file_encode(uint64_t rows, uint64_t cols, int32_t dtype, int32_t fl
         memcpy(&bits, &quant_scale, 4);
         put(32, bits, 4);
     }
-    if (bm) memcpy(o + hdr, bitmap, bm);
-    if (vb) memcpy(o + hdr + bm, values, vb);
-    put(hdr + bm + vb, host_crc().update(0, o, hdr + bm + vb), 4);
+    if (bm) memcpy(o + boff, bitmap, bm);
+    if (vb) memcpy(o + voff, values, vb);
+    put(voff + vb, host_crc().update(0, o, voff + vb), 4);
     return total;
+}
+
+extern "C" {
+
+size_t endor_file_encode(uint64_t rows, uint64_t cols, int32_t dtype, int32_t flags, float quant_scale,
+                         const void* bitmap, const void* values, uint64_t nnz, void* out, size_t out_cap) {
+    return encode_container(1, rows, cols, dtype, flags, quant_scale, bitmap, values, nnz, out, out_cap);
+}
+
+size_t endor_file_encode_v2(uint64_t rows, uint64_t cols, int32_t dtype, int32_t flags, float quant_scale,
+                            const void* bitmap, const void* values, uint64_t nnz, void* out, size_t out_cap) {
+    return encode_container(2, rows, cols, dtype, flags, quant_scale, bitmap, values, nnz, out, out_cap);
 }
 
 int endor_file_probe(const char* path, endor_file_info* out) {
@@ -303,7 +360,7 @@ int endor_file_probe(const char* path, endor_file_info* out) {
     const int fd = open(path, O_RDONLY);
     if (fd < 0) return set_last_error(ENDOR_ERR_IO, (std::string("cannot open ") + path).c_str());
     struct stat sb;
-    uint8_t h[36];
+    static thread_local uint8_t h[kV2Align];  // the header (v2: its whole zero-filled page)
     ssize_t got = 0;
     if (fstat(fd, &sb) != 0 || (got = pread(fd, h, sizeof(h), 0)) < 0) {
         close(fd);
@@ -317,7 +374,7 @@ int endor_file_probe(const char* path, endor_file_info* out) {
     if (!need(4)) st = fmt_fail(ENDOR_FMT_TRUNCATED, "file ends mid-field");
     else if (memcmp(h, "ENDR", 4) != 0) st = fmt_fail(ENDOR_FMT_BAD_MAGIC, "not an .endor container");
     else if (!need(6)) st = fmt_fail(ENDOR_FMT_TRUNCATED, "file ends mid-field");
-    else if (le(h + 4, 2) != 1) st = fmt_fail(ENDOR_FMT_BAD_VERSION, "unsupported container version");
+    else if (le(h + 4, 2) != 1 && le(h + 4, 2) != 2) st = fmt_fail(ENDOR_FMT_BAD_VERSION, "unsupported container version");
     else if (!need(7)) st = fmt_fail(ENDOR_FMT_TRUNCATED, "file ends mid-field");
     else if (h[6] > 1) st = fmt_fail(ENDOR_FMT_MALFORMED, "unknown dtype code");
     else if (!need(8)) st = fmt_fail(ENDOR_FMT_TRUNCATED, "file ends mid-field");
@@ -330,6 +387,7 @@ int endor_file_probe(const char* path, endor_file_info* out) {
         f.cols = le(h + 16, 8);
         f.nnz = le(h + 24, 8);
         const uint64_t hdr = 32 + ((f.flags & 1) ? 4 : 0);
+        const bool v2 = le(h + 4, 2) == 2;
         if (f.flags & 1) {
             const uint32_t bits = uint32_t(le(h + 32, 4));
             memcpy(&f.quant_scale, &bits, 4);
@@ -339,10 +397,12 @@ int endor_file_probe(const char* path, endor_file_info* out) {
         else if (f.nnz > f.rows * f.cols) st = fmt_fail(ENDOR_FMT_MALFORMED, "nnz exceeds rows*cols");
         else {
             f.header_bytes = hdr;
-            f.bitmap_offset = hdr;
+            f.bitmap_offset = v2 ? kV2Align : hdr;
             const uint64_t n = f.rows * f.cols;
             f.bitmap_bytes = n / 8 + ((n & 7) != 0);  // ceil(n/8) without the n + 7 wrap
-            f.values_offset = hdr + f.bitmap_bytes;
+            const uint64_t bpad = v2 ? (kV2Align - f.bitmap_bytes % kV2Align) % kV2Align : 0;
+            f.values_offset = f.bitmap_offset + f.bitmap_bytes + bpad;
+            f.gap_bytes = uint32_t(bpad);
             // the declared layout must be addressable: an overflowing size can
             // only describe a file longer than any file (the reference's cursor
             // runs off the end: Truncated)
@@ -357,7 +417,17 @@ int endor_file_probe(const char* path, endor_file_info* out) {
                 uint8_t c[4];
                 if (pread(fd, c, 4, off_t(f.file_bytes - 4)) != 4) st = set_last_error(ENDOR_ERR_IO, "short read");
                 f.crc = uint32_t(le(c, 4));
-                f.header_crc = host_crc().update(0, h, hdr);
+                // CRC of every byte before the bitmap (v2: the header page)
+                f.header_crc = host_crc().update(0, h, f.bitmap_offset);
+                if (v2 && st == ENDOR_OK) {  // v2 fill bytes must be zero (the CRC covers them too)
+                    bool dirty = false;
+                    for (uint64_t i = hdr; i < kV2Align; ++i) dirty |= h[i] != 0;
+                    uint8_t g[kV2Align];
+                    if (bpad && pread(fd, g, bpad, off_t(f.bitmap_offset + f.bitmap_bytes)) != ssize_t(bpad))
+                        st = set_last_error(ENDOR_ERR_IO, "short read");
+                    for (uint64_t i = 0; i < bpad; ++i) dirty |= g[i] != 0;
+                    if (st == ENDOR_OK && dirty) st = fmt_fail(ENDOR_FMT_MALFORMED, "nonzero fill bytes in a v2 container");
+                }
             }
         }
     }
@@ -379,13 +449,14 @@ int endor_reader_create(int device, size_t bounce_bytes, int mode, endor_reader*
         delete r;
         return set_last_error(ENDOR_ERR_IO, mode == ENDOR_IO_GDS
                                                 ? "GPUDirect Storage (nvidia-fs) is not loaded on this host"
-                                                : "cuFile compatibility mode needs ENDOR_ALLOW_CUFILE_COMPAT=1");
+                                                : "cuFile compatibility mode disabled (ENDOR_ALLOW_CUFILE_COMPAT=0)");
     }
     if (mode != ENDOR_IO_POSIX) {
         cf.open_driver();
         if (!cf.ok) {
             delete r;
-            return set_last_error(ENDOR_ERR_IO, "cuFileDriverOpen failed");
+            return set_last_error(ENDOR_ERR_IO, cf.timed_out ? "cuFileDriverOpen did not return (watchdog timeout)"
+                                                            : "cuFileDriverOpen failed (or libcufile missing)");
         }
     }
     r->mode = mode;
@@ -568,7 +639,12 @@ int endor_reader_read(endor_reader* r, const char* path, const endor_file_info* 
         (e = cudaStreamSynchronize(s)) != cudaSuccess)
         return set_last_error(ENDOR_ERR_CUDA, cudaGetErrorString(e));
     const HostCrc& H = host_crc();
-    const uint32_t whole = H.combine(H.combine(f->header_crc, c[0], f->bitmap_bytes), c[1], f->values_bytes);
+    uint32_t whole = H.combine(f->header_crc, c[0], f->bitmap_bytes);
+    if (f->gap_bytes) {  // v2: the zero fill between the sections
+        static const uint8_t zeros[kV2Align] = {};
+        whole = H.combine(whole, H.update(0, zeros, f->gap_bytes), f->gap_bytes);
+    }
+    whole = H.combine(whole, c[1], f->values_bytes);
     if (whole != f->crc) return fmt_fail(ENDOR_FMT_BAD_CRC, "CRC mismatch");
     const uint64_t n = f->rows * f->cols;
     if ((n & 7) && (lastb >> (n & 7))) return fmt_fail(ENDOR_FMT_MALFORMED, "bitmap padding bits must be zero");

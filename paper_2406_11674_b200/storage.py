@@ -30,22 +30,24 @@ def probe(path: str) -> _lib.FileInfo:
     return info
 
 
-def encode_endor(t: EndorTensor) -> bytes:
-    """encode_endor (file_io.hpp:187-210): byte-identical container bytes."""
+def encode_endor(t: EndorTensor, version: int = 1) -> bytes:
+    """encode_endor (file_io.hpp:187-210): byte-identical container bytes
+    (version 2: the same container with 4 KiB-aligned sections, for GDS)."""
     bm = t.bitmap.to_bytes()
     vals = t.values.cpu().numpy().tobytes()
     flags = (1 if t.quant_scale is not None else 0) | (2 if t.negative_zero_collapsed() else 0)
     L = _lib.lib()
     args = (t.rows, t.cols, int(t.dtype), flags, float(t.quant_scale or 0.0), bm, vals, t.nnz())
-    n = L.endor_file_encode(*args, None, 0)
+    enc = {1: L.endor_file_encode, 2: L.endor_file_encode_v2}[version]
+    n = enc(*args, None, 0)
     buf = C.create_string_buffer(n)
-    if n == 0 or L.endor_file_encode(*args, buf, n) != n:
+    if n == 0 or enc(*args, buf, n) != n:
         raise ValueError("cannot encode this tensor")
     return buf.raw
 
 
-def write_endor_file(t: EndorTensor, path: str) -> int:
-    data = encode_endor(t)
+def write_endor_file(t: EndorTensor, path: str, version: int = 1) -> int:
+    data = encode_endor(t, version)
     with open(path, "wb") as f:
         f.write(data)
     return len(data)

@@ -107,6 +107,53 @@ def test_probe_rejects_layout_sizes_that_wrap(L, tmp_path):
         assert st == 7 and k == KIND["Truncated"]
 
 
+def encode_v2(L, rows, cols, dtype, bm, vals, nnz, flags=0, scale=0.0):
+    args = (rows, cols, dtype, flags, scale, bm.ctypes.data if bm.size else None,
+            vals.ctypes.data if vals.size else None, nnz)
+    n = L.endor_file_encode_v2(*args, None, 0)
+    buf = C.create_string_buffer(n)
+    assert L.endor_file_encode_v2(*args, buf, n) == n
+    return buf.raw
+
+
+@pytest.mark.parametrize("rows,cols,eb,flags", [(2, 2, 2, 0), (300, 1000, 2, 0), (77, 333, 1, 1), (128, 256, 2, 2),
+                                                (4, 4, 2, 0)])
+def test_v2_container_layout(L, tmp_path, rows, cols, eb, flags):
+    """Version 2: the v1 fields with the bitmap at byte 4096 and the values at
+    the next 4 KiB boundary (GDS-ready offsets), zero fill, CRC-32 over every
+    preceding byte; the v1 encoder is unchanged (golden test above)."""
+    import zlib
+    w = O.random_dense(rows, cols, eb, rows * cols, 0.5)
+    bm, vals, nnz, _ = O.compress(w, rows, cols, eb)
+    v1 = encode(L, rows, cols, 0 if eb == 2 else 1, bm, vals, nnz, flags, 0.25)
+    v2 = encode_v2(L, rows, cols, 0 if eb == 2 else 1, bm, vals, nnz, flags, 0.25)
+    hdr = 36 if flags & 1 else 32
+    assert v2[:4] == b"ENDR" and v2[4:6] == b"\x02\x00" and v2[6:hdr] == v1[6:hdr]
+    voff = 4096 + (bm.size + 4095) // 4096 * 4096
+    assert len(v2) == voff + vals.size + 4
+    assert v2[4096:4096 + bm.size] == bm.tobytes() and v2[voff:voff + vals.size] == vals.tobytes()
+    assert not any(v2[hdr:4096]) and not any(v2[4096 + bm.size:voff])
+    assert int.from_bytes(v2[-4:], "little") == zlib.crc32(v2[:-4]) & 0xFFFFFFFF
+    st, _, info = probe_kind(L, tmp_path, v2)
+    assert st == 0
+    assert (info.bitmap_offset, info.bitmap_bytes, info.values_offset, info.values_bytes, info.file_bytes) == \
+        (4096, bm.size, voff, vals.size, len(v2))
+    assert info.gap_bytes == voff - 4096 - bm.size
+    assert info.header_crc == zlib.crc32(v2[:4096]) & 0xFFFFFFFF
+    # a dirty fill byte (header page or the gap) is Malformed even with a fixed-up CRC
+    for at in ([100] + ([4096 + bm.size] if voff > 4096 + bm.size else [])):
+        bad = bytearray(v2)
+        bad[at] = 1
+        bad[-4:] = (zlib.crc32(bytes(bad[:-4])) & 0xFFFFFFFF).to_bytes(4, "little")
+        st, k, _ = probe_kind(L, tmp_path, bad)
+        assert st == 7 and k == KIND["Malformed"]
+    # truncated / trailing as v1
+    st, k, _ = probe_kind(L, tmp_path, v2[:-1])
+    assert st == 7 and k == KIND["Truncated"]
+    st, k, _ = probe_kind(L, tmp_path, v2 + b"\0")
+    assert st == 7 and k == KIND["Malformed"]
+
+
 # ---------------------------------------------------------------------------- GPU
 
 torch = pytest.importorskip("torch")
@@ -225,3 +272,61 @@ def test_pipeline_file_sourced_ops_match_host_sourced(S, E, tmp_path):
         ys[src] = [o.y_host.clone() for o in ops]
     for a, b in zip(ys["host"], ys["file"]):
         assert torch.equal(a, b)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rows,cols,s,dtype", [(2, 2, 0.5, 0), (300, 1000, 0.5, 0), (1024, 9216, 0.7, 0),
+                                               (77, 333, 0.4, 1)])
+def test_reader_v2_round_trip_and_crc(S, E, L, tmp_path, rows, cols, s, dtype):
+    """v2 containers through the GPU reader: the sections land at their 4 KiB
+    offsets, the device CRC check folds in the zero fill, corruption is caught."""
+    eb = 2 if dtype == 0 else 1
+    w = O.random_dense(rows, cols, eb, rows + cols, s)
+    bm, vals, nnz, _ = O.compress(w, rows, cols, eb)
+    t = E.EndorTensor(rows, cols, E.Dtype(dtype), E.Bitmap.from_bytes(bm.tobytes(), rows * cols, device="cuda"),
+                      torch.from_numpy(vals.copy()).cuda())
+    p = str(tmp_path / "w2.endor")
+    n = S.write_endor_file(t, p, version=2)
+    assert n == os.path.getsize(p) and S.probe(p).bitmap_offset == 4096
+    r = S.Reader("cuda", mode=3, bounce_bytes=1 << 16)
+    got = r.read(p, verify=True)
+    assert got.bitmap.to_bytes() == bm.tobytes()
+    assert got.values.cpu().numpy().tobytes() == vals.tobytes()
+    assert E.decompress(got).bytes() == w.tobytes()
+    data = bytearray(open(p, "rb").read())
+    if vals.size:
+        data[S.probe(p).values_offset] ^= 0x20
+        open(p, "wb").write(bytes(data))
+        with pytest.raises(E.FormatError) as ei:
+            r.read(p, verify=True)
+        assert ei.value.kind.name == "BadCrc"
+    r.close()
+
+
+@pytest.mark.gpu
+def test_cufile_compat_mode_never_hangs(tmp_path):
+    """ENDOR_IO_CUFILE_COMPAT runs cuFileDriverOpen under a watchdog: on a box
+    without nvidia-fs (where the open blocks) the reader reports an IO error
+    within the timeout instead of hanging; where it opens, reads are exact.
+    Run in a child process -- a parked driver thread must not outlive the test."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, torch; sys.path.insert(0, %r)\n"
+        "from oracle import oracle as O\n"
+        "from paper_2406_11674_b200 import codec as E, storage as S\n"
+        "w = O.random_dense(64, 128, 2, 1, 0.5); bm, vals, nnz, _ = O.compress(w, 64, 128, 2)\n"
+        "t = E.EndorTensor(64, 128, E.Dtype.F16, E.Bitmap.from_bytes(bm.tobytes(), 8192, device='cuda'),"
+        " torch.from_numpy(vals.copy()).cuda())\n"
+        "p = %r; S.write_endor_file(t, p, version=2)\n"
+        "try:\n"
+        "    r = S.Reader('cuda', mode=2)\n"
+        "except E.Error as e:\n"
+        "    print('IOERR', e); sys.stdout.flush(); import os; os._exit(0)\n"
+        "got = r.read(p, verify=True); assert E.decompress(got).bytes() == w.tobytes(); print('OK', r.mode)\n"
+        "sys.stdout.flush(); import os; os._exit(0)\n"
+    ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), str(tmp_path / "c.endor"))
+    env = dict(os.environ, ENDOR_CUFILE_OPEN_TIMEOUT_S="5")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.startswith("OK") or "cuFileDriverOpen" in out.stdout, out.stdout
