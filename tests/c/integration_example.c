@@ -32,6 +32,17 @@ int integration_example(uint64_t rows, uint64_t cols, uint64_t nnz, const void* 
                                            endor_cuda_workspace_bytes_batch(views, 6), stream);
     st |= endor_cuda_gemv_batch(op_rows, op_cols, dense_ws, xs, ys, NULL, 6, stream);
 
+    const uint64_t tokens = 16, x_ld = cols;
+    const size_t gws = endor_cuda_gemm_workspace_bytes(rows, cols, tokens);
+    st |= endor_cuda_gemm_compressed(&t, NULL, d_x, tokens, x_ld, d_y, NULL, ws, gws, stream);
+    st |= endor_cuda_gemm(rows, cols, d_dense, d_x, tokens, x_ld, d_y, NULL, ws, gws, stream);
+    endor_pipeline_op gop = {0};
+    gop.tokens = tokens;
+    gop.prefix1024_host = NULL;
+    (void)gop;
+    size_t v2 = endor_file_encode_v2(rows, cols, ENDOR_DTYPE_F16, 0, 0.f, h_bitmap, h_values, nnz, NULL, 0);
+    (void)v2;
+
     st |= endor_cuda_extract_rows(&t, d_rows, nsel, d_out, ws, ws_bytes, stream);
     st |= endor_cuda_extract_cols(&t, d_cols, nsel, d_out, ws, ws_bytes, stream);
     float scale;
