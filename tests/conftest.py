@@ -60,7 +60,9 @@ def gemv_check(y, W, x, tol=1e-3):
     """North star GEMV tolerance, element-wise:
     every row r satisfies |y_r - y_ref_r| <= tol * sum_j |W_rj x_j| (the
     conditioning of that dot product), and rows whose |y_ref_r| is not
-    dominated by cancellation (|y_ref_r| >= 0.1 sum_j |W_rj x_j|) also satisfy
+    dominated by cancellation (|y_ref_r| >= 0.01 sum_j |W_rj x_j|; a random
+    row of length n sits near 1.25/sqrt(n) of that sum, so at the catalog
+    widths most rows qualify) also satisfy
     the plain relative bound |y_r - y_ref_r| <= tol * |y_ref_r|.  y_ref is the
     float64 product over the same f16 W and x.  Returns (max error/mag,
     max relative error over well-conditioned rows)."""
@@ -77,7 +79,7 @@ def gemv_check(y, W, x, tol=1e-3):
     bound = tol * mag + 1e-30
     bad = err > bound
     assert not bad.any(), f"{int(bad.sum())} rows exceed {tol} * sum|W x|; worst {float((err / bound).max())}"
-    good = (ref.abs() >= 0.1 * mag) & (mag > 0)
+    good = (ref.abs() >= 0.01 * mag) & (mag > 0)
     rel = (err[good] / ref[good].abs()).max().item() if good.any() else 0.0
     assert rel <= tol, f"per-element relative error {rel} > {tol}"
     return float((err / (mag + 1e-30)).max()) if err.numel() else 0.0, rel
@@ -100,7 +102,7 @@ def gemm_check(y, W, X, tol=1e-3):
     bound = tol * mag + 1e-30
     bad = err > bound
     assert not bad.any(), f"{int(bad.sum())} entries exceed {tol} * sum|X W|; worst {float((err / bound).max())}"
-    good = (ref.abs() >= 0.1 * mag) & (mag > 0)
+    good = (ref.abs() >= 0.01 * mag) & (mag > 0)
     rel = (err[good] / ref[good].abs()).max().item() if good.any() else 0.0
     assert rel <= tol, f"per-element relative error {rel} > {tol}"
     return float((err / (mag + 1e-30)).max()) if err.numel() else 0.0, rel

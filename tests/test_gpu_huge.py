@@ -79,7 +79,7 @@ def test_f16_past_2p32(cuda_lib):
     wabs = E.DenseMatrix(ROWS, COLS, E.Dtype.F16, w.data.view(torch.float16).abs().view(torch.uint8))
     mag = E.gemv(wabs, x.abs())  # sum_j |W_ij x_j| (the row's conditioning), element-wise bound
     assert ((y - ref).abs() <= 1e-3 * mag).all()
-    good = ref.abs() >= 0.1 * mag
+    good = ref.abs() >= 0.01 * mag
     assert ((y - ref)[good].abs() <= 1e-3 * ref[good].abs()).all()
     del wabs, mag
     del w, t, wb
