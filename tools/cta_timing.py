@@ -37,8 +37,8 @@ def run(label, tensors):
         buf = (C.c_ulonglong * (3 * 296))()
         L.endor_debug_cta_times(buf, 296)
         t = np.array(buf, dtype=np.float64).reshape(296, 3)
+        t = t[t[:, 0] > 0]  # the grid is one CTA per SM: drop the unused slots
         st, en, sm = t[:, 0], t[:, 1], t[:, 2].astype(int)
-        life = (en - st) / 1e3
         life = (en - st) / 1e3
         res.append({"event_us": round(a.elapsed_time(b) * 1e3, 2), "span_us": round((en.max() - st.min()) / 1e3, 2),
                     "start_spread_us": round((st.max() - st.min()) / 1e3, 2),

@@ -2,9 +2,21 @@
 and 4 at G = 8) timed with the L2 flushed between repetitions, plus the count
 pass alone.  Measurement aid (VERDICT r1 "small shards >= 0.70").
 
-Each repetition: write a 512 MiB scratch buffer (evicts the 126 MB L2), then
-events around ONE decompress call on the same stream.  Also reported: the
-back-to-back figure (no flush) for comparison.
+Three timings per workload (CUDA events on the launching stream):
+  flushed       -- before each repetition write a 512 MiB scratch buffer and
+                   then READ it back (a sum), so the 126 MB L2 holds only clean
+                   lines of scratch: the inputs are cold and the timed call does
+                   not pay for write-backs of someone else's dirty lines (a
+                   write-only flush leaves ~126 MB of dirty scratch in L2 that
+                   the timed kernel must evict -- ~20 us of HBM write time,
+                   which is most of a G = 8 shard's budget);
+  flushed_dirty -- the write-only flush (the r01/r02a method, kept for
+                   comparison);
+  rotating      -- back-to-back calls over R distinct copies of the workload
+                   (R copies > 2x L2), i.e. the steady state of a layer-after-
+                   layer pass: inputs never hit in L2, and each call drains the
+                   previous call's dirty output lines as it would in the pass;
+  back_to_back  -- the same inputs repeatedly (partly L2-resident).
 
 Usage: python tools/small_shards.py [--out FILE] [--reps N]
 """
@@ -25,6 +37,7 @@ from paper_2406_11674_b200 import catalog, codec as E, shard as S  # noqa: E402
 PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
 DEV = torch.device("cuda", 0)
+L2_BYTES = 126 << 20
 
 
 def shard_of(rows, cols, seed, s, g, G):
@@ -39,9 +52,25 @@ def shard_of(rows, cols, seed, s, g, G):
 def timed(plan, reps, flush, phase=0):
     st = torch.cuda.Stream(device=DEV)
     scratch = torch.empty(512 << 20, dtype=torch.uint8, device=DEV)
-    for _ in range(3):
-        plan.launch(st.cuda_stream, phase=phase)
+    plans = plan if isinstance(plan, list) else [plan]
+    plan = plans[0]
+    with torch.cuda.stream(st):
+        for p in plans:
+            for _ in range(2):
+                p.launch(st.cuda_stream, phase=phase)
     torch.cuda.synchronize()
+    if flush == "rotating":
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n = reps * len(plans)
+        a.record(st)
+        with torch.cuda.stream(st):
+            for i in range(n):
+                plans[i % len(plans)].launch(st.cuda_stream, phase=phase)
+        b.record(st)
+        torch.cuda.synchronize()
+        for p in plans:
+            p.sync(st.cuda_stream)
+        return a.elapsed_time(b) / n
     if not flush:
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
@@ -55,6 +84,8 @@ def timed(plan, reps, flush, phase=0):
     with torch.cuda.stream(st):
         for r in range(reps):
             scratch.fill_(r & 0xFF)
+            if flush == "clean":
+                scratch.sum(dtype=torch.int64)  # read back: L2 left holding clean lines
             if phase == 2:
                 plan.launch(st.cuda_stream, phase=1)  # the count pass, untimed
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -77,15 +108,54 @@ def measure(label, tensors, reps):
     res = {"label": label, "elements": n, "alg_bytes": alg}
     pi = E.BatchPlan(tensors, outs, indices=idx)
     pn = E.BatchPlan(tensors, outs)
-    for name, plan, phase in (("chunked_idx1024", pi, 0), ("decompress", pn, 0), ("count_only", pn, 1),
-                              ("expand_only", pn, 2)):
+    # rotating copies: R distinct (inputs, outputs) sets with R * bytes > 2 x L2
+    R = max(2, min(16, -(-2 * L2_BYTES // max(alg, 1))))
+    rot_i, rot_n = [pi], [pn]
+    res["rotating_copies"] = R
+    for _ in range(R - 1):
+        ct = [E.EndorTensor(t.rows, t.cols, t.dtype, E.Bitmap(t.bitmap.size(), t.bitmap.data.clone()),
+                            t.values.clone(), validate=False, nnz=t.nnz()) for t in tensors]
+        co = [E.DenseMatrix.empty(t.rows, t.cols, E.Dtype.F16, DEV) for t in tensors]
+        rot_i.append(E.BatchPlan(ct, co, indices=idx))
+        rot_n.append(E.BatchPlan(ct, co))
+    for name, plan, rot, phase in (("chunked_idx1024", pi, rot_i, 0), ("decompress", pn, rot_n, 0),
+                                   ("count_only", pn, rot_n, 1), ("expand_only", pn, rot_n, 2)):
         r = {}
-        for flush in (True, False):
-            ms = timed(plan, reps, flush, phase)
+        for mode, key in (("clean", "flushed"), (True, "flushed_dirty"), ("rotating", "rotating"),
+                          (False, "back_to_back")):
+            if mode == "rotating" and phase == 2:
+                continue  # expand_only needs its count pass in front of every call
+            ms = timed(rot if mode == "rotating" else plan, reps, mode, phase)
             byts = bm if phase == 1 else alg
-            r["flushed" if flush else "back_to_back"] = {"ms": round(ms, 4),
-                                                          "frac": round(byts / (ms * 1e-3) / 1e9 / PEAK, 4)}
+            r[key] = {"ms": round(ms, 4), "frac": round(byts / (ms * 1e-3) / 1e9 / PEAK, 4)}
         res[name] = r
+    del rot_i, rot_n
+    # size-matched ceiling: a device-to-device copy moving the same number of
+    # bytes (alg / 2 read + alg / 2 written), timed the same ways -- the
+    # launch + pipeline-fill floor every kernel of this size pays
+    half = alg // 2
+    srcs = [torch.empty(half, dtype=torch.uint8, device=DEV) for _ in range(R)]
+    dsts = [torch.empty(half, dtype=torch.uint8, device=DEV) for _ in range(R)]
+
+    class _Copy:
+        def __init__(self, k):
+            self.k = k
+
+        def launch(self, stream_ptr=None, phase=0):
+            dsts[self.k].copy_(srcs[self.k])
+
+        def sync(self, stream_ptr=None):
+            pass
+
+    cps = [_Copy(k) for k in range(R)]
+    r = {}
+    for mode, key in (("clean", "flushed"), ("rotating", "rotating")):
+        ms = timed(cps if mode == "rotating" else cps[0], reps, mode, 0)
+        r[key] = {"ms": round(ms, 4), "frac": round(alg / (ms * 1e-3) / 1e9 / PEAK, 4)}
+    res["d2d_copy_same_bytes"] = r
+    for name in ("chunked_idx1024", "decompress"):
+        res[name]["frac_of_d2d_copy"] = {k: round(r[k]["ms"] / res[name][k]["ms"], 4) for k in ("flushed", "rotating")}
+    del srcs, dsts
     return res
 
 
