@@ -27,7 +27,26 @@ namespace endor_b200 {
 // ---------------------------------------------------------------------------
 // count_kernel (batched)
 // ---------------------------------------------------------------------------
+#ifdef ENDOR_CTA_TIMING  // development aid (tools/count_timeline.py): per-CTA phase timestamps
+__device__ unsigned long long g_count_times[8 * 4096];
+#define CT_STAMP(k)                                                                        \
+    do {                                                                                   \
+        if (threadIdx.x == 0) {                                                            \
+            unsigned long long t_;                                                         \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                         \
+            g_count_times[8 * blockIdx.x + (k)] = t_;                                      \
+        }                                                                                  \
+    } while (0)
+extern "C" int endor_debug_count_times(unsigned long long* host_out, int n) {
+    return int(cudaMemcpyFromSymbol(host_out, g_count_times, sizeof(unsigned long long) * 8 * n));
+}
+#else
+#define CT_STAMP(k) \
+    do {            \
+    } while (0)
+#endif
 __global__ void __launch_bounds__(kScanThreads) count_kernel(const __grid_constant__ Batch b) {
+    CT_STAMP(0);
     constexpr int kVecPerThread = kCountBlockWords / 4 / kScanThreads;  // uint4 per thread per block
     static_assert(kVecPerThread * kScanThreads * 4 == kCountBlockWords, "block / thread geometry");
     __shared__ uint32_t s_sub[2][kCountSubs];  // double-buffered: one barrier per block
@@ -59,6 +78,7 @@ __global__ void __launch_bounds__(kScanThreads) count_kernel(const __grid_consta
     }
     __syncthreads();
     pdl_wait();  // every global access below may depend on the previous kernel
+    CT_STAMP(1);
     pdl_launch_dependents();
     if (tid == 0)
         for (int st = 0; st < kCountStages; ++st)
@@ -75,6 +95,7 @@ __global__ void __launch_bounds__(kScanThreads) count_kernel(const __grid_consta
         if (full_block(cb)) {
             // full block: 8 consecutive lanes (128 B) = one 1024-bit sub-tile
             mbar_wait(full0 + 8 * st, (it / kCountStages) & 1);
+            if (it == 0) CT_STAMP(2);
             uint4 v[kVecPerThread];
 #pragma unroll
             for (int j = 0; j < kVecPerThread; ++j) v[j] = s_blk[st * (kCountBlockWords / 4) + j * kScanThreads + tid];
@@ -133,6 +154,7 @@ __global__ void __launch_bounds__(kScanThreads) count_kernel(const __grid_consta
         // (no second barrier: the next block writes the other sub[] buffer, and
         // warp 0 finishes this scan before it reaches the next barrier)
     }
+    CT_STAMP(3);
     if (tid == 0) {
         b.blk[T.blk0 + lc] = running;  // warp 0's lane 0 holds the range aggregate
         __threadfence();
@@ -140,36 +162,45 @@ __global__ void __launch_bounds__(kScanThreads) count_kernel(const __grid_consta
         s_last = (d == gridDim.x - 1);
     }
     __syncthreads();
+    CT_STAMP(4);
     if (!s_last) return;
 
     // ---- last CTA: per tensor, exclusive scan of its CTA aggregates -> bases -----
-    // One warp per tensor, all tensors at once: lane l sums a contiguous run of
-    // the tensor's aggregates (independent loads, one L2 round trip), a warp scan
-    // turns the run sums into bases, and the lane rewrites its run.
+    // One warp per tensor, all tensors at once.  The aggregates are read kAggK
+    // per lane at a time with independent loads (lane-strided, one L2 round
+    // trip per 32 kAggK entries -- a serial per-lane loop would pay one round
+    // trip per entry), scanned in registers, and rewritten as bases.
     __threadfence();
+    constexpr int kAggK = 8;
     for (int i = warp; i < b.count; i += kScanThreads / 32) {
         const BatchTensor& U = b.t[i];
         if (U.idx) continue;  // caller-indexed: not counted here (expand checks its tail)
         unsigned long long* blk = b.blk + U.blk0;
         const uint32_t nb = U.ncta;  // one aggregate per count CTA of this tensor
-        const uint32_t per = (nb + 31) / 32;
-        const uint32_t r0 = min(nb, lane * per), r1 = min(nb, r0 + per);
-        unsigned long long sum = 0;
-        for (uint32_t x = r0; x < r1; ++x) sum += __ldcg(&blk[x]);
-        const unsigned long long incl = warp_incl_scan(sum, lane);
-        unsigned long long run = incl - sum;
-        for (uint32_t x = r0; x < r1; ++x) {
-            const unsigned long long v = __ldcg(&blk[x]);
-            blk[x] = run;
-            run += v;
+        unsigned long long run = 0;
+        for (uint32_t base = 0; base < nb; base += 32 * kAggK) {
+            unsigned long long v[kAggK];
+#pragma unroll
+            for (int k = 0; k < kAggK; ++k) {
+                const uint32_t x = base + 32 * k + lane;
+                v[k] = x < nb ? __ldcg(&blk[x]) : 0ull;
+            }
+#pragma unroll
+            for (int k = 0; k < kAggK; ++k) {
+                const uint32_t x = base + 32 * k + lane;
+                const unsigned long long incl = warp_incl_scan(v[k], lane);
+                if (x < nb) blk[x] = run + incl - v[k];
+                run += __shfl_sync(0xffffffffu, incl, 31);
+            }
         }
-        if (lane == 31) {
-            blk[nb] = incl;  // grand total of the tensor
-            b.hdr->total = incl;
-            if (b.check_total && incl != U.nnz) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
+        if (lane == 0) {
+            blk[nb] = run;  // grand total of the tensor
+            b.hdr->total = run;
+            if (b.check_total && run != U.nnz) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
         }
     }
     if (tid == 0) b.hdr->done = 0;
+    CT_STAMP(5);
 }
 
 void batch_plan(Batch& b, uint64_t* sub_total, uint64_t* blk_total, int count_ctas) {
