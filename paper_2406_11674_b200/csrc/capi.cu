@@ -144,6 +144,10 @@ ExpandArgs expand_args(const endor_tensor_view* t, uint64_t n, uint64_t e0, uint
 
 // Count CTAs per batch: 3 per SM (each holds a 2 x 32 KiB TMA ring), each
 // streaming a contiguous bitmap range.
+// RankIndex chunk sizes the one-launch coarse-index expand takes (a tile of
+// 8192 elements holds whole chunks)
+bool derive_chunk(uint64_t cs) { return cs == 2048 || cs == 4096 || cs == 8192; }
+
 int count_ctas() {
     static thread_local int dev_cached = -1, sms = 148;
     int dev = 0;
@@ -733,9 +737,11 @@ int endor_cuda_decompress_chunked(const endor_tensor_view* t, uint64_t cs, const
     WsLayout L;
     if ((st = check_ws(ws, ws_bytes, n, &L))) return st;
     const auto* idx = reinterpret_cast<const unsigned long long*>(prefix);
-    if (cs == uint64_t(kSubElems) && aligned(t->bitmap, 16) && aligned(prefix, 16)) {
-        // fast path: the index supplies every sub-tile offset -> one expand launch,
-        // check_index's tail test inside it (codec.hpp:177-183)
+    if ((cs == uint64_t(kSubElems) || derive_chunk(cs)) && aligned(t->bitmap, 16) && aligned(prefix, 16)) {
+        // fast path: the index supplies every sub-tile offset (chunk 1024), or
+        // every chunk start with the producer deriving the sub-tile starts from
+        // the staged bitmap (2048 / 4096 / 8192, checking every entry) -> one
+        // expand launch, check_index's tail test inside it (codec.hpp:177-183)
         void* outs[1] = {dense_out};
         const uint64_t* pres[1] = {prefix};
         return endor_cuda_decompress_chunked_batch(t, pres, cs, outs, 1, ws, ws_bytes, stream);
@@ -783,7 +789,7 @@ int endor_cuda_decompress_chunked_batch(const endor_tensor_view* views, const ui
                                         size_t ws_bytes, void* stream) {
     if (count < 0 || count > kMaxBatch || (count > 0 && (!views || !prefixes || !dense_outs)))
         return fail(ENDOR_ERR_INVALID_ARGUMENT, "batch must hold 0..64 tensors with prefixes and outputs");
-    bool fast = cs == uint64_t(kSubElems);
+    bool fast = cs == uint64_t(kSubElems) || derive_chunk(cs);
     for (int i = 0; i < count && fast; ++i) fast = aligned(views[i].bitmap, 16) && aligned(prefixes[i], 16);
     if (!fast) {  // general path, one tensor at a time (verifies every index entry)
         for (int i = 0; i < count; ++i) {
@@ -806,6 +812,7 @@ int endor_cuda_decompress_chunked_batch(const endor_tensor_view* views, const ui
     for (int i = 0, j = 0; i < count; ++i) {
         if (views[i].rows * views[i].cols == 0) continue;
         if (!prefixes[i]) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null prefix");
+        b.t[j].idx_subs = uint32_t(cs / kSubElems);
         b.t[j++].idx = reinterpret_cast<const unsigned long long*>(prefixes[i]);
     }
     if (b.count == 0) return ENDOR_OK;
@@ -817,7 +824,8 @@ int endor_cuda_decompress_chunked_batch(const endor_tensor_view* views, const ui
     b.hdr = static_cast<WsHeader*>(ws);  // only the status word is used on this path
     b.tsub = nullptr;
     b.blk = nullptr;
-    CK(launch_expand_tma(b, eb, S(stream)));
+    if (cs == uint64_t(kSubElems)) CK(launch_expand_tma(b, eb, S(stream)));
+    else CK(launch_expand_tma_derive(b, eb, S(stream)));
     return ENDOR_OK;
 }
 

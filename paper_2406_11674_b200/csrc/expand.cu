@@ -83,10 +83,20 @@ struct Stage {
 // kBatch tile slots of 12 u64 (a claimed tile's index entries, via cp.async)
 constexpr uint32_t kSlotBytes = 12 * 8;
 constexpr uint32_t kTmaHeader = 256 + ((kPipes * kLook * kBatch * kSlotBytes + 127) & ~127u);
-template <int EB>
+// Coarse-index (DERIVE) kernels add, per pipe, after every pipe's stages: a
+// ring of kDesc tile descriptors {tile, window start, 9 sub-tile starts}
+// with its full/empty mbarriers, and the prefetched bitmaps of the claims in
+// flight (kLook x kBatch x 1 KiB).
+constexpr uint32_t kDesc = 8;
+constexpr uint32_t kDescBytes = 64;
+constexpr uint32_t kBmSlotBytes = kTileElems / 8;
+constexpr uint32_t kDerivePipeBytes = 16 * kDesc + kDesc * kDescBytes + kLook * kBatch * kBmSlotBytes;
+template <int EB, bool DERIVE = false>
 constexpr uint32_t tma_smem_bytes() {
-    return kTmaHeader + kPipes * kStages * Stage<EB>::kBytes;
+    return kTmaHeader + kPipes * kStages * Stage<EB>::kBytes + (DERIVE ? kPipes * kDerivePipeBytes : 0);
 }
+template <bool DERIVE>
+constexpr int tma_threads() { return kTmaThreads + (DERIVE ? 32 * kPipes : 0); }  // + a deriver warp per pipe
 static_assert(2 * kPipes * kStages * 8 + 8 <= 256, "mbarrier area");
 static_assert(256 + kPipes * kLook * kSlotBytes <= kTmaHeader, "claim slot area");
 
@@ -99,8 +109,18 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #endif
 
-template <int MODE>
-__global__ void __launch_bounds__(kTmaThreads, 1) expand_tma_kernel(const __grid_constant__ Batch b) {
+// DERIVE: the caller's RankIndex has a coarser chunk (2048 / 4096 / 8192 --
+// the reference's default is 4096, codec.hpp:19).  A deriver warp per pipe
+// takes over the claims: with each claim it also prefetches the claimed
+// tiles' bitmaps (cp.async), popcounts every 1024-element sub-tile (one lane
+// per sub-tile of the claim), derives the sub-tile starts from the chunk
+// entries with a segmented scan, checks every entry against the bitmap
+// (check_index, codec.hpp:170-184, and the middle entries, as the
+// multi-launch path does), and posts one descriptor per tile to a ring; the
+// pipe's TMA warp only turns descriptors into bulk copies, so a stage never
+// waits behind that work, and the consumers run unchanged.
+template <int MODE, bool DERIVE = false>
+__global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(const __grid_constant__ Batch b) {
 #ifdef ENDOR_CTA_TIMING
     if (threadIdx.x == 0) {
         unsigned smid;
@@ -113,12 +133,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1) expand_tma_kernel(const __grid
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t sbase = smem_u32(smem);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // pipe p: producer warp p, consumer warps kPipes + 8 p .. +7
-    const int pipe = warp < kPipes ? warp : (warp - kPipes) / kConsumerWarps;
+    // pipe p: producer warp p, consumer warps kPipes + 8 p .. +7 (DERIVE: deriver warp kPipes * 9 + p)
+    constexpr int kFirstDeriver = kPipes * (kConsumerWarps + 1);
+    const bool deriver = DERIVE && warp >= kFirstDeriver;
+    const int pipe = warp < kPipes ? warp : (deriver ? warp - kFirstDeriver : (warp - kPipes) / kConsumerWarps);
     const uint32_t full0 = sbase + 16 * kStages * pipe, empty0 = full0 + 8 * kStages;
     const uint32_t claim = sbase + 16 * kStages * kPipes;  // shared u32 tile-claim counter
     const uint32_t st0 = sbase + kTmaHeader + pipe * kStages * Stage<EB>::kBytes;
     const uint32_t slot0 = sbase + 256 + pipe * kLook * kBatch * kSlotBytes;  // this pipe's claim slots
+    // DERIVE: this pipe's descriptor ring (full / empty barriers, descriptors) and claim bitmaps
+    const uint32_t dsc0 = sbase + kTmaHeader + kPipes * kStages * Stage<EB>::kBytes + pipe * kDerivePipeBytes;
+    const uint32_t dfull0 = dsc0, dempty0 = dsc0 + 8 * kDesc, desc0 = dsc0 + 16 * kDesc;
+    const uint32_t bslot0 = desc0 + kDesc * kDescBytes;
     const uint64_t ntiles = b.ntiles;
     // this CTA's tiles: blockIdx.x + j * gridDim.x, j < nj
     const uint32_t nj = blockIdx.x < ntiles ? uint32_t((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0u;
@@ -129,6 +155,15 @@ __global__ void __launch_bounds__(kTmaThreads, 1) expand_tma_kernel(const __grid
             mbar_init(sbase + 16 * kStages * (s / kStages) + 8 * (s % kStages), 2);  // expect_tx + fix-up
             mbar_init(sbase + 16 * kStages * (s / kStages) + 8 * kStages + 8 * (s % kStages), kConsumerWarps);
         }
+        if (DERIVE) {
+            for (int p = 0; p < kPipes; ++p) {
+                const uint32_t d0 = sbase + kTmaHeader + kPipes * kStages * Stage<EB>::kBytes + p * kDerivePipeBytes;
+                for (uint32_t k = 0; k < kDesc; ++k) {
+                    mbar_init(d0 + 8 * k, 1);               // descriptor posted
+                    mbar_init(d0 + 8 * kDesc + 8 * k, 1);   // descriptor consumed
+                }
+            }
+        }
         asm volatile("st.shared.u32 [%0], 0;" ::"r"(claim) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -138,12 +173,32 @@ __global__ void __launch_bounds__(kTmaThreads, 1) expand_tma_kernel(const __grid
     if (cta_error_latched(b.hdr)) return;
     pdl_launch_dependents();
 
-    if (warp < kPipes) {
-        // ================= producer warp of pipe `pipe` =================
+    if (warp < kPipes || deriver) {
+        // ====== producer warp of pipe `pipe` (DERIVE: its TMA warp or its deriver warp) ======
         constexpr uint32_t kSubsPerBlk = kCountSubs;  // sub-tiles per count block
+        if (DERIVE && deriver && blockIdx.x == 0 && pipe == 0) {
+            // check_index's tail test: the last chunk spans up to idx_subs sub-tiles
+            for (int k = 0; k < b.count; ++k) {
+                const BatchTensor& T = b.t[k];
+                const uint64_t cs = uint64_t(T.idx_subs) * kSubElems, last = ceil_div(T.n, cs) - 1;
+                const uint64_t nw = (T.n + 31) / 32, nbytes = (T.n + 7) / 8;
+                uint32_t tail = 0;
+                for (uint64_t w = last * cs / 32 + lane; w < nw; w += 32) {
+                    uint32_t v = load_word32(T.bitmap, w, nbytes);
+                    if (w * 32 + 32 > T.n) {
+                        const uint32_t keep = uint32_t(T.n - w * 32);
+                        if ((T.n & 7) && (v >> keep)) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
+                        v &= (1u << keep) - 1u;
+                    }
+                    tail += __popc(v);
+                }
+                tail = __reduce_add_sync(0xffffffffu, tail);
+                if (lane == 0 && T.idx[last] + tail != T.nnz) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
+            }
+        }
         // check_index's tail test (codec.hpp:177-183) for caller-indexed tensors:
         // idx[last] + popcount(last chunk) == nnz, plus the padding bits
-        if (blockIdx.x == 0 && pipe == 0) {
+        if (!DERIVE && blockIdx.x == 0 && pipe == 0) {
             for (int k = 0; k < b.count; ++k) {
                 const BatchTensor& T = b.t[k];
                 if (!T.idx) continue;
@@ -182,7 +237,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1) expand_tma_kernel(const __grid
             auto cp8 = [&](int k, const unsigned long long* src) {
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(slot + 8 * k), "l"(src) : "memory");
             };
-            if (T.idx) {
+            if (DERIVE) {  // the chunk entries covering the tile and the next one's first
+                const uint32_t S = T.idx_subs;
+                const uint64_t nch = ceil_div(nsub, S), c0 = a / S;
+#pragma unroll
+                for (int k = 0; k <= 4; ++k)
+                    if (uint32_t(k) * S <= 8 && c0 + k < nch) cp8(k, T.idx + c0 + k);
+            } else if (T.idx) {
 #pragma unroll
                 for (int k = 0; k <= 8; ++k)
                     if (a + k < nsub) cp8(k, T.idx + a + k);
@@ -200,6 +261,34 @@ __global__ void __launch_bounds__(kTmaThreads, 1) expand_tma_kernel(const __grid
             const BatchTensor& T = b.t[batch_tensor_of_tile(b, t)];
             const uint64_t lt = t - T.tile0, nsub = ceil_div(T.n, kSubElems), a = lt * 8;
             unsigned long long e[9];
+            if (DERIVE) {
+                // chunk entries: monotone, within [0, nnz], at most one chunk of
+                // values apart (clamp + latch).  rel[0..4] = the chunk starts
+                // relative to the window (the window end past the tile's last
+                // chunk), rel[8] = the window end; derive() fills in rel[0..7].
+                const uint32_t S = T.idx_subs, m = 8 / S;
+                const uint64_t nch = ceil_div(nsub, S), c0 = a / S;
+                bool bad = false;
+                unsigned long long lo = 0, ce[5];
+#pragma unroll
+                for (int k = 0; k <= 4; ++k) {
+                    if (uint32_t(k) > m) {
+                        ce[k] = lo;
+                        continue;
+                    }
+                    const unsigned long long r = c0 + k < nch ? lds64(slot + 8 * k) : T.nnz;
+                    unsigned long long v = r < lo ? lo : (r > T.nnz ? T.nnz : r);
+                    if (k > 0 && v - lo > uint64_t(S) * kSubElems) v = lo + uint64_t(S) * kSubElems;
+                    bad |= v != r;
+                    ce[k] = lo = v;
+                }
+                if (bad) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
+                s0 = ce[0];
+#pragma unroll
+                for (int k = 0; k <= 4; ++k) rel[k] = uint32_t(ce[k] - ce[0]);
+                rel[8] = rel[4];
+                return;
+            }
             if (T.idx) {
                 // monotone, within [0, nnz], at most 1024 values per sub-tile: clamp
                 // and latch (memory safety; an entry that passes but disagrees with
@@ -231,29 +320,141 @@ __global__ void __launch_bounds__(kTmaThreads, 1) expand_tma_kernel(const __grid
             j = __shfl_sync(0xffffffffu, j, 0);
             const uint64_t t = tile_of(j + lane);
             if (lane < kBatch && t < ntiles) fetch(slot0 + ((c % kLook) * kBatch + lane) * kSlotBytes, t);
+            if (DERIVE) {  // the claimed full tiles' bitmaps, 32 bytes per lane each
+#pragma unroll
+                for (int k = 0; k < kBatch; ++k) {
+                    const uint64_t tk = tile_of(j + k);
+                    if (tk >= ntiles) break;
+                    const BatchTensor& T = b.t[batch_tensor_of_tile(b, tk)];
+                    const uint64_t lt = tk - T.tile0;
+                    if ((lt + 1) * kTileElems > T.n) continue;  // a partial tile: derive() reads global memory
+                    const uint32_t dst = bslot0 + ((c % kLook) * kBatch + k) * kBmSlotBytes + 32 * lane;
+                    const uint8_t* src = T.bitmap + lt * kBmSlotBytes + 32 * lane;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16), "l"(src + 16) : "memory");
+                }
+            }
             asm volatile("cp.async.commit_group;" ::: "memory");
             return j;
         };
+        // DERIVE: lane l takes sub-tile l % 8 of the claim's tile l / 8:
+        // popcount, a segmented scan over the chunk's lanes turns the chunk
+        // start into the sub-tile start, the chunk's last lane checks that the
+        // chunk ends where the next entry says, and lane k gathers tile k's
+        // eight starts
+        static_assert(kBatch * 8 == 32, "one lane per sub-tile of a claim");
+        auto derive = [&](uint32_t c, uint32_t j0, uint32_t (&rel)[9]) {
+            const int k = lane >> 3, q = lane & 7;
+            const uint64_t tk = tile_of(j0 + k);
+            uint32_t p = 0, S = 1;
+            if (tk < ntiles) {
+                const BatchTensor& T = b.t[batch_tensor_of_tile(b, tk)];
+                const uint64_t lt = tk - T.tile0;
+                const uint32_t count = uint32_t(umin64(kTileElems, T.n - lt * kTileElems));
+                S = T.idx_subs;
+                if (count == kTileElems) {
+                    const uint32_t src = bslot0 + ((c % kLook) * kBatch + k) * kBmSlotBytes + 128 * q;
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) {
+                        uint32_t x0, x1, x2, x3;
+                        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                     : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3) : "r"(src + 16 * v));
+                        p += __popc(x0) + __popc(x1) + __popc(x2) + __popc(x3);
+                    }
+                } else {  // a partial tile (not prefetched): words from global memory, bits past the end masked
+                    const uint64_t nbytes = (T.n + 7) / 8, wb = lt * (kTileElems / 32) + 32 * q;
+                    for (uint32_t x = 0; x < 32; ++x) {
+                        const int32_t keep = int32_t(count) - int32_t(1024 * q + 32 * x);
+                        if (keep <= 0) break;
+                        const uint32_t v = load_word32(T.bitmap, wb + x, nbytes);
+                        p += __popc(keep >= 32 ? v : v & ((1u << keep) - 1u));
+                    }
+                }
+            }
+            uint32_t st[5];  // tile k's chunk starts, then the window end
+#pragma unroll
+            for (int x = 0; x < 5; ++x) st[x] = __shfl_sync(0xffffffffu, rel[x], k);
+            const uint32_t cq = uint32_t(q) >> (__ffs(S) - 1), pos = uint32_t(q) & (S - 1);
+            const uint32_t start = cq == 0 ? st[0] : cq == 1 ? st[1] : cq == 2 ? st[2] : st[3];
+            const uint32_t next = cq == 0 ? st[1] : cq == 1 ? st[2] : cq == 2 ? st[3] : st[4];
+            uint32_t x = p;
+#pragma unroll
+            for (uint32_t d = 1; d < 8; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+                if (d < S && pos >= d) x += y;
+            }
+            const uint32_t r = start + x - p;  // this sub-tile's first value
+            if (tk < ntiles && pos == S - 1 && start + x != next) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
+            const int src0 = lane < kBatch ? 8 * lane : 0;
+#pragma unroll
+            for (int x2 = 0; x2 < 8; ++x2) {
+                const uint32_t v = __shfl_sync(0xffffffffu, r, src0 + x2);
+                if (lane < kBatch) rel[x2] = v;
+            }
+        };
         uint32_t qj[kLook];  // first j of the claims in flight, oldest first
-#pragma unroll
-        for (int k = 0; k < kLook; ++k) qj[k] = claim_batch(k);
         int i = 0, ti = 0;
-        for (uint32_t c = 0; qj[0] < nj; ++c) {
-            asm volatile("cp.async.wait_group %0;" ::"n"(kLook - 1) : "memory");
-            __syncwarp();
-            unsigned long long tp_l = 0;
-            uint32_t rel_l[9] = {};
-            const uint64_t tl = tile_of(qj[0] + lane);
-            if (lane < kBatch && tl < ntiles) finish(slot0 + ((c % kLook) * kBatch + lane) * kSlotBytes, tl, tp_l, rel_l);
-            __syncwarp();  // the slots are read before the claim below refills them
+        if (DERIVE && deriver) {
+            // ---- deriver: claims, chunk entries, bitmaps, sub-tile starts -> descriptors
 #pragma unroll
-            for (int k = 0; k + 1 < kLook; ++k) qj[k] = qj[k + 1];
-            qj[kLook - 1] = claim_batch(c + kLook);
-            for (uint32_t own = 0; own < uint32_t(kBatch); ++own, ++i) {
-            const uint64_t t = __shfl_sync(0xffffffffu, tl, own);
-            if (t >= ntiles) break;
-            const unsigned long long tp = __shfl_sync(0xffffffffu, tp_l, own);
-            const unsigned long long te = tp + __shfl_sync(0xffffffffu, rel_l[8], own);
+            for (int k = 0; k < kLook; ++k) qj[k] = claim_batch(k);
+            uint32_t d = 0;
+            for (uint32_t c = 0; qj[0] < nj; ++c) {
+                asm volatile("cp.async.wait_group %0;" ::"n"(kLook - 1) : "memory");
+                __syncwarp();
+                unsigned long long tp_l = 0;
+                uint32_t rel_l[9] = {};
+                const uint64_t tl = tile_of(qj[0] + lane);
+                if (lane < kBatch && tl < ntiles) finish(slot0 + ((c % kLook) * kBatch + lane) * kSlotBytes, tl, tp_l, rel_l);
+                derive(c, qj[0], rel_l);
+                __syncwarp();  // the slots are read before the claim below refills them
+#pragma unroll
+                for (int k = 0; k + 1 < kLook; ++k) qj[k] = qj[k + 1];
+                qj[kLook - 1] = claim_batch(c + kLook);
+                for (uint32_t own = 0; own < uint32_t(kBatch); ++own, ++d) {
+                    const uint64_t t = __shfl_sync(0xffffffffu, tl, own);
+                    if (t >= ntiles) break;
+                    const uint32_t ds = d % kDesc, da = desc0 + ds * kDescBytes;
+                    if (d >= kDesc) mbar_wait(dempty0 + 8 * ds, ((d / kDesc) - 1) & 1);
+                    if (lane == own) {
+                        asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(da), "l"(t), "l"(tp_l) : "memory");
+                        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(da + 16), "r"(rel_l[0]),
+                                     "r"(rel_l[1]), "r"(rel_l[2]), "r"(rel_l[3]) : "memory");
+                        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(da + 32), "r"(rel_l[4]),
+                                     "r"(rel_l[5]), "r"(rel_l[6]), "r"(rel_l[7]) : "memory");
+                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(da + 48), "r"(rel_l[8]) : "memory");
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(dfull0 + 8 * ds);
+                }
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            {  // end of work
+                const uint32_t ds = d % kDesc, da = desc0 + ds * kDescBytes;
+                if (d >= kDesc) mbar_wait(dempty0 + 8 * ds, ((d / kDesc) - 1) & 1);
+                if (lane == 0) {
+                    asm volatile("st.shared.u64 [%0], %1;" ::"r"(da), "l"(~0ull) : "memory");
+                    mbar_arrive(dfull0 + 8 * ds);
+                }
+            }
+            return;
+        }
+        if (DERIVE) {
+            // ---- TMA warp: descriptors -> stages (the same stage fill as below)
+            for (uint32_t d = 0;; ++d, ++i) {
+                const uint32_t ds = d % kDesc, da = desc0 + ds * kDescBytes;
+                mbar_wait(dfull0 + 8 * ds, (d / kDesc) & 1);
+                const uint64_t t = lds64(da);
+                if (t >= ntiles) break;
+                const unsigned long long tp = lds64(da + 8);
+                const unsigned long long te = tp + lds32(da + 48);
+                uint32_t dr[8];
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(dr[0]), "=r"(dr[1]), "=r"(dr[2]),
+                             "=r"(dr[3]) : "r"(da + 16));
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(dr[4]), "=r"(dr[5]), "=r"(dr[6]),
+                             "=r"(dr[7]) : "r"(da + 32));
+                __syncwarp();
+                if (lane == 0) mbar_arrive(dempty0 + 8 * ds);  // the descriptor is in registers
             const int s = i % kStages;
             const uint32_t stg = st0 + s * Stage<EB>::kBytes;
             const uint32_t full = full0 + 8 * s;
@@ -280,11 +481,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) expand_tma_kernel(const __grid
                              "r"(uint32_t(ws - as)) : "memory");
                 asm volatile("st.shared.u64 [%0], %1;" ::"r"(stg + Stage<EB>::kSub + 72), "l"(t) : "memory");
             }
-            if (lane == own) {  // the 8 sub-tile starts, relative to the window start
-                asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(stg + Stage<EB>::kSub), "r"(rel_l[0]),
-                             "r"(rel_l[1]), "r"(rel_l[2]), "r"(rel_l[3]) : "memory");
+            if (lane == 0) {  // the 8 sub-tile starts, relative to the window start (from the descriptor)
+                asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(stg + Stage<EB>::kSub), "r"(dr[0]),
+                             "r"(dr[1]), "r"(dr[2]), "r"(dr[3]) : "memory");
                 asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(stg + Stage<EB>::kSub + 16),
-                             "r"(rel_l[4]), "r"(rel_l[5]), "r"(rel_l[6]), "r"(rel_l[7]) : "memory");
+                             "r"(dr[4]), "r"(dr[5]), "r"(dr[6]), "r"(dr[7]) : "memory");
             }
             // edge bytes the bulk copies cannot move (the ends of the bitmap and of
             // the values buffer): only the bytes outside [bs, be) are visited
@@ -302,6 +503,75 @@ __global__ void __launch_bounds__(kTmaThreads, 1) expand_tma_kernel(const __grid
             if (edges) fence_proxy_async_smem();  // st.shared edges vs the TMA that later reuses the stage
             __syncwarp();
             if (lane == 0) mbar_arrive(full);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kLook; ++k) qj[k] = claim_batch(k);
+            for (uint32_t c = 0; qj[0] < nj; ++c) {
+                asm volatile("cp.async.wait_group %0;" ::"n"(kLook - 1) : "memory");
+                __syncwarp();
+                unsigned long long tp_l = 0;
+                uint32_t rel_l[9] = {};
+                const uint64_t tl = tile_of(qj[0] + lane);
+                if (lane < kBatch && tl < ntiles) finish(slot0 + ((c % kLook) * kBatch + lane) * kSlotBytes, tl, tp_l, rel_l);
+                __syncwarp();  // the slots are read before the claim below refills them
+#pragma unroll
+                for (int k = 0; k + 1 < kLook; ++k) qj[k] = qj[k + 1];
+                qj[kLook - 1] = claim_batch(c + kLook);
+                for (uint32_t own = 0; own < uint32_t(kBatch); ++own, ++i) {
+                const uint64_t t = __shfl_sync(0xffffffffu, tl, own);
+                if (t >= ntiles) break;
+                const unsigned long long tp = __shfl_sync(0xffffffffu, tp_l, own);
+                const unsigned long long te = tp + __shfl_sync(0xffffffffu, rel_l[8], own);
+                const int s = i % kStages;
+                const uint32_t stg = st0 + s * Stage<EB>::kBytes;
+                const uint32_t full = full0 + 8 * s;
+                while (ti + 1 < b.count && t >= b.t[ti + 1].tile0) ++ti;
+                const BatchTensor& T = b.t[ti];
+                const uint64_t lt = t - T.tile0;
+                const uintptr_t vlo = reinterpret_cast<uintptr_t>(T.values);
+                const uintptr_t vhi = vlo + T.nnz * EB;
+                const uintptr_t vlo16 = (vlo + 15) & ~uintptr_t(15), vhi16 = vhi & ~uintptr_t(15);
+                if (i >= kStages) mbar_wait(empty0 + 8 * s, ((i / kStages) - 1) & 1);
+                const uint64_t t0 = lt * kTileElems;
+                const uint32_t count = uint32_t(umin64(kTileElems, T.n - t0));
+                const uint32_t bm_bytes = (count + 7) / 8;
+                const uint32_t bm_bulk = count == kTileElems ? 1024u : (bm_bytes & ~15u);
+                const uintptr_t ws = vlo + tp * EB, we = vlo + te * EB;
+                const uintptr_t as = ws & ~uintptr_t(15), ae = (we + 15) & ~uintptr_t(15);
+                const uintptr_t bs = as > vlo16 ? as : vlo16, be = ae < vhi16 ? ae : vhi16;
+                const uint32_t vbulk = be > bs ? uint32_t(be - bs) : 0u;
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(full, bm_bulk + vbulk);
+                    if (bm_bulk) bulk_g2s(stg + Stage<EB>::kBm, T.bitmap + t0 / 8, bm_bulk, full);
+                    if (vbulk) bulk_g2s(stg + Stage<EB>::kVals + uint32_t(bs - as), reinterpret_cast<const void*>(bs), vbulk, full);
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(stg + Stage<EB>::kSub + 64),  // window start
+                                 "r"(uint32_t(ws - as)) : "memory");
+                    asm volatile("st.shared.u64 [%0], %1;" ::"r"(stg + Stage<EB>::kSub + 72), "l"(t) : "memory");
+                }
+                if (lane == own) {  // the 8 sub-tile starts, relative to the window start
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(stg + Stage<EB>::kSub), "r"(rel_l[0]),
+                                 "r"(rel_l[1]), "r"(rel_l[2]), "r"(rel_l[3]) : "memory");
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(stg + Stage<EB>::kSub + 16),
+                                 "r"(rel_l[4]), "r"(rel_l[5]), "r"(rel_l[6]), "r"(rel_l[7]) : "memory");
+                }
+                // edge bytes the bulk copies cannot move (the ends of the bitmap and of
+                // the values buffer): only the bytes outside [bs, be) are visited
+                bool edges = bm_bulk != bm_bytes;
+                for (uint32_t x = bm_bulk + lane; x < bm_bytes; x += 32)
+                    sts8(stg + Stage<EB>::kBm + x, __ldg(T.bitmap + t0 / 8 + x));
+                if (bs > ws || be < we) {
+                    edges = true;
+                    const uintptr_t h1 = vbulk ? bs : we, t1 = vbulk ? be : we;  // head [ws, h1), tail [t1, we)
+                    for (uintptr_t p = ws + lane; p < h1 && p < we; p += 32)
+                        sts8(stg + Stage<EB>::kVals + uint32_t(p - as), *reinterpret_cast<const uint8_t*>(p));
+                    for (uintptr_t p = (t1 > ws ? t1 : ws) + lane; p < we; p += 32)
+                        sts8(stg + Stage<EB>::kVals + uint32_t(p - as), *reinterpret_cast<const uint8_t*>(p));
+                }
+                if (edges) fence_proxy_async_smem();  // st.shared edges vs the TMA that later reuses the stage
+                __syncwarp();
+                if (lane == 0) mbar_arrive(full);
+                }
             }
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
@@ -461,16 +731,24 @@ cudaError_t launch_expand(const ExpandArgs& a, int mode, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <int MODE>
+template <int MODE, bool DERIVE = false>
 static cudaError_t launch_tma_mode(const Batch& b, cudaStream_t s) {
-    constexpr uint32_t smem = tma_smem_bytes<mode_in(MODE)>();
+    constexpr uint32_t smem = tma_smem_bytes<mode_in(MODE), DERIVE>();
+    constexpr int threads = tma_threads<DERIVE>();
     int blocks_per_sm = 1, sms = 148;
-    cudaError_t e = kernel_slots(reinterpret_cast<const void*>(expand_tma_kernel<MODE>), kTmaThreads, smem,
+    cudaError_t e = kernel_slots(reinterpret_cast<const void*>(expand_tma_kernel<MODE, DERIVE>), threads, smem,
                                  &blocks_per_sm, &sms);
     if (e != cudaSuccess) return e;
     const uint64_t grid = umin64(b.ntiles, uint64_t(blocks_per_sm) * sms);
     if (grid == 0) return cudaSuccess;
-    return launch_pdl(expand_tma_kernel<MODE>, dim3(unsigned(grid)), dim3(kTmaThreads), smem, s, b);
+    return launch_pdl(expand_tma_kernel<MODE, DERIVE>, dim3(unsigned(grid)), dim3(threads), smem, s, b);
+}
+
+// decompress_chunked with a caller's RankIndex at chunk 2048 / 4096 / 8192
+// (every tensor's idx and idx_subs = chunk / 1024 set): one launch.
+cudaError_t launch_expand_tma_derive(const Batch& b, int mode, cudaStream_t s) {
+    if (mode == kModeF16) return launch_tma_mode<kModeF16, true>(b, s);
+    return launch_tma_mode<kModeI8, true>(b, s);
 }
 
 // Whole-tensor expand of a batch through the TMA ring (needs count_kernel's

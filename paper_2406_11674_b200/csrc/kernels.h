@@ -96,6 +96,7 @@ struct BatchTensor {
     // (absolute offsets, idx[k] = rank(1024 k)); when set, no count pass runs
     // and tsub/blk are unused for this tensor.
     const unsigned long long* idx;
+    uint32_t idx_subs;      // coarse-index expand (launch_expand_tma_derive): 1024-element sub-tiles per idx entry
     float scale;            // dequant mode: f16 = f32_to_f16(float(q) * scale)
     uint32_t deq_fast;      // dequant mode: scale finite with its sign bit clear
     // fused GEMV mode: y = W x with W this tensor (rows = outputs, cols % 1024 == 0);
@@ -137,6 +138,7 @@ cudaError_t launch_verify_index(const unsigned long long* idx, uint64_t chunks, 
                                 uint64_t n, const unsigned long long* tsub, const unsigned long long* blk,
                                 uint64_t spc, WsHeader* hdr, cudaStream_t s);
 cudaError_t launch_expand_tma(const Batch& b, int mode, cudaStream_t s);  // 1 i8, 2 f16, 3 dequant
+cudaError_t launch_expand_tma_derive(const Batch& b, int mode, cudaStream_t s);  // idx at 2048/4096/8192
 // fused decompress -> GEMV over a batch (f16, cols % 1024 == 0, part set per tensor),
 // then y[r] = sum of row r's cols/1024 segment partials in a fixed order
 cudaError_t launch_gemv_fused(Batch& b, cudaStream_t s);

@@ -42,8 +42,8 @@ def test_large_shapes(cuda_lib, large_cases):
         assert crc(out.data) == c["crc_dense"], c["name"]     # == reference decompress
         idx = E.build_rank_index(t.bitmap, 4096)
         assert crc(idx.prefix.view(torch.uint8)) == c["crc_prefix_4096"], c["name"]
-        if c["name"] == "opt-66b.fc1.seed7":
-            assert torch.equal(E.decompress_chunked(t, idx).data, w.data)
+        # the reference's default chunk: one launch, sub-tile starts derived on chip
+        assert torch.equal(E.decompress_chunked(t, idx).data, w.data), c["name"]
         idx1k = E.build_rank_index(t.bitmap, 1024)  # load-time index: single-launch path
         assert torch.equal(E.decompress_chunked(t, idx1k).data, w.data), c["name"]
         del w, t, out, idx
