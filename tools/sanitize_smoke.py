@@ -38,7 +38,7 @@ for (rows, cols, eb, zf, off) in [(2, 2, 2, 0.5, 0), (37, 1000, 2, 0.5, 2), (64,
                                   (9, 4096, 1, 0.6, 1), (300, 1024, 2, 0.9, 10)]:
     w, t = tensor(rows, cols, eb, rows + cols, zf, off)
     assert E.decompress(t).bytes() == w.tobytes()                                  # count + TMA expand
-    for cs in (64, 1024, 4096):
+    for cs in (64, 1024, 2048, 4096, 8192):
         idx = E.build_rank_index(t.bitmap, cs)                                     # scan_kernel
         assert E.decompress_chunked(t, idx).bytes() == w.tobytes()                 # fallback / fast / coarse
         buf = torch.zeros(t.dense_bytes(), dtype=torch.uint8, device=dev)
@@ -79,6 +79,19 @@ for _ in range(5):
         E.decompress_chunked(ta, E.RankIndex(1024, torch.from_numpy(bad).to(dev)))
     except E.CorruptionError:
         pass
+
+# coarse (2048 / 4096 / 8192) indices: every wrong entry is reported, never an out-of-bounds access
+for cs in (2048, 4096, 8192):
+    gc = E.build_rank_index(ta.bitmap, cs).prefix.cpu().numpy().astype(np.int64)
+    for _ in range(4):
+        bad = np.sort(rng.integers(0, int(ta.nnz()) + 1, size=len(gc))).astype(np.int64)
+        bad[0] = 0
+        for v in (bad, gc + np.arange(len(gc)), np.full_like(gc, 10 ** 12)):
+            try:
+                E.decompress_chunked(ta, E.RankIndex(cs, torch.from_numpy(v).to(dev)))
+            except E.CorruptionError:
+                pass
+    assert E.decompress_chunked(ta, E.RankIndex(cs, torch.from_numpy(gc).to(dev))).bytes() == wa.tobytes()
 
 # the fused GEMV's set-bit consumer (density <= 0.2), odd value offset
 w9, t9 = tensor(48, 4096, 2, 99, 0.9, 3)
