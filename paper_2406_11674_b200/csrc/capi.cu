@@ -148,17 +148,6 @@ ExpandArgs expand_args(const endor_tensor_view* t, uint64_t n, uint64_t e0, uint
 // 8192 elements holds whole chunks)
 bool derive_chunk(uint64_t cs) { return cs == 2048 || cs == 4096 || cs == 8192; }
 
-// decompress without an index: one expand launch with an in-kernel look-back
-// (default), or count_kernel + expand (ENDOR_DECOMPRESS_TWO_PASS=1; the
-// phase-split entry point always runs the two passes)
-bool one_launch_decompress() {
-    static const bool v = [] {
-        const char* e = getenv("ENDOR_DECOMPRESS_TWO_PASS");
-        return !(e && atoi(e) != 0);
-    }();
-    return v;
-}
-
 int count_ctas() {
     static thread_local int dev_cached = -1, sms = 148;
     int dev = 0;
@@ -192,10 +181,6 @@ int full_expand(const endor_tensor_view* t, uint64_t n, int eb, void* dst, const
         b.tsub = L.tsub;
         b.blk = L.blk;
         b.hdr = L.hdr;
-        if (phase == 0 && one_launch_decompress() && eb != 3) {
-            CK(launch_expand_tma_lookback(b, eb, s));
-            return ENDOR_OK;
-        }
         if (phase != 2) CK(launch_count(b, s));
         if (phase != 1) CK(launch_expand_tma(b, eb, s));
         return ENDOR_OK;
@@ -342,10 +327,6 @@ int endor_cuda_decompress_batch_phase(const endor_tensor_view* views, void* cons
     b.tsub = L.tsub;
     b.blk = L.blk;
     b.hdr = L.hdr;
-    if (phase == 0 && one_launch_decompress()) {
-        CK(launch_expand_tma_lookback(b, eb, S(stream)));
-        return ENDOR_OK;
-    }
     if (phase != 2) CK(launch_count(b, S(stream)));
     if (phase != 1) CK(launch_expand_tma(b, eb, S(stream)));
     return ENDOR_OK;

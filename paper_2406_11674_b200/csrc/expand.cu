@@ -87,10 +87,7 @@ constexpr uint32_t kTmaHeader = 256 + ((kPipes * kLook * kBatch * kSlotBytes + 1
 // ring of kDesc tile descriptors {tile, window start, 9 sub-tile starts}
 // with its full/empty mbarriers, and the prefetched bitmaps of the claims in
 // flight (kLook x kBatch x 1 KiB).
-#ifndef ENDOR_DESC
-#define ENDOR_DESC 8
-#endif
-constexpr uint32_t kDesc = ENDOR_DESC;
+constexpr uint32_t kDesc = 8;
 constexpr uint32_t kDescBytes = 64;
 constexpr uint32_t kBmSlotBytes = kTileElems / 8;
 constexpr uint32_t kDerivePipeBytes = 16 * kDesc + kDesc * kDescBytes + kLook * kBatch * kBmSlotBytes;
@@ -122,17 +119,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // multi-launch path does), and posts one descriptor per tile to a ring; the
 // pipe's TMA warp only turns descriptors into bulk copies, so a stage never
 // waits behind that work, and the consumers run unchanged.
-//
-// LB (with DERIVE): no index at all -- the reference's decompress
-// (codec.hpp:157-166) in one launch.  The deriver popcounts each claimed tile,
-// publishes the tile total, and finds the tile's first value by a decoupled
-// look-back over the tiles before it (the CTAs' tiles interleave, and the
-// CTA's own previous tile is G tiles back, so a look-back window of 160
-// entries almost always ends at an inclusive prefix); the tensor's last tile
-// checks popcount == nnz (codec.hpp:158-160).
-template <int MODE, bool DERIVE = false, bool LB = false>
+template <int MODE, bool DERIVE = false>
 __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(const __grid_constant__ Batch b) {
-    static_assert(!LB || DERIVE, "the look-back runs in the deriver warps");
 #ifdef ENDOR_CTA_TIMING
     if (threadIdx.x == 0) {
         unsigned smid;
@@ -159,9 +147,7 @@ __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(co
     const uint32_t bslot0 = desc0 + kDesc * kDescBytes;
     const uint64_t ntiles = b.ntiles;
     // this CTA's tiles: blockIdx.x + j * gridDim.x, j < nj
-    // LB: tiles go out in blocks of 4 consecutive tiles (one claim), block k to CTA k % grid
-    const uint64_t nblk = LB ? ceil_div(ntiles, 4) : ntiles;
-    const uint32_t nj = blockIdx.x < nblk ? uint32_t((nblk - 1 - blockIdx.x) / gridDim.x + 1) * (LB ? 4u : 1u) : 0u;
+    const uint32_t nj = blockIdx.x < ntiles ? uint32_t((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0u;
 
     init_luts(tid);
     if (tid == 0) {
@@ -190,15 +176,7 @@ __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(co
     if (warp < kPipes || deriver) {
         // ====== producer warp of pipe `pipe` (DERIVE: its TMA warp or its deriver warp) ======
         constexpr uint32_t kSubsPerBlk = kCountSubs;  // sub-tiles per count block
-        if (LB && deriver && blockIdx.x == 0 && pipe == 0 && lane == 0) {
-            // padding bits of each tensor's final byte must be zero (bitmap.hpp:78-84)
-            for (int k = 0; k < b.count; ++k) {
-                const BatchTensor& T = b.t[k];
-                if ((T.n & 7) && (__ldg(T.bitmap + (T.n - 1) / 8) >> (T.n & 7)))
-                    latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
-            }
-        }
-        if (DERIVE && !LB && deriver && blockIdx.x == 0 && pipe == 0) {
+        if (DERIVE && deriver && blockIdx.x == 0 && pipe == 0) {
             // check_index's tail test: the last chunk spans up to idx_subs sub-tiles
             for (int k = 0; k < b.count; ++k) {
                 const BatchTensor& T = b.t[k];
@@ -252,21 +230,14 @@ __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(co
         // register for successive claims would serialise on each other) into
         // its slot of the claim, one commit group per claim, and the claim is
         // issued kLook claims later after cp.async.wait_group(kLook - 1).
-        auto tile_of = [&](uint32_t j) -> uint64_t {
-            if (LB) {
-                const uint64_t t = ((uint64_t(j / 4) * gridDim.x + blockIdx.x) * 4 + (j % 4));
-                return j < nj && t < ntiles ? t : ntiles;
-            }
-            return j < nj ? blockIdx.x + uint64_t(j) * gridDim.x : ntiles;
-        };
+        auto tile_of = [&](uint32_t j) -> uint64_t { return j < nj ? blockIdx.x + uint64_t(j) * gridDim.x : ntiles; };
         auto fetch = [&](uint32_t slot, uint64_t t) {  // one lane per tile; t < ntiles
             const BatchTensor& T = b.t[batch_tensor_of_tile(b, t)];
             const uint64_t lt = t - T.tile0, nsub = ceil_div(T.n, kSubElems), a = lt * 8;
             auto cp8 = [&](int k, const unsigned long long* src) {
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(slot + 8 * k), "l"(src) : "memory");
             };
-            if (LB) {  // no index: nothing to fetch
-            } else if (DERIVE) {  // the chunk entries covering the tile and the next one's first
+            if (DERIVE) {  // the chunk entries covering the tile and the next one's first
                 const uint32_t S = T.idx_subs;
                 const uint64_t nch = ceil_div(nsub, S), c0 = a / S;
 #pragma unroll
@@ -290,12 +261,6 @@ __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(co
             const BatchTensor& T = b.t[batch_tensor_of_tile(b, t)];
             const uint64_t lt = t - T.tile0, nsub = ceil_div(T.n, kSubElems), a = lt * 8;
             unsigned long long e[9];
-            if (LB) {  // the tile's start comes from the look-back, its sub-tile starts from derive()
-                s0 = 0;
-#pragma unroll
-                for (int k = 0; k <= 8; ++k) rel[k] = 0;
-                return;
-            }
             if (DERIVE) {
                 // chunk entries: monotone, within [0, nnz], at most one chunk of
                 // values apart (clamp + latch).  rel[0..4] = the chunk starts
@@ -378,7 +343,7 @@ __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(co
         // chunk ends where the next entry says, and lane k gathers tile k's
         // eight starts
         static_assert(kBatch * 8 == 32, "one lane per sub-tile of a claim");
-        auto derive = [&](uint32_t c, uint32_t j0, uint32_t (&rel)[9], uint32_t& tot) {
+        auto derive = [&](uint32_t c, uint32_t j0, uint32_t (&rel)[9]) {
             const int k = lane >> 3, q = lane & 7;
             const uint64_t tk = tile_of(j0 + k);
             uint32_t p = 0, S = 1;
@@ -386,7 +351,7 @@ __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(co
                 const BatchTensor& T = b.t[batch_tensor_of_tile(b, tk)];
                 const uint64_t lt = tk - T.tile0;
                 const uint32_t count = uint32_t(umin64(kTileElems, T.n - lt * kTileElems));
-                S = LB ? 8u : T.idx_subs;
+                S = T.idx_subs;
                 if (count == kTileElems) {
                     const uint32_t src = bslot0 + ((c % kLook) * kBatch + k) * kBmSlotBytes + 128 * q;
 #pragma unroll
@@ -419,164 +384,33 @@ __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(co
                 if (d < S && pos >= d) x += y;
             }
             const uint32_t r = start + x - p;  // this sub-tile's first value
-            if (!LB && tk < ntiles && pos == S - 1 && start + x != next) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
+            if (tk < ntiles && pos == S - 1 && start + x != next) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
             const int src0 = lane < kBatch ? 8 * lane : 0;
-            {
-                const uint32_t v = __shfl_sync(0xffffffffu, x, src0 + 7);  // the tile's popcount (LB)
-                if (lane < kBatch) tot = v;
-            }
 #pragma unroll
             for (int x2 = 0; x2 < 8; ++x2) {
                 const uint32_t v = __shfl_sync(0xffffffffu, r, src0 + x2);
                 if (lane < kBatch) rel[x2] = v;
             }
         };
-        // LB: publish the claim's tile totals, then give each tile its first value
-        // by a decoupled look-back (state[t] = flag | epoch | value in b.tsub)
-        constexpr unsigned long long kLbV = (1ull << 40) - 1, kLbE = (1ull << 22) - 1;
-        const unsigned long long ep = LB ? (lb_load(&b.hdr->aux[0]) & kLbE) : 0ull;
-        unsigned long long* const state = b.tsub;
-        // LB: a claim is one block of four consecutive tiles.  prep() publishes the
-        // block's total (an inclusive prefix outright when the block holds the
-        // first tile of its last tile's tensor); resolve() finds the prefix at the
-        // block start with one decoupled look-back over blocks (lanes read 160
-        // blocks at a time; the CTA's own previous block is G blocks back), then
-        // gives each tile its first value locally.
-        static_assert(kBatch == 4, "LB: a claim is one block of four tiles");
-        // lanes k < 4: tile tl's tensor start / block-local prefix (first values
-        // relative to the block start, restarting at a tensor's first tile)
-        auto block_local = [&](uint64_t tl, uint32_t tot_l, bool& restart, unsigned long long& loc,
-                               unsigned long long& blk_tot, bool& blk_incl) {
-            const bool valid = lane < kBatch && tl < ntiles;
-            const bool start = valid && tl == b.t[batch_tensor_of_tile(b, tl)].tile0;
-            const uint32_t sm = __ballot_sync(0xffffffffu, start) & 0xFu;
-            const uint32_t x = valid ? tot_l : 0u;
-            unsigned long long acc = 0;
-            loc = 0;
-#pragma unroll
-            for (int q = 0; q < kBatch; ++q) {
-                const uint32_t xq = __shfl_sync(0xffffffffu, x, q);
-                if ((sm >> q) & 1u) acc = 0;  // a tensor's first tile starts at 0
-                if (q == lane) loc = acc;
-                acc += xq;
-            }
-            restart = (sm & ((2u << (lane < kBatch ? lane : kBatch - 1)) - 1u)) != 0;
-            blk_tot = acc;        // from the block start or its last tensor start, through its last tile
-            blk_incl = sm != 0;   // then the block's value is already an inclusive prefix
-        };
-        auto resolve = [&](uint64_t tl, uint32_t tot_l, unsigned long long& tp_l, uint32_t (&rel)[9]) {
-            const uint64_t t0k = __shfl_sync(0xffffffffu, tl, 0);
-            if (t0k >= ntiles) return;
-            const uint64_t blk = t0k / 4;
-            bool restart, blk_incl;
-            unsigned long long loc, blk_tot;
-            block_local(tl, tot_l, restart, loc, blk_tot, blk_incl);
-            // prefix at the block start: 0 when the block begins a tensor, else the look-back
-            const BatchTensor& T0 = b.t[batch_tensor_of_tile(b, t0k)];
-            unsigned long long excl = 0;
-            const int64_t b0 = int64_t(T0.tile0 / 4);  // the block holding the tensor's first tile (an inclusive)
-            if (t0k != T0.tile0) {
-                for (int64_t base = int64_t(blk) - 1; base >= b0;) {
-                    unsigned long long w[5];
-                    uint32_t inc[5], emp[5];
-#pragma unroll
-                    for (int r = 0; r < 5; ++r) {
-                        const int64_t idx = base - lane - 32 * r;
-                        uint32_t f2 = 2;  // below b0: never reached (b0 itself is inclusive)
-                        w[r] = 0;
-                        if (idx >= b0) {
-                            const unsigned long long st = lb_load(&state[idx]);
-                            f2 = ((st >> 40) & kLbE) == ep ? uint32_t(st >> 62) : 0u;
-                            w[r] = st & kLbV;
-                        }
-                        inc[r] = __ballot_sync(0xffffffffu, f2 == 2);
-                        emp[r] = __ballot_sync(0xffffffffu, f2 == 0);
-                    }
-                    int dmin = 160;
-#pragma unroll
-                    for (int r = 4; r >= 0; --r)
-                        if (inc[r]) dmin = 32 * r + __ffs(inc[r]) - 1;
-                    bool empty = false;
-#pragma unroll
-                    for (int r = 0; r < 5; ++r) {
-                        const int lim = dmin - 32 * r;
-                        const uint32_t m = lim >= 32 ? 0xffffffffu : (lim > 0 ? (1u << lim) - 1u : 0u);
-                        empty |= (emp[r] & m) != 0;
-                    }
-                    if (empty) {
-                        __nanosleep(64);
-                        continue;
-                    }
-                    unsigned long long part = 0;
-#pragma unroll
-                    for (int r = 0; r < 5; ++r)
-                        if (lane + 32 * r <= dmin) part += w[r];
-#pragma unroll
-                    for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(0xffffffffu, part, d);
-                    excl += part;
-                    if (dmin < 160) break;
-                    base -= 160;
-                }
-            }
-            if (!blk_incl && lane == 0) lb_store(&state[blk], kLbPrefix | (ep << 40) | ((excl + blk_tot) & kLbV));
-            if (lane < kBatch && tl < ntiles) {
-                const BatchTensor& T = b.t[batch_tensor_of_tile(b, tl)];
-                unsigned long long s = restart ? loc : excl + loc, e = s + tot_l;
-                // popcount == nnz at the tensor's last tile (codec.hpp:158-160); a window past
-                // nnz is clamped (the values TMA never leaves the buffer)
-                const bool last = tl + 1 == T.tile0 + ceil_div(T.n, kTileElems);
-                if ((last && e != T.nnz) || e > T.nnz) {
-                    latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
-                    s = s < T.nnz ? s : T.nnz;
-                    e = e < T.nnz ? e : T.nnz;
-                }
-                tp_l = s;
-                rel[8] = uint32_t(e - s);
-            }
-        };
         uint32_t qj[kLook];  // first j of the claims in flight, oldest first
         int i = 0, ti = 0;
         if (DERIVE && deriver) {
-            // ---- deriver: claims, chunk entries, bitmaps, sub-tile starts -> descriptors.
-            // Claim c is prepared (entries, popcounts, sub-tile starts; LB: the tile
-            // totals published) one claim before it is resolved and posted, so the
-            // totals other CTAs' look-backs wait for appear a claim early.
-            static_assert(kLook == 2, "prepare one claim ahead, refill the slot just consumed");
-            auto prep = [&](uint32_t c, uint32_t j0, uint64_t& tl, unsigned long long& tp_l, uint32_t (&rel_l)[9],
-                            uint32_t& tot_l) {
-                tp_l = 0;
-#pragma unroll
-                for (int k = 0; k < 9; ++k) rel_l[k] = 0;
-                tl = tile_of(j0 + lane);
-                if (lane < kBatch && tl < ntiles) finish(slot0 + ((c % kLook) * kBatch + lane) * kSlotBytes, tl, tp_l, rel_l);
-                tot_l = 0;
-                derive(c, j0, rel_l, tot_l);
-                const uint64_t first = __shfl_sync(0xffffffffu, tl, 0);
-                if (LB && first < ntiles) {  // publish the block's total early
-                    bool restart, blk_incl;
-                    unsigned long long loc, blk_tot;
-                    block_local(tl, tot_l, restart, loc, blk_tot, blk_incl);
-                    if (lane == 0)
-                        lb_store(&state[first / 4], (blk_incl ? kLbPrefix : kLbAgg) | (ep << 40) | (blk_tot & kLbV));
-                }
-            };
+            // ---- deriver: claims, chunk entries, bitmaps, sub-tile starts -> descriptors
 #pragma unroll
             for (int k = 0; k < kLook; ++k) qj[k] = claim_batch(k);
             uint32_t d = 0;
-            uint64_t tl, ntl;
-            unsigned long long tp_l, ntp_l;
-            uint32_t rel_l[9], nrel_l[9], tot_l, ntot_l;
-            asm volatile("cp.async.wait_group %0;" ::"n"(kLook - 1) : "memory");
-            __syncwarp();
-            prep(0, qj[0], tl, tp_l, rel_l, tot_l);
             for (uint32_t c = 0; qj[0] < nj; ++c) {
-                asm volatile("cp.async.wait_group 0;" ::: "memory");  // claim c + 1 has landed
+                asm volatile("cp.async.wait_group %0;" ::"n"(kLook - 1) : "memory");
                 __syncwarp();
-                prep(c + 1, qj[1], ntl, ntp_l, nrel_l, ntot_l);
-                if (LB) resolve(tl, tot_l, tp_l, rel_l);
-                __syncwarp();  // claim c's slots are read before the claim below refills them
-                qj[0] = qj[1];
-                qj[1] = claim_batch(c + kLook);
+                unsigned long long tp_l = 0;
+                uint32_t rel_l[9] = {};
+                const uint64_t tl = tile_of(qj[0] + lane);
+                if (lane < kBatch && tl < ntiles) finish(slot0 + ((c % kLook) * kBatch + lane) * kSlotBytes, tl, tp_l, rel_l);
+                derive(c, qj[0], rel_l);
+                __syncwarp();  // the slots are read before the claim below refills them
+#pragma unroll
+                for (int k = 0; k + 1 < kLook; ++k) qj[k] = qj[k + 1];
+                qj[kLook - 1] = claim_batch(c + kLook);
                 for (uint32_t own = 0; own < uint32_t(kBatch); ++own, ++d) {
                     const uint64_t t = __shfl_sync(0xffffffffu, tl, own);
                     if (t >= ntiles) break;
@@ -593,11 +427,6 @@ __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(co
                     __syncwarp();
                     if (lane == 0) mbar_arrive(dfull0 + 8 * ds);
                 }
-                tl = ntl;
-                tp_l = ntp_l;
-                tot_l = ntot_l;
-#pragma unroll
-                for (int k = 0; k < 9; ++k) rel_l[k] = nrel_l[k];
             }
             asm volatile("cp.async.wait_all;" ::: "memory");
             {  // end of work
@@ -606,16 +435,6 @@ __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(co
                 if (lane == 0) {
                     asm volatile("st.shared.u64 [%0], %1;" ::"r"(da), "l"(~0ull) : "memory");
                     mbar_arrive(dfull0 + 8 * ds);
-                }
-            }
-            if (LB && lane == 0) {
-                // the last deriver out advances the look-back epoch (every deriver read it at
-                // its start; the next launch reads it after griddepcontrol.wait)
-                __threadfence();
-                const unsigned long long n_der = uint64_t(kPipes) * gridDim.x;
-                if (atomicAdd(&b.hdr->done, 1ull) == n_der - 1) {
-                    b.hdr->done = 0;
-                    lb_store(&b.hdr->aux[0], (ep + 1) & kLbE);
                 }
             }
             return;
@@ -912,25 +731,17 @@ cudaError_t launch_expand(const ExpandArgs& a, int mode, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <int MODE, bool DERIVE = false, bool LB = false>
+template <int MODE, bool DERIVE = false>
 static cudaError_t launch_tma_mode(const Batch& b, cudaStream_t s) {
     constexpr uint32_t smem = tma_smem_bytes<mode_in(MODE), DERIVE>();
     constexpr int threads = tma_threads<DERIVE>();
     int blocks_per_sm = 1, sms = 148;
-    cudaError_t e = kernel_slots(reinterpret_cast<const void*>(expand_tma_kernel<MODE, DERIVE, LB>), threads, smem,
+    cudaError_t e = kernel_slots(reinterpret_cast<const void*>(expand_tma_kernel<MODE, DERIVE>), threads, smem,
                                  &blocks_per_sm, &sms);
     if (e != cudaSuccess) return e;
-    // LB: every CTA must be resident (the look-back waits on other CTAs' tiles)
     const uint64_t grid = umin64(b.ntiles, uint64_t(blocks_per_sm) * sms);
     if (grid == 0) return cudaSuccess;
-    return launch_pdl(expand_tma_kernel<MODE, DERIVE, LB>, dim3(unsigned(grid)), dim3(threads), smem, s, b);
-}
-
-// the reference's decompress (no index) in one launch: b.tsub holds the
-// look-back state (one u64 per tile of the batch), b.hdr its epoch
-cudaError_t launch_expand_tma_lookback(const Batch& b, int mode, cudaStream_t s) {
-    if (mode == kModeF16) return launch_tma_mode<kModeF16, true, true>(b, s);
-    return launch_tma_mode<kModeI8, true, true>(b, s);
+    return launch_pdl(expand_tma_kernel<MODE, DERIVE>, dim3(unsigned(grid)), dim3(threads), smem, s, b);
 }
 
 // decompress_chunked with a caller's RankIndex at chunk 2048 / 4096 / 8192

@@ -139,7 +139,6 @@ cudaError_t launch_verify_index(const unsigned long long* idx, uint64_t chunks, 
                                 uint64_t spc, WsHeader* hdr, cudaStream_t s);
 cudaError_t launch_expand_tma(const Batch& b, int mode, cudaStream_t s);  // 1 i8, 2 f16, 3 dequant
 cudaError_t launch_expand_tma_derive(const Batch& b, int mode, cudaStream_t s);  // idx at 2048/4096/8192
-cudaError_t launch_expand_tma_lookback(const Batch& b, int mode, cudaStream_t s);  // no index: one launch
 // fused decompress -> GEMV over a batch (f16, cols % 1024 == 0, part set per tensor),
 // then y[r] = sum of row r's cols/1024 segment partials in a fixed order
 cudaError_t launch_gemv_fused(Batch& b, cudaStream_t s);
