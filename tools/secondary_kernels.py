@@ -6,7 +6,7 @@ extract_rows / extract_cols.  Measurement aid.
 
 C ABI calls straight from ctypes (no host sync inside the timed region), CUDA
 events on the current stream, the 126 MB L2 flushed (512 MiB write) before
-every repetition, median of 7.  Algorithmic bytes per path in the JSON.
+every repetition (write then read back, so the L2 holds clean lines), median of 7.  Algorithmic bytes per path in the JSON.
 
 Usage: python tools/secondary_kernels.py [--out gpurun_out/secondary.json]
 """
@@ -34,6 +34,7 @@ def timed(fn, flush, reps=7):
     ts = []
     for _ in range(reps):
         flush.fill_(1)
+        flush.sum(dtype=torch.int64)  # read back: the timed call does not pay for dirty write-backs
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         fn()
