@@ -27,3 +27,12 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemv
 timeout 300 python tools/fused_bench.py > "$O/fused_bench.log" 2>&1
 timeout 300 python tools/extract_probe.py > "$O/extract.log" 2>&1 && cp gpurun_out/extract_probe.json "$O/extract.json"
 echo done2
+# r02 additions: secondary paths (clean L2 flush), small shards, coarse-index and count timings,
+# and an ncu capture of the coarse-index (chunk 4096) expand
+timeout 300 python tools/secondary_kernels.py --out "$O/secondary.json" > "$O/secondary.log" 2>&1
+timeout 600 python tools/small_shards.py --reps 20 --out "$O/small_shards.json" > "$O/small_shards.log" 2>&1
+timeout 300 python tools/chunked_time.py > "$O/chunked_time.txt" 2>&1
+timeout 300 python tools/count_time.py > "$O/count_time.txt" 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:expand_tma_kernel -s 2 -c 1 \
+    -o "$O/full_expand_chunk4096" -f python tools/chunked_one.py 4096 > "$O/full_expand_chunk4096.log" 2>&1
+echo done3

@@ -86,14 +86,14 @@ def main():
     add("count_kernel alone",
         timed(lambda: ck(L.endor_cuda_decompress_batch_phase(views, outs, 1, 1, ws.data_ptr(), ws.numel(), stream)),
               flush), bm_bytes, 1, "reads the bitmap once")
-    # decompress_chunked at 1024 (one launch) and at the reference default 4096
+    # decompress_chunked at 1024 and at the reference default 4096 (both one launch)
     for cs in (1024, 4096):
         idx = E.build_rank_index(t.bitmap, cs)
         pre = idx.prefix.to(torch.int64).contiguous()
         add(f"decompress_chunked cs={cs}",
             timed(lambda: ck(L.endor_cuda_decompress_chunked(C.byref(v), cs, pre.data_ptr(), pre.numel(),
                                                              out.data_ptr(), ws.data_ptr(), ws.numel(), stream)),
-                  flush), alg_full + pre.numel() * 8, 1 if cs == 1024 else 3)
+                  flush), alg_full + pre.numel() * 8, 1)
     # decompress_chunk_into: the fallback expand_kernel over every 4096-chunk
     # (codec.hpp:191-201: the reference's parallel unit), one call per chunk
     idx = E.build_rank_index(t.bitmap, 1 << 20)
