@@ -384,9 +384,11 @@ def run_ours(args):
     if os.path.exists(mp):
         with open(mp) as f:
             mix_ceiling = json.load(f).get("mix_ceiling_gbs")
-    roofline = {"bound": "hbm", "kernel": "expand_tma_kernel<2>", "achieved": round(achieved, 1),
+    roofline = {"bound": "hbm", "kernel": "expand_tma_kernel<2, 0>", "achieved": round(achieved, 1),
                 "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
+                "traffic_source": "recorded ncu --set full capture of this kernel on this build "
+                                  "(profiles/bench_expand_traffic.json), not measured in this run",
                 "alg_bytes_per_launch": expand_alg,
                 "avg_launch_us": round(expand_ms * 1e3, 2),
                 "count_kernel_avg_us_no_index_path": round(count_ms * 1e3, 2),
