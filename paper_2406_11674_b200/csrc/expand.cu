@@ -54,7 +54,7 @@ namespace endor_b200 {
 #define ENDOR_TMA_STAGES 5  // per pipe: 5 x 17.6 KB (f16); 4 / 5 / 6 / 7 measured 3590 / 3950 / 3904 / 3115 dense-GB/s in r1
 #endif
 #ifndef ENDOR_TMA_BATCH
-#define ENDOR_TMA_BATCH 4  // tiles per claim (the two pipes end within about one claim of each other)
+#define ENDOR_TMA_BATCH 6  // tiles per claim: 2 / 4 / 5 / 6 / 7 / 8 / 10 / 12 measured, 6 best (profiles/r02/claim_size_sweep.txt)
 #endif
 #ifndef ENDOR_TMA_LOOKAHEAD
 #define ENDOR_TMA_LOOKAHEAD 2  // claims in flight per producer: their index loads land meanwhile
@@ -342,54 +342,58 @@ __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(co
         // start into the sub-tile start, the chunk's last lane checks that the
         // chunk ends where the next entry says, and lane k gathers tile k's
         // eight starts
-        static_assert(kBatch * 8 == 32, "one lane per sub-tile of a claim");
+        static_assert(kBatch <= 32, "lane k holds claim tile k");
         auto derive = [&](uint32_t c, uint32_t j0, uint32_t (&rel)[9]) {
-            const int k = lane >> 3, q = lane & 7;
-            const uint64_t tk = tile_of(j0 + k);
-            uint32_t p = 0, S = 1;
-            if (tk < ntiles) {
-                const BatchTensor& T = b.t[batch_tensor_of_tile(b, tk)];
-                const uint64_t lt = tk - T.tile0;
-                const uint32_t count = uint32_t(umin64(kTileElems, T.n - lt * kTileElems));
-                S = T.idx_subs;
-                if (count == kTileElems) {
-                    const uint32_t src = bslot0 + ((c % kLook) * kBatch + k) * kBmSlotBytes + 128 * q;
 #pragma unroll
-                    for (int v = 0; v < 8; ++v) {
-                        uint32_t x0, x1, x2, x3;
-                        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                                     : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3) : "r"(src + 16 * v));
-                        p += __popc(x0) + __popc(x1) + __popc(x2) + __popc(x3);
-                    }
-                } else {  // a partial tile (not prefetched): words from global memory, bits past the end masked
-                    const uint64_t nbytes = (T.n + 7) / 8, wb = lt * (kTileElems / 32) + 32 * q;
-                    for (uint32_t x = 0; x < 32; ++x) {
-                        const int32_t keep = int32_t(count) - int32_t(1024 * q + 32 * x);
-                        if (keep <= 0) break;
-                        const uint32_t v = load_word32(T.bitmap, wb + x, nbytes);
-                        p += __popc(keep >= 32 ? v : v & ((1u << keep) - 1u));
+            for (int g0 = 0; g0 < kBatch; g0 += 4) {  // four tiles (32 sub-tiles) per pass
+                const int k = g0 + (lane >> 3), q = lane & 7;
+                const uint64_t tk = k < kBatch ? tile_of(j0 + k) : ntiles;
+                uint32_t p = 0, S = 1;
+                if (tk < ntiles) {
+                    const BatchTensor& T = b.t[batch_tensor_of_tile(b, tk)];
+                    const uint64_t lt = tk - T.tile0;
+                    const uint32_t count = uint32_t(umin64(kTileElems, T.n - lt * kTileElems));
+                    S = T.idx_subs;
+                    if (count == kTileElems) {
+                        const uint32_t src = bslot0 + ((c % kLook) * kBatch + k) * kBmSlotBytes + 128 * q;
+#pragma unroll
+                        for (int v = 0; v < 8; ++v) {
+                            uint32_t x0, x1, x2, x3;
+                            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                         : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3) : "r"(src + 16 * v));
+                            p += __popc(x0) + __popc(x1) + __popc(x2) + __popc(x3);
+                        }
+                    } else {  // a partial tile (not prefetched): words from global memory, bits past the end masked
+                        const uint64_t nbytes = (T.n + 7) / 8, wb = lt * (kTileElems / 32) + 32 * q;
+                        for (uint32_t x = 0; x < 32; ++x) {
+                            const int32_t keep = int32_t(count) - int32_t(1024 * q + 32 * x);
+                            if (keep <= 0) break;
+                            const uint32_t v = load_word32(T.bitmap, wb + x, nbytes);
+                            p += __popc(keep >= 32 ? v : v & ((1u << keep) - 1u));
+                        }
                     }
                 }
-            }
-            uint32_t st[5];  // tile k's chunk starts, then the window end
+                uint32_t st[5];  // tile k's chunk starts, then the window end
 #pragma unroll
-            for (int x = 0; x < 5; ++x) st[x] = __shfl_sync(0xffffffffu, rel[x], k);
-            const uint32_t cq = uint32_t(q) >> (__ffs(S) - 1), pos = uint32_t(q) & (S - 1);
-            const uint32_t start = cq == 0 ? st[0] : cq == 1 ? st[1] : cq == 2 ? st[2] : st[3];
-            const uint32_t next = cq == 0 ? st[1] : cq == 1 ? st[2] : cq == 2 ? st[3] : st[4];
-            uint32_t x = p;
+                for (int x = 0; x < 5; ++x) st[x] = __shfl_sync(0xffffffffu, rel[x], k < kBatch ? k : 0);
+                const uint32_t cq = uint32_t(q) >> (__ffs(S) - 1), pos = uint32_t(q) & (S - 1);
+                const uint32_t start = cq == 0 ? st[0] : cq == 1 ? st[1] : cq == 2 ? st[2] : st[3];
+                const uint32_t next = cq == 0 ? st[1] : cq == 1 ? st[2] : cq == 2 ? st[3] : st[4];
+                uint32_t x = p;
 #pragma unroll
-            for (uint32_t d = 1; d < 8; d <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
-                if (d < S && pos >= d) x += y;
-            }
-            const uint32_t r = start + x - p;  // this sub-tile's first value
-            if (tk < ntiles && pos == S - 1 && start + x != next) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
-            const int src0 = lane < kBatch ? 8 * lane : 0;
+                for (uint32_t d = 1; d < 8; d <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+                    if (d < S && pos >= d) x += y;
+                }
+                const uint32_t r = start + x - p;  // this sub-tile's first value
+                if (tk < ntiles && pos == S - 1 && start + x != next) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
+                const bool mine = lane >= g0 && lane < g0 + 4 && lane < kBatch;  // lane k gathers tile k's starts
+                const int src0 = mine ? 8 * (lane - g0) : 0;
 #pragma unroll
-            for (int x2 = 0; x2 < 8; ++x2) {
-                const uint32_t v = __shfl_sync(0xffffffffu, r, src0 + x2);
-                if (lane < kBatch) rel[x2] = v;
+                for (int x2 = 0; x2 < 8; ++x2) {
+                    const uint32_t v = __shfl_sync(0xffffffffu, r, src0 + x2);
+                    if (mine) rel[x2] = v;
+                }
             }
         };
         uint32_t qj[kLook];  // first j of the claims in flight, oldest first
