@@ -646,7 +646,16 @@ static int extract_common(const endor_tensor_view* t, const uint64_t* sel, uint6
     rt.ncta = b.t[0].ncta;
     rt.nsub = ceil_div(n, kSubElems);
     const auto* vals = static_cast<const uint8_t*>(t->values);
-    if (rows)
+    if (rows && t->cols % kSubElems == 0 && aligned(out, 16)) {
+        // rows start on sub-tile boundaries: the persistent TMA expand, tile t =
+        // piece t % tpr of row sel[t / tpr], written to output row t / tpr
+        b.t[0].dst = static_cast<uint8_t*>(out);
+        b.sel = idx;
+        b.rcols = t->cols;
+        b.tpr = uint32_t(ceil_div(t->cols, kTileElems));
+        b.ntiles = nsel * b.tpr;
+        CK(launch_expand_tma_rows(b, eb, S(stream)));
+    } else if (rows)
         CK(launch_extract_rows(rt, vals, t->nnz, t->cols, eb, idx, nsel, static_cast<uint8_t*>(out), L.hdr,
                                S(stream)));
     else

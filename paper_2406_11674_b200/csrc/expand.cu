@@ -81,7 +81,7 @@ struct Stage {
 // entries either (codec.hpp:170-184) -- never an out-of-bounds access.
 // header: [0, 256) mbarriers + claim counter; then per pipe kLook claims x
 // kBatch tile slots of 12 u64 (a claimed tile's index entries, via cp.async)
-constexpr uint32_t kSlotBytes = 12 * 8;
+constexpr uint32_t kSlotBytes = 16 * 8;  // 12 u64 of index entries / bases; ROWS: + the tile's sub-tile span
 constexpr uint32_t kTmaHeader = 256 + ((kPipes * kLook * kBatch * kSlotBytes + 127) & ~127u);
 // Coarse-index (DERIVE) kernels add, per pipe, after every pipe's stages: a
 // ring of kDesc tile descriptors {tile, window start, 9 sub-tile starts}
@@ -119,8 +119,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // multi-launch path does), and posts one descriptor per tile to a ring; the
 // pipe's TMA warp only turns descriptors into bulk copies, so a stage never
 // waits behind that work, and the consumers run unchanged.
-template <int MODE, bool DERIVE = false>
+//
+// ROWS: extract_rows (codec.hpp:239-266) through the same pipeline: tile t is
+// 8192-element piece t % tpr of selected row sel[t / tpr] (rows start on
+// 1024-element sub-tile boundaries: cols % 1024 == 0), its starts come from
+// the count tables, and it lands in output row t / tpr.
+template <int MODE, bool DERIVE = false, bool ROWS = false>
 __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(const __grid_constant__ Batch b) {
+    static_assert(!(DERIVE && ROWS), "row extraction reads the count tables");
 #ifdef ENDOR_CTA_TIMING
     if (threadIdx.x == 0) {
         unsigned smid;
@@ -237,7 +243,21 @@ __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(co
             auto cp8 = [&](int k, const unsigned long long* src) {
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(slot + 8 * k), "l"(src) : "memory");
             };
-            if (DERIVE) {  // the chunk entries covering the tile and the next one's first
+            if (ROWS) {  // the selected row's piece: sub-tiles [a, a + m) of tensor 0
+                const uint64_t row = b.sel[t / b.tpr], j = t % b.tpr;
+                const uint64_t a2 = (row * b.rcols + j * kTileElems) / kSubElems;
+                const uint32_t m = uint32_t(umin64(kTileElems, b.rcols - j * kTileElems) / kSubElems);
+                const uint64_t spc = uint64_t(kSubsPerBlk) * T.cbpc;  // one count CTA's range
+#pragma unroll
+                for (int k = 0; k <= 8; ++k)
+                    if (uint32_t(k) <= m && a2 + k < nsub) cp8(k, b.tsub + T.sub0 + a2 + k);
+                // range bases of entry 0 and of the piece's last sub-tile (a piece spans at most
+                // two count ranges), then the base of entry m -- or the total at the tensor's end
+                cp8(9, b.blk + T.blk0 + a2 / spc);
+                cp8(10, b.blk + T.blk0 + (a2 + m - 1) / spc);
+                cp8(11, b.blk + T.blk0 + (a2 + m < nsub ? (a2 + m) / spc : uint64_t(T.ncta)));
+                asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(slot + 96), "l"(a2), "l"(uint64_t(m)) : "memory");
+            } else if (DERIVE) {  // the chunk entries covering the tile and the next one's first
                 const uint32_t S = T.idx_subs;
                 const uint64_t nch = ceil_div(nsub, S), c0 = a / S;
 #pragma unroll
@@ -257,10 +277,28 @@ __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(co
                 cp8(11, b.blk + T.blk0 + T.ncta);                           // total
             }
         };
+        uint64_t src_lane = 0;  // ROWS: finish() leaves the piece's first element (of tensor 0) here
         auto finish = [&](uint32_t slot, uint64_t t, unsigned long long& s0, uint32_t* rel) {  // one lane per tile
             const BatchTensor& T = b.t[batch_tensor_of_tile(b, t)];
             const uint64_t lt = t - T.tile0, nsub = ceil_div(T.n, kSubElems), a = lt * 8;
             unsigned long long e[9];
+            if (ROWS) {  // at most two count ranges per piece (8 sub-tiles < one range)
+                const uint64_t a2 = lds64(slot + 96), m = lds64(slot + 104);
+                src_lane = a2 * kSubElems;
+                const uint64_t spc = uint64_t(kSubsPerBlk) * T.cbpc;
+                const unsigned long long b0 = lds64(slot + 72), b1 = lds64(slot + 80), bm = lds64(slot + 88);
+                e[0] = b0 + lds64(slot);
+#pragma unroll
+                for (int k = 1; k <= 8; ++k) {
+                    if (uint64_t(k) < m) e[k] = ((a2 + k) / spc == a2 / spc ? b0 : b1) + lds64(slot + 8 * k);
+                    else if (uint64_t(k) == m) e[k] = a2 + m < nsub ? bm + lds64(slot + 8 * k) : bm;
+                    else e[k] = e[k - 1];  // past the piece: the window end
+                }
+                s0 = e[0];
+#pragma unroll
+                for (int k = 0; k <= 8; ++k) rel[k] = uint32_t(e[k] - e[0]);
+                return;
+            }
             if (DERIVE) {
                 // chunk entries: monotone, within [0, nnz], at most one chunk of
                 // values apart (clamp + latch).  rel[0..4] = the chunk starts
@@ -536,9 +574,11 @@ __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(co
                 const uintptr_t vlo = reinterpret_cast<uintptr_t>(T.values);
                 const uintptr_t vhi = vlo + T.nnz * EB;
                 const uintptr_t vlo16 = (vlo + 15) & ~uintptr_t(15), vhi16 = vhi & ~uintptr_t(15);
+                const uint64_t src_t = ROWS ? __shfl_sync(0xffffffffu, src_lane, own) : 0ull;
                 if (i >= kStages) mbar_wait(empty0 + 8 * s, ((i / kStages) - 1) & 1);
-                const uint64_t t0 = lt * kTileElems;
-                const uint32_t count = uint32_t(umin64(kTileElems, T.n - t0));
+                const uint64_t t0 = ROWS ? src_t : lt * kTileElems;  // the tile's first element in T
+                const uint32_t count = uint32_t(ROWS ? umin64(kTileElems, b.rcols - (t % b.tpr) * kTileElems)
+                                                     : umin64(kTileElems, T.n - t0));
                 const uint32_t bm_bytes = (count + 7) / 8;
                 const uint32_t bm_bulk = count == kTileElems ? 1024u : (bm_bytes & ~15u);
                 const uintptr_t ws = vlo + tp * EB, we = vlo + te * EB;
@@ -602,8 +642,10 @@ __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(co
             if (t >= ntiles) break;  // the producer's end-of-work sentinel
             while (ti + 1 < b.count && t >= b.t[ti + 1].tile0) ++ti;  // a pipe's tiles only move forward
             const BatchTensor& T = b.t[ti];
-            const uint64_t t0 = (t - T.tile0) * kTileElems;
-            const int32_t count = int32_t(umin64(kTileElems, T.n - t0));
+            // the tile's first element in the output: tensor T's own, or (ROWS) output row t / tpr
+            const uint64_t t0 = ROWS ? (t / b.tpr) * b.rcols + (t % b.tpr) * kTileElems : (t - T.tile0) * kTileElems;
+            const int32_t count = int32_t(ROWS ? umin64(kTileElems, b.rcols - (t % b.tpr) * kTileElems)
+                                               : umin64(kTileElems, T.n - t0));
             const int32_t wfirst = cw * kWarpElems;
             if (wfirst < count) {
                 const int32_t valid = min(count - wfirst, kWarpElems);
@@ -735,17 +777,25 @@ cudaError_t launch_expand(const ExpandArgs& a, int mode, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <int MODE, bool DERIVE = false>
+template <int MODE, bool DERIVE = false, bool ROWS = false>
 static cudaError_t launch_tma_mode(const Batch& b, cudaStream_t s) {
     constexpr uint32_t smem = tma_smem_bytes<mode_in(MODE), DERIVE>();
     constexpr int threads = tma_threads<DERIVE>();
     int blocks_per_sm = 1, sms = 148;
-    cudaError_t e = kernel_slots(reinterpret_cast<const void*>(expand_tma_kernel<MODE, DERIVE>), threads, smem,
-                                 &blocks_per_sm, &sms);
+    cudaError_t e = kernel_slots(reinterpret_cast<const void*>(expand_tma_kernel<MODE, DERIVE, ROWS>), threads,
+                                 smem, &blocks_per_sm, &sms);
     if (e != cudaSuccess) return e;
     const uint64_t grid = umin64(b.ntiles, uint64_t(blocks_per_sm) * sms);
     if (grid == 0) return cudaSuccess;
-    return launch_pdl(expand_tma_kernel<MODE, DERIVE>, dim3(unsigned(grid)), dim3(threads), smem, s, b);
+    return launch_pdl(expand_tma_kernel<MODE, DERIVE, ROWS>, dim3(unsigned(grid)), dim3(threads), smem, s, b);
+}
+
+// extract_rows (codec.hpp:239-266) through the TMA pipeline: count tables of
+// tensor 0 in b.tsub / b.blk, b.sel / b.rcols / b.tpr / b.ntiles set, the
+// output rows at b.t[0].dst (16-byte aligned rows: cols % 1024 == 0)
+cudaError_t launch_expand_tma_rows(const Batch& b, int mode, cudaStream_t s) {
+    if (mode == kModeF16) return launch_tma_mode<kModeF16, false, true>(b, s);
+    return launch_tma_mode<kModeI8, false, true>(b, s);
 }
 
 // decompress_chunked with a caller's RankIndex at chunk 2048 / 4096 / 8192

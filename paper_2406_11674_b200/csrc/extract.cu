@@ -9,10 +9,13 @@
 //                 invalid_argument; the first failing position wins)
 //
 // Both read ranks from count_kernel's two-level table (the GPU RankIndex at
-// 1024-element granularity) plus a popcount of at most 1023 bits.  Rows stage
-// each 8192-element tile's packed values in shared memory and place them with
-// the expand gather; columns rank 4 rows' bits per CTA in shared memory and
-// look the selected values up directly (8 in flight per thread).
+// 1024-element granularity) plus a popcount of at most 1023 bits.  Rows whose
+// starts fall on 1024-element sub-tiles (cols % 1024 == 0, every catalog
+// shape) run through the persistent TMA expand (expand.cu, ROWS: tile t =
+// piece t % tpr of row sel[t / tpr]); other rows here stage each 8192-element
+// tile's packed values in shared memory and place them with the expand
+// gather.  Columns rank 4 rows' bits per CTA in shared memory and look the
+// selected values up directly (8 in flight per thread).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>

@@ -115,6 +115,11 @@ struct Batch {
     unsigned long long* tsub;  // CTA-local exclusive offset per 1024-element sub-tile
     unsigned long long* blk;   // per-count-CTA aggregates -> exclusive bases; total at [nblk]
     WsHeader* hdr;
+    // extract_rows through the TMA expand (launch_expand_tma_rows): tensor 0's
+    // rows sel[0..nsel) -> output rows 0..nsel; tile t = (t / tpr, t % tpr)
+    const unsigned long long* sel;
+    uint64_t rcols;
+    uint32_t tpr;
 };
 __host__ __device__ inline int batch_tensor_of_tile(const Batch& b, uint64_t tile) {
     int i = b.count - 1;
@@ -139,6 +144,7 @@ cudaError_t launch_verify_index(const unsigned long long* idx, uint64_t chunks, 
                                 uint64_t spc, WsHeader* hdr, cudaStream_t s);
 cudaError_t launch_expand_tma(const Batch& b, int mode, cudaStream_t s);  // 1 i8, 2 f16, 3 dequant
 cudaError_t launch_expand_tma_derive(const Batch& b, int mode, cudaStream_t s);  // idx at 2048/4096/8192
+cudaError_t launch_expand_tma_rows(const Batch& b, int mode, cudaStream_t s);  // extract_rows (count tables)
 // fused decompress -> GEMV over a batch (f16, cols % 1024 == 0, part set per tensor),
 // then y[r] = sum of row r's cols/1024 segment partials in a fixed order
 cudaError_t launch_gemv_fused(Batch& b, cudaStream_t s);
