@@ -173,8 +173,12 @@ int endor_cuda_popcount(const void* bitmap, uint64_t n, uint64_t* total_out, voi
  * chunk_count must equal ceil(n/cs) (else CORRUPTION, codec.hpp:174-176).
  * Any nonzero chunk size is accepted, as by the reference's RankIndex
  * constructor (bitmap.hpp:104).  cs == 1024: single-launch fast path,
- * check_index semantics (see endor_cuda_decompress_chunked_batch).  Other
- * sizes: every prefix entry is verified on device (a superset of check_index). */
+ * check_index semantics (see endor_cuda_decompress_chunked_batch).
+ * cs == 2048 / 4096 / 8192 (4096 is the reference's kDefaultChunkSize,
+ * codec.hpp:19): also one launch (16-byte aligned bitmap and prefix), the
+ * sub-tile starts derived from the bitmap on chip and EVERY entry verified.
+ * Other sizes: a counting pass, then every prefix entry is verified on device
+ * (a superset of check_index), then the expand. */
 int endor_cuda_decompress_chunked(const endor_tensor_view* t, uint64_t chunk_size,
                                   const uint64_t* prefix, uint64_t chunk_count, void* dense_out,
                                   void* ws, size_t ws_bytes, void* stream);
@@ -185,8 +189,10 @@ int endor_cuda_decompress_chunked(const endor_tensor_view* t, uint64_t chunk_siz
  * the whole batch is ONE expand launch with no counting pass; like the
  * reference's check_index (codec.hpp:170-184) only the last entry is
  * verified (prefix[last] + tail popcount == nnz), and an inconsistent middle
- * entry produces unspecified output (never an out-of-bounds access).  Other
- * chunk sizes fall back to endor_cuda_decompress_chunked per tensor.
+ * entry produces unspecified output (never an out-of-bounds access).  Chunk
+ * sizes 2048 / 4096 / 8192 are one launch for the batch too (every entry
+ * verified, see endor_cuda_decompress_chunked); other chunk sizes fall back
+ * to endor_cuda_decompress_chunked per tensor.
  * prefixes[i] must hold ceil(n_i / chunk_size) entries. */
 int endor_cuda_decompress_chunked_batch(const endor_tensor_view* views, const uint64_t* const* prefixes,
                                         uint64_t chunk_size, void* const* dense_outs, int count, void* ws,
