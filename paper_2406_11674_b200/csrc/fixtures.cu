@@ -263,6 +263,132 @@ __global__ void __launch_bounds__(256) compact_kernel(const uint8_t* dense, uint
     }
 }
 
+// ---- compress, vectorised (16-byte aligned dense input) -----------------------
+// The same predicate as bitmap_kernel / compact_kernel (f16 zero iff
+// (h & 0x7FFF) == 0, float16.hpp:75; i8 zero iff 0), but coalesced: a thread
+// owns 16-byte chunks (8 f16 / 16 i8 elements).  bitmap: one mask byte (or
+// two) per chunk.  compact: CTA per 8192-element tile, the chunk masks are
+// recomputed from the data, one block scan places every chunk's values, the
+// tile's packed values are staged in shared memory at the destination's
+// 16-byte phase and leave with 16-byte stores.
+template <int EB>
+__device__ __forceinline__ uint32_t chunk_mask(const uint4 v, bool& negzero) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t m = 0;
+    if constexpr (EB == 2) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t h = (w[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
+            m |= uint32_t((h & 0x7FFFu) != 0) << k;
+            negzero |= h == 0x8000u;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) m |= uint32_t(((w[k >> 2] >> (8 * (k & 3))) & 0xFFu) != 0) << k;
+    }
+    return m;
+}
+
+template <int EB>
+__global__ void __launch_bounds__(256) bitmap_vec_kernel(const uint4* __restrict__ dense, uint64_t n,
+                                                         uint8_t* __restrict__ bitmap, WsHeader* hdr) {
+    constexpr int EPC = 16 / EB;
+    const uint64_t nfull = n / EPC, nbytes = (n + 7) / 8;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    bool negzero = false;
+    for (uint64_t c = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < nfull; c += stride) {
+        const uint32_t m = chunk_mask<EB>(__ldcs(dense + c), negzero);
+        if constexpr (EB == 2) bitmap[c] = uint8_t(m);
+        else reinterpret_cast<uint16_t*>(bitmap)[c] = uint16_t(m);  // bitmap is 4-byte aligned
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && nfull * EPC < n) {  // the ragged last chunk, elementwise
+        const uint8_t* d = reinterpret_cast<const uint8_t*>(dense);
+        uint32_t m = 0;
+        for (uint64_t i = nfull * EPC; i < n; ++i) {
+            bool nz;
+            if constexpr (EB == 2) {
+                const uint16_t h = reinterpret_cast<const uint16_t*>(d)[i];
+                nz = (h & 0x7FFFu) != 0;
+                negzero |= h == 0x8000u;
+            } else {
+                nz = d[i] != 0;
+            }
+            m |= uint32_t(nz) << (i - nfull * EPC);
+        }
+        for (uint64_t b = nfull * EPC / 8; b < nbytes; ++b) bitmap[b] = uint8_t(m >> (8 * (b - nfull * EPC / 8)));
+    }
+    if (negzero) hdr->aux[2] = 1;
+}
+
+template <int EB>
+__global__ void __launch_bounds__(256) compact_vec_kernel(const uint4* __restrict__ dense, uint64_t n,
+                                                          const unsigned long long* __restrict__ tprefix,
+                                                          uint8_t* __restrict__ values) {
+    constexpr int EPC = 16 / EB, CPT = kTileElems / EPC / 256;  // chunks per thread (consecutive)
+    __shared__ __align__(16) uint8_t s_out[kTileElems * EB + 16];
+    __shared__ uint32_t s_warp[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t c0 = uint64_t(blockIdx.x) * (kTileElems / EPC) + uint64_t(tid) * CPT;  // first chunk
+    uint4 v[CPT];
+    uint32_t m[CPT], cnt = 0;
+    bool nz0 = false;
+#pragma unroll
+    for (int r = 0; r < CPT; ++r) {
+        const uint64_t e0 = (c0 + r) * EPC;
+        v[r] = make_uint4(0, 0, 0, 0);
+        if (e0 + EPC <= n) {
+            v[r] = __ldcs(dense + c0 + r);
+        } else if (e0 < n) {  // the ragged last chunk: only the elements inside the matrix
+            uint32_t w[4] = {0, 0, 0, 0};
+            const uint8_t* d = reinterpret_cast<const uint8_t*>(dense);
+            for (uint64_t i = e0; i < n; ++i) w[((i - e0) * EB) >> 2] |= uint32_t(d[i * EB]) << (8 * (((i - e0) * EB) & 3)) |
+                                                                   (EB == 2 ? uint32_t(d[i * EB + 1]) << (8 * (((i - e0) * EB + 1) & 3)) : 0u);
+            v[r] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        m[r] = chunk_mask<EB>(v[r], nz0);
+        cnt += __popc(m[r]);
+    }
+    const uint32_t incl = warp_incl_scan(cnt, lane);
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    uint32_t base = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        base += w < warp ? s_warp[w] : 0u;
+        total += s_warp[w];
+    }
+    uint8_t* dst = values + tprefix[blockIdx.x] * EB;
+    const uint32_t ph = uint32_t(reinterpret_cast<uintptr_t>(dst) & 15);  // stage at the destination's phase
+    uint32_t pos = base + incl - cnt;
+#pragma unroll
+    for (int r = 0; r < CPT; ++r) {
+        const uint32_t w[4] = {v[r].x, v[r].y, v[r].z, v[r].w};
+#pragma unroll
+        for (int k = 0; k < EPC; ++k) {
+            if ((m[r] >> k) & 1u) {
+                if constexpr (EB == 2) {
+                    *reinterpret_cast<uint16_t*>(s_out + ph + 2 * pos) = uint16_t(w[k >> 1] >> (16 * (k & 1)));
+                } else {
+                    s_out[ph + pos] = uint8_t(w[k >> 2] >> (8 * (k & 3)));
+                }
+                ++pos;
+            }
+        }
+    }
+    __syncthreads();
+    const uint32_t bytes = total * EB, head = (16 - ph) & 15;
+    if (bytes <= head) {
+        for (uint32_t b = tid; b < bytes; b += 256) dst[b] = s_out[ph + b];
+        return;
+    }
+    for (uint32_t b = tid; b < head; b += 256) dst[b] = s_out[ph + b];
+    const uint32_t nvec = (bytes - head) / 16;
+    const uint4* src4 = reinterpret_cast<const uint4*>(s_out + ph + head);
+    uint4* dst4 = reinterpret_cast<uint4*>(dst + head);
+    for (uint32_t q = tid; q < nvec; q += 256) dst4[q] = src4[q];
+    for (uint32_t b = head + nvec * 16 + tid; b < bytes; b += 256) dst[b] = s_out[ph + b];
+}
+
 // ---- quantize_values (codec.hpp:306-331) ---------------------------------------
 // absmax over |f16_to_f32(v)| (NaNs never win, like std::max(absmax, x)),
 // then q = clamp(lround(v / scale), -127, 127) with IEEE float division.
@@ -373,6 +499,12 @@ cudaError_t launch_prune(uint8_t* w, uint64_t n, int eb, uint64_t target, const 
 
 cudaError_t launch_bitmap(const void* dense, uint64_t n, int eb, void* bitmap, const WsLayout& L,
                           cudaStream_t s) {
+    if ((reinterpret_cast<uintptr_t>(dense) & 15) == 0) {  // coalesced 16-byte chunks
+        const unsigned g = grid_for(ceil_div(n, 16 / eb), 256);
+        if (eb == 2) bitmap_vec_kernel<2><<<g, 256, 0, s>>>(static_cast<const uint4*>(dense), n, static_cast<uint8_t*>(bitmap), L.hdr);
+        else bitmap_vec_kernel<1><<<g, 256, 0, s>>>(static_cast<const uint4*>(dense), n, static_cast<uint8_t*>(bitmap), L.hdr);
+        return cudaGetLastError();
+    }
     const unsigned g = grid_for(ceil_div(n, 32), 256);
     if (eb == 2) bitmap_kernel<2><<<g, 256, 0, s>>>(static_cast<const uint8_t*>(dense), n, static_cast<uint8_t*>(bitmap), L.hdr);
     else bitmap_kernel<1><<<g, 256, 0, s>>>(static_cast<const uint8_t*>(dense), n, static_cast<uint8_t*>(bitmap), L.hdr);
@@ -383,6 +515,11 @@ cudaError_t launch_compact(const void* dense, uint64_t n, int eb, const void* bi
                            const WsLayout& L, void* values, cudaStream_t s) {
     const unsigned nt = unsigned(ceil_div(n, kTileElems));
     if (nt == 0) return cudaSuccess;
+    if ((reinterpret_cast<uintptr_t>(dense) & 15) == 0) {  // coalesced 16-byte chunks, staged 16-byte stores
+        if (eb == 2) compact_vec_kernel<2><<<nt, 256, 0, s>>>(static_cast<const uint4*>(dense), n, L.tprefix, static_cast<uint8_t*>(values));
+        else compact_vec_kernel<1><<<nt, 256, 0, s>>>(static_cast<const uint4*>(dense), n, L.tprefix, static_cast<uint8_t*>(values));
+        return cudaGetLastError();
+    }
     const uint64_t nbytes = (n + 7) / 8;
     if (eb == 2)
         compact_kernel<2><<<nt, 256, 0, s>>>(static_cast<const uint8_t*>(dense), n, static_cast<const uint8_t*>(bitmap), nbytes, L.tprefix, static_cast<uint8_t*>(values));
