@@ -384,7 +384,7 @@ def run_ours(args):
     if os.path.exists(mp):
         with open(mp) as f:
             mix_ceiling = json.load(f).get("mix_ceiling_gbs")
-    roofline = {"bound": "hbm", "kernel": "expand_tma_kernel<2, 0>", "achieved": round(achieved, 1),
+    roofline = {"bound": "hbm", "kernel": "expand_tma_kernel<2, 0, 0, 1>", "achieved": round(achieved, 1),
                 "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "traffic_source": "recorded ncu --set full capture of this kernel on this build "

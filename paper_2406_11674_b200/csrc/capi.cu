@@ -238,6 +238,9 @@ int endor_cuda_sync_status(void* ws, void* stream) {
     CK(cudaMemcpy(&st, &hdr->status, sizeof(st), cudaMemcpyDeviceToHost));
     if (st) {
         CK(cudaMemset(&hdr->status, 0, sizeof(uint32_t)));
+        // CTAs that saw the latched status skipped the self-resetting tile
+        // pool protocol (expand.cu): start the next launch from zero
+        CK(cudaMemset(&hdr->tile_claim, 0, 2 * sizeof(unsigned long long)));
         return fail(int(st), st == ENDOR_ERR_CORRUPTION
                                  ? "device check failed: bitmap popcount / rank index / padding bits "
                                    "disagree with the tensor (codec.hpp:158-160,170-184, bitmap.hpp:78-84)"

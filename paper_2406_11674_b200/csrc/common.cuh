@@ -49,6 +49,8 @@ struct WsHeader {
     unsigned long long done;    // scan CTA completion counter (self-resetting)
     unsigned long long total;   // last scan total (p0 + popcount of range)
     unsigned long long aux[4];
+    unsigned long long tile_claim;  // expand_tma_kernel's global tile-claim counter (self-resetting)
+    unsigned long long tile_done;   // ... and its count of claimers done (self-resetting)
 };
 static_assert(sizeof(WsHeader) <= 256, "the workspace header occupies the first 256 bytes");
 

@@ -59,6 +59,24 @@ namespace endor_b200 {
 #ifndef ENDOR_TMA_LOOKAHEAD
 #define ENDOR_TMA_LOOKAHEAD 2  // claims in flight per producer: their index loads land meanwhile
 #endif
+// Tile claims: each SM first works through its own static sequence
+// (blockIdx.x + j * grid, claimed from a shared-memory counter: no global
+// round trip at the start), then -- for the last ~15 % of the tiles --
+// both pipes claim runs of consecutive tiles from one global pool counter.
+// With a fixed 1/148 of the tiles per SM the SMs' finish times spread by ~5 %
+// of a layer (tools/cta_timing.py) and the kernel ends with the slowest; an
+// all-global counter balances the end but puts a round trip in front of
+// every claim, which costs small tensors (profiles/r02/claim_size_sweep.txt).
+// 0 = static only, for comparison.
+#ifndef ENDOR_TMA_GLOBAL_CLAIMS
+#define ENDOR_TMA_GLOBAL_CLAIMS 1
+#endif
+#ifndef ENDOR_TMA_POOL_MIN
+#define ENDOR_TMA_POOL_MIN 512
+#endif
+#ifndef ENDOR_TMA_POOL_PCT
+#define ENDOR_TMA_POOL_PCT 15
+#endif
 constexpr int kPipes = ENDOR_TMA_PIPES;
 constexpr int kStages = ENDOR_TMA_STAGES;
 constexpr int kLook = ENDOR_TMA_LOOKAHEAD;
@@ -124,7 +142,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // 8192-element piece t % tpr of selected row sel[t / tpr] (rows start on
 // 1024-element sub-tile boundaries: cols % 1024 == 0), its starts come from
 // the count tables, and it lands in output row t / tpr.
-template <int MODE, bool DERIVE = false, bool ROWS = false>
+template <int MODE, bool DERIVE = false, bool ROWS = false, bool POOL = false>
 __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(const __grid_constant__ Batch b) {
     static_assert(!(DERIVE && ROWS), "row extraction reads the count tables");
 #ifdef ENDOR_CTA_TIMING
@@ -153,7 +171,17 @@ __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(co
     const uint32_t bslot0 = desc0 + kDesc * kDescBytes;
     const uint64_t ntiles = b.ntiles;
     // this CTA's tiles: blockIdx.x + j * gridDim.x, j < nj
-    const uint32_t nj = blockIdx.x < ntiles ? uint32_t((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0u;
+    // static claims j < jstat (a multiple of kBatch, so no claim straddles the
+    // split), then pool claims: j = jstat + p, tile = grid * jstat + p
+    // (POOL is chosen by the launcher: small launches -- under ENDOR_TMA_POOL_MIN
+    // tiles per SM -- stay fully static, where the pool's round trips would
+    // cost more than the imbalance they remove; a template parameter, so the
+    // static instantiation carries none of the pool's code)
+    constexpr bool pool = POOL;
+    const uint32_t jstat =
+        pool ? uint32_t((ntiles / gridDim.x) * (100 - ENDOR_TMA_POOL_PCT) / 100 / kBatch * kBatch) : 0u;
+    const uint32_t nj = pool ? uint32_t(jstat + (ntiles - uint64_t(jstat) * gridDim.x))
+                             : (blockIdx.x < ntiles ? uint32_t((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0u);
 
     init_luts(tid);
     if (tid == 0) {
@@ -236,7 +264,11 @@ __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(co
         // register for successive claims would serialise on each other) into
         // its slot of the claim, one commit group per claim, and the claim is
         // issued kLook claims later after cp.async.wait_group(kLook - 1).
-        auto tile_of = [&](uint32_t j) -> uint64_t { return j < nj ? blockIdx.x + uint64_t(j) * gridDim.x : ntiles; };
+        auto tile_of = [&](uint32_t j) -> uint64_t {
+            if (j >= nj) return ntiles;
+            if (pool && j >= jstat) return uint64_t(jstat) * gridDim.x + (j - jstat);  // the shared pool
+            return blockIdx.x + uint64_t(j) * gridDim.x;
+        };
         auto fetch = [&](uint32_t slot, uint64_t t) {  // one lane per tile; t < ntiles
             const BatchTensor& T = b.t[batch_tensor_of_tile(b, t)];
             const uint64_t lt = t - T.tile0, nsub = ceil_div(T.n, kSubElems), a = lt * 8;
@@ -354,7 +386,11 @@ __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(co
         };
         auto claim_batch = [&](uint32_t c) -> uint32_t {  // claim c's first j (lane-uniform), fetch its tiles
             uint32_t j = 0;
-            if (lane == 0) asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(j) : "r"(claim), "n"(kBatch) : "memory");
+            if (lane == 0) {
+                asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(j) : "r"(claim), "n"(kBatch) : "memory");
+                if (pool && j >= jstat)  // this SM's static run is used up: the pool
+                    j = jstat + uint32_t(atomicAdd(&b.hdr->tile_claim, (unsigned long long)kBatch));
+            }
             j = __shfl_sync(0xffffffffu, j, 0);
             const uint64_t t = tile_of(j + lane);
             if (lane < kBatch && t < ntiles) fetch(slot0 + ((c % kLook) * kBatch + lane) * kSlotBytes, t);
@@ -381,6 +417,17 @@ __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(co
         // chunk ends where the next entry says, and lane k gathers tile k's
         // eight starts
         static_assert(kBatch <= 32, "lane k holds claim tile k");
+        // every claimer (producer warp, or the deriver with DERIVE) reports once it has
+        // drawn a claim past the end; the last one resets the counter for the next launch
+        auto claims_done = [&]() {
+            if (pool && lane == 0) {
+                const unsigned long long n_cl = uint64_t(kPipes) * gridDim.x;
+                if (atomicAdd(&b.hdr->tile_done, 1ull) == n_cl - 1) {
+                    b.hdr->tile_claim = 0;
+                    b.hdr->tile_done = 0;
+                }
+            }
+        };
         auto derive = [&](uint32_t c, uint32_t j0, uint32_t (&rel)[9]) {
 #pragma unroll
             for (int g0 = 0; g0 < kBatch; g0 += 4) {  // four tiles (32 sub-tiles) per pass
@@ -471,6 +518,7 @@ __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(co
                 }
             }
             asm volatile("cp.async.wait_all;" ::: "memory");
+            claims_done();
             {  // end of work
                 const uint32_t ds = d % kDesc, da = desc0 + ds * kDescBytes;
                 if (d >= kDesc) mbar_wait(dempty0 + 8 * ds, ((d / kDesc) - 1) & 1);
@@ -619,6 +667,7 @@ __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(co
             }
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
+        if (!DERIVE) claims_done();  // (DERIVE: the deriver claimed)
         // end of work: a sentinel tile id releases the consumers
         {
             const int s = i % kStages;
@@ -787,6 +836,14 @@ static cudaError_t launch_tma_mode(const Batch& b, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     const uint64_t grid = umin64(b.ntiles, uint64_t(blocks_per_sm) * sms);
     if (grid == 0) return cudaSuccess;
+    if (ENDOR_TMA_GLOBAL_CLAIMS && b.ntiles / grid >= ENDOR_TMA_POOL_MIN) {
+        // (kernel_slots also sets the pool instantiation's shared-memory limit)
+        if ((e = kernel_slots(reinterpret_cast<const void*>(expand_tma_kernel<MODE, DERIVE, ROWS, true>), threads,
+                              smem, nullptr, nullptr)) != cudaSuccess)
+            return e;
+        return launch_pdl(expand_tma_kernel<MODE, DERIVE, ROWS, true>, dim3(unsigned(grid)), dim3(threads), smem, s,
+                          b);
+    }
     return launch_pdl(expand_tma_kernel<MODE, DERIVE, ROWS>, dim3(unsigned(grid)), dim3(threads), smem, s, b);
 }
 

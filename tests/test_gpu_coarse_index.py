@@ -117,3 +117,24 @@ def test_coarse_index_layer_shape(E):
     t = E.compress(w)
     for cs in (2048, 4096, 8192):
         assert torch.equal(E.decompress_chunked(t, E.build_rank_index(t.bitmap, cs)).data, w.data), cs
+
+
+def test_pool_claims_recover_after_latched_error(E):
+    """A layer-sized launch takes its last tiles from the shared pool counter
+    in the workspace (expand.cu, ENDOR_TMA_GLOBAL_CLAIMS); CTAs that see a
+    latched error skip that protocol, so the status reset must also reset the
+    counter -- every later launch on the same (cached) workspace is bit-exact."""
+    w = E.synth_weight(8192, 32768, 11, device="cuda")
+    E.magnitude_prune(w, 0.5, inplace=True)
+    t = E.compress(w)
+    for cs in (1024, 4096):
+        good = E.build_rank_index(t.bitmap, cs)
+        pre = good.prefix.cpu().numpy().astype(np.int64)
+        for k in (1, len(pre) // 3, len(pre) - 2):
+            bad = pre.copy()
+            bad[k:] += 3
+            with pytest.raises(E.CorruptionError):
+                E.decompress_chunked(t, E.RankIndex(cs, torch.from_numpy(bad).cuda()))
+            for _ in range(3):
+                assert torch.equal(E.decompress_chunked(t, good).data, w.data), (cs, k)
+            assert torch.equal(E.decompress(t).data, w.data), (cs, k)
