@@ -72,7 +72,7 @@ namespace endor_b200 {
 #define ENDOR_TMA_GLOBAL_CLAIMS 1
 #endif
 #ifndef ENDOR_TMA_POOL_MIN
-#define ENDOR_TMA_POOL_MIN 512
+#define ENDOR_TMA_POOL_MIN 128
 #endif
 #ifndef ENDOR_TMA_POOL_PCT
 #define ENDOR_TMA_POOL_PCT 15
