@@ -18,6 +18,7 @@
 // CUDA headers are needed by the caller.
 #pragma once
 
+#include <bit>
 #include <cstdint>
 #include <cstring>
 #include <span>
@@ -46,6 +47,13 @@ inline void check(int status) {
 
 inline int32_t dtype_code(Dtype d) { return static_cast<int32_t>(d); }
 
+// The bitmap's serialized bytes (bitmap.hpp:65-70: ceil(size/8) bytes,
+// LSB-first) without a copy: Bitmap stores them as little-endian u64 words.
+inline const std::byte* bitmap_bytes(const Bitmap& b) {
+    static_assert(std::endian::native == std::endian::little, "Bitmap words are read as LSB-first bytes");
+    return reinterpret_cast<const std::byte*>(b.words().data());
+}
+
 // decompress (codec.hpp:157-166).  The reference re-checks values vs popcount
 // first (:158-160); EndorTensor's constructor already guarantees it and the
 // device re-verifies popcount == nnz.
@@ -54,8 +62,8 @@ inline DenseMatrix decompress(const EndorTensor& t) {
         throw CorruptionError("values length does not match bitmap popcount");
     DenseMatrix out(t.rows(), t.cols(), t.dtype());
     if (t.element_count() == 0) return out;
-    const auto bm = t.bitmap().to_bytes();
-    check(endor_cuda_decompress_host(t.rows(), t.cols(), dtype_code(t.dtype()), bm.data(),
+    const std::byte* bm = bitmap_bytes(t.bitmap());
+    check(endor_cuda_decompress_host(t.rows(), t.cols(), dtype_code(t.dtype()), bm,
                                      t.values().data(), t.nnz(), out.bytes().data()));
     return out;
 }
@@ -68,8 +76,7 @@ inline RankIndex build_rank_index(const Bitmap& bitmap, std::uint64_t chunk_size
     const std::uint64_t chunks = n == 0 ? 0 : (n + chunk_size - 1) / chunk_size;
     std::vector<std::uint64_t> prefix(chunks);
     if (chunks) {
-        const auto bytes = bitmap.to_bytes();
-        check(endor_cuda_rank_index_host(bytes.data(), n, chunk_size, prefix.data()));
+        check(endor_cuda_rank_index_host(bitmap_bytes(bitmap), n, chunk_size, prefix.data()));
     }
     return RankIndex(chunk_size, std::move(prefix));
 }
@@ -77,8 +84,8 @@ inline RankIndex build_rank_index(const Bitmap& bitmap, std::uint64_t chunk_size
 // decompress_chunked (codec.hpp:205-216).
 inline DenseMatrix decompress_chunked(const EndorTensor& t, const RankIndex& idx) {
     DenseMatrix out(t.rows(), t.cols(), t.dtype());
-    const auto bm = t.bitmap().to_bytes();
-    check(endor_cuda_decompress_chunked_host(t.rows(), t.cols(), dtype_code(t.dtype()), bm.data(),
+    const std::byte* bm = bitmap_bytes(t.bitmap());
+    check(endor_cuda_decompress_chunked_host(t.rows(), t.cols(), dtype_code(t.dtype()), bm,
                                              t.values().data(), t.nnz(), idx.chunk_size(),
                                              idx.prefix().data(), idx.chunk_count(),
                                              out.bytes().data()));
@@ -88,8 +95,8 @@ inline DenseMatrix decompress_chunked(const EndorTensor& t, const RankIndex& idx
 // decompress_chunk_into (codec.hpp:191-201): writes exactly chunk k's range.
 inline void decompress_chunk_into(const EndorTensor& t, const RankIndex& idx, std::uint64_t k,
                                   std::span<std::byte> dst) {
-    const auto bm = t.bitmap().to_bytes();
-    check(endor_cuda_decompress_chunk_into_host(t.rows(), t.cols(), dtype_code(t.dtype()), bm.data(),
+    const std::byte* bm = bitmap_bytes(t.bitmap());
+    check(endor_cuda_decompress_chunk_into_host(t.rows(), t.cols(), dtype_code(t.dtype()), bm,
                                                 t.values().data(), t.nnz(), idx.chunk_size(),
                                                 idx.prefix().data(), idx.chunk_count(), k, dst.data(),
                                                 dst.size()));
@@ -113,18 +120,18 @@ inline EndorTensor compress(const DenseMatrix& w) {
 // reference's order and exception types (check_sorted_unique, :224-232).
 inline DenseMatrix extract_rows(const EndorTensor& t, std::span<const std::size_t> rows) {
     DenseMatrix out(rows.size(), t.cols(), t.dtype());
-    const auto bm = t.bitmap().to_bytes();
+    const std::byte* bm = bitmap_bytes(t.bitmap());
     const std::vector<std::uint64_t> sel(rows.begin(), rows.end());
-    check(endor_cuda_extract_rows_host(t.rows(), t.cols(), dtype_code(t.dtype()), bm.data(), t.values().data(),
+    check(endor_cuda_extract_rows_host(t.rows(), t.cols(), dtype_code(t.dtype()), bm, t.values().data(),
                                        t.nnz(), sel.data(), sel.size(), out.bytes().data()));
     return out;
 }
 
 inline DenseMatrix extract_cols(const EndorTensor& t, std::span<const std::size_t> cols) {
     DenseMatrix out(t.rows(), cols.size(), t.dtype());
-    const auto bm = t.bitmap().to_bytes();
+    const std::byte* bm = bitmap_bytes(t.bitmap());
     const std::vector<std::uint64_t> sel(cols.begin(), cols.end());
-    check(endor_cuda_extract_cols_host(t.rows(), t.cols(), dtype_code(t.dtype()), bm.data(), t.values().data(),
+    check(endor_cuda_extract_cols_host(t.rows(), t.cols(), dtype_code(t.dtype()), bm, t.values().data(),
                                        t.nnz(), sel.data(), sel.size(), out.bytes().data()));
     return out;
 }

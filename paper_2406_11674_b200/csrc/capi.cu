@@ -232,15 +232,17 @@ int endor_cuda_workspace_init(void* ws, size_t ws_bytes, void* stream) {
 
 int endor_cuda_sync_status(void* ws, void* stream) {
     if (!ws) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null workspace");
-    CK(cudaStreamSynchronize(S(stream)));
     WsHeader* hdr = static_cast<WsHeader*>(ws);
     uint32_t st = 0;
-    CK(cudaMemcpy(&st, &hdr->status, sizeof(st), cudaMemcpyDeviceToHost));
+    // stream-ordered read and reset (the stream may be a non-blocking one)
+    CK(cudaMemcpyAsync(&st, &hdr->status, sizeof(st), cudaMemcpyDeviceToHost, S(stream)));
+    CK(cudaStreamSynchronize(S(stream)));
     if (st) {
-        CK(cudaMemset(&hdr->status, 0, sizeof(uint32_t)));
+        CK(cudaMemsetAsync(&hdr->status, 0, sizeof(uint32_t), S(stream)));
         // CTAs that saw the latched status skipped the self-resetting tile
         // pool protocol (expand.cu): start the next launch from zero
-        CK(cudaMemset(&hdr->tile_claim, 0, 2 * sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(&hdr->tile_claim, 0, 2 * sizeof(unsigned long long), S(stream)));
+        CK(cudaStreamSynchronize(S(stream)));
         return fail(int(st), st == ENDOR_ERR_CORRUPTION
                                  ? "device check failed: bitmap popcount / rank index / padding bits "
                                    "disagree with the tensor (codec.hpp:158-160,170-184, bitmap.hpp:78-84)"
@@ -1038,11 +1040,32 @@ struct DevBuf {
     ~DevBuf() { cudaFree(p); }
 };
 
+// Grow-only pinned host staging buffer.
+struct PinBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t need(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocDefault);
+        if (e == cudaSuccess) cap = bytes;
+        return e;
+    }
+    ~PinBuf() { cudaFreeHost(p); }
+};
+
 // Grow-only device buffers reused by the synchronous host-buffer entry points
 // (one set per host thread and device).
 struct HostSession {
     int device = -1;
     DevBuf bm, vals, dense, ws, prefix;
+    PinBuf pin_in, pin_out;  // chunk_into staging: one DMA each way
+    cudaStream_t stream = nullptr;  // non-blocking, so host threads fanning out calls overlap
+    ~HostSession() {
+        if (stream) cudaStreamDestroy(stream);
+    }
 };
 thread_local HostSession* g_sess = nullptr;
 
@@ -1150,36 +1173,82 @@ int endor_cuda_decompress_chunk_into_host(uint64_t rows, uint64_t cols, int32_t 
                                           uint64_t nnz, uint64_t cs, const uint64_t* prefix_host,
                                           uint64_t chunk_count, uint64_t k, void* dense_host,
                                           uint64_t dense_host_bytes) {
-    HostSession* s;
-    endor_tensor_view v;
+    // Moves only what chunk k needs -- the last chunk's bitmap bytes for the
+    // check_index tail, chunk k's bitmap bytes and at most one chunk of values
+    // from prefix[k] -- gathered into a pinned staging buffer and sent as ONE
+    // DMA, and returns chunk k's dense bytes through one pinned DMA, so a
+    // caller fanning decompress_chunk_into out over the chunks from several
+    // host threads (the reference's pattern, codec.hpp:203-204) pays per chunk,
+    // not per tensor, and the threads' host-side copies run in parallel (each
+    // thread has its own session and non-blocking stream).  Each range runs as
+    // its own sub-tensor view starting at the 32-bit word holding its first bit.
     uint64_t n;
-    ST(session(&s, 1));
-    ST(upload(s, rows, cols, dtype, bitmap_host, values_host, nnz, &v, &n));
-    ST(session(&s, n));
     const int eb = eb_of(dtype);
+    if (!eb) return fail(ENDOR_ERR_INVALID_ARGUMENT, "unknown dtype code");
+    if (!checked_n(rows, cols, &n)) return fail(ENDOR_ERR_SIZE, "matrix dimensions overflow the addressable element count");
+    if (nnz > n) return fail(ENDOR_ERR_CORRUPTION, "values length does not match bitmap popcount");
     // check_index first (codec.hpp:193), exactly as the reference orders it
     const uint64_t chunks = (n == 0 || cs == 0) ? 0 : ceil_div(n, cs);
     if (cs == 0 || chunk_count != chunks) return fail(ENDOR_ERR_CORRUPTION, "rank index does not cover the bitmap");
-    if (chunk_count) {  // the tail test runs only when there are chunks (codec.hpp:177)
-        if (!prefix_host) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null prefix");
-        CK(s->prefix.need(chunk_count * 8 + 8));
-        CK(cudaMemcpy(s->prefix.p, prefix_host, chunk_count * 8, cudaMemcpyHostToDevice));
-        const uint64_t last = chunk_count - 1;
-        ST(range_expand(&v, n, eb, last * cs, n, static_cast<const unsigned long long*>(s->prefix.p) + last, true,
-                        nullptr, ws_layout(s->ws.p, n), nullptr));
-        ST(endor_cuda_sync_status(s->ws.p, nullptr));
+    if (chunk_count == 0) return fail(ENDOR_ERR_BOUNDS, "chunk index out of range");  // codec.hpp:177,194
+    if (!prefix_host || !bitmap_host) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null prefix or bitmap");
+    const uint64_t last = chunk_count - 1;
+    const uint64_t lb = last * cs, lb0 = lb & ~uint64_t(31), nt = n - lb0;  // tail view: bits [lb0, n)
+    const bool go = k < chunk_count && dense_host_bytes == n * uint64_t(eb);
+    const uint64_t b = go ? k * cs : 0, e = go ? ((b + cs < n) ? b + cs : n) : 0;
+    // chunk view: bits [b0, e) of a view whose length runs to the next 32-bit
+    // word boundary (or the tensor's end), so the bits after e in its last
+    // bytes belong to the view, not to its padding
+    const uint64_t b0 = b & ~uint64_t(31);
+    const uint64_t nc = ((e + 31) & ~uint64_t(31)) < n ? ((e + 31) & ~uint64_t(31)) - b0 : n - b0;
+    const uint64_t p = go ? prefix_host[k] : 0;
+    const uint64_t w = go && p <= nnz ? ((e - b < nnz - p) ? e - b : nnz - p) : 0;  // values moved
+    if (go && p > nnz) return fail(ENDOR_ERR_CORRUPTION, "rank index entry beyond the values");
+    if (go && ((w && !values_host) || !dense_host)) return fail(ENDOR_ERR_INVALID_ARGUMENT, "null buffer");
+    HostSession* s;
+    ST(session(&s, nt > nc ? nt : nc));
+    if (!s->stream) CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    cudaStream_t st = s->stream;
+    const WsLayout L = ws_layout(s->ws.p, nt > nc ? nt : nc);
+    // one staging image, host and device alike: [prefix[last], 0][tail bitmap][chunk bitmap][values]
+    auto up16 = [](size_t x) { return (x + 15) & ~size_t(15); };
+    const size_t tbm = (nt + 7) / 8, cbm = go ? (nc + 7) / 8 : 0, vb = w * eb;
+    const size_t o_tail = 16, o_chunk = o_tail + up16(tbm), o_vals = o_chunk + up16(cbm), in_bytes = o_vals + vb;
+    CK(s->pin_in.need(in_bytes + 16));
+    CK(s->bm.need(in_bytes + 16));
+    uint8_t* hin = static_cast<uint8_t*>(s->pin_in.p);
+    uint8_t* din = static_cast<uint8_t*>(s->bm.p);
+    const unsigned long long pair[2] = {prefix_host[last], 0ull};  // tail base, chunk base (view-relative)
+    memcpy(hin, pair, 16);
+    memcpy(hin + o_tail, static_cast<const uint8_t*>(bitmap_host) + lb0 / 8, tbm);
+    if (go) {
+        memcpy(hin + o_chunk, static_cast<const uint8_t*>(bitmap_host) + b0 / 8, cbm);
+        if (vb) memcpy(hin + o_vals, static_cast<const uint8_t*>(values_host) + p * eb, vb);
     }
-    if (k >= chunk_count) return fail(ENDOR_ERR_BOUNDS, "chunk index out of range");
-    if (dense_host_bytes != n * uint64_t(eb))
+    CK(cudaMemcpyAsync(din, hin, go ? in_bytes : o_chunk, cudaMemcpyHostToDevice, st));
+    auto* pre = reinterpret_cast<const unsigned long long*>(din);
+    // the tail test: prefix[last] + popcount(bits [lb, n)) == nnz
+    endor_tensor_view tv{1, nt, dtype, 0, din + o_tail, nullptr, nnz};
+    ST(range_expand(&tv, nt, eb, lb - lb0, nt, pre, true, nullptr, L, st));
+    if (!go) {  // the tail's CORRUPTION outranks BOUNDS / INVALID (codec.hpp:193-197)
+        ST(endor_cuda_sync_status(s->ws.p, st));
+        if (k >= chunk_count) return fail(ENDOR_ERR_BOUNDS, "chunk index out of range");
         return fail(ENDOR_ERR_INVALID_ARGUMENT, "destination buffer must hold the full dense matrix");
-    // only chunk k's byte range moves in either direction
-    const uint64_t b = k * cs, e = (b + cs < n) ? b + cs : n;
-    CK(s->dense.need(n * eb + 16));
-    ST(endor_cuda_decompress_chunk_into(&v, cs, static_cast<const uint64_t*>(s->prefix.p), chunk_count,
-                                        k, s->dense.p, n * eb, s->ws.p, s->ws.cap, nullptr));
-    ST(endor_cuda_sync_status(s->ws.p, nullptr));
-    CK(cudaMemcpy(static_cast<uint8_t*>(dense_host) + b * eb, static_cast<uint8_t*>(s->dense.p) + b * eb,
-                  (e - b) * eb, cudaMemcpyDeviceToHost));
+    }
+    CK(s->dense.need(nc * eb + 16));
+    // chunk k's values start at view rank 0 of the window; running past it is CORRUPTION
+    endor_tensor_view cv{1, nc, dtype, 0, din + o_chunk, din + o_vals, w};
+    ST(range_expand(&cv, nc, eb, b - b0, e - b0, pre + 1, false, s->dense.p, L, st));
+    const size_t ob = (e - b) * eb;
+    CK(s->pin_out.need(ob + 16));
+    uint8_t* hout = static_cast<uint8_t*>(s->pin_out.p);
+    CK(cudaMemcpyAsync(hout + 8, static_cast<uint8_t*>(s->dense.p) + (b - b0) * eb, ob, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hout, &L.hdr->status, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    uint32_t status;
+    memcpy(&status, hout, 4);
+    if (status) return endor_cuda_sync_status(s->ws.p, st);  // reports and resets it
+    memcpy(static_cast<uint8_t*>(dense_host) + b * eb, hout + 8, ob);
     return ENDOR_OK;
 }
 
