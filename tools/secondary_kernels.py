@@ -126,11 +126,12 @@ def main():
         k = int(cols * frac)
         sel = torch.arange(0, cols, cols // k, device=DEV, dtype=torch.int64)[:k].contiguous()
         ob = torch.empty(k * rows * 2 + 16, dtype=torch.uint8, device=DEV)
-        alg = bm_bytes + int(k * rows * 0.5) * 32 + k * rows * 2  # bits + one sector per selected value + out
+        # bits + the values (or one 32-byte sector per selected value, if fewer) + out
+        alg = bm_bytes + min(val_bytes, int(k * rows * 0.5) * 32) + k * rows * 2
         add(f"extract_cols {frac:.0%}",
             timed(lambda: ck(L.endor_cuda_extract_cols(C.byref(v), sel.data_ptr(), k, ob.data_ptr(), ws.data_ptr(),
                                                        ws.numel(), stream)), flush), alg, 3,
-            "alg bytes count one 32-byte sector per selected value")
+            "alg bytes: bitmap + min(all values, one 32-byte sector per selected value) + output")
     os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
     with open(args.out, "w") as f:
         json.dump(res, f, indent=1)
