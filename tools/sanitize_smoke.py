@@ -132,5 +132,21 @@ with tempfile.TemporaryDirectory() as d:
     pipe.run(ops, sync=True)
     pipe.close()
     assert torch.equal(ops[0].y, ops[1].y)
+# host-buffer decompress_chunk_into (pinned staging, per-thread stream), arbitrary chunk size
+from paper_2406_11674_b200 import _lib  # noqa: E402
+L = _lib.lib()
+for rows, cols, cs in ((5, 2049, 2000), (40, 3000, 4096)):
+    w = O.random_dense(rows, cols, 2, rows + cols, 0.5)
+    bm, vals, nnz, _ = O.compress(w, rows, cols, 2)
+    n = rows * cols
+    bits = np.unpackbits(bm, bitorder="little")[:n].astype(np.uint64)
+    cum = np.concatenate([[0], np.cumsum(bits, dtype=np.uint64)])
+    pre = np.ascontiguousarray(cum[np.arange((n + cs - 1) // cs) * cs], dtype=np.uint64)
+    dst = np.zeros(n * 2, np.uint8)
+    for k in range(len(pre)):
+        assert L.endor_cuda_decompress_chunk_into_host(rows, cols, 0, bm.ctypes.data, vals.ctypes.data, nnz, cs,
+                                                       pre.ctypes.data, len(pre), k, dst.ctypes.data, dst.size) == 0
+    assert dst.tobytes() == w.tobytes()
+    checks += 1
 torch.cuda.synchronize()
 print(f"sanitize smoke ok ({checks} shapes)")
