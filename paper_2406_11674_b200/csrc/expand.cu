@@ -210,9 +210,12 @@ __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(co
     if (warp < kPipes || deriver) {
         // ====== producer warp of pipe `pipe` (DERIVE: its TMA warp or its deriver warp) ======
         constexpr uint32_t kSubsPerBlk = kCountSubs;  // sub-tiles per count block
-        if (DERIVE && deriver && blockIdx.x == 0 && pipe == 0) {
+        // (tensor k's tail test runs on CTA grid - 1 - k: one test per CTA, not
+        // all of a batch's on CTA 0 -- seven serial tests held CTA 0 ~4 us past
+        // the others on a Llama2-70B G = 8 shard, profiles/r02/small_shard_timeline.txt)
+        if (DERIVE && deriver && pipe == 0) {
             // check_index's tail test: the last chunk spans up to idx_subs sub-tiles
-            for (int k = 0; k < b.count; ++k) {
+            for (int k = int(gridDim.x - 1 - blockIdx.x); k < b.count; k += int(gridDim.x)) {
                 const BatchTensor& T = b.t[k];
                 const uint64_t cs = uint64_t(T.idx_subs) * kSubElems, last = ceil_div(T.n, cs) - 1;
                 const uint64_t nw = (T.n + 31) / 32, nbytes = (T.n + 7) / 8;
@@ -232,8 +235,8 @@ __global__ void __launch_bounds__(tma_threads<DERIVE>(), 1) expand_tma_kernel(co
         }
         // check_index's tail test (codec.hpp:177-183) for caller-indexed tensors:
         // idx[last] + popcount(last chunk) == nnz, plus the padding bits
-        if (!DERIVE && blockIdx.x == 0 && pipe == 0) {
-            for (int k = 0; k < b.count; ++k) {
+        if (!DERIVE && pipe == 0) {
+            for (int k = int(gridDim.x - 1 - blockIdx.x); k < b.count; k += int(gridDim.x)) {
                 const BatchTensor& T = b.t[k];
                 if (!T.idx) continue;
                 const uint64_t last = ceil_div(T.n, kSubElems) - 1, w0 = last * 32;

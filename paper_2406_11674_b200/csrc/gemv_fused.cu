@@ -187,6 +187,17 @@ __global__ void __launch_bounds__(kGvThreads, ENDOR_GV_MINB) gemv_fused_kernel(c
     pdl_wait();
     if (cta_error_latched(b.hdr)) return;  // a latched error: write nothing (+ publishes the prologue)
     pdl_launch_dependents();
+    if (warp == kGvWarps) {
+        // check_index's tail test (codec.hpp:177-183), tensor t on CTA grid - 1 - t
+        // (one test per CTA instead of a batch's worth serially on CTA 0)
+        for (int t = int(gridDim.x - 1 - blockIdx.x); t < b.count; t += int(gridDim.x)) {
+            const BatchTensor& T = b.t[t];
+            const uint64_t last = T.n / kSubElems - 1;  // n % 1024 == 0 here
+            const uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(T.bitmap) + last * 32 + lane);
+            const uint32_t tail = __reduce_add_sync(0xffffffffu, __popc(v));
+            if (lane == 0 && T.idx[last] + tail != T.nnz) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
+        }
+    }
     // this CTA's contiguous range of the column-major item order
     const uint64_t u0 = nitems * blockIdx.x / gridDim.x, u1 = nitems * (blockIdx.x + 1) / gridDim.x;
     if (u0 >= u1) return;
@@ -194,16 +205,6 @@ __global__ void __launch_bounds__(kGvThreads, ENDOR_GV_MINB) gemv_fused_kernel(c
 
     if (warp == kGvWarps) {
         // ================= producer warp =================
-        if (blockIdx.x == 0) {
-            // check_index's tail test (codec.hpp:177-183)
-            for (int t = 0; t < b.count; ++t) {
-                const BatchTensor& T = b.t[t];
-                const uint64_t last = T.n / kSubElems - 1;  // n % 1024 == 0 here
-                const uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(T.bitmap) + last * 32 + lane);
-                const uint32_t tail = __reduce_add_sync(0xffffffffu, __popc(v));
-                if (lane == 0 && T.idx[last] + tail != T.nnz) latch_status(b.hdr, ENDOR_ERR_CORRUPTION);
-            }
-        }
         // lane l holds item i + l of the current / next 32-item group: its
         // nine sub-tile starts idx[8t .. 8t+8] (nnz past the end), fetched one
         // group ahead and validated here -- monotone and within [0, nnz] --
