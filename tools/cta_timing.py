@@ -20,10 +20,10 @@ from paper_2406_11674_b200 import _lib, catalog, codec as E, shard as S  # noqa:
 DEV = torch.device("cuda", 0)
 
 
-def run(label, tensors):
+def run(label, tensors, cs=1024):
     L = _lib.lib()
     outs = [E.DenseMatrix.empty(t.rows, t.cols, E.Dtype.F16, DEV) for t in tensors]
-    idx = [E.build_rank_index(t.bitmap, 1024) for t in tensors]
+    idx = [E.build_rank_index(t.bitmap, cs) for t in tensors]
     plan = E.BatchPlan(tensors, outs, indices=idx)
     scratch = torch.empty(512 << 20, dtype=torch.uint8, device=DEV)
     res = []
@@ -58,6 +58,14 @@ def run(label, tensors):
 def main():
     L = _lib.lib()
     L.endor_debug_cta_times.argtypes = [C.c_void_p, C.c_int]
+    if "--fc1" in sys.argv:  # fc1 alone at chunk 1024 and at the coarse 4096 (deriver path)
+        w = E.synth_weight(9216, 36864, 7, device=DEV)
+        E.magnitude_prune(w, 0.5, inplace=True)
+        t = E.compress(w)
+        del w
+        run("fc1 cs=1024", [t], 1024)
+        run("fc1 cs=4096", [t], 4096)
+        return
     w = E.synth_weight(16384, 16384, 150, device=DEV)
     E.magnitude_prune(w, 0.5, inplace=True)
     t = E.compress(w)
