@@ -21,6 +21,7 @@ Reference anchors:
 from __future__ import annotations
 
 import ctypes as C
+import threading
 import enum
 from dataclasses import dataclass
 from typing import Dict, List, Optional, Sequence, Tuple
@@ -148,14 +149,16 @@ def _alloc(nbytes: int, device: torch.device, pad: int = 16) -> torch.Tensor:
     return torch.empty(nbytes + pad, dtype=torch.uint8, device=device)[:nbytes]
 
 
-_WS: Dict[Tuple[int, int], torch.Tensor] = {}
+_WS: Dict[Tuple[int, int, int], torch.Tensor] = {}
 
 
 def workspace(n: int, device: torch.device, min_bytes: int = 0) -> torch.Tensor:
     """Zero-initialised workspace for tensors of up to n elements (and at
-    least min_bytes), one per (device, stream), grown on demand -- the library
-    leaves it zeroed after every call."""
-    key = (device.index, _stream_ptr(device))
+    least min_bytes), one per (device, stream, host thread), grown on demand --
+    the library leaves it zeroed after every call.  Per thread because host
+    threads sharing a stream would interleave their launch sequences (the
+    reference allows concurrent per-chunk calls, codec.hpp:188-190)."""
+    key = (device.index, _stream_ptr(device), threading.get_ident())
     need = max(_lib.lib().endor_cuda_workspace_bytes(max(n, 1), 1), min_bytes)
     ws = _WS.get(key)
     if ws is None or ws.numel() < need:

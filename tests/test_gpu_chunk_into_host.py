@@ -117,3 +117,34 @@ def test_threads_fan_out(L):
         t.join()
     assert not errs
     assert dst.tobytes() == w.tobytes()
+
+
+def test_device_chunk_into_threads_fan_out(L):
+    """The device-pointer decompress_chunk_into from several Python threads on
+    one tensor and one output (each thread gets its own workspace)."""
+    from paper_2406_11674_b200 import codec as E
+    rows, cols, eb, cs = 300, 5000, 2, 32768
+    w = O.random_dense(rows, cols, eb, 21, 0.5)
+    bm, vals, nnz, _ = O.compress(w, rows, cols, eb)
+    t = E.EndorTensor(rows, cols, E.Dtype.F16, E.Bitmap(rows * cols, data=torch.from_numpy(bm.copy()).cuda()),
+                      torch.from_numpy(vals.copy()).cuda(), validate=False, nnz=nnz)
+    idx = E.build_rank_index(t.bitmap, cs)
+    out = torch.zeros(rows * cols * eb, dtype=torch.uint8, device="cuda")
+    errs = []
+
+    def run(tid, T):
+        try:
+            torch.cuda.set_device(0)
+            for k in range(tid, idx.chunk_count(), T):
+                E.decompress_chunk_into(t, idx, k, out)
+        except Exception as e:  # noqa: BLE001
+            errs.append(repr(e))
+
+    ts = [threading.Thread(target=run, args=(i, 4)) for i in range(4)]
+    for x in ts:
+        x.start()
+    for x in ts:
+        x.join()
+    torch.cuda.synchronize()
+    assert not errs, errs
+    assert out.cpu().numpy().tobytes() == w.tobytes()
