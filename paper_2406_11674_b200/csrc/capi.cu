@@ -9,6 +9,7 @@
 
 #include <cstdio>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <utility>
@@ -1067,14 +1068,15 @@ struct HostSession {
         if (stream) cudaStreamDestroy(stream);
     }
 };
-thread_local HostSession* g_sess = nullptr;
+// owned per thread: a thread's buffers and stream are released when it exits
+// (callers may fan chunk calls out over short-lived threads)
+thread_local std::unique_ptr<HostSession> g_sess;
 
 int session(HostSession** out, uint64_t n) {
     int dev = 0;
     CK(cudaGetDevice(&dev));
     if (!g_sess || g_sess->device != dev) {
-        delete g_sess;
-        g_sess = new HostSession();
+        g_sess = std::make_unique<HostSession>();
         g_sess->device = dev;
     }
     const size_t wsb = ws_layout(nullptr, n).bytes;
@@ -1082,7 +1084,7 @@ int session(HostSession** out, uint64_t n) {
         CK(g_sess->ws.need(wsb));
         CK(cudaMemset(g_sess->ws.p, 0, g_sess->ws.cap));
     }
-    *out = g_sess;
+    *out = g_sess.get();
     return ENDOR_OK;
 }
 

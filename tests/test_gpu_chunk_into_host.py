@@ -148,3 +148,37 @@ def test_device_chunk_into_threads_fan_out(L):
     torch.cuda.synchronize()
     assert not errs, errs
     assert out.cpu().numpy().tobytes() == w.tobytes()
+
+
+def test_short_lived_threads_release_their_sessions(L):
+    """Each host thread owns its device buffers, pinned staging and stream;
+    they are released when the thread exits, so fanning calls out over
+    short-lived threads does not accumulate device memory."""
+    rows, cols, eb, cs = 64, 16384, 2, 1 << 18
+    n = rows * cols
+    w = O.random_dense(rows, cols, eb, 5, 0.5)
+    bm, vals, nnz, _ = O.compress(w, rows, cols, eb)
+    pre = prefix_of(bm, n, cs)
+    dst = np.zeros(n * eb, np.uint8)
+
+    def one(k):
+        torch.cuda.set_device(0)
+        assert call(L, rows, cols, eb, bm, vals, nnz, cs, pre, k, dst) == 0
+
+    def wave():
+        ts = [threading.Thread(target=one, args=(k % len(pre),)) for k in range(16)]
+        for x in ts:
+            x.start()
+        for x in ts:
+            x.join()
+
+    wave()  # warm-up: the runtime's own per-thread state
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(5):
+        wave()
+    torch.cuda.synchronize()
+    free1 = torch.cuda.mem_get_info()[0]
+    # 80 sessions of ~1.7 MiB device buffers each would be > 100 MiB
+    assert free0 - free1 < 32 << 20, (free0 - free1) >> 20
+    assert dst.tobytes() == w.tobytes()
