@@ -489,6 +489,38 @@ def run_ours(args):
                 "layer_ms": round(q_ms / world, 4), "h2d_bytes_per_step": world * sq["h2d_bytes"] // args.steps,
                 "speedup_vs_f16_endor": round(e2e_step / q_ms, 3),
                 "note": "values quantized to int8 (lossy, codec.hpp:306-331); f16 W rebuilt on the fly"}
+        # lossless coded values (csrc/vcode.cu): low bytes raw, high bytes as k-bit dictionary codes,
+        # encoded once at load time on the host; decoded on the compute stream before the fused GEMV
+        if not args.no_extras:
+            pipe.run(hops, sync=True)
+            y_raw = [h.y_host.clone() for h in hops]
+            t_enc = time.perf_counter()
+            blobs = [E.encode_values(h.values) for h in hops]
+            enc_s = time.perf_counter() - t_enc
+            cops = [HostOp(h.rows, h.cols, 0, h.bitmap, torch.empty(0, dtype=torch.uint8), h.nnz, x=h.x, y=h.y,
+                           y_host=h.y_host, vcode=bl) for h, bl in zip(hops, blobs)]
+            pipe.run(cops, sync=True)
+            y_same = all(torch.equal(a, h.y_host) for a, h in zip(y_raw, hops))
+            barrier()
+            pipe.run(cops * args.steps, sync=True)
+            sc = pipe.stats()
+            c_ms = max_over_ranks(sc["total_ms"]) / args.steps
+            vals_raw = sum(h.values.numel() for h in hops)
+            vals_coded = sum(bl.numel() for bl in blobs)
+            e2e["coded_values"] = {
+                "value": round(world * dense_rank / (c_ms * 1e-3) / 1e9, 2), "unit": UNIT,
+                "layer_ms": round(c_ms / world, 4), "h2d_bytes_per_step": world * sc["h2d_bytes"] // args.steps,
+                "speedup_vs_f16_endor": round(e2e_step / c_ms, 3),
+                "values_bytes_raw": vals_raw, "values_bytes_coded": vals_coded,
+                "values_ratio": round(vals_coded / vals_raw, 4),
+                "code_bits": [E.vcode_info(bl)["k"] for bl in blobs],
+                "decode_plus_fused_gemv_ms_per_step": round(sc["decompress_ms"] / args.steps, 4),
+                "exposed_compute_ms_per_run": round(sc["exposed_compute_ms"], 4),
+                "host_encode_s_per_layer": round(enc_s, 3),
+                "y_bit_exact_vs_raw_values": y_same,
+                "note": "lossless (csrc/vcode.cu): values' high bytes as k-bit dictionary codes + exceptions, "
+                        "low bytes raw; the ratio depends on the weights' exponent spread (reference synth_weight "
+                        "here)"}
         # the same layer with the load-time RankIndex shipped per op (prefix1024_host):
         # the fused decompress -> GEMV runs no counting / flatten pass
         if not args.no_extras:

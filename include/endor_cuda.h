@@ -59,7 +59,7 @@
 extern "C" {
 #endif
 
-#define ENDOR_CUDA_ABI_VERSION 3
+#define ENDOR_CUDA_ABI_VERSION 4
 
 typedef enum endor_status {
     ENDOR_OK = 0,
@@ -280,6 +280,43 @@ int endor_cuda_quantize_values(const void* values_f16, uint64_t nnz, void* q_out
  * Async on the stream. */
 int endor_cuda_dequantize_values(const void* q_i8, uint64_t nnz, float scale, void* out_f16, void* stream);
 
+/* ---- lossless transport coding of the packed values (no reference counterpart) ----
+ * The Endor mode is bound by the host -> GPU link (sim.hpp:200-204, 322-325):
+ * every byte of the values section crosses it.  The high byte of a pruned f16
+ * weight (sign, exponent, top two mantissa bits) takes few distinct values, the
+ * low byte is noise, so the blob keeps the low bytes raw and codes the high
+ * byte in k bits (1..7) through a dictionary of the 2^k - 1 most frequent high
+ * bytes; code 2^k - 1 marks an exception, listed as (index << 8 | high byte).
+ * k minimises the blob per tensor.  Decoding reproduces the values bit for bit.
+ * Blob (little-endian; every section 16-byte aligned):
+ *   endor_vcode_header (256 B) | lo: nnz low bytes (zero-padded to a multiple
+ *   of 32) | codes: ceil(nnz / 32) * k u32 words, value i's code at bits
+ *   [k i, k i + k) of the word stream (zero-padded to 16 B) | exc: n_exc u64,
+ *   ascending index. */
+typedef struct endor_vcode_header {
+    uint32_t magic;          /* "EVC1" = 0x31435645 */
+    uint32_t k;              /* code bits per value, 1..7 */
+    uint64_t nnz;            /* values */
+    uint64_t n_exc;          /* exceptions */
+    uint64_t lo_off, code_off, exc_off, blob_bytes;  /* section offsets, total size */
+    uint8_t reserved[8];
+    uint8_t dict[128];       /* high byte of code c (c < 2^k - 1) */
+    uint8_t pad[64];
+} endor_vcode_header;
+
+/* Encode nnz packed f16 values (host memory) into a blob.  blob_out == NULL:
+ * only *blob_bytes is computed (size query).  k_max (1..7) bounds the code
+ * width.  Multi-threaded on the host; an offline, load-time step like compress. */
+int endor_values_encode(const void* values_f16, uint64_t nnz, int k_max, void* blob_out, size_t blob_cap,
+                        size_t* blob_bytes);
+/* Validate a blob header (host copy): magic, k, and offsets recomputed from
+ * nnz / k / n_exc.  CORRUPTION when inconsistent. */
+int endor_values_decode_host_check(const void* header_host);
+/* Decode a device copy of the blob into nnz f16 values (values_out, 16-byte
+ * aligned); header_host is a host copy of its header (for the launch shape).
+ * Two launches (decode, exception patch), async on the stream. */
+int endor_cuda_values_decode(const void* header_host, const void* blob_dev, void* values_out, void* stream);
+
 /* ---- consumer ------------------------------------------------------------ */
 
 /* y[rows] = W[rows, cols] . x[cols]; f16 W and x, fp32 accumulate.  y_f32
@@ -439,6 +476,9 @@ typedef struct endor_pipeline_op {
                                 u64, built once at load time like the compression): copied
                                 with the op, so the decompress / fused GEMV / GEMM run no
                                 counting pass */
+    const void* vcode_host;  /* optional pinned coded-values blob (endor_values_encode) of this
+                                op's f16 values: crosses the link instead of values_host and is
+                                decoded on the compute stream before the decompress / GEMV */
 } endor_pipeline_op;
 
 typedef struct endor_pipeline_stats {

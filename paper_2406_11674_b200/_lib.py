@@ -29,7 +29,7 @@ class PipelineOp(C.Structure):
                 ("bitmap_host", _vp), ("values_host", _vp), ("nnz", _u64),
                 ("x_dev", _vp), ("y_dev", _vp), ("dense_dev", _vp), ("y_host", _vp),
                 ("quant_scale", C.c_float), ("reserved2", _i32), ("path", C.c_char_p),
-                ("tokens", _u64), ("prefix1024_host", _vp)]
+                ("tokens", _u64), ("prefix1024_host", _vp), ("vcode_host", _vp)]
 
 
 class PipelineStats(C.Structure):
@@ -116,6 +116,9 @@ SIGNATURES = {
     "endor_reader_mode": (C.c_int, [_vp]),
     "endor_reader_read": (C.c_int, [_vp, C.c_char_p, C.POINTER(FileInfo), _vp, _vp, C.c_int, _vp, _sz, _vp]),
     "endor_reader_stats": (C.c_int, [_vp, C.POINTER(_f64), C.POINTER(_u64)]),
+    "endor_values_encode": (C.c_int, [_vp, _u64, C.c_int, _vp, _sz, C.POINTER(_sz)]),
+    "endor_values_decode_host_check": (C.c_int, [_vp]),
+    "endor_cuda_values_decode": (C.c_int, [_vp, _vp, _vp, _vp]),
     "endor_host_alloc": (_vp, [_sz]),
     "endor_host_free": (None, [_vp]),
 }

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libendor_cuda.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["scan.cu", "expand.cu", "extract.cu", "fixtures.cu", "gemv.cu", "gemv_fused.cu", "gemm_fused.cu", "capi.cu", "pipeline.cu", "storage.cu"]
+SOURCES = ["scan.cu", "expand.cu", "extract.cu", "fixtures.cu", "gemv.cu", "gemv_fused.cu", "gemm_fused.cu", "capi.cu", "pipeline.cu", "storage.cu", "vcode.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC] + os.environ.get("ENDOR_NVCC_FLAGS", "").split()

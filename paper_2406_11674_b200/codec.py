@@ -518,6 +518,51 @@ def dequantize_values(t: EndorTensor) -> EndorTensor:
                        negative_zero_collapsed=t.negative_zero_collapsed(), validate=False, nnz=t.nnz())
 
 
+VCODE_HEADER_BYTES = 256  # endor_vcode_header
+
+
+def encode_values(values: torch.Tensor, k_max: int = 7, pin: bool = True) -> torch.Tensor:
+    """Lossless transport coding of packed f16 values (vcode.cu; no reference
+    counterpart): low bytes raw, high bytes as k-bit dictionary codes plus an
+    exception list.  ``values`` is the uint8 view of the packed f16 values
+    (host or device); returns the blob as a (pinned) host uint8 tensor.  An
+    offline, load-time step, like ``compress``."""
+    v = values.reshape(-1).view(torch.uint8)
+    if v.numel() % 2:
+        raise InvalidArgument("f16 values must hold an even number of bytes")
+    v = v.cpu().contiguous()
+    nnz = v.numel() // 2
+    L = _lib.lib()
+    need = C.c_size_t(0)
+    check(L.endor_values_encode(_ptr(v), nnz, k_max, None, 0, C.byref(need)))
+    blob = torch.empty(need.value, dtype=torch.uint8, pin_memory=pin)
+    check(L.endor_values_encode(_ptr(v), nnz, k_max, blob.data_ptr(), blob.numel(), C.byref(need)))
+    return blob
+
+
+def vcode_info(blob: torch.Tensor) -> dict:
+    """Header fields of a coded-values blob (host tensor)."""
+    h = blob[:VCODE_HEADER_BYTES].numpy()
+    u32, u64 = h[:8].view("<u4"), h[8:56].view("<u8")
+    return {"k": int(u32[1]), "nnz": int(u64[0]), "n_exc": int(u64[1]), "blob_bytes": int(u64[5])}
+
+
+def decode_values(blob: torch.Tensor, device=None) -> torch.Tensor:
+    """Decode a coded-values blob on the GPU: returns the packed f16 values as
+    a device uint8 tensor (bit-exact with the values that were encoded)."""
+    dev = _dev(device)
+    hb = blob[:VCODE_HEADER_BYTES].cpu().contiguous()
+    L = _lib.lib()
+    check(L.endor_values_decode_host_check(hb.data_ptr()))
+    info = vcode_info(hb)
+    bd = _alloc(blob.numel(), dev)
+    bd.copy_(blob.reshape(-1).view(torch.uint8))
+    out = _alloc(info["nnz"] * 2, dev)
+    check(L.endor_cuda_values_decode(hb.data_ptr(), _ptr(bd), _ptr(out), _stream_ptr(dev)))
+    torch.cuda.synchronize(dev)
+    return out
+
+
 def _index_list(idx, dev) -> torch.Tensor:
     t = torch.as_tensor(idx, dtype=torch.int64) if not isinstance(idx, torch.Tensor) else idx
     return t.to(device=dev, dtype=torch.int64).contiguous().reshape(-1)

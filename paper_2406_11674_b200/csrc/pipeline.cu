@@ -33,6 +33,7 @@ struct endor_pipeline {
         uint8_t* bitmap = nullptr;  // ceil(max/8) rounded up
         uint8_t* values = nullptr;  // max*2 bytes
         uint64_t* prefix = nullptr; // ceil(max/1024) u64: the op's optional RankIndex at chunk 1024
+        uint8_t* coded = nullptr;   // coded-values blob (vcode.cu), allocated on the first coded op
         cudaEvent_t free_ev = nullptr;
     };
     std::vector<Slot> slots;
@@ -119,6 +120,7 @@ int endor_pipeline_destroy(endor_pipeline* p) {
         cudaFree(s.bitmap);
         cudaFree(s.values);
         cudaFree(s.prefix);
+        cudaFree(s.coded);
         cudaEventDestroy(s.free_ev);
     }
     for (auto& d : p->dense) cudaFree(d);
@@ -183,9 +185,21 @@ int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops
         const bool gemm = op.tokens > 1 && op.x_dev && op.y_dev;
         if (gemm && (deq || op.dtype != ENDOR_DTYPE_F16 || op.cols % 8 || op.dense_dev))
             return pbad("GEMM ops need an f16 W with cols % 8 == 0 and no dense_dev");
-        if (!op.path && ((n && !op.bitmap_host) || (op.nnz && !op.values_host))) return pbad("null host buffer");
+        // coded values (vcode.cu): the blob crosses the link instead of the packed values
+        const auto* vc = static_cast<const endor_vcode_header*>(op.vcode_host);
+        if (vc) {
+            if ((st = endor_values_decode_host_check(vc))) return st;
+            if (op.path || deq || op.dtype != ENDOR_DTYPE_F16 || vc->nnz != op.nnz)
+                return pbad("coded values need an f16 host op whose blob holds exactly nnz values");
+            if (vc->blob_bytes > p->max_elems * 2 + 4096) return pbad("coded-values blob larger than the staging slot");
+        }
+        if (!op.path && ((n && !op.bitmap_host) || (op.nnz && !op.values_host && !vc))) return pbad("null host buffer");
         auto& slot = p->slots[i % p->depth];
-        const size_t bmb = (n + 7) / 8, vb = op.nnz * eb;
+        if (vc && !slot.coded) {
+            PK(cudaStreamSynchronize(p->copy));
+            PK(cudaMalloc(&slot.coded, align256(p->max_elems * 2 + 4096)));
+        }
+        const size_t bmb = (n + 7) / 8, vb = vc ? size_t(vc->blob_bytes) : op.nnz * eb;
         const size_t pb = op.prefix1024_host ? (n + 1023) / 1024 * 8 : 0;
         // copy stream: wait until the slot's previous occupant was decompressed
         NvtxRange h2d_range(op.path ? "endor op: storage -> HBM" : "endor op: H2D compressed");
@@ -202,7 +216,8 @@ int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops
                 return st;
         } else {
             PK(cudaMemcpyAsync(slot.bitmap, op.bitmap_host, bmb, cudaMemcpyHostToDevice, p->copy));
-            if (vb) PK(cudaMemcpyAsync(slot.values, op.values_host, vb, cudaMemcpyHostToDevice, p->copy));
+            if (vc) PK(cudaMemcpyAsync(slot.coded, vc, vb, cudaMemcpyHostToDevice, p->copy));
+            else if (vb) PK(cudaMemcpyAsync(slot.values, op.values_host, vb, cudaMemcpyHostToDevice, p->copy));
         }
         if (pb) PK(cudaMemcpyAsync(slot.prefix, op.prefix1024_host, pb, cudaMemcpyHostToDevice, p->copy));
         const uint64_t* pre = pb ? slot.prefix : nullptr;
@@ -211,6 +226,10 @@ int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops
         NvtxRange compute_range("endor op: decompress + GEMV");
         PK(cudaStreamWaitEvent(p->compute, p->h2d_end[i], 0));
         PK(cudaEventRecord(p->dec_beg[i], p->compute));
+        if (vc) {  // blob -> packed f16 values in the slot (decode + exception patch)
+            if ((st = endor_cuda_values_decode(vc, slot.coded, slot.values, p->compute))) return st;
+            launches += vc->n_exc ? 2 : 1;
+        }
         endor_tensor_view v{op.rows, op.cols, op.dtype, 0, slot.bitmap, slot.values, op.nnz};
         // y = W x with W never observed by the caller: fused decompress -> GEMV
         // (no dense W in HBM) unless flags bit1 asks for the materialised path

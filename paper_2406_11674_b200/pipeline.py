@@ -40,6 +40,7 @@ class HostOp:
     path: Optional[str] = None             # EndorDirect: read bitmap + values from this .endor file
     tokens: int = 0                        # > 1: GEMM, x f16 [tokens, cols] -> y f32 [tokens, rows]
     prefix1024: Optional[torch.Tensor] = None  # pinned int64 RankIndex at chunk 1024 (no counting pass)
+    vcode: Optional[torch.Tensor] = None   # pinned coded-values blob (codec.encode_values): sent instead of values
 
     @property
     def compressed_bytes(self) -> int:
@@ -47,7 +48,8 @@ class HostOp:
             eb = 2 if self.dtype == 0 else 1
             return (self.rows * self.cols + 7) // 8 + self.nnz * eb
         pb = (self.rows * self.cols + 1023) // 1024 * 8 if self.prefix1024 is not None else 0
-        return self.bitmap.numel() + self.values.numel() + pb
+        vb = self.vcode.numel() if self.vcode is not None else self.values.numel()
+        return self.bitmap.numel() + vb + pb
 
     @property
     def dense_bytes(self) -> int:
@@ -90,7 +92,7 @@ class OffloadPipeline:
                                      _p(o.x), _p(o.y), _p(o.dense), _p(o.y_host),
                                      float(o.quant_scale) if deq else 0.0, 0,
                                      os.fsencode(o.path) if o.path is not None else None,
-                                     int(o.tokens), _p(o.prefix1024))
+                                     int(o.tokens), _p(o.prefix1024), _p(o.vcode))
         self._keep = (arr, ops)
         check(self._lib.endor_pipeline_run(self._h, arr, len(ops), 1 if sync else 0))
 

@@ -42,7 +42,7 @@ def test_library_exports_every_declared_symbol(L):
 
 
 def test_abi_and_geometry(L):
-    assert L.endor_cuda_abi_version() == 3
+    assert L.endor_cuda_abi_version() == 4
     assert L.endor_cuda_tile_elems() == 8192
     assert L.endor_cuda_status_name(2) == b"CorruptionError"
     assert L.endor_cuda_status_name(1) == b"SizeError"

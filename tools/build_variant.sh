@@ -8,7 +8,7 @@ root=$(cd "$(dirname "$0")/.." && pwd)
 out=$root/tools/_build/var_$name
 mkdir -p "$out"
 objs=()
-for src in scan expand extract fixtures gemv gemv_fused gemm_fused capi pipeline storage; do
+for src in scan expand extract fixtures gemv gemv_fused gemm_fused capi pipeline storage vcode; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2 \
     --expt-relaxed-constexpr -I"$root/include" -I"$root/paper_2406_11674_b200/csrc" "$@" \
     -c "$root/paper_2406_11674_b200/csrc/$src.cu" -o "$out/$src.o" &
