@@ -64,6 +64,16 @@ int integration_example(uint64_t rows, uint64_t cols, uint64_t nnz, const void* 
     op.x_dev = d_x;
     op.y_dev = d_y;
     op.path = path;
+    size_t nb = 0;
+    st |= endor_values_encode(h_values, nnz, 7, NULL, 0, &nb);
+    void* blob = endor_host_alloc(nb);
+    st |= endor_values_encode(h_values, nnz, 7, blob, nb, &nb);
+    endor_pipeline_op cop = ops[0];
+    cop.values_host = NULL;
+    cop.vcode_host = blob;
+    st |= endor_cuda_values_decode(blob, d_dense, d_vals_out, stream);
+    st |= endor_pipeline_run(p, &cop, 1, 1);
+    endor_host_free(blob);
     st |= endor_reader_destroy(r);
     st |= endor_pipeline_destroy(p);
     return st + (int)op.rows;
