@@ -476,7 +476,7 @@ typedef struct endor_pipeline_op {
                                 u64, built once at load time like the compression): copied
                                 with the op, so the decompress / fused GEMV / GEMM run no
                                 counting pass */
-    const void* vcode_host;  /* optional pinned coded-values blob (endor_values_encode) of this
+    const void* vcode_host;  /* optional coded-values blob in pinned HOST memory (endor_values_encode) of this
                                 op's f16 values: crosses the link instead of values_host and is
                                 decoded on the compute stream before the decompress / GEMV */
 } endor_pipeline_op;

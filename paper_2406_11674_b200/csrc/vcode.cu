@@ -20,6 +20,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <exception>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -142,10 +144,8 @@ void parallel_groups(uint64_t groups, int nt, F f) {
 
 }  // namespace
 
-extern "C" {
-
-int endor_values_encode(const void* values_f16, uint64_t nnz, int k_max, void* blob_out, size_t blob_cap,
-                        size_t* blob_bytes) {
+static int values_encode(const void* values_f16, uint64_t nnz, int k_max, void* blob_out, size_t blob_cap,
+                         size_t* blob_bytes) {
     if (!blob_bytes) return set_last_error(ENDOR_ERR_INVALID_ARGUMENT, "null blob_bytes");
     if (k_max < 1 || k_max > kMaxK) return set_last_error(ENDOR_ERR_INVALID_ARGUMENT, "k_max must be 1..7");
     if (nnz && !values_f16) return set_last_error(ENDOR_ERR_INVALID_ARGUMENT, "null values");
@@ -225,6 +225,17 @@ int endor_values_encode(const void* values_f16, uint64_t nnz, int k_max, void* b
         exc += ex.size() * 8;
     }
     return ENDOR_OK;
+}
+
+extern "C" {
+
+int endor_values_encode(const void* values_f16, uint64_t nnz, int k_max, void* blob_out, size_t blob_cap,
+                        size_t* blob_bytes) {
+    try {  // worker threads and buffers: no C++ exception crosses the C ABI
+        return values_encode(values_f16, nnz, k_max, blob_out, blob_cap, blob_bytes);
+    } catch (const std::exception& e) {
+        return set_last_error(ENDOR_ERR_CUDA, (std::string("host encoder: ") + e.what()).c_str());
+    }
 }
 
 int endor_values_decode_host_check(const void* header_host) {
