@@ -513,14 +513,14 @@ def run_ours(args):
                 "speedup_vs_f16_endor": round(e2e_step / c_ms, 3),
                 "values_bytes_raw": vals_raw, "values_bytes_coded": vals_coded,
                 "values_ratio": round(vals_coded / vals_raw, 4),
-                "code_bits": [E.vcode_info(bl)["k"] for bl in blobs],
+                "modes": [E.vcode_info(bl)["mode"] for bl in blobs],
                 "decode_plus_fused_gemv_ms_per_step": round(sc["decompress_ms"] / args.steps, 4),
                 "exposed_compute_ms_per_run": round(sc["exposed_compute_ms"], 4),
                 "host_encode_s_per_layer": round(enc_s, 3),
                 "y_bit_exact_vs_raw_values": y_same,
-                "note": "lossless (csrc/vcode.cu): values' high bytes as k-bit dictionary codes + exceptions, "
-                        "low bytes raw; the ratio depends on the weights' exponent spread (reference synth_weight "
-                        "here)"}
+                "note": "lossless (csrc/vcode.cu): values' high bytes as a chunked canonical Huffman stream (or "
+                        "k-bit dictionary codes + exceptions, whichever is smaller), low bytes raw; the ratio depends "
+                        "on the weights' exponent spread (reference synth_weight here)"}
         # the same layer with the load-time RankIndex shipped per op (prefix1024_host):
         # the fused decompress -> GEMV runs no counting / flatten pass
         if not args.no_extras:

@@ -521,10 +521,11 @@ def dequantize_values(t: EndorTensor) -> EndorTensor:
 VCODE_HEADER_BYTES = 256  # endor_vcode_header
 
 
-def encode_values(values: torch.Tensor, k_max: int = 7, pin: bool = True) -> torch.Tensor:
+def encode_values(values: torch.Tensor, k_max: int = 0, pin: bool = True) -> torch.Tensor:
     """Lossless transport coding of packed f16 values (vcode.cu; no reference
     counterpart): low bytes raw, high bytes as k-bit dictionary codes plus an
-    exception list.  ``values`` is the uint8 view of the packed f16 values
+    exception list (k_max 1..7), or -- k_max 0, automatic -- a chunked
+    canonical Huffman stream of the high bytes when that is smaller.  ``values`` is the uint8 view of the packed f16 values
     (host or device); returns the blob as a (pinned) host uint8 tensor.  An
     offline, load-time step, like ``compress``."""
     v = values.reshape(-1).view(torch.uint8)
@@ -544,7 +545,8 @@ def vcode_info(blob: torch.Tensor) -> dict:
     """Header fields of a coded-values blob (host tensor)."""
     h = blob[:VCODE_HEADER_BYTES].numpy()
     u32, u64 = h[:8].view("<u4"), h[8:56].view("<u8")
-    return {"k": int(u32[1]), "nnz": int(u64[0]), "n_exc": int(u64[1]), "blob_bytes": int(u64[5])}
+    mode = "huffman" if int(u32[0]) == 0x31485645 else "fixed"
+    return {"mode": mode, "k": int(u32[1]), "nnz": int(u64[0]), "n_exc": int(u64[1]), "blob_bytes": int(u64[5])}
 
 
 def decode_values(blob: torch.Tensor, device=None) -> torch.Tensor:

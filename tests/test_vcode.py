@@ -16,10 +16,35 @@ from paper_2406_11674_b200 import _lib
 from paper_2406_11674_b200 import codec as E
 
 
+def decode_huff_np(blob: np.ndarray) -> np.ndarray:
+    """Huffman mode ("EVH1"): chunks of 512 values, each from its own word
+    offset, decoded LSB-first through the blob's 4096-entry table."""
+    u64 = blob[8:56].view("<u8")
+    nnz, words, lo_off, offs_off, stream_off, nbytes = map(int, u64)
+    assert nbytes == blob.size == stream_off + (4 * words + 15) // 16 * 16 and int(blob[4:8].view("<u4")[0]) == 12
+    lut = blob[256:256 + 8192].view("<u2")
+    lo = blob[lo_off:lo_off + nnz].astype(np.uint16)
+    nch = (nnz + 511) // 512
+    offs = blob[offs_off:offs_off + 4 * (nch + 1)].view("<u4")
+    stream = blob[stream_off:stream_off + 4 * words].view("<u4")
+    assert offs[0] == 0 and offs[-1] == words and np.all(np.diff(offs.astype(np.int64)) >= 0)
+    hi = np.zeros(nnz, np.uint16)
+    for c in range(nch):
+        bits = int.from_bytes(stream[offs[c]:offs[c + 1]].tobytes(), "little")
+        for i in range(c * 512, min(nnz, c * 512 + 512)):
+            e = int(lut[bits & 0xFFF])
+            assert e >> 8, "unassigned table entry"
+            hi[i] = e & 0xFF
+            bits >>= e >> 8
+    return (lo | (hi << 8)).astype(np.uint16)
+
+
 def decode_np(blob: np.ndarray) -> np.ndarray:
     """The blob format of include/endor_cuda.h (endor_vcode_header), restated."""
     u32 = blob[:8].view("<u4")
     u64 = blob[8:56].view("<u8")
+    if u32[0] == 0x31485645:
+        return decode_huff_np(blob)
     assert u32[0] == 0x31435645
     k, nnz, n_exc, lo_off, code_off, exc_off, nbytes = int(u32[1]), *map(int, u64)
     dic = blob[64:192]
@@ -37,7 +62,7 @@ def decode_np(blob: np.ndarray) -> np.ndarray:
     return (lo | (hi << 8)).astype(np.uint16)
 
 
-def encode(vals_u16: np.ndarray, k_max: int = 7) -> np.ndarray:
+def encode(vals_u16: np.ndarray, k_max: int = 0) -> np.ndarray:
     L = _lib.lib()
     v = np.ascontiguousarray(vals_u16.astype(np.uint16))
     need = C.c_size_t(0)
@@ -69,11 +94,20 @@ CASES = {
 }
 
 
+@pytest.mark.parametrize("k_max", [0, 7])
 @pytest.mark.parametrize("name", sorted(CASES))
-def test_encode_round_trip_numpy(name):
+def test_encode_round_trip_numpy(name, k_max):
     v = CASES[name]
-    blob = encode(v)
+    blob = encode(v, k_max)
     assert np.array_equal(decode_np(blob), v)
+
+
+def test_automatic_mode_picks_the_smaller_blob():
+    for name, v in CASES.items():
+        auto, fixed = encode(v, 0), encode(v, 7)
+        assert auto.size <= fixed.size, name
+    v = CASES["pruned_100k"]
+    assert int(encode(v, 0)[:4].view("<u4")[0]) == 0x31485645  # Huffman wins on pruned weights
 
 
 @pytest.mark.parametrize("k_max", [1, 2, 3, 5, 7])
@@ -87,14 +121,15 @@ def test_k_max_bounds_code_width(k_max):
 def test_pruned_weights_shrink():
     # the high byte of pruned (Gaussian) weights is low-entropy: the blob beats 2 B per value
     v = CASES["pruned_100k"]
-    blob = encode(v)
+    blob = encode(v, 7)
     assert blob.size < 0.85 * 2 * v.size
     assert int(blob[4:8].view("<u4")[0]) <= 6
+    assert encode(v).size < encode(v, 7).size  # Huffman: near the high byte entropy (3.95 bits here) + an 8 KiB table
 
 
 def test_single_high_byte_is_one_bit_without_exceptions():
     v = CASES["one_hi_byte"]
-    blob = encode(v)
+    blob = encode(v, 7)
     u64 = blob[8:56].view("<u8")
     assert int(blob[4:8].view("<u4")[0]) == 1 and int(u64[1]) == 0
 
@@ -109,8 +144,14 @@ def test_header_check_and_arguments():
         assert L.endor_values_decode_host_check(bad.ctypes.data) == 2  # CORRUPTION
     need = C.c_size_t(0)
     v = CASES["pruned_1000"]
-    assert L.endor_values_encode(v.ctypes.data, v.size, 0, None, 0, C.byref(need)) == 4
+    assert L.endor_values_encode(v.ctypes.data, v.size, -1, None, 0, C.byref(need)) == 4
     assert L.endor_values_encode(v.ctypes.data, v.size, 8, None, 0, C.byref(need)) == 4
+    hb = encode(CASES["pruned_100k"])  # Huffman header: recomputed offsets too
+    assert L.endor_values_decode_host_check(hb.ctypes.data) == 0
+    for off in (4, 16, 40):  # LUT width, stream words, stream offset
+        bad = hb.copy()
+        bad[off] ^= 0x01
+        assert L.endor_values_decode_host_check(bad.ctypes.data) == 2
     small = np.zeros(16, np.uint8)
     assert L.endor_values_encode(v.ctypes.data, v.size, 7, small.ctypes.data, small.size, C.byref(need)) == 4
 
@@ -118,22 +159,23 @@ def test_header_check_and_arguments():
 # ---- GPU: the decoder and the pipeline ----------------------------------------
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("k_max", [0, 7])
 @pytest.mark.parametrize("name", sorted(CASES))
-def test_gpu_decode_bit_exact(name):
+def test_gpu_decode_bit_exact(name, k_max):
     v = CASES[name]
-    blob = torch.from_numpy(encode(v))
+    blob = torch.from_numpy(encode(v, k_max))
     out = E.decode_values(blob)
     assert np.array_equal(out.cpu().numpy().view(np.uint16), v)
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("k_max", [1, 3, 7])
+@pytest.mark.parametrize("k_max", [0, 1, 3, 7])
 def test_gpu_decode_large_with_exceptions(k_max):
     rng = np.random.default_rng(11)
     v = pruned_f16((1 << 22) + 5, 12)
     v[rng.integers(0, v.size, 5000)] = rng.integers(0, 1 << 16, 5000, dtype=np.uint16)  # rare high bytes
     blob = torch.from_numpy(encode(v, k_max))
-    assert E.vcode_info(blob)["n_exc"] > 0
+    assert E.vcode_info(blob)["n_exc"] > 0  # exceptions (fixed k) / stream words (Huffman)
     assert np.array_equal(E.decode_values(blob).cpu().numpy().view(np.uint16), v)
 
 

@@ -45,7 +45,7 @@ for i, o in enumerate(catalog.model_catalog("opt-66b").ops):
     ok = torch.equal(out[: t.nnz() * 2].cpu(), t.values.cpu())
     m = sorted(ms)[len(ms) // 2]
     alg = blob.numel() + t.nnz() * 2
-    rows.append({"op": o.name, "nnz": t.nnz(), "k": info["k"], "n_exc": info["n_exc"],
+    rows.append({"op": o.name, "nnz": t.nnz(), "mode": info["mode"], "k": info["k"], "n_exc": info["n_exc"],
                  "ratio": round(blob.numel() / (2 * t.nnz()), 4), "encode_s": round(enc, 3),
                  "decode_ms": round(m, 4), "decode_gbs": round(alg / (m * 1e-3) / 1e9, 1),
                  "frac_of_peak": round(alg / (m * 1e-3) / 1e9 / PEAK, 3), "bit_exact": ok})
