@@ -177,28 +177,38 @@ __global__ void __launch_bounds__(kHuffThreads) vcode_huff_kernel(const uint16_t
         uint32_t nb = 0;
         const uint64_t v0 = c * kHuffChunk;
         const uint32_t cnt = uint32_t(umin64(kHuffChunk, nnz - v0));
-        for (uint32_t j = 0; j < cnt; j += 4) {
-            uint32_t hi4 = 0;
+        // low bytes 16 at a time, the next 16 loaded one block (16 symbols) ahead
+        const uint4* lo4 = reinterpret_cast<const uint4*>(lo + v0);
+        uint4 cur = __ldg(lo4);
+        for (uint32_t j = 0; j < cnt; j += 16) {
+            const uint4 nxt = j + 16 < cnt ? __ldg(lo4 + j / 16 + 1) : make_uint4(0, 0, 0, 0);
+            const uint32_t lw[4] = {cur.x, cur.y, cur.z, cur.w};
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (nb < uint32_t(kHuffBits)) {
-                    buf |= uint64_t(p < pend ? src[p] : 0u) << nb;
-                    ++p;
-                    nb += 32;
+            for (int s4 = 0; s4 < 4; ++s4) {
+                const uint32_t jj = j + 4 * s4;
+                if (jj >= cnt) break;
+                uint32_t hi4 = 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (nb < uint32_t(kHuffBits)) {
+                        buf |= uint64_t(p < pend ? src[p] : 0u) << nb;
+                        ++p;
+                        nb += 32;
+                    }
+                    const uint32_t en = lut[buf & ((1u << kHuffBits) - 1u)], len = en >> 8;
+                    buf >>= len;
+                    nb -= len;
+                    hi4 |= (en & 0xFFu) << (8 * q);
                 }
-                const uint32_t en = lut[buf & ((1u << kHuffBits) - 1u)], len = en >> 8;
-                buf >>= len;
-                nb -= len;
-                hi4 |= (en & 0xFFu) << (8 * q);
+                const uint2 o = make_uint2(__byte_perm(lw[s4], hi4, 0x5140), __byte_perm(lw[s4], hi4, 0x7362));
+                if (jj + 4 <= cnt) {
+                    *reinterpret_cast<uint2*>(out + v0 + jj) = o;
+                } else {
+                    for (uint32_t q = 0; q < cnt - jj; ++q)
+                        out[v0 + jj + q] = uint16_t((q < 2 ? o.x : o.y) >> (16 * (q & 1)));
+                }
             }
-            const uint32_t l4 = __ldg(reinterpret_cast<const uint32_t*>(lo + v0 + j));
-            const uint2 o = make_uint2(__byte_perm(l4, hi4, 0x5140), __byte_perm(l4, hi4, 0x7362));
-            if (j + 4 <= cnt) {
-                *reinterpret_cast<uint2*>(out + v0 + j) = o;
-            } else {
-                for (uint32_t q = 0; q < cnt - j; ++q)
-                    out[v0 + j + q] = uint16_t((q < 2 ? o.x : o.y) >> (16 * (q & 1)));
-            }
+            cur = nxt;
         }
     }
 }
