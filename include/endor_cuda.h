@@ -305,8 +305,15 @@ typedef struct endor_vcode_header {
 } endor_vcode_header;
 
 /* Encode nnz packed f16 values (host memory) into a blob.  blob_out == NULL:
- * only *blob_bytes is computed (size query).  k_max (1..7) bounds the code
- * width.  Multi-threaded on the host; an offline, load-time step like compress. */
+ * only *blob_bytes is computed (size query).  k_max 1..7: the fixed-width
+ * dictionary code above with at most k_max bits; k_max 0: automatic -- that,
+ * or a Huffman blob ("EVH1", magic 0x31485645) when smaller: the high bytes
+ * as a canonical Huffman stream (codes <= 12 bits, LSB first) in chunks of 512
+ * values, each starting on a u32 word.  EVH1 layout: header (k = 12, n_exc =
+ * stream words) | 4096 x u16 decode table (symbol | length << 8, indexed by
+ * the next 12 stream bits) | lo (nnz, padded to 32) | chunk word offsets (u32
+ * x (chunks + 1), padded to 16) | stream (zero-padded to 16 bytes).
+ * Multi-threaded on the host; an offline, load-time step like compress. */
 int endor_values_encode(const void* values_f16, uint64_t nnz, int k_max, void* blob_out, size_t blob_cap,
                         size_t* blob_bytes);
 /* Validate a blob header (host copy): magic, k, and offsets recomputed from
