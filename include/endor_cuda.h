@@ -313,7 +313,9 @@ typedef struct endor_vcode_header {
  * stream words) | 4096 x u16 decode table (symbol | length << 8, indexed by
  * the next 12 stream bits) | lo (nnz, padded to 32) | chunk word offsets (u32
  * x (chunks + 1), padded to 16) | stream (zero-padded to 16 bytes).
- * Multi-threaded on the host; an offline, load-time step like compress. */
+ * The blob is not capped at the raw size: ship it only when *blob_bytes < 2 nnz
+ * (incompressible high bytes make it larger).  Multi-threaded on the host; an
+ * offline, load-time step like compress. */
 int endor_values_encode(const void* values_f16, uint64_t nnz, int k_max, void* blob_out, size_t blob_cap,
                         size_t* blob_bytes);
 /* Validate a blob header (host copy): magic, k, and offsets recomputed from

@@ -527,7 +527,8 @@ def encode_values(values: torch.Tensor, k_max: int = 0, pin: bool = True) -> tor
     exception list (k_max 1..7), or -- k_max 0, automatic -- a chunked
     canonical Huffman stream of the high bytes when that is smaller.  ``values`` is the uint8 view of the packed f16 values
     (host or device); returns the blob as a (pinned) host uint8 tensor.  An
-    offline, load-time step, like ``compress``."""
+    offline, load-time step, like ``compress``.  The blob can be larger than
+    the raw values (incompressible high bytes): ship it only when smaller."""
     v = values.reshape(-1).view(torch.uint8)
     if v.numel() % 2:
         raise InvalidArgument("f16 values must hold an even number of bytes")
