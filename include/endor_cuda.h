@@ -398,7 +398,7 @@ int endor_cuda_gemm_compressed(const endor_tensor_view* t, const uint64_t* prefi
 
 typedef struct endor_file_info {
     uint64_t rows, cols, nnz;
-    int32_t dtype, flags;          /* flags bit0 quantized, bit1 negative-zero collapsed */
+    int32_t dtype, flags;          /* flags bit0 quantized, bit1 negative-zero collapsed, bit2 coded values (v3) */
     float quant_scale;             /* flags bit0 */
     uint32_t crc;                  /* stored CRC-32 (IEEE, zlib) of every preceding byte */
     uint32_t header_crc;           /* CRC-32 of the header bytes alone */
@@ -413,6 +413,15 @@ typedef struct endor_file_info {
  * the same fields with the bitmap at byte 4096 and the values at the next 4 KiB
  * boundary, zero fill in between, CRC-32 over every preceding byte -- aligned
  * file offsets, which a GPUDirect Storage DMA needs; nonzero fill is Malformed). */
+/* v3 container (no reference counterpart): the v2 layout with flags bit 2 set
+ * and the values section holding a coded-values blob of the f16 values
+ * (endor_values_encode; not quantized): fewer bytes leave storage, and
+ * endor_reader_read decodes them on the GPU after the CRC / padding / popcount
+ * checks, so values_dev must hold nnz * 2 bytes.  endor_file_probe reports the
+ * blob's length as values_bytes.  Returns the container size (0 on a bad
+ * argument or a blob that does not hold nnz values). */
+size_t endor_file_encode_v3(uint64_t rows, uint64_t cols, int32_t flags, const void* bitmap, const void* blob,
+                            uint64_t nnz, void* out, size_t out_cap);
 int endor_file_probe(const char* path, endor_file_info* out);
 int endor_cuda_last_format_kind(void);
 

@@ -111,6 +111,7 @@ SIGNATURES = {
     "endor_file_probe": (C.c_int, [C.c_char_p, C.POINTER(FileInfo)]),
     "endor_file_encode": (_sz, [_u64, _u64, _i32, _i32, C.c_float, _vp, _vp, _u64, _vp, _sz]),
     "endor_file_encode_v2": (_sz, [_u64, _u64, _i32, _i32, C.c_float, _vp, _vp, _u64, _vp, _sz]),
+    "endor_file_encode_v3": (_sz, [_u64, _u64, _i32, _vp, _vp, _u64, _vp, _sz]),
     "endor_reader_create": (C.c_int, [C.c_int, _sz, C.c_int, C.POINTER(_vp)]),
     "endor_reader_destroy": (C.c_int, [_vp]),
     "endor_reader_mode": (C.c_int, [_vp]),

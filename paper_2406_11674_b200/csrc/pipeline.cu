@@ -199,7 +199,8 @@ int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops
             PK(cudaStreamSynchronize(p->copy));
             PK(cudaMalloc(&slot.coded, align256(p->max_elems * 2 + 4096)));
         }
-        const size_t bmb = (n + 7) / 8, vb = vc ? size_t(vc->blob_bytes) : op.nnz * eb;
+        const size_t bmb = (n + 7) / 8;
+        size_t vb = vc ? size_t(vc->blob_bytes) : op.nnz * eb;  // bytes that cross the link / leave storage
         const size_t pb = op.prefix1024_host ? (n + 1023) / 1024 * 8 : 0;
         // copy stream: wait until the slot's previous occupant was decompressed
         NvtxRange h2d_range(op.path ? "endor op: storage -> HBM" : "endor op: H2D compressed");
@@ -214,6 +215,7 @@ int endor_pipeline_run(endor_pipeline* p, const endor_pipeline_op* ops, int nops
             if (!p->reader && (st = endor_reader_create(p->device, 0, ENDOR_IO_AUTO, &p->reader))) return st;
             if ((st = endor_reader_read(p->reader, op.path, &fi, slot.bitmap, slot.values, 0, nullptr, 0, p->copy)))
                 return st;
+            vb = fi.values_bytes;  // v3 containers: the coded section
         } else {
             PK(cudaMemcpyAsync(slot.bitmap, op.bitmap_host, bmb, cudaMemcpyHostToDevice, p->copy));
             if (vc) PK(cudaMemcpyAsync(slot.coded, vc, vb, cudaMemcpyHostToDevice, p->copy));

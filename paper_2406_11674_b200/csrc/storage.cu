@@ -293,6 +293,8 @@ struct endor_reader {
     uint32_t* crc_scratch = nullptr;
     size_t crc_cap = 0;  // u32 entries
     uint32_t* crc_out = nullptr;  // 2 section CRCs
+    uint8_t* coded = nullptr;     // v3: the coded-values section before decoding
+    size_t coded_cap = 0;
     double seconds = 0;
     uint64_t bytes = 0;
 };
@@ -306,28 +308,31 @@ int endor_cuda_last_format_kind(void) { return g_format_kind; }
 // v1 (file_io.hpp:187-210, byte-identical) and v2 (the same fields, sections at
 // 4 KiB boundaries, zero fill between them: a GDS DMA target needs aligned file
 // offsets; the reference reads v1 only)
+// v3 (no reference counterpart): the v2 layout with flags bit 2 set and the
+// values section holding a coded-values blob (vcode.cu) of the f16 values --
+// fewer bytes from storage, decoded on the GPU after the read.
 static size_t encode_container(int version, uint64_t rows, uint64_t cols, int32_t dtype, int32_t flags,
                                float quant_scale, const void* bitmap, const void* values, uint64_t nnz, void* out,
-                               size_t out_cap) {
+                               size_t out_cap, uint64_t values_len = 0) {
     const int eb = dtype == ENDOR_DTYPE_F16 ? 2 : (dtype == ENDOR_DTYPE_I8 ? 1 : 0);
     if (!eb || (rows && cols > UINT64_MAX / rows) || nnz > rows * cols) return 0;
     const bool q = flags & 1;
-    const uint64_t n = rows * cols, bm = (n + 7) / 8, vb = nnz * eb;
+    const uint64_t n = rows * cols, bm = (n + 7) / 8, vb = version == 3 ? values_len : nnz * eb;
     const size_t hdr = 32 + (q ? 4 : 0);
-    const size_t boff = version == 2 ? kV2Align : hdr;
-    const size_t voff = version == 2 ? boff + ((bm + kV2Align - 1) & ~uint64_t(kV2Align - 1)) : boff + bm;
+    const size_t boff = version >= 2 ? kV2Align : hdr;
+    const size_t voff = version >= 2 ? boff + ((bm + kV2Align - 1) & ~uint64_t(kV2Align - 1)) : boff + bm;
     const size_t total = voff + vb + 4;
     if (!out) return total;
     if (out_cap < total || (bm && !bitmap) || (vb && !values)) return 0;
     uint8_t* o = static_cast<uint8_t*>(out);
-    if (version == 2) memset(o, 0, voff);  // zero fill of the header page and the bitmap's last page
+    if (version >= 2) memset(o, 0, voff);  // zero fill of the header page and the bitmap's last page
     memcpy(o, "ENDR", 4);
     auto put = [&](size_t at, uint64_t v, int nb) {
         for (int i = 0; i < nb; ++i) o[at + i] = uint8_t(v >> (8 * i));
     };
     put(4, uint64_t(version), 2);  // file_io.hpp:189-199
     o[6] = uint8_t(dtype);
-    o[7] = uint8_t(flags & 3);
+    o[7] = uint8_t((flags & 3) | (version == 3 ? 4 : 0));
     put(8, rows, 8);
     put(16, cols, 8);
     put(24, nnz, 8);
@@ -354,6 +359,14 @@ size_t endor_file_encode_v2(uint64_t rows, uint64_t cols, int32_t dtype, int32_t
     return encode_container(2, rows, cols, dtype, flags, quant_scale, bitmap, values, nnz, out, out_cap);
 }
 
+size_t endor_file_encode_v3(uint64_t rows, uint64_t cols, int32_t flags, const void* bitmap, const void* blob,
+                            uint64_t nnz, void* out, size_t out_cap) {
+    const auto* h = static_cast<const endor_vcode_header*>(blob);
+    if (!h || (flags & 1) || endor_values_decode_host_check(h) != ENDOR_OK || h->nnz != nnz) return 0;
+    return encode_container(3, rows, cols, ENDOR_DTYPE_F16, flags, 0.f, bitmap, blob, nnz, out, out_cap,
+                            h->blob_bytes);
+}
+
 int endor_file_probe(const char* path, endor_file_info* out) {
     g_format_kind = -1;
     if (!path || !out) return set_last_error(ENDOR_ERR_INVALID_ARGUMENT, "null path or output");
@@ -374,11 +387,13 @@ int endor_file_probe(const char* path, endor_file_info* out) {
     if (!need(4)) st = fmt_fail(ENDOR_FMT_TRUNCATED, "file ends mid-field");
     else if (memcmp(h, "ENDR", 4) != 0) st = fmt_fail(ENDOR_FMT_BAD_MAGIC, "not an .endor container");
     else if (!need(6)) st = fmt_fail(ENDOR_FMT_TRUNCATED, "file ends mid-field");
-    else if (le(h + 4, 2) != 1 && le(h + 4, 2) != 2) st = fmt_fail(ENDOR_FMT_BAD_VERSION, "unsupported container version");
+    else if (le(h + 4, 2) < 1 || le(h + 4, 2) > 3) st = fmt_fail(ENDOR_FMT_BAD_VERSION, "unsupported container version");
     else if (!need(7)) st = fmt_fail(ENDOR_FMT_TRUNCATED, "file ends mid-field");
     else if (h[6] > 1) st = fmt_fail(ENDOR_FMT_MALFORMED, "unknown dtype code");
     else if (!need(8)) st = fmt_fail(ENDOR_FMT_TRUNCATED, "file ends mid-field");
-    else if (h[7] & ~3u) st = fmt_fail(ENDOR_FMT_MALFORMED, "unknown flag bits set");
+    else if (h[7] & ~(le(h + 4, 2) == 3 ? 7u : 3u)) st = fmt_fail(ENDOR_FMT_MALFORMED, "unknown flag bits set");
+    else if (le(h + 4, 2) == 3 && ((h[7] & 5u) != 4u || h[6] != ENDOR_DTYPE_F16))
+        st = fmt_fail(ENDOR_FMT_MALFORMED, "a v3 container holds coded f16 values (flags bit 2, not quantized)");
     else if (!need(32 + ((h[7] & 1) ? 4 : 0))) st = fmt_fail(ENDOR_FMT_TRUNCATED, "file ends mid-field");
     if (st == ENDOR_OK) {
         f.dtype = h[6];
@@ -387,7 +402,7 @@ int endor_file_probe(const char* path, endor_file_info* out) {
         f.cols = le(h + 16, 8);
         f.nnz = le(h + 24, 8);
         const uint64_t hdr = 32 + ((f.flags & 1) ? 4 : 0);
-        const bool v2 = le(h + 4, 2) == 2;
+        const bool v2 = le(h + 4, 2) >= 2, v3 = le(h + 4, 2) == 3;
         if (f.flags & 1) {
             const uint32_t bits = uint32_t(le(h + 32, 4));
             memcpy(&f.quant_scale, &bits, 4);
@@ -409,8 +424,21 @@ int endor_file_probe(const char* path, endor_file_info* out) {
             const bool wraps = f.nnz > UINT64_MAX / eb || f.values_offset < hdr ||
                                f.nnz * eb > UINT64_MAX - f.values_offset - 4;
             f.values_bytes = wraps ? 0 : f.nnz * eb;
+            if (v3 && !wraps) {  // the values section is a coded-values blob: its header gives the length
+                endor_vcode_header vh{};
+                if (pread(fd, &vh, sizeof(vh), off_t(f.values_offset)) != ssize_t(sizeof(vh)))
+                    st = fmt_fail(ENDOR_FMT_TRUNCATED, "file shorter than declared layout");
+                else if (endor_values_decode_host_check(&vh) != ENDOR_OK || vh.nnz != f.nnz ||
+                         vh.blob_bytes > UINT64_MAX - f.values_offset - 4)
+                    st = fmt_fail(ENDOR_FMT_MALFORMED, "coded-values section header is inconsistent");
+                else
+                    f.values_bytes = vh.blob_bytes;
+            }
             f.file_bytes = wraps ? UINT64_MAX : f.values_offset + f.values_bytes + 4;
-            if (wraps || size < f.file_bytes) st = fmt_fail(ENDOR_FMT_TRUNCATED, "file shorter than declared layout");
+            if (st != ENDOR_OK)
+                ;  // the coded-values header already failed
+            else if (wraps || size < f.file_bytes)
+                st = fmt_fail(ENDOR_FMT_TRUNCATED, "file shorter than declared layout");
             else if (size > f.file_bytes)
                 st = fmt_fail(ENDOR_FMT_MALFORMED, "trailing bytes after declared layout");
             else {
@@ -486,6 +514,7 @@ int endor_reader_destroy(endor_reader* r) {
     }
     cudaFree(r->crc_tab);
     cudaFree(r->crc_scratch);
+    cudaFree(r->coded);
     cudaFree(r->crc_out);
     delete r;
     return ENDOR_OK;
@@ -563,6 +592,18 @@ static int read_posix(endor_reader* r, int fd, uint64_t off, uint64_t len, uint8
     return st;
 }
 
+// v3: a verified coded-values section in device memory -> nnz f16 values
+static int decode_section(const void* blob_dev, void* values_dev, cudaStream_t s) {
+    endor_vcode_header h{};
+    cudaError_t e;
+    if ((e = cudaMemcpyAsync(&h, blob_dev, sizeof(h), cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(s)) != cudaSuccess)
+        return set_last_error(ENDOR_ERR_CUDA, cudaGetErrorString(e));
+    if (endor_values_decode_host_check(&h) != ENDOR_OK)
+        return fmt_fail(ENDOR_FMT_MALFORMED, "coded-values section header is inconsistent");
+    return endor_cuda_values_decode(&h, blob_dev, values_dev, s);
+}
+
 int endor_reader_read(endor_reader* r, const char* path, const endor_file_info* f, void* bitmap_dev,
                       void* values_dev, int verify, void* ws, size_t ws_bytes, void* stream) {
     g_format_kind = -1;
@@ -572,6 +613,22 @@ int endor_reader_read(endor_reader* r, const char* path, const endor_file_info* 
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaError_t e = cudaSetDevice(r->device);
     if (e != cudaSuccess) return set_last_error(ENDOR_ERR_CUDA, cudaGetErrorString(e));
+    // v3: the values section (a coded-values blob) lands in reader scratch and is
+    // decoded into values_dev (nnz f16 values) after the checks
+    const bool coded = (f->flags & 4) != 0;
+    void* const values_out = values_dev;
+    if (coded) {
+        if (f->values_bytes > r->coded_cap) {
+            if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return set_last_error(ENDOR_ERR_CUDA, cudaGetErrorString(e));
+            cudaFree(r->coded);
+            r->coded = nullptr;
+            r->coded_cap = 0;
+            if ((e = cudaMalloc(&r->coded, f->values_bytes + 16)) != cudaSuccess)
+                return set_last_error(ENDOR_ERR_CUDA, cudaGetErrorString(e));
+            r->coded_cap = f->values_bytes;
+        }
+        values_dev = r->coded;
+    }
     const double t0 = now_s();
     int st = ENDOR_OK;
     if (r->mode == ENDOR_IO_POSIX) {
@@ -613,7 +670,8 @@ int endor_reader_read(endor_reader* r, const char* path, const endor_file_info* 
     }
     r->seconds += now_s() - t0;
     r->bytes += f->bitmap_bytes + f->values_bytes;
-    if (st || !verify) return st;
+    if (st) return st;
+    if (!verify) return coded ? decode_section(values_dev, values_out, s) : ENDOR_OK;
 
     // ---- decode_endor's remaining checks on the device copy (file_io.hpp:253-270) ----
     const uint64_t mb = (f->bitmap_bytes + kCrcChunk - 1) / kCrcChunk, mv = (f->values_bytes + kCrcChunk - 1) / kCrcChunk;
@@ -659,7 +717,7 @@ int endor_reader_read(endor_reader* r, const char* path, const endor_file_info* 
         if ((st2 = endor_cuda_sync_status(ws, stream))) return st2;
         if (total != f->nnz) return fmt_fail(ENDOR_FMT_COUNT_MISMATCH, "nnz field disagrees with bitmap popcount");
     }
-    return ENDOR_OK;
+    return coded ? decode_section(values_dev, values_out, s) : ENDOR_OK;
 }
 
 }  // extern "C"

@@ -18,7 +18,7 @@ from typing import Optional
 import torch
 
 from . import _lib
-from .codec import Bitmap, Dtype, EndorTensor, _dev, _stream_ptr, check, workspace
+from .codec import Bitmap, Dtype, EndorTensor, _dev, _stream_ptr, check, encode_values, workspace
 
 MODES = {0: "auto", 1: "gds", 2: "cufile-compat", 3: "posix-odirect"}
 
@@ -32,11 +32,23 @@ def probe(path: str) -> _lib.FileInfo:
 
 def encode_endor(t: EndorTensor, version: int = 1) -> bytes:
     """encode_endor (file_io.hpp:187-210): byte-identical container bytes
-    (version 2: the same container with 4 KiB-aligned sections, for GDS)."""
+    (version 2: the same container with 4 KiB-aligned sections, for GDS;
+    version 3: v2 with the f16 values as a lossless coded-values blob, which
+    the reader decodes on the GPU -- fewer bytes from storage)."""
     bm = t.bitmap.to_bytes()
-    vals = t.values.cpu().numpy().tobytes()
     flags = (1 if t.quant_scale is not None else 0) | (2 if t.negative_zero_collapsed() else 0)
     L = _lib.lib()
+    if version == 3:
+        if t.dtype != Dtype.F16 or t.quant_scale is not None:
+            raise ValueError("a v3 container holds coded f16 values")
+        blob = encode_values(t.values, pin=False).numpy().tobytes()
+        args3 = (t.rows, t.cols, flags, bm, blob, t.nnz())
+        n = L.endor_file_encode_v3(*args3, None, 0)
+        buf = C.create_string_buffer(n)
+        if n == 0 or L.endor_file_encode_v3(*args3, buf, n) != n:
+            raise ValueError("cannot encode this tensor")
+        return buf.raw
+    vals = t.values.cpu().numpy().tobytes()
     args = (t.rows, t.cols, int(t.dtype), flags, float(t.quant_scale or 0.0), bm, vals, t.nnz())
     enc = {1: L.endor_file_encode, 2: L.endor_file_encode_v2}[version]
     n = enc(*args, None, 0)
@@ -76,14 +88,15 @@ class Reader:
         dev = self.device
         n = info.rows * info.cols
         bm = torch.zeros(((info.bitmap_bytes + 15) // 16) * 16 + 16, dtype=torch.uint8, device=dev)
-        vals = torch.empty(max(info.values_bytes, 1), dtype=torch.uint8, device=dev)
+        nvals = info.nnz * 2 if info.flags & 4 else info.values_bytes  # v3: decoded f16 values
+        vals = torch.empty(max(nvals, 1) + 16, dtype=torch.uint8, device=dev)
         ws = workspace(max(n, 1), dev)
         check(_lib.lib().endor_reader_read(self._h, os.fsencode(path), C.byref(info), bm.data_ptr(),
                                            vals.data_ptr(), 1 if verify else 0, ws.data_ptr(), ws.numel(),
                                            _stream_ptr(dev)))
         dt = Dtype(info.dtype)
         return EndorTensor(info.rows, info.cols, dt, Bitmap(n, data=bm[: info.bitmap_bytes]),
-                           vals[: info.values_bytes],
+                           vals[:nvals],
                            quant_scale=info.quant_scale if info.flags & 1 else None,
                            negative_zero_collapsed=bool(info.flags & 2), validate=False, nnz=info.nnz)
 

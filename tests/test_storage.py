@@ -154,6 +154,52 @@ def test_v2_container_layout(L, tmp_path, rows, cols, eb, flags):
     assert st == 7 and k == KIND["Malformed"]
 
 
+def encode_v3(L, rows, cols, bm, vals, nnz, flags=0, k_max=0):
+    """v3 container: v2 with the values as a coded-values blob (csrc/vcode.cu)."""
+    need = C.c_size_t(0)
+    vp = vals.ctypes.data if vals.size else None
+    assert L.endor_values_encode(vp, nnz, k_max, None, 0, C.byref(need)) == 0
+    blob = np.zeros(need.value, np.uint8)
+    assert L.endor_values_encode(vp, nnz, k_max, blob.ctypes.data, blob.size, C.byref(need)) == 0
+    bmp = bm.ctypes.data if bm.size else None
+    n = L.endor_file_encode_v3(rows, cols, flags, bmp, blob.ctypes.data, nnz, None, 0)
+    buf = C.create_string_buffer(n)
+    assert n and L.endor_file_encode_v3(rows, cols, flags, bmp, blob.ctypes.data, nnz, buf, n) == n
+    return buf.raw, blob
+
+
+@pytest.mark.parametrize("rows,cols,flags,k_max", [(2, 2, 0, 0), (300, 1000, 0, 0), (128, 256, 2, 4), (64, 4096, 0, 0)])
+def test_v3_container_layout(L, tmp_path, rows, cols, flags, k_max):
+    """Version 3 (no reference counterpart): the v2 layout, flags bit 2, and the
+    values section holding the coded-values blob, whose header gives its
+    length; the CRC covers it like any section."""
+    import zlib
+    w = O.synth_weight(rows, cols, 2, rows + cols)
+    _, w = O.magnitude_prune(w, rows * cols, 2, 0.5)
+    bm, vals, nnz, _ = O.compress(w, rows, cols, 2)
+    v3, blob = encode_v3(L, rows, cols, bm, vals, nnz, flags, k_max)
+    assert v3[:4] == b"ENDR" and v3[4:6] == b"\x03\x00" and v3[7] == (flags | 4)
+    voff = 4096 + (bm.size + 4095) // 4096 * 4096
+    assert len(v3) == voff + blob.size + 4 and v3[voff:voff + blob.size] == blob.tobytes()
+    assert int.from_bytes(v3[-4:], "little") == zlib.crc32(v3[:-4]) & 0xFFFFFFFF
+    st, _, info = probe_kind(L, tmp_path, v3)
+    assert st == 0 and info.flags == flags | 4
+    assert (info.values_offset, info.values_bytes, info.file_bytes) == (voff, blob.size, len(v3))
+    # a blob header that disagrees with the container, bit 2 missing, or a quantized v3: Malformed
+    for at, x in ((voff + 8, 1), (voff, 0x10), (7, 4), (7, 1)):
+        bad = bytearray(v3)
+        bad[at] ^= x
+        bad[-4:] = (zlib.crc32(bytes(bad[:-4])) & 0xFFFFFFFF).to_bytes(4, "little")
+        st, k, _ = probe_kind(L, tmp_path, bad)
+        assert st == 7 and k == KIND["Malformed"], (at, x)
+    st, k, _ = probe_kind(L, tmp_path, v3[:voff + 100])
+    assert st == 7 and k == KIND["Truncated"]
+    # v1 / v2 readers of other tools: version 3 is its own version number
+    assert L.endor_file_encode_v3(rows, cols, 1, None, blob.ctypes.data, nnz, None, 0) == 0  # quantized
+    assert L.endor_file_encode_v3(rows, cols, 0, None, blob.ctypes.data, nnz + 1, None, 0) == 0  # nnz mismatch
+
+
+
 # ---------------------------------------------------------------------------- GPU
 
 torch = pytest.importorskip("torch")
@@ -330,3 +376,70 @@ def test_cufile_compat_mode_never_hangs(tmp_path):
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120, env=env)
     assert out.returncode == 0, out.stderr[-2000:]
     assert out.stdout.startswith("OK") or "cuFileDriverOpen" in out.stdout, out.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rows,cols,s,synth", [(2, 2, 0.5, True), (300, 1000, 0.5, True), (1024, 9216, 0.5, True),
+                                               (1024, 9216, 0.7, False), (5, 5, 1.0, True)])
+def test_reader_v3_decodes_coded_values(S, E, L, tmp_path, rows, cols, s, synth):
+    """v3 containers: the reader moves the coded section, checks the CRC over it,
+    and decodes it on the GPU into the exact packed values."""
+    if synth:
+        w = O.synth_weight(rows, cols, 2, rows + cols)
+        _, w = O.magnitude_prune(w, rows * cols, 2, s)
+    else:
+        w = O.random_dense(rows, cols, 2, rows + cols, s)
+    bm, vals, nnz, _ = O.compress(w, rows, cols, 2)
+    t = E.EndorTensor(rows, cols, E.Dtype.F16, E.Bitmap.from_bytes(bm.tobytes(), rows * cols, device="cuda"),
+                      torch.from_numpy(vals.copy()).cuda())
+    p = str(tmp_path / "w3.endor")
+    n = S.write_endor_file(t, p, version=3)
+    info = S.probe(p)
+    assert n == os.path.getsize(p) and info.flags & 4 and info.bitmap_offset == 4096
+    r = S.Reader("cuda", mode=3, bounce_bytes=1 << 16)
+    got = r.read(p, verify=True)
+    assert got.bitmap.to_bytes() == bm.tobytes()
+    assert got.values.cpu().numpy().tobytes() == vals.tobytes()
+    assert E.decompress(got).bytes() == w.tobytes()
+    assert r.read(p, verify=False).values.cpu().numpy().tobytes() == vals.tobytes()
+    if nnz:
+        data = bytearray(open(p, "rb").read())
+        data[info.values_offset + info.values_bytes // 2] ^= 0x20  # inside the coded section
+        open(p, "wb").write(bytes(data))
+        with pytest.raises(E.FormatError) as ei:
+            r.read(p, verify=True)
+        assert ei.value.kind.name == "BadCrc"
+    r.close()
+
+
+@pytest.mark.gpu
+def test_pipeline_v3_file_ops_match_host_sourced(S, E, tmp_path):
+    """EndorDirect from v3 files through the offload pipeline: fewer bytes read,
+    the same y as the raw host-sourced ops."""
+    from paper_2406_11674_b200.pipeline import HostOp, OffloadPipeline, pinned_copy
+    shapes = [(64, 2048), (33, 1000), (128, 4096)]
+    ys, nbytes = {}, {}
+    for src in ("host", "file"):
+        ops = []
+        for i, (r, c) in enumerate(shapes):
+            w = E.synth_weight(r, c, 70 + i, device="cuda")
+            E.magnitude_prune(w, 0.5, inplace=True)
+            t = E.compress(w)
+            x = ((torch.rand(c, generator=torch.Generator().manual_seed(i)) * 2 - 1).half()).cuda()
+            kw = dict(x=x, y=torch.empty(r, dtype=torch.float32, device="cuda"),
+                      y_host=torch.empty(r, dtype=torch.float32, pin_memory=True))
+            if src == "file":
+                p = str(tmp_path / f"v3op{i}.endor")
+                S.write_endor_file(t, p, version=3)
+                e = torch.empty(0, dtype=torch.uint8)
+                ops.append(HostOp(r, c, 0, e, e, t.nnz(), path=p, **kw))
+            else:
+                ops.append(HostOp(r, c, 0, pinned_copy(t.bitmap.data), pinned_copy(t.values), t.nnz(), **kw))
+        pipe = OffloadPipeline(0, max(r * c for r, c in shapes))
+        pipe.run(ops, sync=True)
+        nbytes[src] = pipe.stats()["h2d_bytes"]
+        pipe.close()
+        ys[src] = [o.y_host.clone() for o in ops]
+    assert nbytes["file"] < nbytes["host"]
+    for a, b in zip(ys["host"], ys["file"]):
+        assert torch.equal(a, b)
