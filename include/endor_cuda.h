@@ -404,6 +404,8 @@ typedef struct endor_file_info {
     uint32_t header_crc;           /* CRC-32 of the header bytes alone */
     uint32_t gap_bytes;            /* v2: zero fill between the bitmap and values sections */
     uint64_t header_bytes, bitmap_offset, bitmap_bytes, values_offset, values_bytes, file_bytes;
+    uint64_t values_out_bytes;     /* bytes endor_reader_read writes to values_dev: nnz * elem bytes
+                                      (= values_bytes, except v3: the decoded values, not the blob) */
 } endor_file_info;
 
 /* Parse and validate the header and the declared layout in decode_endor's
@@ -417,8 +419,8 @@ typedef struct endor_file_info {
  * and the values section holding a coded-values blob of the f16 values
  * (endor_values_encode; not quantized): fewer bytes leave storage, and
  * endor_reader_read decodes them on the GPU after the CRC / padding / popcount
- * checks, so values_dev must hold nnz * 2 bytes.  endor_file_probe reports the
- * blob's length as values_bytes.  Returns the container size (0 on a bad
+ * checks, so values_dev must hold nnz * 2 bytes (values_out_bytes).
+ * endor_file_probe reports the blob's length as values_bytes.  Returns the container size (0 on a bad
  * argument or a blob that does not hold nnz values). */
 size_t endor_file_encode_v3(uint64_t rows, uint64_t cols, int32_t flags, const void* bitmap, const void* blob,
                             uint64_t nnz, void* out, size_t out_cap);

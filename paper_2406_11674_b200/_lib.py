@@ -44,7 +44,8 @@ class FileInfo(C.Structure):
     _fields_ = [("rows", _u64), ("cols", _u64), ("nnz", _u64), ("dtype", _i32), ("flags", _i32),
                 ("quant_scale", C.c_float), ("crc", C.c_uint32), ("header_crc", C.c_uint32),
                 ("gap_bytes", C.c_uint32), ("header_bytes", _u64), ("bitmap_offset", _u64),
-                ("bitmap_bytes", _u64), ("values_offset", _u64), ("values_bytes", _u64), ("file_bytes", _u64)]
+                ("bitmap_bytes", _u64), ("values_offset", _u64), ("values_bytes", _u64), ("file_bytes", _u64),
+                ("values_out_bytes", _u64)]
 
 
 # name -> (restype, argtypes): every symbol include/endor_cuda.h declares

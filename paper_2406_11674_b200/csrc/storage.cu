@@ -435,6 +435,7 @@ int endor_file_probe(const char* path, endor_file_info* out) {
                     f.values_bytes = vh.blob_bytes;
             }
             f.file_bytes = wraps ? UINT64_MAX : f.values_offset + f.values_bytes + 4;
+            f.values_out_bytes = wraps ? 0 : f.nnz * eb;
             if (st != ENDOR_OK)
                 ;  // the coded-values header already failed
             else if (wraps || size < f.file_bytes)

@@ -88,7 +88,7 @@ class Reader:
         dev = self.device
         n = info.rows * info.cols
         bm = torch.zeros(((info.bitmap_bytes + 15) // 16) * 16 + 16, dtype=torch.uint8, device=dev)
-        nvals = info.nnz * 2 if info.flags & 4 else info.values_bytes  # v3: decoded f16 values
+        nvals = info.values_out_bytes  # v3: the decoded f16 values, not the coded section
         vals = torch.empty(max(nvals, 1) + 16, dtype=torch.uint8, device=dev)
         ws = workspace(max(n, 1), dev)
         check(_lib.lib().endor_reader_read(self._h, os.fsencode(path), C.byref(info), bm.data_ptr(),

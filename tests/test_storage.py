@@ -139,6 +139,7 @@ def test_v2_container_layout(L, tmp_path, rows, cols, eb, flags):
     assert (info.bitmap_offset, info.bitmap_bytes, info.values_offset, info.values_bytes, info.file_bytes) == \
         (4096, bm.size, voff, vals.size, len(v2))
     assert info.gap_bytes == voff - 4096 - bm.size
+    assert info.values_out_bytes == info.values_bytes
     assert info.header_crc == zlib.crc32(v2[:4096]) & 0xFFFFFFFF
     # a dirty fill byte (header page or the gap) is Malformed even with a fixed-up CRC
     for at in ([100] + ([4096 + bm.size] if voff > 4096 + bm.size else [])):
@@ -185,6 +186,7 @@ def test_v3_container_layout(L, tmp_path, rows, cols, flags, k_max):
     st, _, info = probe_kind(L, tmp_path, v3)
     assert st == 0 and info.flags == flags | 4
     assert (info.values_offset, info.values_bytes, info.file_bytes) == (voff, blob.size, len(v3))
+    assert info.values_out_bytes == 2 * nnz  # what the reader writes: the decoded values
     # a blob header that disagrees with the container, bit 2 missing, or a quantized v3: Malformed
     for at, x in ((voff + 8, 1), (voff, 0x10), (7, 4), (7, 1)):
         bad = bytearray(v3)
