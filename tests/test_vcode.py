@@ -91,6 +91,9 @@ CASES = {
     "uniform_u16": np.random.default_rng(6).integers(0, 1 << 16, 50_001, dtype=np.uint16),
     "specials": np.array([0x7C00, 0xFC00, 0x7E00, 0x7C01, 0xFFFF, 0x8000, 0x0001, 0x8001] * 37, np.uint16),
     "one_hi_byte": (np.random.default_rng(7).integers(0, 256, 4097, dtype=np.uint16) | 0x3A00).astype(np.uint16),
+    # geometric high bytes: Huffman lengths past 12 bits, flattened to fit the table
+    "geometric": ((np.minimum(np.random.default_rng(8).geometric(0.5, 70_001) - 1, 40).astype(np.uint16) + 0x30) << 8
+                  | np.random.default_rng(9).integers(0, 256, 70_001, dtype=np.uint16)).astype(np.uint16),
 }
 
 
@@ -99,6 +102,20 @@ CASES = {
 def test_encode_round_trip_numpy(name, k_max):
     v = CASES[name]
     blob = encode(v, k_max)
+    assert np.array_equal(decode_np(blob), v)
+
+
+def test_huffman_code_lengths_are_limited_to_the_table():
+    # geometric high-byte frequencies (2^-1, 2^-2, ...): an unbounded Huffman code
+    # would go past 12 bits; the lengths are flattened until they fit the table
+    rng = np.random.default_rng(21)
+    hi = np.minimum(rng.geometric(0.5, 400_000) - 1, 40).astype(np.uint16)
+    v = ((hi + 0x30) << 8 | rng.integers(0, 256, hi.size, dtype=np.uint16)).astype(np.uint16)
+    blob = encode(v, 0)
+    assert int(blob[:4].view("<u4")[0]) == 0x31485645
+    lut = blob[256:256 + 8192].view("<u2")
+    assert (lut >> 8).max() <= 12 and (lut >> 8).min() >= 1  # every entry assigned, no code past 12 bits
+    assert len(np.unique(hi)) > 13  # more symbols than a 12-bit chain of halvings could hold
     assert np.array_equal(decode_np(blob), v)
 
 
